@@ -1,0 +1,211 @@
+// Batched interface flux (minimum slice of the hot path) and the library's
+// error plumbing.  Replaces gks3d flux.build_interface / evolve_flux /
+// point_value (flux.py:69-188) for arbitrary point batches.
+#include <stdarg.h>
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "gks_common.cuh"
+#include "gks_kinetic.cuh"
+
+namespace gks {
+
+static thread_local std::string g_err;
+static thread_local int64_t g_err_index = -1;
+std::atomic<int64_t> g_launches{0};
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+void set_error_index(int64_t i) { g_err_index = i; }
+
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  set_error("CUDA error %s (%s) at %s:%d in %s", cudaGetErrorName(e), cudaGetErrorString(e), file,
+            line, what);
+  return GKS_ERR_CUDA;
+}
+
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+__global__ void __launch_bounds__(128) k_flux_batch(int64_t n, const double* __restrict__ wl,
+                                                    const double* __restrict__ wr,
+                                                    const double* __restrict__ sl,
+                                                    const double* __restrict__ sr,
+                                                    const double* __restrict__ tau,
+                                                    const double* __restrict__ dt,
+                                                    const double* __restrict__ tp, KinConst kc,
+                                                    double* __restrict__ flux,
+                                                    double* __restrict__ point, int* status) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  FluxIn in;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    in.wl[k] = wl[i * 5 + k];
+    in.wr[k] = wr[i * 5 + k];
+  }
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      in.sl[d][k] = sl ? sl[i * 15 + d * 5 + k] : 0.0;
+      in.sr[d][k] = sr ? sr[i * 15 + d * 5 + k] : 0.0;
+    }
+  double f[5], p[5];
+  const bool want_point = tp != nullptr;
+  const int rc = interface_flux(in, tau[i], dt[i], MODEL_INVISCID, 0.0, kc, f, want_point,
+                                want_point ? tp[i] : 0.0, p, nullptr);
+  if (rc) {
+    raise_dev(status, GKS_ERR_UNPHYSICAL, (int)i);
+    return;
+  }
+  if (flux) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) flux[i * 5 + k] = f[k];
+  }
+  if (point) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) point[i * 5 + k] = p[k];
+  }
+}
+
+}  // namespace gks
+
+using namespace gks;
+
+extern "C" {
+
+int gks_abi_version(void) { return GKS_ABI_VERSION; }
+const char* gks_last_error(void) { return g_err.c_str(); }
+int64_t gks_last_error_index(void) { return g_err_index; }
+int64_t gks_kernel_launches(void) { return g_launches.load(); }
+
+int gks_flux_batch(int64_t n, const double* wl, const double* wr, const double* sl,
+                   const double* sr, const double* tau, const double* dt, const double* tp,
+                   double gamma, double* flux_out, double* point_out) {
+  g_err_index = -1;
+  if (n < 0 || !wl || !wr || !tau || !dt) {
+    set_error("gks_flux_batch: bad arguments");
+    return GKS_ERR_BAD_ARG;
+  }
+  if (n == 0) return GKS_OK;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    set_error("gks_flux_batch: no CUDA device visible");
+    return GKS_ERR_NO_DEVICE;
+  }
+  const size_t s5 = (size_t)n * 5 * sizeof(double), s15 = 3 * s5, s1 = (size_t)n * sizeof(double);
+  double *d_wl, *d_wr, *d_sl = nullptr, *d_sr = nullptr, *d_tau, *d_dt, *d_tp = nullptr;
+  double *d_f = nullptr, *d_p = nullptr;
+  int* d_status;
+  GKS_CUDA(cudaMalloc(&d_wl, s5));
+  GKS_CUDA(cudaMalloc(&d_wr, s5));
+  GKS_CUDA(cudaMalloc(&d_tau, s1));
+  GKS_CUDA(cudaMalloc(&d_dt, s1));
+  GKS_CUDA(cudaMalloc(&d_status, 4 * sizeof(int)));
+  GKS_CUDA(cudaMemcpy(d_wl, wl, s5, cudaMemcpyHostToDevice));
+  GKS_CUDA(cudaMemcpy(d_wr, wr, s5, cudaMemcpyHostToDevice));
+  GKS_CUDA(cudaMemcpy(d_tau, tau, s1, cudaMemcpyHostToDevice));
+  GKS_CUDA(cudaMemcpy(d_dt, dt, s1, cudaMemcpyHostToDevice));
+  if (sl) {
+    GKS_CUDA(cudaMalloc(&d_sl, s15));
+    GKS_CUDA(cudaMemcpy(d_sl, sl, s15, cudaMemcpyHostToDevice));
+  }
+  if (sr) {
+    GKS_CUDA(cudaMalloc(&d_sr, s15));
+    GKS_CUDA(cudaMemcpy(d_sr, sr, s15, cudaMemcpyHostToDevice));
+  }
+  if (tp) {
+    GKS_CUDA(cudaMalloc(&d_tp, s1));
+    GKS_CUDA(cudaMemcpy(d_tp, tp, s1, cudaMemcpyHostToDevice));
+  }
+  if (flux_out) GKS_CUDA(cudaMalloc(&d_f, s5));
+  if (point_out) GKS_CUDA(cudaMalloc(&d_p, s5));
+  const int st0[4] = {0, 0x7fffffff, 0, 0};
+  GKS_CUDA(cudaMemcpy(d_status, st0, sizeof(st0), cudaMemcpyHostToDevice));
+  k_flux_batch<<<blocks_for(n, 128), 128>>>(n, d_wl, d_wr, d_sl, d_sr, d_tau, d_dt,
+                                            point_out ? d_tp : nullptr, make_kin(gamma), d_f,
+                                            d_p, d_status);
+  count_launch(1);
+  GKS_CUDA(cudaGetLastError());
+  int st[4];
+  GKS_CUDA(cudaMemcpy(st, d_status, sizeof(st), cudaMemcpyDeviceToHost));
+  int rc = GKS_OK;
+  if (st[0]) {
+    set_error("unphysical interface state at point %d", st[1]);
+    g_err_index = st[1];
+    rc = st[0];
+  } else {
+    if (flux_out) GKS_CUDA(cudaMemcpy(flux_out, d_f, s5, cudaMemcpyDeviceToHost));
+    if (point_out) GKS_CUDA(cudaMemcpy(point_out, d_p, s5, cudaMemcpyDeviceToHost));
+  }
+  cudaFree(d_wl); cudaFree(d_wr); cudaFree(d_tau); cudaFree(d_dt); cudaFree(d_status);
+  if (d_sl) cudaFree(d_sl);
+  if (d_sr) cudaFree(d_sr);
+  if (d_tp) cudaFree(d_tp);
+  if (d_f) cudaFree(d_f);
+  if (d_p) cudaFree(d_p);
+  return rc;
+}
+
+// Kernel-only timing of the fused interface flux on n device-resident random
+// interfaces (measurement hook for tools/ and profiles/; not part of the
+// reference API).  Writes the mean ms per launch.
+int gks_flux_bench(int64_t n, int reps, double gamma, double* ms_per_launch) {
+  std::vector<double> h(n * 5 * 2 + n * 15 * 2 + 2 * n);
+  uint64_t st = 88172645463325252ull;
+  auto rnd = [&]() {
+    st ^= st << 13; st ^= st >> 7; st ^= st << 17;
+    return (double)(st >> 11) * (1.0 / 9007199254740992.0);
+  };
+  double* wl = h.data();
+  double* wr = wl + n * 5;
+  double* sl = wr + n * 5;
+  double* sr = sl + n * 15;
+  double* tau = sr + n * 15;
+  double* dt = tau + n;
+  for (int64_t i = 0; i < n; ++i) {
+    for (double* w : {wl + i * 5, wr + i * 5}) {
+      w[0] = 0.4 + 1.2 * rnd(); w[1] = -1 + 2 * rnd(); w[2] = -0.6 + 1.2 * rnd();
+      w[3] = -0.6 + 1.2 * rnd(); w[4] = 0.5 + 2 * rnd();
+    }
+    for (int k = 0; k < 15; ++k) { sl[i * 15 + k] = 0.3 * (rnd() - 0.5); sr[i * 15 + k] = 0.3 * (rnd() - 0.5); }
+    dt[i] = 0.01 + 0.09 * rnd();
+    tau[i] = 1e-4 + 0.05 * rnd();
+  }
+  double* d;
+  int* d_status;
+  GKS_CUDA(cudaMalloc(&d, h.size() * sizeof(double) + n * 5 * sizeof(double)));
+  GKS_CUDA(cudaMalloc(&d_status, 4 * sizeof(int)));
+  GKS_CUDA(cudaMemset(d_status, 0, 4 * sizeof(int)));
+  GKS_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+  double* df = d + h.size();
+  double* dwl = d; double* dwr = dwl + n * 5; double* dsl = dwr + n * 5; double* dsr = dsl + n * 15;
+  double* dtau = dsr + n * 15; double* ddt = dtau + n;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  for (int r = 0; r < 3; ++r)
+    k_flux_batch<<<blocks_for(n, 128), 128>>>(n, dwl, dwr, dsl, dsr, dtau, ddt, nullptr, make_kin(gamma), df, nullptr, d_status);
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r)
+    k_flux_batch<<<blocks_for(n, 128), 128>>>(n, dwl, dwr, dsl, dsr, dtau, ddt, nullptr, make_kin(gamma), df, nullptr, d_status);
+  cudaEventRecord(e1);
+  GKS_CUDA(cudaEventSynchronize(e1));
+  count_launch(3 + reps);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *ms_per_launch = ms / reps;
+  cudaFree(d); cudaFree(d_status);
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
+  return GKS_OK;
+}
+
+}  // extern "C"
