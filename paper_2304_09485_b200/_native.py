@@ -35,6 +35,78 @@ c_int32_p = C.POINTER(C.c_int32)
 c_void_p = C.c_void_p
 
 
+class GksMeshDesc(C.Structure):
+    _fields_ = [("ncells", C.c_int64), ("nfaces", C.c_int64), ("nfq", C.c_int64), ("ncq", C.c_int64),
+                ("cell_kind", C.c_void_p), ("cell_volume", C.c_void_p), ("cell_h", C.c_void_p),
+                ("cell_centroid", C.c_void_p), ("cell_cq_start", C.c_void_p), ("cq_point", C.c_void_p),
+                ("cq_weight", C.c_void_p), ("cell_face_start", C.c_void_p), ("cell_face_list", C.c_void_p),
+                ("face_owner", C.c_void_p), ("face_neighbor", C.c_void_p), ("face_patch", C.c_void_p),
+                ("face_area", C.c_void_p), ("face_normal", C.c_void_p), ("face_frame", C.c_void_p),
+                ("face_shift", C.c_void_p), ("face_fq_start", C.c_void_p), ("fq_face", C.c_void_p),
+                ("fq_point", C.c_void_p), ("fq_weight", C.c_void_p)]
+
+
+_DESC_FIELDS = {
+    "cell_kind": np.int8, "cell_volume": np.float64, "cell_h": np.float64, "cell_centroid": np.float64,
+    "cell_cq_start": np.int64, "cq_point": np.float64, "cq_weight": np.float64,
+    "cell_face_start": np.int64, "cell_face_list": np.int64, "face_owner": np.int64,
+    "face_neighbor": np.int64, "face_patch": np.int64, "face_area": np.float64, "face_normal": np.float64,
+    "face_frame": np.float64, "face_shift": np.float64, "face_fq_start": np.int64, "fq_face": np.int64,
+    "fq_point": np.float64, "fq_weight": np.float64,
+}
+
+
+def mesh_desc(mesh):
+    """GksMeshDesc view of a host Mesh; returns (desc, keepalive)."""
+    keep = {}
+    desc = GksMeshDesc()
+    desc.ncells = mesh.ncells
+    desc.nfaces = mesh.nfaces
+    desc.nfq = len(mesh.fq_face)
+    desc.ncq = len(mesh.cq_weight)
+    for name, dt in _DESC_FIELDS.items():
+        arr = np.ascontiguousarray(getattr(mesh, name), dtype=dt)
+        keep[name] = arr
+        setattr(desc, name, arr.ctypes.data)
+    return desc, keep
+
+
+_DTYPES = {0: np.float64, 1: np.int64, 2: np.int8}
+
+
+class NativeSetup:
+    """Owner of a GksSetup* (stencils + reconstruction operators)."""
+
+    def __init__(self, mesh, schemes=3, nthreads=0):
+        lib = load()
+        self._desc, self._keep = mesh_desc(mesh)
+        h = C.c_void_p()
+        check(lib.gks_setup_build(C.byref(self._desc), int(schemes), int(nthreads), C.byref(h)))
+        self.handle = h
+        self.schemes = schemes
+        self._cache = {}
+
+    def array(self, name):
+        if name in self._cache:
+            return self._cache[name]
+        lib = load()
+        dt, nd = C.c_int(), C.c_int()
+        shape = (C.c_int64 * 4)()
+        check(lib.gks_setup_query(self.handle, name.encode(), C.byref(dt), C.byref(nd), shape))
+        shp = tuple(int(shape[i]) for i in range(nd.value))
+        out = np.empty(shp, dtype=_DTYPES[dt.value])
+        check(lib.gks_setup_copy(self.handle, name.encode(), out.ctypes.data_as(C.c_void_p), out.nbytes))
+        out.setflags(write=False)
+        self._cache[name] = out
+        return out
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.gks_setup_free(h)
+            self.handle = None
+
+
 class GksError(RuntimeError):
     def __init__(self, code, message, index=-1):
         super().__init__(message)
@@ -53,6 +125,11 @@ SIGNATURES = [
                                  c_double_p, c_double_p, c_double_p, C.c_double, c_double_p,
                                  c_double_p]),
     ("gks_flux_bench", C.c_int, [C.c_int64, C.c_int, C.c_double, c_double_p]),
+    ("gks_setup_build", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    ("gks_setup_free", None, [C.c_void_p]),
+    ("gks_setup_query", C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                  C.POINTER(C.c_int64)]),
+    ("gks_setup_copy", C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int64]),
 ]
 
 

@@ -69,7 +69,7 @@ def build(verbose=False, force=False, ptxas_verbose=False):
         objs.append(obj)
     for src in cpp:
         obj = BUILD / (src.stem + ".o")
-        _run(["g++", *CXX_FLAGS, "-c", str(src), "-o", str(obj)], verbose)
+        _run(["g++", *CXX_FLAGS, "-ffp-contract=off", "-c", str(src), "-o", str(obj)], verbose)
         objs.append(obj)
     tmp = LIB.with_suffix(".so.tmp")
     _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-Xcompiler", "-fopenmp", "-o", str(tmp),

@@ -75,7 +75,197 @@ def make_flux():
     print("flux_batch.npz", {k: v.shape for k, v in out.items()})
 
 
-SECTIONS = {"flux": make_flux}
+GAMMA = 1.4
+
+MESH_CASES = {
+    "tet3p": dict(extent=(1, 1, 1), divisions=(3, 3, 3), split="tet", periodic=("x", "y", "z")),
+    "tet3j": dict(extent=(1, 1, 1), divisions=(3, 3, 3), split="tet", perturb=0.15, seed=202403),
+    "hex4p": dict(extent=(1, 1, 1), divisions=(4, 4, 4), split="hex", periodic=("x", "y", "z")),
+    "hex332": dict(extent=(1, 2, 1), divisions=(3, 3, 2), split="hex"),
+    "tet2x": dict(extent=(1, 1, 1), divisions=(2, 2, 2), split="tet", periodic=("x",)),
+}
+
+MESH_ARRAYS = ("cell_kind", "cell_nodes", "cell_volume", "cell_centroid", "cell_h", "face_nodes",
+               "face_owner", "face_neighbor", "face_patch", "face_area", "face_normal", "face_frame",
+               "face_shift", "fq_point", "fq_weight", "fq_face", "face_fq_start", "cq_point", "cq_weight",
+               "cell_cq_start")
+
+
+def _flat_stencils(st, nc):
+    """Flatten a reference StencilTable into CSR arrays (ids + shifts)."""
+    out = {}
+    nf = max(len(st[c].neighbor_ids) for c in range(nc))
+    nb = np.full((nc, nf), -1, dtype=np.int64)
+    nbs = np.zeros((nc, nf, 3))
+    big_start, big_ids, big_shift = [0], [], []
+    sub_cell_start, sub_member_start, sub_ids, sub_shift = [0], [0], [], []
+    wfb, hfb = [], []
+    for c in range(nc):
+        s = st[c]
+        nb[c, : len(s.neighbor_ids)] = s.neighbor_ids
+        nbs[c, : len(s.neighbor_ids)] = s.neighbor_shifts
+        big_ids.extend(s.big_ids.tolist())
+        big_shift.extend(np.asarray(s.big_shifts).reshape(-1, 3).tolist())
+        big_start.append(len(big_ids))
+        for ids, sh in zip(s.sub_ids, s.sub_shifts):
+            sub_ids.extend(ids.tolist())
+            sub_shift.extend(np.asarray(sh).reshape(-1, 3).tolist())
+            sub_member_start.append(len(sub_ids))
+        sub_cell_start.append(len(sub_member_start) - 1)
+        wfb.append(s.weno_fallback)
+        hfb.append(s.hweno_fallback)
+    out.update(nbr_ids=nb, nbr_shift=nbs, big_start=np.array(big_start), big_ids=np.array(big_ids),
+               big_shift=np.array(big_shift).reshape(-1, 3), sub_cell_start=np.array(sub_cell_start),
+               sub_member_start=np.array(sub_member_start), sub_ids=np.array(sub_ids, dtype=np.int64),
+               sub_shift=np.array(sub_shift).reshape(-1, 3), weno_fallback=np.array(wfb, dtype=np.int8),
+               hweno_fallback=np.array(hfb, dtype=np.int8))
+    return out
+
+
+def make_mesh():
+    from gks3d.hweno import HwenoReconstructor
+    from gks3d.mesh import build_stencils, generate_box_mesh
+    from gks3d.recon import ReconGeometry, WenoReconstructor
+
+    for name, kw in MESH_CASES.items():
+        m = generate_box_mesh(**kw)
+        out = {f"mesh_{k}": np.asarray(getattr(m, k)) for k in MESH_ARRAYS}
+        out["mesh_cell_face_list"] = np.concatenate(m.cell_faces)
+        st = build_stencils(m)
+        out.update({f"st_{k}": v for k, v in _flat_stencils(st, m.ncells).items()})
+        g = ReconGeometry(m, st)
+        w = WenoReconstructor(g)
+        h = HwenoReconstructor(g)
+        out.update(avg0=g.avg0, beta_mat=g.beta_mat,
+                   weno_big_op=w.big_op, weno_big_gather=w.big_gather, weno_big_degree=w.big_degree,
+                   weno_sub_op=w.sub_op, weno_sub_gather=w.sub_gather,
+                   weno_sub_active=w.sub_active.astype(np.int8),
+                   hweno_big_op=h.big_op, hweno_big_avg_gather=h.big_avg_gather,
+                   hweno_big_grad_gather=h.big_grad_gather, hweno_big_grad_scale=h.big_grad_scale,
+                   hweno_big_ncols=h.big_ncols, hweno_big_degree=h.big_degree, hweno_sub_op=h.sub_op,
+                   hweno_sub_gather=h.sub_gather, hweno_sub_active=h.sub_active.astype(np.int8))
+        np.savez_compressed(HERE / f"mesh_{name}.npz", **out)
+        print(f"mesh_{name}.npz", m.ncells, "cells")
+
+
+# solver cases: mesh, options, patch table, initial field recipe
+def _patch_specs(case, mesh):
+    from gks3d.boundary import PatchSpec
+
+    ref = np.array(case.get("reference", (1.0, 0.5, 0.0, 0.0, 1.0 / GAMMA)))
+    kinds = case.get("patches", {})
+    out = {}
+    for n in mesh.patch_names:
+        spec = kinds.get(n, kinds.get("*"))
+        if spec is None:
+            continue
+        kind, kw = spec
+        kw = dict(kw)
+        if kind in ("farfield_riemann", "supersonic_inlet") and "reference" not in kw:
+            kw["reference"] = ref
+        out[n] = PatchSpec(n, kind, **kw)
+    return out
+
+
+SOLVER_CASES = {
+    # smooth density wave on the periodic Kuhn-tet box (config-1 shape)
+    "s1_tet_weno": dict(mesh="tet3p", scheme="weno_gmres", field="wave"),
+    # perturbed tets, farfield everywhere, noisy near-uniform state
+    "s2_tetj_weno_far": dict(mesh="tet3j", scheme="weno_gmres", field="noise",
+                             patches={"*": ("farfield_riemann", {})}),
+    "s3_tetj_hweno_far": dict(mesh="tet3j", scheme="hweno_gmres", field="noise",
+                              patches={"*": ("farfield_riemann", {})}),
+    # compact scheme, linear weights, periodic hexes (criterion-4 shape)
+    "s4_hex_hweno_lin": dict(mesh="hex4p", scheme="hweno_gmres", weights="linear", field="wave"),
+    # viscous cavity walls (isothermal no-slip with lid)
+    "s5_tet_cavity": dict(mesh="tet3j", scheme="weno_gmres", model="viscous", mu=0.01, field="rest",
+                          reference=(1.0, 0.0, 0.0, 0.0, 1.0 / GAMMA),
+                          patches={"*": ("wall_noslip_isothermal", {"lambda_wall": 0.7}),
+                                   "ymax": ("wall_noslip_isothermal",
+                                            {"lambda_wall": 0.7, "velocity": np.array([0.15, 0.0, 0.0])})}),
+    # supersonic channel: inlet/outlet, slip walls, farfield
+    "s6_tet_supersonic": dict(mesh="tet3j", scheme="hweno_gmres", field="noise",
+                              reference=(1.0, 2.0, 0.1, 0.0, 1.0 / GAMMA),
+                              patches={"xmin": ("supersonic_inlet", {}), "xmax": ("supersonic_outlet", {}),
+                                       "ymin": ("wall_slip_adiabatic", {}), "ymax": ("wall_slip_adiabatic", {}),
+                                       "zmin": ("farfield_riemann", {}), "zmax": ("farfield_riemann", {})}),
+    # hexes with adiabatic no-slip walls + farfield
+    "s7_hex_walls": dict(mesh="hex332", scheme="weno_gmres", model="viscous", mu=0.005, field="noise",
+                         patches={"*": ("farfield_riemann", {}), "ymin": ("wall_noslip_adiabatic", {}),
+                                  "ymax": ("wall_noslip_adiabatic", {})}),
+}
+
+
+def initial_q(case, mesh, compact):
+    from gks3d.kinetic import primitive_to_conserved
+
+    rng = np.random.default_rng({"wave": 11, "noise": 12, "rest": 13}[case["field"]])
+    x = mesh.cell_centroid
+    nc = mesh.ncells
+    ref = np.array(case.get("reference", (1.0, 0.5, 0.0, 0.0, 1.0 / GAMMA)))
+    w = np.tile(np.array([ref[0], ref[1], ref[2], ref[3], ref[0] / (2.0 * ref[4])]), (nc, 1))
+    tp = 2 * np.pi
+    if case["field"] == "wave":
+        w[:, 0] = 1.0 + 0.2 * np.sin(tp * x[:, 0]) * np.cos(tp * x[:, 1])
+        w[:, 1] = 0.5 + 0.1 * np.cos(tp * x[:, 2])
+        w[:, 2] = 0.1 * np.sin(tp * x[:, 1])
+        w[:, 4] = w[:, 4] * (1.0 + 0.1 * np.cos(tp * x[:, 0]))
+    elif case["field"] == "noise":
+        w[:, 0] *= 1.0 + 0.05 * rng.normal(size=nc)
+        w[:, 1:4] += 0.05 * rng.normal(size=(nc, 3))
+        w[:, 4] *= 1.0 + 0.05 * rng.normal(size=nc)
+    q = primitive_to_conserved(w)
+    grad = None
+    if compact:
+        grad = 0.1 * np.random.default_rng(5).normal(size=(nc, 3, 5))
+    return q, grad
+
+
+def make_solver():
+    from gks3d.jacobian import assemble_jacobian
+    from gks3d.krylov import gmres_solve
+    from gks3d.mesh import generate_box_mesh
+    from gks3d.stepping import SolutionField, Solver, SolverOptions
+
+    for name, case in SOLVER_CASES.items():
+        mesh = generate_box_mesh(**MESH_CASES[case["mesh"]])
+        patches = _patch_specs(case, mesh)
+        opts = SolverOptions(scheme=case["scheme"], model=case.get("model", "inviscid"), mu=case.get("mu", 0.0),
+                             weights=case.get("weights", "nonlinear"), patches=patches)
+        solver = Solver(mesh, opts)
+        q, grad = initial_q(case, mesh, solver.compact)
+        fld = SolutionField(q, grad)
+        dt = solver.local_time_step(fld)
+        res, grad_new = solver.residual(fld, dt)
+        ghosts = solver._boundary_ghosts(fld)
+        a = assemble_jacobian(mesh, q, dt, GAMMA, ghosts)
+        x, info = gmres_solve(a, res, m=10, restarts=3, k_max=2)
+        rng = np.random.default_rng(99)
+        v = rng.normal(size=q.shape)
+        fm = solver.frechet_matvec(fld, v, dt)
+        out = dict(q=q, dt=dt, res=res, ghosts=np.zeros((0, 5)) if ghosts is None else ghosts,
+                   jac_diag=a.diag, jac_off=a.off, jac_off_col=a.off_col, jac_off_row=a.off_row,
+                   jac_rowptr=a.rowptr, gmres_x=x, gmres_matvecs=np.array(info.matvecs),
+                   gmres_cycle_norms=np.array([n for cyc in info.cycle_residuals for n in cyc]),
+                   gmres_cycle_len=np.array([len(c) for c in info.cycle_residuals]), frechet_v=v, frechet=fm)
+        if grad is not None:
+            out.update(grad=grad, grad_new=grad_new)
+        # a short nonlinear history
+        hist = []
+        qs = []
+        f = fld
+        for _ in range(4):
+            f, si = solver.advance(f)
+            hist.append((si.res_rho_l1, si.res_l2, si.dt_min, si.solver_cycles, float(si.retried)))
+            qs.append(f.q.copy())
+        out.update(hist=np.array(hist), q_after=np.array(qs))
+        if f.grad is not None:
+            out["grad_after"] = f.grad
+        np.savez_compressed(HERE / f"solver_{name}.npz", **out)
+        print(f"solver_{name}.npz", mesh.ncells, "cells", "matvecs", info.matvecs)
+
+
+SECTIONS = {"flux": make_flux, "mesh": make_mesh, "solver": make_solver}
 
 
 def main(argv):
