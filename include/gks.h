@@ -106,6 +106,126 @@ void gks_setup_free(GksSetup* setup);
 int gks_setup_query(const GksSetup* setup, const char* name, int* dtype, int* ndim, int64_t* shape);
 int gks_setup_copy(const GksSetup* setup, const char* name, void* dst, int64_t nbytes);
 
+/* ------------------------------------------------------------------ */
+/* Solver handle: device-resident mesh, operators, state and Krylov     */
+/* work space on one GPU.  Replaces gks3d.stepping.Solver               */
+/* (stepping.py:87-313) underneath the Python Solver mirror.            */
+/* ------------------------------------------------------------------ */
+enum {  /* boundary.py:18-19 PATCH_KINDS */
+  GKS_PATCH_NONE = -1,
+  GKS_PATCH_WALL_NOSLIP_ISOTHERMAL = 0,
+  GKS_PATCH_WALL_NOSLIP_ADIABATIC = 1,
+  GKS_PATCH_WALL_SLIP_ADIABATIC = 2,
+  GKS_PATCH_FARFIELD_RIEMANN = 3,
+  GKS_PATCH_SUPERSONIC_INLET = 4,
+  GKS_PATCH_SUPERSONIC_OUTLET = 5
+};
+
+typedef struct GksPatchDesc {  /* boundary.PatchSpec (boundary.py:26-48) */
+  int kind;
+  double reference[5];  /* (rho, U, V, W, p) */
+  double lambda_wall;
+  double velocity[3];
+} GksPatchDesc;
+
+enum { GKS_SCHEME_WENO_GMRES = 0, GKS_SCHEME_HWENO_GMRES = 1, GKS_SCHEME_WENO_LUSGS = 2 };
+enum { GKS_JAC_ROE = 0, GKS_JAC_FRECHET = 1 };
+
+typedef struct GksOptions {  /* stepping.SolverOptions (stepping.py:61-84) */
+  int scheme;
+  int model;             /* 0 inviscid, 1 viscous */
+  double mu, gamma, cfl;
+  int krylov_dim, restarts, jacobi_sweeps;
+  double gmres_rtol;
+  double weno_eps, linear_weight;
+  int linear_weights;    /* weights="linear" */
+  int global_time_step;  /* time_step="global" */
+  int jacobian_mode;     /* GKS_JAC_ROE (reference) or GKS_JAC_FRECHET (matrix-free) */
+  int npatch;            /* == number of mesh patches; indexed by mesh patch id */
+  const GksPatchDesc* patches;
+} GksOptions;
+
+typedef struct GksHandle GksHandle;
+
+/* Build device state; setup may be NULL (built internally). */
+int gks_create(const GksMeshDesc* mesh, const GksSetup* setup, const GksOptions* opt, int device,
+               GksHandle** out);
+void gks_destroy(GksHandle* h);
+
+/* Solver.local_time_step (stepping.py:135-157): q (nc,5) -> dt (nc) */
+int gks_local_dt(GksHandle* h, const double* q, double* dt_out);
+
+/* Solver.residual (stepping.py:212-238).  grad (nc,3,5) required for the
+   compact scheme; grad_out (nc,3,5) written when with_gradients != 0. */
+int gks_residual(GksHandle* h, const double* q, const double* grad, const double* dt,
+                 int with_gradients, double* res_out, double* grad_out);
+
+/* Solver._boundary_ghosts (stepping.py:242-249): ghost of the cell-average
+   owner state per boundary face, (nbf,5) in ascending boundary-face order */
+int gks_boundary_ghosts(GksHandle* h, const double* q, double* ghosts_out);
+int64_t gks_num_boundary_faces(const GksHandle* h);
+
+/* ------------------------------------------------------------------ */
+/* Block systems (BlockJacobian, jacobian.py:74-126) and GMRES          */
+/* ------------------------------------------------------------------ */
+typedef struct GksBlockSystem GksBlockSystem;
+
+#define GKS_GMRES_MAX_DIM 64
+#define GKS_GMRES_MAX_RESTARTS 64
+
+typedef struct GksGmresInfo {  /* krylov.GmresInfo (krylov.py:37-52) */
+  int ncycles;
+  int matvecs;
+  int breakdown;
+  double ortho_error;
+  int cycle_len[GKS_GMRES_MAX_RESTARTS];
+  double norms[GKS_GMRES_MAX_RESTARTS * (GKS_GMRES_MAX_DIM + 1)]; /* row c: cycle c norms */
+} GksGmresInfo;
+
+typedef struct GksStepInfo {  /* stepping.StepInfo (stepping.py:52-58) */
+  double res_rho_l1, res_l2, dt_min;
+  int solver_cycles;
+  int retried;
+  int matvecs;
+  int nbad;                   /* on GKS_ERR_INVALID_UPDATE: number of bad cells */
+  int64_t first_bad[8];       /* ... and the first (up to) 8 of them */
+} GksStepInfo;
+
+/* assemble_jacobian(mesh, q, dt, gamma, ghosts) (jacobian.py:133-196) into
+   the handle's device Jacobian; ghosts (nbf,5) may be NULL */
+int gks_assemble_jacobian(GksHandle* h, const double* q, const double* dt, const double* ghosts);
+/* the handle's Jacobian as a block system (owned by the handle) */
+GksBlockSystem* gks_jacobian(GksHandle* h);
+
+/* upload an arbitrary block system (random_block_system, jacobian.py:199-226) */
+int gks_blocksys_create(int64_t ncells, int64_t nnz, const double* diag, const double* off,
+                        const int64_t* off_col, const int64_t* rowptr, int device, GksBlockSystem** out);
+void gks_blocksys_destroy(GksBlockSystem* a);
+int64_t gks_blocksys_ncells(const GksBlockSystem* a);
+int64_t gks_blocksys_nnz(const GksBlockSystem* a);
+/* download (any pointer may be NULL) */
+int gks_blocksys_export(GksBlockSystem* a, double* diag, double* off, int64_t* off_col, int64_t* off_row,
+                        int64_t* rowptr);
+int gks_blocksys_spmv(GksBlockSystem* a, const double* x, double* y);          /* BlockJacobian.spmv */
+int gks_blocksys_offdiag_mv(GksBlockSystem* a, const double* x, double* y);    /* .offdiag_mv */
+int gks_blocksys_diag_inverses(GksBlockSystem* a, double* out);               /* .diag_inverses */
+int gks_blocksys_jacobi(GksBlockSystem* a, const double* b, int k_max, double* z); /* krylov.py:24-34 */
+/* gmres_solve (krylov.py:55-140): x_out (nc,5) */
+int gks_gmres(GksBlockSystem* a, const double* b, double* x_out, int m, int restarts, int k_max, double rtol,
+              double atol, int check_orthogonality, GksGmresInfo* info);
+
+/* Solver.advance (stepping.py:270-296): one backward-Euler step in place.
+   grad_inout (nc,3,5) for the compact scheme (NULL otherwise). */
+int gks_advance(GksHandle* h, double* q_inout, double* grad_inout, GksStepInfo* info);
+/* device-resident variant for the outer loop / benchmark */
+int gks_state_upload(GksHandle* h, const double* q, const double* grad);
+int gks_state_download(GksHandle* h, double* q, double* grad);
+int gks_advance_resident(GksHandle* h, GksStepInfo* info);
+/* Solver.frechet_matvec (stepping.py:298-313); sigma <= 0 selects the
+   reference's automatic step.  out = (L(q + s v) - L(q)) / s */
+int gks_frechet_matvec(GksHandle* h, const double* q, const double* grad, const double* dt, const double* v,
+                       double sigma, double* out);
+
 /* measurement hook: kernel-only time of the fused flux on n random
    device-resident interfaces (not a reference API) */
 int gks_flux_bench(int64_t n, int reps, double gamma, double* ms_per_launch);

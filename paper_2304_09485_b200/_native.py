@@ -107,6 +107,25 @@ class NativeSetup:
             self.handle = None
 
 
+class GksPatchDesc(C.Structure):
+    _fields_ = [("kind", C.c_int), ("reference", C.c_double * 5), ("lambda_wall", C.c_double),
+                ("velocity", C.c_double * 3)]
+
+
+class GksOptions(C.Structure):
+    _fields_ = [("scheme", C.c_int), ("model", C.c_int), ("mu", C.c_double), ("gamma", C.c_double),
+                ("cfl", C.c_double), ("krylov_dim", C.c_int), ("restarts", C.c_int), ("jacobi_sweeps", C.c_int),
+                ("gmres_rtol", C.c_double), ("weno_eps", C.c_double), ("linear_weight", C.c_double),
+                ("linear_weights", C.c_int), ("global_time_step", C.c_int), ("jacobian_mode", C.c_int),
+                ("npatch", C.c_int), ("patches", C.POINTER(GksPatchDesc))]
+
+
+class GksStepInfo(C.Structure):
+    _fields_ = [("res_rho_l1", C.c_double), ("res_l2", C.c_double), ("dt_min", C.c_double),
+                ("solver_cycles", C.c_int), ("retried", C.c_int), ("matvecs", C.c_int), ("nbad", C.c_int),
+                ("first_bad", C.c_int64 * 8)]
+
+
 class GksError(RuntimeError):
     def __init__(self, code, message, index=-1):
         super().__init__(message)
@@ -130,6 +149,33 @@ SIGNATURES = [
     ("gks_setup_query", C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                   C.POINTER(C.c_int64)]),
     ("gks_setup_copy", C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int64]),
+    ("gks_create", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    ("gks_destroy", None, [C.c_void_p]),
+    ("gks_local_dt", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
+    ("gks_residual", C.c_int, [C.c_void_p, c_double_p, c_double_p, c_double_p, C.c_int, c_double_p,
+                               c_double_p]),
+    ("gks_boundary_ghosts", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
+    ("gks_num_boundary_faces", C.c_int64, [C.c_void_p]),
+    ("gks_assemble_jacobian", C.c_int, [C.c_void_p, c_double_p, c_double_p, c_double_p]),
+    ("gks_jacobian", C.c_void_p, [C.c_void_p]),
+    ("gks_blocksys_create", C.c_int, [C.c_int64, C.c_int64, c_double_p, c_double_p, c_int64_p, c_int64_p,
+                                      C.c_int, C.POINTER(C.c_void_p)]),
+    ("gks_blocksys_destroy", None, [C.c_void_p]),
+    ("gks_blocksys_ncells", C.c_int64, [C.c_void_p]),
+    ("gks_blocksys_nnz", C.c_int64, [C.c_void_p]),
+    ("gks_blocksys_export", C.c_int, [C.c_void_p, c_double_p, c_double_p, c_int64_p, c_int64_p, c_int64_p]),
+    ("gks_blocksys_spmv", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
+    ("gks_blocksys_offdiag_mv", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
+    ("gks_blocksys_diag_inverses", C.c_int, [C.c_void_p, c_double_p]),
+    ("gks_blocksys_jacobi", C.c_int, [C.c_void_p, c_double_p, C.c_int, c_double_p]),
+    ("gks_gmres", C.c_int, [C.c_void_p, c_double_p, c_double_p, C.c_int, C.c_int, C.c_int, C.c_double,
+                            C.c_double, C.c_int, C.c_void_p]),
+    ("gks_advance", C.c_int, [C.c_void_p, c_double_p, c_double_p, C.c_void_p]),
+    ("gks_state_upload", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
+    ("gks_state_download", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
+    ("gks_advance_resident", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("gks_frechet_matvec", C.c_int, [C.c_void_p, c_double_p, c_double_p, c_double_p, c_double_p, C.c_double,
+                                     c_double_p]),
 ]
 
 

@@ -1,0 +1,762 @@
+// C ABI of the solver handle: creation (host CSR construction + upload),
+// residual / Jacobian / GMRES / advance entry points.  Every entry point
+// copies host arrays in, runs the device path and copies results out; the
+// *_device variants keep the state resident for the benchmark loop.
+#include <stddef.h>
+#include <string.h>
+
+#include <algorithm>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "gks_implicit.cuh"
+
+extern "C" {
+// native setup internals (gks_setup.cpp)
+int gks_setup_query(const GksSetup* setup, const char* name, int* dtype, int* ndim, int64_t* shape);
+int gks_setup_copy(const GksSetup* setup, const char* name, void* dst, int64_t nbytes);
+}
+
+struct GksBlockSystem {
+  gks::BlockSys sys;
+  bool owned = true;  // false for the handle's Jacobian view
+};
+
+struct GksHandle {
+  gks::Handle H;
+  GksBlockSystem jac;
+  bool jac_valid = false;
+};
+
+namespace gks {
+
+static int setup_array(const GksSetup* S, const char* name, std::vector<double>* f, std::vector<int64_t>* i,
+                       std::vector<int8_t>* b, std::vector<int64_t>* shape) {
+  int dt, nd;
+  int64_t shp[4];
+  int rc = gks_setup_query(S, name, &dt, &nd, shp);
+  if (rc) return rc;
+  int64_t n = 1;
+  shape->assign(shp, shp + nd);
+  for (int k = 0; k < nd; ++k) n *= shp[k];
+  if (dt == 0) { f->resize(n); return gks_setup_copy(S, name, f->data(), n * 8); }
+  if (dt == 1) { i->resize(n); return gks_setup_copy(S, name, i->data(), n * 8); }
+  b->resize(n);
+  return gks_setup_copy(S, name, b->data(), n);
+}
+
+template <class T>
+static int upload(Handle* H, T** dst, const T* src, size_t n) {
+  GKS_CUDA(cudaMalloc(dst, std::max<size_t>(n, 1) * sizeof(T)));
+  H->allocs.push_back(*dst);
+  if (n) GKS_CUDA(cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice));
+  return GKS_OK;
+}
+
+template <class T>
+static int alloc(Handle* H, T** dst, size_t n) {
+  GKS_CUDA(cudaMalloc(dst, std::max<size_t>(n, 1) * sizeof(T)));
+  H->allocs.push_back(*dst);
+  return GKS_OK;
+}
+
+static std::vector<int> to_i32(const int64_t* p, size_t n) {
+  std::vector<int> out(n);
+  for (size_t k = 0; k < n; ++k) out[k] = (int)p[k];
+  return out;
+}
+
+#define TRY(x)                 \
+  do {                         \
+    int _rc = (x);             \
+    if (_rc) return _rc;       \
+  } while (0)
+
+int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const GksOptions* o, int device) {
+  Handle* H = &G->H;
+  H->device = device;
+  GKS_CUDA(cudaSetDevice(device));
+  GKS_CUDA(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
+  const int64_t nc = m->ncells, nf = m->nfaces, nfq = m->nfq;
+  if (nc > INT32_MAX / 16 || nfq > INT32_MAX / 2) {
+    set_error("mesh too large for 32-bit device indices");
+    return GKS_ERR_BAD_ARG;
+  }
+  H->nc = nc; H->nf = nf; H->nfq = nfq;
+  H->scheme = o->scheme;
+  H->compact = o->scheme == GKS_SCHEME_HWENO_GMRES;
+  H->model = o->model;
+  H->mu = o->mu; H->gamma = o->gamma; H->cfl = o->cfl;
+  H->eps = o->weno_eps; H->lw = o->linear_weight;
+  H->linear_weights = o->linear_weights;
+  H->global_dt = o->global_time_step;
+  H->jac_mode = o->jacobian_mode;
+  H->krylov_dim = o->krylov_dim; H->restarts = o->restarts; H->jacobi_sweeps = o->jacobi_sweeps;
+  H->gmres_rtol = o->gmres_rtol;
+  H->kc = make_kin(o->gamma);
+
+  // patches
+  int maxpatch = -1;
+  for (int64_t f = 0; f < nf; ++f) maxpatch = std::max<int>(maxpatch, (int)m->face_patch[f]);
+  if (o->npatch < maxpatch + 1) {
+    set_error("options list %d patches, mesh uses %d", o->npatch, maxpatch + 1);
+    return GKS_ERR_BAD_ARG;
+  }
+  H->npatch = o->npatch;
+  H->patches_h.resize(std::max(o->npatch, 1));
+  for (int p = 0; p < o->npatch; ++p) {
+    const GksPatchDesc& d = o->patches[p];
+    DevPatch& P = H->patches_h[p];
+    P.kind = d.kind;
+    P.wall = d.kind == PK_WALL_NOSLIP_ISOTHERMAL || d.kind == PK_WALL_NOSLIP_ADIABATIC ||
+             d.kind == PK_WALL_SLIP_ADIABATIC;
+    P.wall_moving = d.velocity[0] != 0.0 || d.velocity[1] != 0.0 || d.velocity[2] != 0.0;
+    P.ref[0] = d.reference[0]; P.ref[1] = d.reference[1]; P.ref[2] = d.reference[2];
+    P.ref[3] = d.reference[3];
+    P.ref[4] = d.reference[0] / (2.0 * d.reference[4]);
+    P.lambda_wall = d.lambda_wall;
+    for (int k = 0; k < 3; ++k) P.vel[k] = d.velocity[k];
+  }
+  for (int64_t f = 0; f < nf; ++f) {
+    if (m->face_neighbor[f] < 0) {
+      const int p = (int)m->face_patch[f];
+      if (p < 0 || H->patches_h[p].kind < 0) {
+        set_error("boundary face %lld has no patch spec", (long long)f);
+        return GKS_ERR_BAD_ARG;
+      }
+    }
+  }
+  TRY(upload(H, &H->patches, H->patches_h.data(), H->patches_h.size()));
+
+  // cells
+  std::vector<double> hf;
+  std::vector<int64_t> hi, shp;
+  std::vector<int8_t> hb;
+  TRY(upload(H, &H->vol, m->cell_volume, nc));
+  TRY(upload(H, &H->h, m->cell_h, nc));
+  TRY(upload(H, &H->cen, m->cell_centroid, nc * 3));
+  TRY(setup_array(S, "avg0", &hf, &hi, &hb, &shp));
+  TRY(upload(H, &H->avg0, hf.data(), hf.size()));
+  TRY(setup_array(S, "beta_mat", &hf, &hi, &hb, &shp));
+  TRY(upload(H, &H->beta, hf.data(), hf.size()));
+
+  // faces
+  {
+    auto own = to_i32(m->face_owner, nf), nbr = to_i32(m->face_neighbor, nf), pat = to_i32(m->face_patch, nf);
+    TRY(upload(H, &H->f_own, own.data(), nf));
+    TRY(upload(H, &H->f_nbr, nbr.data(), nf));
+    TRY(upload(H, &H->f_patch, pat.data(), nf));
+  }
+  TRY(upload(H, &H->f_area, m->face_area, nf));
+  TRY(upload(H, &H->f_normal, m->face_normal, nf * 3));
+  TRY(upload(H, &H->f_frame, m->face_frame, nf * 9));
+  TRY(upload(H, &H->f_shift, m->face_shift, nf * 3));
+  {
+    auto fqf = to_i32(m->fq_face, nfq);
+    TRY(upload(H, &H->fq_face, fqf.data(), nfq));
+    std::vector<double> ws(nfq);
+    for (int64_t i = 0; i < nfq; ++i) ws[i] = m->fq_weight[i] * m->face_area[m->fq_face[i]];
+    TRY(upload(H, &H->fq_ws, ws.data(), nfq));
+  }
+  TRY(upload(H, &H->fq_point, m->fq_point, nfq * 3));
+
+  // CSR lists (counting sorts keep ascending order inside each group)
+  {
+    // assembly: owner fq entries, then neighbour fq entries (stepping.py:225-228)
+    std::vector<int> cnt(nc + 1, 0);
+    for (int64_t i = 0; i < nfq; ++i) {
+      const int64_t f = m->fq_face[i];
+      cnt[m->face_owner[f] + 1]++;
+      if (m->face_neighbor[f] >= 0) cnt[m->face_neighbor[f] + 1]++;
+    }
+    std::partial_sum(cnt.begin(), cnt.end(), cnt.begin());
+    std::vector<int> pos(cnt.begin(), cnt.end() - 1), list(cnt[nc]);
+    for (int64_t i = 0; i < nfq; ++i) list[pos[m->face_owner[m->fq_face[i]]]++] = (int)(i << 1);
+    for (int64_t i = 0; i < nfq; ++i) {
+      const int64_t nb = m->face_neighbor[m->fq_face[i]];
+      if (nb >= 0) list[pos[nb]++] = (int)((i << 1) | 1);
+    }
+    TRY(upload(H, &H->cfq_start, cnt.data(), nc + 1));
+    TRY(upload(H, &H->cfq, list.data(), list.size()));
+  }
+  {
+    // local dt: owner faces then neighbour faces (stepping.py:144-154)
+    std::vector<int> cnt(nc + 1, 0);
+    for (int64_t f = 0; f < nf; ++f) {
+      cnt[m->face_owner[f] + 1]++;
+      if (m->face_neighbor[f] >= 0) cnt[m->face_neighbor[f] + 1]++;
+    }
+    std::partial_sum(cnt.begin(), cnt.end(), cnt.begin());
+    std::vector<int> pos(cnt.begin(), cnt.end() - 1), list(cnt[nc]);
+    for (int64_t f = 0; f < nf; ++f) list[pos[m->face_owner[f]]++] = (int)(f << 1);
+    for (int64_t f = 0; f < nf; ++f)
+      if (m->face_neighbor[f] >= 0) list[pos[m->face_neighbor[f]]++] = (int)((f << 1) | 1);
+    TRY(upload(H, &H->cdt_start, cnt.data(), nc + 1));
+    TRY(upload(H, &H->cdt, list.data(), list.size()));
+    // Jacobian diagonal: interior own, interior nbr, boundary own (jacobian.py:582-610)
+    std::vector<int> pos2(cnt.begin(), cnt.end() - 1), list2(cnt[nc]);
+    for (int64_t f = 0; f < nf; ++f)
+      if (m->face_neighbor[f] >= 0) list2[pos2[m->face_owner[f]]++] = (int)(f << 1);
+    for (int64_t f = 0; f < nf; ++f)
+      if (m->face_neighbor[f] >= 0) list2[pos2[m->face_neighbor[f]]++] = (int)((f << 1) | 1);
+    for (int64_t f = 0; f < nf; ++f)
+      if (m->face_neighbor[f] < 0) list2[pos2[m->face_owner[f]]++] = (int)(f << 1);
+    TRY(upload(H, &H->cjd_start, cnt.data(), nc + 1));
+    TRY(upload(H, &H->cjd, list2.data(), list2.size()));
+  }
+  {
+    // interior / boundary face lists, Jacobian CSR (lexsort by (row, col), stable)
+    std::vector<int> ifaces, bfaces, bidx(nf, -1);
+    for (int64_t f = 0; f < nf; ++f) {
+      if (m->face_neighbor[f] >= 0) ifaces.push_back((int)f);
+      else { bidx[f] = (int)bfaces.size(); bfaces.push_back((int)f); }
+    }
+    H->nfi = ifaces.size();
+    H->nbf = bfaces.size();
+    const int64_t nnz = 2 * H->nfi;
+    H->nnz = nnz;
+    std::vector<int64_t> erow(nnz), ecol(nnz);
+    for (int64_t k = 0; k < H->nfi; ++k) {
+      const int64_t f = ifaces[k];
+      erow[2 * k] = m->face_owner[f]; ecol[2 * k] = m->face_neighbor[f];
+      erow[2 * k + 1] = m->face_neighbor[f]; ecol[2 * k + 1] = m->face_owner[f];
+    }
+    std::vector<int64_t> order(nnz);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+      if (erow[a] != erow[b]) return erow[a] < erow[b];
+      return ecol[a] < ecol[b];
+    });
+    std::vector<int> rowptr(nc + 1, 0), col(nnz), fslot(2 * nf, -1);
+    for (int64_t p = 0; p < nnz; ++p) {
+      const int64_t e = order[p];
+      col[p] = (int)ecol[e];
+      rowptr[erow[e] + 1]++;
+      fslot[2 * ifaces[e / 2] + (e & 1)] = (int)p;
+    }
+    std::partial_sum(rowptr.begin(), rowptr.end(), rowptr.begin());
+    TRY(upload(H, &H->interior_faces, ifaces.data(), ifaces.size()));
+    TRY(upload(H, &H->boundary_faces, bfaces.data(), bfaces.size()));
+    TRY(upload(H, &H->face_slot, fslot.data(), fslot.size()));
+    TRY(upload(H, &H->bidx, bidx.data(), bidx.size()));
+    BlockSys* A = &G->jac.sys;
+    TRY(blocksys_alloc(A, nc, nnz, H->stream));
+    GKS_CUDA(cudaMemcpy(A->rowptr, rowptr.data(), (nc + 1) * sizeof(int), cudaMemcpyHostToDevice));
+    if (nnz) GKS_CUDA(cudaMemcpy(A->col, col.data(), nnz * sizeof(int), cudaMemcpyHostToDevice));
+    G->jac.owned = false;
+  }
+
+  // reconstruction operators
+  if (H->compact) {
+    TRY(setup_array(S, "hweno_big_op", &hf, &hi, &hb, &shp));
+    H->HA = 0;
+    TRY(upload(H, &H->big_op, hf.data(), hf.size()));
+    TRY(setup_array(S, "hweno_big_avg_gather", &hf, &hi, &hb, &shp));
+    H->HA = (int)shp[1];
+    { auto v = to_i32(hi.data(), hi.size()); TRY(upload(H, &H->avg_gather, v.data(), v.size())); }
+    TRY(setup_array(S, "hweno_big_grad_gather", &hf, &hi, &hb, &shp));
+    H->HG = (int)shp[1];
+    { auto v = to_i32(hi.data(), hi.size()); TRY(upload(H, &H->grad_gather, v.data(), v.size())); }
+    TRY(setup_array(S, "hweno_big_grad_scale", &hf, &hi, &hb, &shp));
+    TRY(upload(H, &H->grad_scale, hf.data(), hf.size()));
+    TRY(setup_array(S, "hweno_sub_op", &hf, &hi, &hb, &shp));
+    H->HM = (int)shp[1];
+    TRY(upload(H, &H->sub_op, hf.data(), hf.size()));
+    TRY(setup_array(S, "hweno_sub_gather", &hf, &hi, &hb, &shp));
+    { auto v = to_i32(hi.data(), hi.size()); TRY(upload(H, &H->sub_gather, v.data(), v.size())); }
+    TRY(setup_array(S, "hweno_sub_active", &hf, &hi, &hb, &shp));
+    TRY(upload(H, &H->sub_active, hb.data(), hb.size()));
+    if (H->HM > 8) { set_error("HWENO: more than 8 sub-stencils per cell"); return GKS_ERR_BAD_ARG; }
+  } else {
+    TRY(setup_array(S, "weno_big_op", &hf, &hi, &hb, &shp));
+    H->K = (int)shp[2];
+    TRY(upload(H, &H->big_op, hf.data(), hf.size()));
+    TRY(setup_array(S, "weno_big_gather", &hf, &hi, &hb, &shp));
+    { auto v = to_i32(hi.data(), hi.size()); TRY(upload(H, &H->big_gather, v.data(), v.size())); }
+    TRY(setup_array(S, "weno_sub_op", &hf, &hi, &hb, &shp));
+    H->M = (int)shp[1];
+    H->S = (int)shp[3];
+    TRY(upload(H, &H->sub_op, hf.data(), hf.size()));
+    TRY(setup_array(S, "weno_sub_gather", &hf, &hi, &hb, &shp));
+    { auto v = to_i32(hi.data(), hi.size()); TRY(upload(H, &H->sub_gather, v.data(), v.size())); }
+    TRY(setup_array(S, "weno_sub_active", &hf, &hi, &hb, &shp));
+    TRY(upload(H, &H->sub_active, hb.data(), hb.size()));
+    if (H->M > 8) { set_error("WENO: more than 8 sub-stencils per cell"); return GKS_ERR_BAD_ARG; }
+  }
+
+  // state and work buffers
+  TRY(alloc(H, &H->q, nc * 5));
+  TRY(alloc(H, &H->grad, nc * 15));
+  TRY(alloc(H, &H->dt, nc));
+  TRY(alloc(H, &H->coef, nc * 45));
+  TRY(alloc(H, &H->contrib, nfq * 5));
+  TRY(alloc(H, &H->qpt, H->compact ? nfq * 5 : 1));
+  TRY(alloc(H, &H->res, nc * 5));
+  TRY(alloc(H, &H->grad_new, nc * 15));
+  TRY(alloc(H, &H->ghosts, std::max<int64_t>(H->nbf, 1) * 5));
+  TRY(alloc(H, &H->q_new, nc * 5));
+  TRY(alloc(H, &H->dq, nc * 5));
+  TRY(alloc(H, &H->qtmp, nc * 5));
+  TRY(alloc(H, &H->res2, nc * 5));
+  TRY(alloc(H, &H->bad, nc));
+  TRY(alloc(H, &H->scal, 1));
+  TRY(alloc(H, &H->status, 4));
+  {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    H->red_blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nc + 255) / 256, (int64_t)sms * 4));
+  }
+  TRY(alloc(H, &H->partial, (size_t)H->red_blocks * 4));
+  TRY(alloc(H, &H->counter, 1));
+  GKS_CUDA(cudaMemset(H->counter, 0, sizeof(unsigned int)));
+  GKS_CUDA(cudaMemset(H->grad, 0, nc * 15 * sizeof(double)));
+  return GKS_OK;
+}
+
+void destroy_handle(GksHandle* G) {
+  Handle* H = &G->H;
+  cudaSetDevice(H->device);
+  if (H->stream) cudaStreamSynchronize(H->stream);
+  for (void* p : H->allocs) cudaFree(p);
+  blocksys_free(&G->jac.sys);
+  if (H->stream) cudaStreamDestroy(H->stream);
+}
+
+int jacobian_assemble(Handle* H, BlockSys* A, const double* ghosts_dev);
+
+}  // namespace gks
+
+using namespace gks;
+
+static int no_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    set_error("no CUDA device visible: the B200 path has no CPU fallback");
+    return GKS_ERR_NO_DEVICE;
+  }
+  return GKS_OK;
+}
+
+extern "C" {
+
+int gks_create(const GksMeshDesc* mesh, const GksSetup* setup, const GksOptions* opt, int device,
+               GksHandle** out) {
+  set_error_index(-1);
+  if (!mesh || !opt || !out) {
+    set_error("gks_create: bad arguments");
+    return GKS_ERR_BAD_ARG;
+  }
+  if (int rc = no_device()) return rc;
+  GksSetup* own = nullptr;
+  if (!setup) {
+    const int schemes = opt->scheme == GKS_SCHEME_HWENO_GMRES ? 2 : 1;
+    int rc = gks_setup_build(mesh, schemes, 0, &own);
+    if (rc) return rc;
+    setup = own;
+  }
+  GksHandle* G = new GksHandle();
+  int rc = create_handle(G, mesh, setup, opt, device);
+  if (own) gks_setup_free(own);
+  if (rc) {
+    destroy_handle(G);
+    delete G;
+    return rc;
+  }
+  *out = G;
+  return GKS_OK;
+}
+
+void gks_destroy(GksHandle* G) {
+  if (!G) return;
+  destroy_handle(G);
+  delete G;
+}
+
+int64_t gks_num_boundary_faces(const GksHandle* G) { return G ? G->H.nbf : -1; }
+
+int gks_local_dt(GksHandle* G, const double* q, double* dt_out) {
+  Handle* H = &G->H;
+  set_error_index(-1);
+  GKS_CUDA(cudaSetDevice(H->device));
+  GKS_CUDA(cudaMemcpyAsync(H->q, q, H->nc * 5 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  reset_status(H);
+  if (int rc = local_dt_device(H)) return rc;
+  if (int rc = check_status(H, "local_time_step")) return rc;
+  GKS_CUDA(cudaMemcpyAsync(dt_out, H->dt, H->nc * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaStreamSynchronize(H->stream));
+  return GKS_OK;
+}
+
+int gks_residual(GksHandle* G, const double* q, const double* grad, const double* dt, int with_gradients,
+                 double* res_out, double* grad_out) {
+  Handle* H = &G->H;
+  set_error_index(-1);
+  GKS_CUDA(cudaSetDevice(H->device));
+  if (H->compact && !grad) {
+    set_error("compact scheme needs a gradient field");
+    return GKS_ERR_BAD_ARG;
+  }
+  GKS_CUDA(cudaMemcpyAsync(H->q, q, H->nc * 5 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  if (grad) GKS_CUDA(cudaMemcpyAsync(H->grad, grad, H->nc * 15 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  GKS_CUDA(cudaMemcpyAsync(H->dt, dt, H->nc * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  reset_status(H);
+  if (int rc = residual_device(H, H->q, H->res, with_gradients != 0, nullptr)) return rc;
+  if (int rc = check_status(H, "residual")) return rc;
+  GKS_CUDA(cudaMemcpyAsync(res_out, H->res, H->nc * 5 * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  if (with_gradients && grad_out)
+    GKS_CUDA(cudaMemcpyAsync(grad_out, H->grad_new, H->nc * 15 * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaStreamSynchronize(H->stream));
+  return GKS_OK;
+}
+
+int gks_boundary_ghosts(GksHandle* G, const double* q, double* ghosts_out) {
+  Handle* H = &G->H;
+  set_error_index(-1);
+  GKS_CUDA(cudaSetDevice(H->device));
+  if (H->nbf == 0) return GKS_OK;
+  GKS_CUDA(cudaMemcpyAsync(H->qtmp, q, H->nc * 5 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  reset_status(H);
+  if (int rc = boundary_ghosts_device(H, H->qtmp)) return rc;
+  if (int rc = check_status(H, "boundary_ghosts")) return rc;
+  GKS_CUDA(cudaMemcpyAsync(ghosts_out, H->ghosts, H->nbf * 5 * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaStreamSynchronize(H->stream));
+  return GKS_OK;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// implicit-solve entry points
+// ===========================================================================
+namespace gks {
+__global__ void k_update(int64_t nc, const double* q, const double* dq, double* qn, int8_t* bad);
+__global__ void k_stats(int64_t nc, const double* res, const double* dt, const int8_t* bad, double* partial,
+                        unsigned int* counter, DevScalars* out);
+__global__ void k_halve_dt(int64_t nc, const int8_t* bad, double* dt);
+__global__ void k_sigma(const double* vv_qq, double* sigma, double* out_zero_flag);
+__global__ void k_perturb(int64_t n, const double* q, const double* v, const double* sigma, double* out,
+                          const int* gate);
+__global__ void k_frechet_combine(int64_t nc, const double* r1, const double* r0, const double* sigma,
+                                  const double* v, const double* vol, const double* dt, int mode, double* out,
+                                  const int* gate);
+void dot2(KrylovWS* W, cudaStream_t s, int64_t n, const double* a, const double* b, const double* c,
+          const double* d, double* o0, double* o1, const int* gate);
+
+// J v (mode 0: Frechet derivative; mode 1: V/dt v - derivative) with the step
+// residual H->res as the base point; q_base = H->q, dt = H->dt.
+static void frechet_apply(Handle* H, BlockSys* A, const double* v, double* out, int mode, const int* gate,
+                          const double* fixed_sigma) {
+  const int64_t n = H->nc * 5;
+  double* sig = &H->scal->sigma;
+  if (!fixed_sigma) {
+    dot2(&A->ws, H->stream, n, v, v, H->q, H->q, &H->scal->red[0], &H->scal->red[1], gate);
+    k_sigma<<<1, 1, 0, H->stream>>>(H->scal->red, sig, nullptr);
+    count_launch(1);
+  } else {
+    sig = const_cast<double*>(fixed_sigma);
+  }
+  k_perturb<<<blocks_for(n, 256), 256, 0, H->stream>>>(n, H->q, v, sig, H->qtmp, gate);
+  residual_device(H, H->qtmp, H->res2, false, gate);
+  k_frechet_combine<<<blocks_for(n, 256), 256, 0, H->stream>>>(H->nc, H->res2, H->res, sig, v, H->vol, H->dt, mode,
+                                                                out, gate);
+  count_launch(2);
+}
+
+static int advance_device(GksHandle* G, GksStepInfo* info) {
+  Handle* H = &G->H;
+  BlockSys* A = &G->jac.sys;
+  memset(info, 0, sizeof(*info));
+  if (H->scheme == GKS_SCHEME_WENO_LUSGS) {
+    set_error("scheme 'weno_lusgs' (sequential LUSGS sweep) is not part of the device path");
+    return GKS_ERR_BAD_ARG;
+  }
+  reset_status(H);
+  TRY(local_dt_device(H));
+  TRY(check_status(H, "local_time_step"));
+  int retried = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    reset_status(H);
+    TRY(residual_device(H, H->q, H->res, H->compact != 0, nullptr));
+    TRY(check_status(H, "residual"));
+    if (H->nbf) {
+      TRY(boundary_ghosts_device(H, H->q));
+      TRY(check_status(H, "boundary_ghosts"));
+    }
+    TRY(jacobian_assemble(H, A, H->nbf ? H->ghosts : nullptr));
+    GmresParams P;
+    P.m = H->krylov_dim;
+    P.restarts = H->restarts;
+    P.kmax = H->jacobi_sweeps;
+    P.rtol = H->gmres_rtol;
+    GmresHost gh;
+    MatvecFn mf = [H, A](const double* v, double* out, const int* gate) {
+      frechet_apply(H, A, v, out, 1, gate, nullptr);
+    };
+    TRY(gmres_device(A, H->res, H->dq, P, &gh, H->jac_mode == GKS_JAC_FRECHET ? &mf : nullptr));
+    k_update<<<blocks_for(H->nc, 256), 256, 0, H->stream>>>(H->nc, H->q, H->dq, H->q_new, H->bad);
+    k_stats<<<H->red_blocks, 256, 0, H->stream>>>(H->nc, H->res, H->dt, H->bad, H->partial, H->counter, H->scal);
+    count_launch(2);
+    DevScalars sc;
+    GKS_CUDA(cudaMemcpyAsync(&sc, H->scal, sizeof(sc), cudaMemcpyDeviceToHost, H->stream));
+    GKS_CUDA(cudaStreamSynchronize(H->stream));
+    info->matvecs += gh.matvecs;
+    if (sc.nbad == 0) {
+      std::swap(H->q, H->q_new);
+      if (H->compact) std::swap(H->grad, H->grad_new);
+      info->res_rho_l1 = sc.res_rho_l1;
+      info->res_l2 = sc.res_l2;
+      info->dt_min = sc.dt_min;
+      info->solver_cycles = gh.ncycles;
+      info->retried = retried;
+      return GKS_OK;
+    }
+    info->nbad = sc.nbad;
+    if (attempt == 0) {
+      k_halve_dt<<<blocks_for(H->nc, 256), 256, 0, H->stream>>>(H->nc, H->bad, H->dt);
+      count_launch(1);
+      retried = 1;
+    }
+  }
+  std::vector<int8_t> bad(H->nc);
+  GKS_CUDA(cudaMemcpy(bad.data(), H->bad, H->nc, cudaMemcpyDeviceToHost));
+  int k = 0;
+  std::string lst;
+  for (int64_t c = 0; c < H->nc && k < 8; ++c)
+    if (bad[c]) {
+      info->first_bad[k++] = c;
+      lst += (lst.empty() ? "" : ", ") + std::to_string(c);
+    }
+  for (; k < 8; ++k) info->first_bad[k] = -1;
+  set_error("unphysical update persists after dt halving at cells [%s]", lst.c_str());
+  return GKS_ERR_INVALID_UPDATE;
+}
+
+}  // namespace gks
+
+static int bs_check_size(GksBlockSystem* a) {
+  if (!a) {
+    set_error("null block system");
+    return GKS_ERR_BAD_ARG;
+  }
+  return GKS_OK;
+}
+
+extern "C" {
+
+int gks_assemble_jacobian(GksHandle* G, const double* q, const double* dt, const double* ghosts) {
+  Handle* H = &G->H;
+  set_error_index(-1);
+  GKS_CUDA(cudaSetDevice(H->device));
+  GKS_CUDA(cudaMemcpyAsync(H->q, q, H->nc * 5 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  GKS_CUDA(cudaMemcpyAsync(H->dt, dt, H->nc * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  if (ghosts && H->nbf)
+    GKS_CUDA(cudaMemcpyAsync(H->ghosts, ghosts, H->nbf * 5 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  TRY(jacobian_assemble(H, &G->jac.sys, ghosts && H->nbf ? H->ghosts : nullptr));
+  G->jac_valid = true;
+  return GKS_OK;
+}
+
+GksBlockSystem* gks_jacobian(GksHandle* G) { return G ? &G->jac : nullptr; }
+
+int gks_blocksys_create(int64_t nc, int64_t nnz, const double* diag, const double* off, const int64_t* off_col,
+                        const int64_t* rowptr, int device, GksBlockSystem** out) {
+  set_error_index(-1);
+  if (nc <= 0 || nnz < 0 || !diag || !rowptr || !out || (nnz && (!off || !off_col))) {
+    set_error("gks_blocksys_create: bad arguments");
+    return GKS_ERR_BAD_ARG;
+  }
+  if (int rc = no_device()) return rc;
+  GKS_CUDA(cudaSetDevice(device));
+  GksBlockSystem* a = new GksBlockSystem();
+  cudaStream_t s;
+  GKS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  TRY(blocksys_alloc(&a->sys, nc, nnz, s));
+  std::vector<int> rp = to_i32(rowptr, nc + 1), cl = to_i32(off_col, nnz);
+  GKS_CUDA(cudaMemcpy(a->sys.rowptr, rp.data(), (nc + 1) * sizeof(int), cudaMemcpyHostToDevice));
+  if (nnz) {
+    GKS_CUDA(cudaMemcpy(a->sys.col, cl.data(), nnz * sizeof(int), cudaMemcpyHostToDevice));
+    GKS_CUDA(cudaMemcpy(a->sys.off, off, nnz * 25 * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  GKS_CUDA(cudaMemcpy(a->sys.diag, diag, nc * 25 * sizeof(double), cudaMemcpyHostToDevice));
+  TRY(blocksys_invert_diag(&a->sys));
+  a->owned = true;
+  *out = a;
+  return GKS_OK;
+}
+
+void gks_blocksys_destroy(GksBlockSystem* a) {
+  if (!a || !a->owned) return;
+  cudaStream_t s = a->sys.stream;
+  blocksys_free(&a->sys);
+  if (s) cudaStreamDestroy(s);
+  delete a;
+}
+
+int64_t gks_blocksys_ncells(const GksBlockSystem* a) { return a ? a->sys.nc : -1; }
+int64_t gks_blocksys_nnz(const GksBlockSystem* a) { return a ? a->sys.nnz : -1; }
+
+int gks_blocksys_export(GksBlockSystem* a, double* diag, double* off, int64_t* off_col, int64_t* off_row,
+                        int64_t* rowptr) {
+  TRY(bs_check_size(a));
+  BlockSys* A = &a->sys;
+  GKS_CUDA(cudaStreamSynchronize(A->stream));
+  if (diag) GKS_CUDA(cudaMemcpy(diag, A->diag, A->nc * 25 * sizeof(double), cudaMemcpyDeviceToHost));
+  if (off && A->nnz) GKS_CUDA(cudaMemcpy(off, A->off, A->nnz * 25 * sizeof(double), cudaMemcpyDeviceToHost));
+  std::vector<int> rp(A->nc + 1), cl(std::max<int64_t>(A->nnz, 1));
+  GKS_CUDA(cudaMemcpy(rp.data(), A->rowptr, (A->nc + 1) * sizeof(int), cudaMemcpyDeviceToHost));
+  if (A->nnz) GKS_CUDA(cudaMemcpy(cl.data(), A->col, A->nnz * sizeof(int), cudaMemcpyDeviceToHost));
+  if (rowptr)
+    for (int64_t c = 0; c <= A->nc; ++c) rowptr[c] = rp[c];
+  if (off_col)
+    for (int64_t e = 0; e < A->nnz; ++e) off_col[e] = cl[e];
+  if (off_row)
+    for (int64_t c = 0; c < A->nc; ++c)
+      for (int e = rp[c]; e < rp[c + 1]; ++e) off_row[e] = c;
+  return GKS_OK;
+}
+
+static int bs_vec_op(GksBlockSystem* a, const double* x, double* y, int which) {
+  TRY(bs_check_size(a));
+  BlockSys* A = &a->sys;
+  const int64_t n = A->nc * 5;
+  TRY(krylov_ensure(&A->ws, n, 1));
+  GKS_CUDA(cudaMemcpyAsync(A->ws.x, x, n * sizeof(double), cudaMemcpyHostToDevice, A->stream));
+  if (which == 0) bs_spmv(A, A->ws.x, A->ws.b, nullptr);
+  else bs_offdiag(A, A->ws.x, A->ws.b, nullptr);
+  GKS_CUDA(cudaGetLastError());
+  GKS_CUDA(cudaMemcpyAsync(y, A->ws.b, n * sizeof(double), cudaMemcpyDeviceToHost, A->stream));
+  GKS_CUDA(cudaStreamSynchronize(A->stream));
+  return GKS_OK;
+}
+
+int gks_blocksys_spmv(GksBlockSystem* a, const double* x, double* y) { return bs_vec_op(a, x, y, 0); }
+int gks_blocksys_offdiag_mv(GksBlockSystem* a, const double* x, double* y) { return bs_vec_op(a, x, y, 1); }
+
+int gks_blocksys_diag_inverses(GksBlockSystem* a, double* out) {
+  TRY(bs_check_size(a));
+  BlockSys* A = &a->sys;
+  GKS_CUDA(cudaStreamSynchronize(A->stream));
+  GKS_CUDA(cudaMemcpy(out, A->dinv, A->nc * 25 * sizeof(double), cudaMemcpyDeviceToHost));
+  return GKS_OK;
+}
+
+int gks_blocksys_jacobi(GksBlockSystem* a, const double* b, int k_max, double* z) {
+  TRY(bs_check_size(a));
+  BlockSys* A = &a->sys;
+  if (!A->dinv_ok) {
+    set_error("singular diagonal block in Jacobi preconditioner");
+    return GKS_ERR_SINGULAR;
+  }
+  const int64_t n = A->nc * 5;
+  TRY(krylov_ensure(&A->ws, n, 1));
+  GKS_CUDA(cudaMemcpyAsync(A->ws.b, b, n * sizeof(double), cudaMemcpyHostToDevice, A->stream));
+  bs_jacobi(A, A->ws.b, A->ws.z, A->ws.w, k_max, nullptr);
+  GKS_CUDA(cudaGetLastError());
+  GKS_CUDA(cudaMemcpyAsync(z, A->ws.z, n * sizeof(double), cudaMemcpyDeviceToHost, A->stream));
+  GKS_CUDA(cudaStreamSynchronize(A->stream));
+  return GKS_OK;
+}
+
+int gks_gmres(GksBlockSystem* a, const double* b, double* x_out, int m, int restarts, int k_max, double rtol,
+              double atol, int check_orthogonality, GksGmresInfo* info) {
+  TRY(bs_check_size(a));
+  set_error_index(-1);
+  BlockSys* A = &a->sys;
+  const int64_t n = A->nc * 5;
+  TRY(krylov_ensure(&A->ws, n, m));
+  double* db;
+  double* dx;
+  GKS_CUDA(cudaMalloc(&db, n * sizeof(double)));
+  GKS_CUDA(cudaMalloc(&dx, n * sizeof(double)));
+  GKS_CUDA(cudaMemcpyAsync(db, b, n * sizeof(double), cudaMemcpyHostToDevice, A->stream));
+  GmresParams P;
+  P.m = m; P.restarts = restarts; P.kmax = k_max; P.rtol = rtol; P.atol = atol;
+  P.check_ortho = check_orthogonality;
+  GmresHost* gh = new GmresHost();
+  int rc = gmres_device(A, db, dx, P, gh, nullptr);
+  if (rc == GKS_OK) {
+    cudaMemcpyAsync(x_out, dx, n * sizeof(double), cudaMemcpyDeviceToHost, A->stream);
+    cudaStreamSynchronize(A->stream);
+  }
+  if (info) {
+    info->ncycles = gh->ncycles;
+    info->matvecs = gh->matvecs;
+    info->breakdown = gh->breakdown;
+    info->ortho_error = gh->ortho_error;
+    for (int c = 0; c < gh->ncycles; ++c) {
+      info->cycle_len[c] = gh->cycle_len[c];
+      for (int k = 0; k < gh->cycle_len[c]; ++k)
+        info->norms[c * (GKS_GMRES_MAX_DIM + 1) + k] = gh->norms[c * (GM_MMAX + 1) + k];
+    }
+  }
+  delete gh;
+  cudaFree(db);
+  cudaFree(dx);
+  return rc;
+}
+
+int gks_state_upload(GksHandle* G, const double* q, const double* grad) {
+  Handle* H = &G->H;
+  GKS_CUDA(cudaSetDevice(H->device));
+  GKS_CUDA(cudaMemcpyAsync(H->q, q, H->nc * 5 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  if (grad) GKS_CUDA(cudaMemcpyAsync(H->grad, grad, H->nc * 15 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  GKS_CUDA(cudaStreamSynchronize(H->stream));
+  return GKS_OK;
+}
+
+int gks_state_download(GksHandle* G, double* q, double* grad) {
+  Handle* H = &G->H;
+  GKS_CUDA(cudaSetDevice(H->device));
+  if (q) GKS_CUDA(cudaMemcpyAsync(q, H->q, H->nc * 5 * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  if (grad) GKS_CUDA(cudaMemcpyAsync(grad, H->grad, H->nc * 15 * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaStreamSynchronize(H->stream));
+  return GKS_OK;
+}
+
+int gks_advance_resident(GksHandle* G, GksStepInfo* info) {
+  set_error_index(-1);
+  GKS_CUDA(cudaSetDevice(G->H.device));
+  return advance_device(G, info);
+}
+
+int gks_advance(GksHandle* G, double* q_inout, double* grad_inout, GksStepInfo* info) {
+  Handle* H = &G->H;
+  if (H->compact && !grad_inout) {
+    set_error("compact scheme needs a gradient field");
+    return GKS_ERR_BAD_ARG;
+  }
+  TRY(gks_state_upload(G, q_inout, H->compact ? grad_inout : nullptr));
+  TRY(gks_advance_resident(G, info));
+  return gks_state_download(G, q_inout, H->compact ? grad_inout : nullptr);
+}
+
+int gks_frechet_matvec(GksHandle* G, const double* q, const double* grad, const double* dt, const double* v,
+                       double sigma, double* out) {
+  Handle* H = &G->H;
+  set_error_index(-1);
+  GKS_CUDA(cudaSetDevice(H->device));
+  const int64_t n = H->nc * 5;
+  BlockSys* A = &G->jac.sys;
+  TRY(krylov_ensure(&A->ws, n, 1));
+  GKS_CUDA(cudaMemcpyAsync(H->q, q, n * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  if (grad) GKS_CUDA(cudaMemcpyAsync(H->grad, grad, H->nc * 15 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  GKS_CUDA(cudaMemcpyAsync(H->dt, dt, H->nc * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  GKS_CUDA(cudaMemcpyAsync(A->ws.x, v, n * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  reset_status(H);
+  TRY(residual_device(H, H->q, H->res, false, nullptr));
+  const double* fixed = nullptr;
+  if (sigma > 0.0) {
+    GKS_CUDA(cudaMemcpyAsync(&H->scal->red[7], &sigma, sizeof(double), cudaMemcpyHostToDevice, H->stream));
+    fixed = &H->scal->red[7];
+  }
+  frechet_apply(H, A, A->ws.x, A->ws.b, 0, nullptr, fixed);
+  TRY(check_status(H, "frechet_matvec"));
+  GKS_CUDA(cudaMemcpyAsync(out, A->ws.b, n * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaStreamSynchronize(H->stream));
+  return GKS_OK;
+}
+
+}  // extern "C"

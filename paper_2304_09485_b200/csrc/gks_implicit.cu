@@ -1,0 +1,834 @@
+// Implicit solve on the device: Roe-split block Jacobian (K5), block spmv and
+// block-Jacobi (K6/K7), left-preconditioned restarted GMRES with modified
+// Gram-Schmidt (K8) and the state update with validity check (K9).
+//
+// Reference: gks3d/jacobian.py:37-196 (euler_flux_jacobian, spectral_radius,
+// BlockJacobian, assemble_jacobian), gks3d/krylov.py:24-140
+// (jacobi_precondition, gmres_solve), gks3d/stepping.py:251-296 (_solve,
+// advance).
+//
+// GMRES control flow lives on the device: the Hessenberg / Givens scalars
+// and the cycle bookkeeping sit in a GmresDev struct in device memory; every
+// vector kernel reads a gate flag and returns immediately once the reference
+// algorithm would have left the loop (happy breakdown, early exit, target
+// reached).  The host enqueues the fixed launch sequence without a single
+// synchronisation and reads the cycle norms back once at the end.
+//
+// Reductions are deterministic: fixed grid, per-block tree, and the last
+// block to finish sums the block partials in index order.
+#include <stddef.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "gks_implicit.cuh"
+
+namespace gks {
+
+static constexpr int RB_THREADS = 256;
+static constexpr int CELLS_PER_BLOCK = 32;  // (cell,row) kernels: 160 threads
+
+// ---------------------------------------------------------------------------
+// deterministic reductions
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double block_sum(double v, double* sm) {
+  sm[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sm[threadIdx.x] += sm[threadIdx.x + s];
+    __syncthreads();
+  }
+  return sm[0];
+}
+
+// Finish a 2-value reduction: block partials -> out0/out1 by the last block.
+// Returns true in the thread that wrote the final values.
+__device__ __forceinline__ bool finish2(double s0, double s1, double* partial, unsigned int* counter,
+                                        double* out0, double* out1, double* sm) {
+  __shared__ bool last;
+  double a = block_sum(s0, sm);
+  __syncthreads();
+  double b = block_sum(s1, sm);
+  if (threadIdx.x == 0) {
+    partial[2 * blockIdx.x] = a;
+    partial[2 * blockIdx.x + 1] = b;
+    __threadfence();
+    const unsigned t = atomicInc(counter, gridDim.x - 1);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    double x0 = 0.0, x1 = 0.0;
+    for (unsigned k = 0; k < gridDim.x; ++k) {
+      x0 += ((volatile double*)partial)[2 * k];
+      x1 += ((volatile double*)partial)[2 * k + 1];
+    }
+    if (out0) *out0 = x0;
+    if (out1) *out1 = x1;
+    return true;
+  }
+  return false;
+}
+
+// out0 = a.b, out1 = c.d   (c may be null)
+__global__ void __launch_bounds__(RB_THREADS) k_dot2(int64_t n, const double* __restrict__ a,
+                                                     const double* __restrict__ b, const double* __restrict__ c,
+                                                     const double* __restrict__ d, double* out0, double* out1,
+                                                     double* partial, unsigned int* counter, const int* gate) {
+  __shared__ double sm[RB_THREADS];
+  if (gate && !*gate) return;
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    s0 += a[i] * b[i];
+    if (c) s1 += c[i] * d[i];
+  }
+  finish2(s0, s1, partial, counter, out0, out1, sm);
+}
+
+// w -= (*coef) * v ; out = w . nxt  (nxt == nullptr: out = w . w)
+__global__ void __launch_bounds__(RB_THREADS) k_axpy_dot(int64_t n, double* __restrict__ w,
+                                                         const double* __restrict__ v, const double* coef,
+                                                         const double* __restrict__ nxt, double* out,
+                                                         double* partial, unsigned int* counter, const int* gate) {
+  __shared__ double sm[RB_THREADS];
+  if (gate && !*gate) return;
+  const double h = *coef;
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double wi = w[i] - h * v[i];
+    w[i] = wi;
+    s += wi * (nxt ? nxt[i] : wi);
+  }
+  finish2(s, 0.0, partial, counter, out, nullptr, sm);
+}
+
+// out = in / *den
+__global__ void k_div(int64_t n, double* __restrict__ out, const double* __restrict__ in, const double* den,
+                      const int* gate) {
+  if (gate && !*gate) return;
+  const double d = *den;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i] / d;
+}
+
+__global__ void k_copy(int64_t n, double* __restrict__ out, const double* __restrict__ in) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
+// ---------------------------------------------------------------------------
+// K5: Roe-split Jacobian assembly (jacobian.py:133-196)
+// ---------------------------------------------------------------------------
+__global__ void k_jac_faces(int64_t nfi, const int* __restrict__ ifaces, const int* __restrict__ f_own,
+                            const int* __restrict__ f_nbr, const double* __restrict__ f_normal,
+                            const double* __restrict__ f_area, const double* __restrict__ q,
+                            const int* __restrict__ fslot, double gam, double* __restrict__ off) {
+  const int64_t fi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (fi >= nfi) return;
+  const int f = ifaces[fi];
+  const int64_t o = f_own[f], nb = f_nbr[f];
+  double qo[5], qn[5], qm[5];
+  for (int k = 0; k < 5; ++k) {
+    qo[k] = q[o * 5 + k];
+    qn[k] = q[nb * 5 + k];
+    qm[k] = 0.5 * (qo[k] + qn[k]);
+  }
+  const double n[3] = {f_normal[3 * f], f_normal[3 * f + 1], f_normal[3 * f + 2]};
+  const double lam = spectral_radius(qm, n, gam);
+  const double hs = 0.5 * f_area[f];
+  double J[5][5];
+  euler_jacobian(qn, n, gam, J);
+  double* B = off + (int64_t)fslot[2 * f] * 25;  // row own, col nbr
+  for (int i = 0; i < 5; ++i)
+    for (int j = 0; j < 5; ++j) B[i * 5 + j] = hs * (J[i][j] - (i == j ? lam : 0.0));
+  euler_jacobian(qo, n, gam, J);
+  B = off + (int64_t)fslot[2 * f + 1] * 25;  // row nbr, col own
+  for (int i = 0; i < 5; ++i)
+    for (int j = 0; j < 5; ++j) B[i * 5 + j] = hs * (-J[i][j] - (i == j ? lam : 0.0));
+}
+
+// 5x5 inverse by LU with partial pivoting (numpy.linalg.inv: LAPACK gesv on I)
+__device__ __forceinline__ bool inv5(const double A[25], double X[25]) {
+  double a[25];
+  int piv[5];
+  for (int i = 0; i < 25; ++i) a[i] = A[i];
+  for (int k = 0; k < 5; ++k) {
+    int p = k;
+    double mx = fabs(a[k * 5 + k]);
+    for (int i = k + 1; i < 5; ++i)
+      if (fabs(a[i * 5 + k]) > mx) { mx = fabs(a[i * 5 + k]); p = i; }
+    piv[k] = p;
+    if (a[p * 5 + k] == 0.0) return false;
+    if (p != k)
+      for (int j = 0; j < 5; ++j) { const double t = a[k * 5 + j]; a[k * 5 + j] = a[p * 5 + j]; a[p * 5 + j] = t; }
+    const double r = 1.0 / a[k * 5 + k];
+    for (int i = k + 1; i < 5; ++i) {
+      const double l = a[i * 5 + k] * r;
+      a[i * 5 + k] = l;
+      for (int j = k + 1; j < 5; ++j) a[i * 5 + j] -= l * a[k * 5 + j];
+    }
+  }
+  for (int col = 0; col < 5; ++col) {
+    double b[5] = {0, 0, 0, 0, 0};
+    b[col] = 1.0;
+    for (int k = 0; k < 5; ++k)
+      if (piv[k] != k) { const double t = b[k]; b[k] = b[piv[k]]; b[piv[k]] = t; }
+    for (int i = 1; i < 5; ++i)
+      for (int j = 0; j < i; ++j) b[i] -= a[i * 5 + j] * b[j];
+    for (int i = 4; i >= 0; --i) {
+      for (int j = i + 1; j < 5; ++j) b[i] -= a[i * 5 + j] * b[j];
+      b[i] /= a[i * 5 + i];
+    }
+    for (int i = 0; i < 5; ++i) X[i * 5 + col] = b[i];
+  }
+  for (int i = 0; i < 25; ++i)
+    if (!isfinite(X[i])) return false;
+  return true;
+}
+
+// diagonal blocks: V/dt I + interior(own) + interior(nbr) + boundary(own), then D^-1
+__global__ void k_jac_diag(int64_t nc, const int* __restrict__ cjd_start, const int* __restrict__ cjd,
+                           const int* __restrict__ face_slot_of_face, const double* __restrict__ off,
+                           const int* __restrict__ f_own, const double* __restrict__ f_normal,
+                           const double* __restrict__ f_area, const int* __restrict__ bidx_of_face,
+                           const double* __restrict__ ghosts, const double* __restrict__ q,
+                           const double* __restrict__ vol, const double* __restrict__ dt, double gam,
+                           double* __restrict__ diag, double* __restrict__ dinv, int* status) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  double D[25];
+  for (int i = 0; i < 25; ++i) D[i] = 0.0;
+  const double vd = vol[c] / dt[c];
+  for (int i = 0; i < 5; ++i) D[i * 6] = vd;
+  double qc[5];
+  for (int k = 0; k < 5; ++k) qc[k] = q[c * 5 + k];
+  for (int e = cjd_start[c]; e < cjd_start[c + 1]; ++e) {
+    const int f = cjd[e] >> 1;
+    const int side = cjd[e] & 1;
+    const int slot = face_slot_of_face[2 * f + (side ^ 1)];
+    if (slot >= 0) {
+      // interior face: the diagonal contribution equals minus the opposite
+      // off-diagonal block (exactly: hs*(J + lam I) = -(hs*(-J - lam I)))
+      const double* B = off + (int64_t)slot * 25;
+      for (int i = 0; i < 25; ++i) D[i] += -B[i];
+    } else {
+      // boundary face, frozen ghost sharpens |lambda| (jacobian.py:597-610)
+      const double n[3] = {f_normal[3 * f], f_normal[3 * f + 1], f_normal[3 * f + 2]};
+      double qb[5];
+      if (ghosts) {
+        const int64_t b = bidx_of_face[f];
+        for (int k = 0; k < 5; ++k) qb[k] = 0.5 * (qc[k] + ghosts[b * 5 + k]);
+      } else {
+        for (int k = 0; k < 5; ++k) qb[k] = qc[k];
+      }
+      const double lb = spectral_radius(qb, n, gam);
+      double J[5][5];
+      euler_jacobian(qc, n, gam, J);
+      const double hs = 0.5 * f_area[f];
+      for (int i = 0; i < 5; ++i)
+        for (int j = 0; j < 5; ++j) D[i * 5 + j] += hs * (J[i][j] + (i == j ? lb : 0.0));
+    }
+  }
+  for (int i = 0; i < 25; ++i) diag[c * 25 + i] = D[i];
+  double X[25];
+  if (!inv5(D, X)) {
+    raise_dev(status, GKS_ERR_SINGULAR, (int)c);
+    for (int i = 0; i < 25; ++i) X[i] = NAN;
+  }
+  for (int i = 0; i < 25; ++i) dinv[c * 25 + i] = X[i];
+}
+
+__global__ void k_dinv_only(int64_t nc, const double* __restrict__ diag, double* __restrict__ dinv, int* status) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  double D[25], X[25];
+  for (int i = 0; i < 25; ++i) D[i] = diag[c * 25 + i];
+  if (!inv5(D, X)) {
+    raise_dev(status, GKS_ERR_SINGULAR, (int)c);
+    for (int i = 0; i < 25; ++i) X[i] = NAN;
+  }
+  for (int i = 0; i < 25; ++i) dinv[c * 25 + i] = X[i];
+}
+
+// ---------------------------------------------------------------------------
+// K6/K7: block products, one thread per (cell,row), 32 cells per block
+// ---------------------------------------------------------------------------
+// mode bits: 1 = include diagonal (spmv), 2 = subtract from rhs b (t = b - ...),
+//            4 = apply D^-1 to the result (cell-local via shared memory)
+template <int MODE>
+__global__ void __launch_bounds__(CELLS_PER_BLOCK * 5) k_block(int64_t nc, const int* __restrict__ rowptr,
+                                                               const int* __restrict__ col,
+                                                               const double* __restrict__ off,
+                                                               const double* __restrict__ diag,
+                                                               const double* __restrict__ dinv,
+                                                               const double* __restrict__ x,
+                                                               const double* __restrict__ b,
+                                                               double* __restrict__ out,
+                                                               double* __restrict__ out_pre, const int* gate) {
+  __shared__ double sm[CELLS_PER_BLOCK * 5];
+  if (gate && !*gate) return;
+  const int lc = threadIdx.x / 5;
+  const int row = threadIdx.x - lc * 5;
+  const int64_t c = (int64_t)blockIdx.x * CELLS_PER_BLOCK + lc;
+  double acc = 0.0;
+  if (c < nc) {
+    double o = 0.0;
+    for (int e = rowptr[c]; e < rowptr[c + 1]; ++e) {
+      const double* B = off + (int64_t)e * 25 + row * 5;
+      const double* xc = x + (int64_t)col[e] * 5;
+      o += B[0] * xc[0] + B[1] * xc[1] + B[2] * xc[2] + B[3] * xc[3] + B[4] * xc[4];
+    }
+    if (MODE & 1) {
+      const double* Dr = diag + c * 25 + row * 5;
+      const double* xc = x + c * 5;
+      const double d = Dr[0] * xc[0] + Dr[1] * xc[1] + Dr[2] * xc[2] + Dr[3] * xc[3] + Dr[4] * xc[4];
+      acc = d + o;
+    } else {
+      acc = o;
+    }
+    if (MODE & 2) acc = b[c * 5 + row] - acc;
+    if (out_pre) out_pre[c * 5 + row] = acc;
+  }
+  if (MODE & 4) {
+    sm[threadIdx.x] = acc;
+    __syncthreads();
+    if (c < nc) {
+      const double* Xr = dinv + c * 25 + row * 5;
+      const double* t = sm + lc * 5;
+      out[c * 5 + row] = Xr[0] * t[0] + Xr[1] * t[1] + Xr[2] * t[2] + Xr[3] * t[3] + Xr[4] * t[4];
+    }
+  } else if (c < nc) {
+    out[c * 5 + row] = acc;
+  }
+}
+
+// z = D^-1 b
+__global__ void k_dinv_apply(int64_t nc, const double* __restrict__ dinv, const double* __restrict__ b,
+                             double* __restrict__ z, const int* gate) {
+  if (gate && !*gate) return;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nc * 5) return;
+  const int64_t c = t / 5;
+  const int row = (int)(t - c * 5);
+  const double* Xr = dinv + c * 25 + row * 5;
+  const double* bc = b + c * 5;
+  z[t] = Xr[0] * bc[0] + Xr[1] * bc[1] + Xr[2] * bc[2] + Xr[3] * bc[3] + Xr[4] * bc[4];
+}
+
+// ---------------------------------------------------------------------------
+// GMRES scalar kernels (single thread): krylov.py:70-131
+// ---------------------------------------------------------------------------
+#define GH(i, jj) g->h[(i) * GM_MMAX + (jj)]
+
+__global__ void k_gm_cycle_begin(GmresDev* g) { g->notdone = !g->done; }
+
+__global__ void k_gm_cycle_start(GmresDev* g, int cyc) {
+  if (!g->notdone) { g->active = 0; return; }
+  g->matvecs += 1;
+  const double beta = sqrt(g->beta2);
+  g->beta = beta;
+  if (!g->target_set) {
+    g->target = g->rtol * beta + g->atol;
+    g->target_set = 1;
+  }
+  g->j_used = 0;
+  g->breakdown = 0;
+  g->norms[cyc * (GM_MMAX + 1)] = beta;
+  g->nnorms[cyc] = 1;
+  if (beta == 0.0 || beta <= g->target) {
+    g->done = 1;
+    g->active = 0;
+    return;
+  }
+  if (!isfinite(beta)) {
+    g->err = GKS_ERR_NONFINITE;
+    g->done = 1;
+    g->active = 0;
+    return;
+  }
+  g->active = 1;
+  for (int i = 0; i < (GM_MMAX + 1) * GM_MMAX; ++i) g->h[i] = 0.0;
+  for (int i = 0; i <= GM_MMAX; ++i) g->gv[i] = 0.0;
+  g->gv[0] = beta;
+}
+
+// after the first MGS pass of column j: Hessenberg column, re-orthogonalisation test
+__global__ void k_gm_reorth_check(GmresDev* g, int j) {
+  if (!g->active) { g->reorth_gate = 0; return; }
+  g->matvecs += 1;
+  for (int i = 0; i <= j; ++i) GH(i, j) = g->dots[i];
+  g->wscale = sqrt(g->wscale2);
+  GH(j + 1, j) = sqrt(g->hnext2);
+  g->reorth = GH(j + 1, j) < 0.5 * g->wscale ? 1 : 0;
+  g->reorth_gate = g->reorth;
+}
+
+__global__ void k_gm_givens(GmresDev* g, int j, int cyc) {
+  if (!g->active) return;
+  if (g->reorth) {
+    for (int i = 0; i <= j; ++i) GH(i, j) += g->corr[i];
+    GH(j + 1, j) = sqrt(g->hnext2);
+  }
+  if (!isfinite(GH(j + 1, j))) {
+    g->err = GKS_ERR_NONFINITE;
+    g->done = 1;
+    g->active = 0;
+    g->j_used = 0;
+    return;
+  }
+  for (int i = 0; i < j; ++i) {
+    const double t = g->cs[i] * GH(i, j) + g->sn[i] * GH(i + 1, j);
+    GH(i + 1, j) = -g->sn[i] * GH(i, j) + g->cs[i] * GH(i + 1, j);
+    GH(i, j) = t;
+  }
+  const double denom = hypot(GH(j, j), GH(j + 1, j));
+  g->cs[j] = GH(j, j) / denom;
+  g->sn[j] = GH(j + 1, j) / denom;
+  GH(j, j) = denom;
+  g->gv[j + 1] = -g->sn[j] * g->gv[j];
+  g->gv[j] = g->cs[j] * g->gv[j];
+  double* norms = g->norms + cyc * (GM_MMAX + 1);
+  const double last = fabs(g->gv[j + 1]);
+  norms[g->nnorms[cyc]++] = last;
+  g->j_used = j + 1;
+  if (GH(j + 1, j) <= 1e-13 * g->wscale) {
+    g->breakdown = 1;
+    g->breakdown_any = 1;
+    g->active = 0;
+  } else if (last <= fmax(1e-15 * norms[0], g->target)) {
+    g->active = 0;
+  } else {
+    g->hdiv = GH(j + 1, j);
+  }
+}
+
+// back substitution (krylov.py:128-131) and cycle bookkeeping
+__global__ void k_gm_cycle_end(GmresDev* g, int cyc) {
+  g->ny = 0;
+  if (!g->notdone) return;
+  const int ju = g->err ? 0 : g->j_used;
+  for (int i = ju - 1; i >= 0; --i) {
+    double dot = 0.0;
+    for (int k = i + 1; k < ju; ++k) dot += GH(i, k) * g->y[k];
+    g->y[i] = (g->gv[i] - dot) / GH(i, i);
+  }
+  g->ny = ju;
+  g->ncycles = cyc + 1;
+  const double last = g->norms[cyc * (GM_MMAX + 1) + g->nnorms[cyc] - 1];
+  if (g->breakdown || last <= g->target) g->done = 1;
+}
+#undef GH
+
+// x += y @ V[:ny]  (the combination is formed first, then added)
+__global__ void k_gm_update_x(int64_t n, double* __restrict__ x, const double* __restrict__ V, const GmresDev* g) {
+  const int ny = g->ny;
+  if (ny == 0) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < ny; ++k) s += g->y[k] * V[k * n + i];
+    x[i] = x[i] + s;
+  }
+}
+
+// r = b - t
+__global__ void k_sub(int64_t n, double* __restrict__ r, const double* __restrict__ b, const double* __restrict__ t,
+                      const int* gate) {
+  if (gate && !*gate) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    r[i] = b[i] - t[i];
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static int red_grid(int64_t n) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (n + RB_THREADS - 1) / RB_THREADS;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 4));
+}
+
+int blocksys_alloc(BlockSys* A, int64_t nc, int64_t nnz, cudaStream_t stream) {
+  A->nc = nc;
+  A->nnz = nnz;
+  A->stream = stream;
+  GKS_CUDA(cudaMalloc(&A->rowptr, (nc + 1) * sizeof(int)));
+  GKS_CUDA(cudaMalloc(&A->col, std::max<int64_t>(nnz, 1) * sizeof(int)));
+  GKS_CUDA(cudaMalloc(&A->off, std::max<int64_t>(nnz, 1) * 25 * sizeof(double)));
+  GKS_CUDA(cudaMalloc(&A->diag, nc * 25 * sizeof(double)));
+  GKS_CUDA(cudaMalloc(&A->dinv, nc * 25 * sizeof(double)));
+  GKS_CUDA(cudaMalloc(&A->status, 4 * sizeof(int)));
+  return GKS_OK;
+}
+
+void blocksys_free(BlockSys* A) {
+  cudaFree(A->rowptr); cudaFree(A->col); cudaFree(A->off); cudaFree(A->diag); cudaFree(A->dinv);
+  cudaFree(A->status);
+  krylov_free(&A->ws);
+}
+
+void krylov_free(KrylovWS* W) {
+  if (W->V) cudaFree(W->V);
+  if (W->bufs) cudaFree(W->bufs);
+  if (W->partial) cudaFree(W->partial);
+  if (W->counter) cudaFree(W->counter);
+  if (W->g) cudaFree(W->g);
+  *W = KrylovWS{};
+}
+
+int krylov_ensure(KrylovWS* W, int64_t n, int m) {
+  if (W->V && W->n == n && W->m >= m) return GKS_OK;
+  krylov_free(W);
+  W->n = n;
+  W->m = m;
+  GKS_CUDA(cudaMalloc(&W->V, (size_t)(m + 1) * n * sizeof(double)));
+  GKS_CUDA(cudaMalloc(&W->bufs, (size_t)6 * n * sizeof(double)));
+  W->w = W->bufs;
+  W->r = W->bufs + n;
+  W->t = W->bufs + 2 * n;
+  W->z = W->bufs + 3 * n;
+  W->b = W->bufs + 4 * n;
+  W->x = W->bufs + 5 * n;
+  W->grid = red_grid(n);
+  GKS_CUDA(cudaMalloc(&W->partial, (size_t)W->grid * 2 * sizeof(double)));
+  GKS_CUDA(cudaMalloc(&W->counter, sizeof(unsigned int)));
+  GKS_CUDA(cudaMemset(W->counter, 0, sizeof(unsigned int)));
+  GKS_CUDA(cudaMalloc(&W->g, sizeof(GmresDev)));
+  return GKS_OK;
+}
+
+static inline int cblocks(int64_t nc) { return (int)((nc + CELLS_PER_BLOCK - 1) / CELLS_PER_BLOCK); }
+
+// y = A x  (diag + off)
+void bs_spmv(BlockSys* A, const double* x, double* y, const int* gate) {
+  k_block<1><<<cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream>>>(A->nc, A->rowptr, A->col, A->off, A->diag,
+                                                                    A->dinv, x, nullptr, y, nullptr, gate);
+  count_launch(1);
+}
+
+// y = (L+U) x
+void bs_offdiag(BlockSys* A, const double* x, double* y, const int* gate) {
+  k_block<0><<<cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream>>>(A->nc, A->rowptr, A->col, A->off, A->diag,
+                                                                    A->dinv, x, nullptr, y, nullptr, gate);
+  count_launch(1);
+}
+
+// z = P^-1 b : z0 = D^-1 b, then kmax sweeps z <- D^-1 (b - (L+U) z)  (krylov.py:24-34)
+// uses tmp as the ping-pong buffer; result in z
+void bs_jacobi(BlockSys* A, const double* b, double* z, double* tmp, int kmax, const int* gate) {
+  const int64_t n5 = A->nc * 5;
+  k_dinv_apply<<<blocks_for(n5, 256), 256, 0, A->stream>>>(A->nc, A->dinv, b, z, gate);
+  count_launch(1);
+  double* cur = z;
+  double* nxt = tmp;
+  for (int k = 0; k < kmax; ++k) {
+    k_block<6><<<cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream>>>(A->nc, A->rowptr, A->col, A->off, A->diag,
+                                                                      A->dinv, cur, b, nxt, nullptr, gate);
+    count_launch(1);
+    std::swap(cur, nxt);
+  }
+  if (cur != z) {
+    k_copy<<<red_grid(n5), RB_THREADS, 0, A->stream>>>(n5, z, cur);
+    count_launch(1);
+  }
+}
+
+// w = P^-1 A v : fused spmv + first D^-1, then sweeps
+void bs_prec_matvec(BlockSys* A, const double* v, double* w, double* t, double* tmp, int kmax, const int* gate) {
+  k_block<5><<<cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream>>>(A->nc, A->rowptr, A->col, A->off, A->diag,
+                                                                    A->dinv, v, nullptr, w, t, gate);
+  count_launch(1);
+  double* cur = w;
+  double* nxt = tmp;
+  for (int k = 0; k < kmax; ++k) {
+    k_block<6><<<cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream>>>(A->nc, A->rowptr, A->col, A->off, A->diag,
+                                                                      A->dinv, cur, t, nxt, nullptr, gate);
+    count_launch(1);
+    std::swap(cur, nxt);
+  }
+  if (cur != w) {
+    const int64_t n5 = A->nc * 5;
+    k_copy<<<red_grid(n5), RB_THREADS, 0, A->stream>>>(n5, w, cur);
+    count_launch(1);
+  }
+}
+
+void dot2(KrylovWS* W, cudaStream_t s, int64_t n, const double* a, const double* b, const double* c,
+          const double* d, double* o0, double* o1, const int* gate) {
+  k_dot2<<<W->grid, RB_THREADS, 0, s>>>(n, a, b, c, d, o0, o1, W->partial, W->counter, gate);
+  count_launch(1);
+}
+
+// Restarted left-preconditioned GMRES (krylov.py:55-140) on device vectors;
+// x_dev receives the solution.  matvec == nullptr: A v is the block spmv.
+int gmres_device(BlockSys* A, const double* b_dev, double* x_dev, const GmresParams& P, GmresHost* out,
+                 const MatvecFn* matvec) {
+  const int64_t n = A->nc * 5;
+  const int m = P.m;
+  if (m < 1 || m > GM_MMAX || P.restarts < 1 || P.restarts > GM_RMAX || P.kmax < 0) {
+    set_error("gmres: krylov_dim must be in [1, %d], restarts in [1, %d]", GM_MMAX, GM_RMAX);
+    return GKS_ERR_BAD_ARG;
+  }
+  if (!A->dinv_ok) {
+    set_error("singular diagonal block in Jacobi preconditioner");
+    return GKS_ERR_SINGULAR;
+  }
+  KrylovWS* W = &A->ws;
+  int rc = krylov_ensure(W, n, m);
+  if (rc) return rc;
+  cudaStream_t s = A->stream;
+  GmresDev* g = W->g;
+  {
+    // only the header of the struct needs initialising
+    GmresDev g0;
+    memset(&g0, 0, offsetof(GmresDev, dots));
+    g0.m = m;
+    g0.restarts = P.restarts;
+    g0.rtol = P.rtol;
+    g0.atol = P.atol;
+    GKS_CUDA(cudaMemcpyAsync(g, &g0, offsetof(GmresDev, dots), cudaMemcpyHostToDevice, s));
+  }
+  GKS_CUDA(cudaMemsetAsync(x_dev, 0, n * sizeof(double), s));
+  const int* act = &g->active;
+  const int* notdone = &g->notdone;
+  const int* rgate = &g->reorth_gate;
+  const int kmax = P.kmax;
+  const int grid = red_grid(n);
+  auto Av = [&](const double* v, double* dst, const int* gate) {
+    if (matvec) (*matvec)(v, dst, gate);
+    else bs_spmv(A, v, dst, gate);
+  };
+  for (int cyc = 0; cyc < P.restarts; ++cyc) {
+    k_gm_cycle_begin<<<1, 1, 0, s>>>(g);
+    count_launch(1);
+    // r = b - A x ; rh = P r ; beta = ||rh||
+    Av(x_dev, W->t, notdone);
+    k_sub<<<grid, RB_THREADS, 0, s>>>(n, W->r, b_dev, W->t, notdone);
+    count_launch(1);
+    bs_jacobi(A, W->r, W->z, W->w, kmax, notdone);
+    dot2(W, s, n, W->z, W->z, nullptr, nullptr, &g->beta2, nullptr, notdone);
+    k_gm_cycle_start<<<1, 1, 0, s>>>(g, cyc);
+    k_div<<<grid, RB_THREADS, 0, s>>>(n, W->V, W->z, &g->beta, act);
+    count_launch(2);
+    for (int j = 0; j < m; ++j) {
+      const double* vj = W->V + (int64_t)j * n;
+      // w = P^-1 A v_j
+      if (matvec) {
+        Av(vj, W->t, act);
+        bs_jacobi(A, W->t, W->w, W->r, kmax, act);
+      } else {
+        bs_prec_matvec(A, vj, W->w, W->t, W->r, kmax, act);
+      }
+      // ||w||^2 and w.v_0 in one pass, then fused axpy + next dot (MGS)
+      dot2(W, s, n, W->w, W->w, W->w, W->V, &g->wscale2, &g->dots[0], act);
+      for (int i = 0; i <= j; ++i) {
+        const double* nxt = i < j ? W->V + (int64_t)(i + 1) * n : nullptr;
+        double* dst = i < j ? &g->dots[i + 1] : &g->hnext2;
+        k_axpy_dot<<<W->grid, RB_THREADS, 0, s>>>(n, W->w, W->V + (int64_t)i * n, &g->dots[i], nxt, dst,
+                                                  W->partial, W->counter, act);
+        count_launch(1);
+      }
+      k_gm_reorth_check<<<1, 1, 0, s>>>(g, j);
+      count_launch(1);
+      // conditional second pass (krylov.py:97-104)
+      dot2(W, s, n, W->w, W->V, nullptr, nullptr, &g->corr[0], nullptr, rgate);
+      for (int i = 0; i <= j; ++i) {
+        const double* nxt = i < j ? W->V + (int64_t)(i + 1) * n : nullptr;
+        double* dst = i < j ? &g->corr[i + 1] : &g->hnext2;
+        k_axpy_dot<<<W->grid, RB_THREADS, 0, s>>>(n, W->w, W->V + (int64_t)i * n, &g->corr[i], nxt, dst,
+                                                  W->partial, W->counter, rgate);
+        count_launch(1);
+      }
+      k_gm_givens<<<1, 1, 0, s>>>(g, j, cyc);
+      k_div<<<grid, RB_THREADS, 0, s>>>(n, W->V + (int64_t)(j + 1) * n, W->w, &g->hdiv, act);
+      count_launch(2);
+    }
+    k_gm_cycle_end<<<1, 1, 0, s>>>(g, cyc);
+    k_gm_update_x<<<grid, RB_THREADS, 0, s>>>(n, x_dev, W->V, g);
+    count_launch(2);
+    if (P.check_ortho && out) {
+      // Gram matrix of the cycle's basis (krylov.py:778-782), host-side check
+      GmresDev gh;
+      GKS_CUDA(cudaMemcpyAsync(&gh, g, offsetof(GmresDev, dots), cudaMemcpyDeviceToHost, s));
+      GKS_CUDA(cudaStreamSynchronize(s));
+      const int ju = gh.ny;
+      if (ju > 1) {
+        std::vector<double> hv((size_t)ju * n);
+        GKS_CUDA(cudaMemcpy(hv.data(), W->V, hv.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        for (int a = 0; a < ju; ++a)
+          for (int b = 0; b < ju; ++b) {
+            double acc = 0.0;
+            for (int64_t i = 0; i < n; ++i) acc += hv[a * n + i] * hv[b * n + i];
+            out->ortho_error = std::max(out->ortho_error, fabs(acc - (a == b ? 1.0 : 0.0)));
+          }
+      }
+    }
+  }
+  GKS_CUDA(cudaGetLastError());
+  GmresDev* gh = new GmresDev;
+  GKS_CUDA(cudaMemcpyAsync(gh, g, sizeof(GmresDev), cudaMemcpyDeviceToHost, s));
+  GKS_CUDA(cudaStreamSynchronize(s));
+  int ret = GKS_OK;
+  if (out) {
+    out->ncycles = gh->ncycles;
+    out->breakdown = gh->breakdown_any;
+    out->err = gh->err;
+    out->matvecs = gh->matvecs;
+    for (int c = 0; c < gh->ncycles; ++c) {
+      out->cycle_len[c] = gh->nnorms[c];
+      for (int k = 0; k < gh->nnorms[c]; ++k) out->norms[c * (GM_MMAX + 1) + k] = gh->norms[c * (GM_MMAX + 1) + k];
+    }
+  }
+  if (gh->err) {
+    set_error(gh->err == GKS_ERR_NONFINITE ? "GMRES diverged: non-finite Arnoldi vector" : "GMRES failed (%d)",
+              gh->err);
+    ret = gh->err;
+  }
+  delete gh;
+  return ret;
+}
+
+// ---------------------------------------------------------------------------
+// Jacobian assembly on the handle's mesh
+// ---------------------------------------------------------------------------
+int jacobian_assemble(Handle* H, BlockSys* A, const double* ghosts_dev) {
+  const int st0[4] = {0, 0x7fffffff, 0, 0};
+  GKS_CUDA(cudaMemcpyAsync(A->status, st0, sizeof(st0), cudaMemcpyHostToDevice, H->stream));
+  if (H->nfi)
+    k_jac_faces<<<blocks_for(H->nfi, 128), 128, 0, H->stream>>>(H->nfi, H->interior_faces, H->f_own, H->f_nbr,
+                                                                 H->f_normal, H->f_area, H->q, H->face_slot,
+                                                                 H->gamma, A->off);
+  k_jac_diag<<<blocks_for(H->nc, 128), 128, 0, H->stream>>>(H->nc, H->cjd_start, H->cjd, H->face_slot, A->off,
+                                                             H->f_own, H->f_normal, H->f_area, H->bidx, ghosts_dev,
+                                                             H->q, H->vol, H->dt, H->gamma, A->diag, A->dinv,
+                                                             A->status);
+  count_launch(2);
+  GKS_CUDA(cudaGetLastError());
+  int st[4];
+  GKS_CUDA(cudaMemcpyAsync(st, A->status, sizeof(st), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaStreamSynchronize(H->stream));
+  A->dinv_ok = st[0] == 0;
+  return GKS_OK;
+}
+
+int blocksys_invert_diag(BlockSys* A) {
+  const int st0[4] = {0, 0x7fffffff, 0, 0};
+  GKS_CUDA(cudaMemcpyAsync(A->status, st0, sizeof(st0), cudaMemcpyHostToDevice, A->stream));
+  k_dinv_only<<<blocks_for(A->nc, 128), 128, 0, A->stream>>>(A->nc, A->diag, A->dinv, A->status);
+  count_launch(1);
+  int st[4];
+  GKS_CUDA(cudaMemcpyAsync(st, A->status, sizeof(st), cudaMemcpyDeviceToHost, A->stream));
+  GKS_CUDA(cudaStreamSynchronize(A->stream));
+  A->dinv_ok = st[0] == 0;
+  return GKS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K9: state update, validity mask and step norms (stepping.py:264-290)
+// ---------------------------------------------------------------------------
+__global__ void k_update(int64_t nc, const double* __restrict__ q, const double* __restrict__ dq,
+                         double* __restrict__ qn, int8_t* __restrict__ bad) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  double v[5];
+  bool fin = true;
+  for (int k = 0; k < 5; ++k) {
+    v[k] = q[c * 5 + k] + dq[c * 5 + k];
+    qn[c * 5 + k] = v[k];
+    fin = fin && isfinite(v[k]);
+  }
+  const double rho = v[0];
+  const double e = v[4] - 0.5 * (v[1] * v[1] + v[2] * v[2] + v[3] * v[3]) / rho;
+  bad[c] = (rho <= 0.0) || (e <= 0.0) || !fin;
+}
+
+// sum|res_rho|, sum res^2, min dt, bad count -> DevScalars (deterministic)
+__global__ void __launch_bounds__(RB_THREADS) k_stats(int64_t nc, const double* __restrict__ res,
+                                                      const double* __restrict__ dt, const int8_t* __restrict__ bad,
+                                                      double* partial, unsigned int* counter, DevScalars* out) {
+  __shared__ double sm[RB_THREADS];
+  __shared__ bool last;
+  double a = 0.0, b = 0.0, mn = INFINITY, nb = 0.0;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
+    a += fabs(res[c * 5]);
+    for (int k = 0; k < 5; ++k) b += res[c * 5 + k] * res[c * 5 + k];
+    mn = fmin(mn, dt[c]);
+    nb += bad[c] ? 1.0 : 0.0;
+  }
+  const double A = block_sum(a, sm);
+  __syncthreads();
+  const double B = block_sum(b, sm);
+  __syncthreads();
+  const double NB = block_sum(nb, sm);
+  __syncthreads();
+  sm[threadIdx.x] = mn;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sm[threadIdx.x] = fmin(sm[threadIdx.x], sm[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partial[4 * blockIdx.x] = A;
+    partial[4 * blockIdx.x + 1] = B;
+    partial[4 * blockIdx.x + 2] = sm[0];
+    partial[4 * blockIdx.x + 3] = NB;
+    __threadfence();
+    last = atomicInc(counter, gridDim.x - 1) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double x0 = 0, x1 = 0, x2 = INFINITY, x3 = 0;
+    volatile double* p = partial;
+    for (unsigned k = 0; k < gridDim.x; ++k) {
+      x0 += p[4 * k]; x1 += p[4 * k + 1]; x2 = fmin(x2, p[4 * k + 2]); x3 += p[4 * k + 3];
+    }
+    out->res_rho_l1 = x0 / (double)nc;
+    out->res_l2 = sqrt(x1 / (double)(5 * nc));
+    out->dt_min = x2;
+    out->nbad = (int)x3;
+  }
+}
+
+__global__ void k_halve_dt(int64_t nc, const int8_t* __restrict__ bad, double* __restrict__ dt) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < nc && bad[c]) dt[c] = 0.5 * dt[c];
+}
+
+// ---------------------------------------------------------------------------
+// matrix-free operator (north-star option): A v = V/dt v - (L(Q + s v) - L(Q)) / s
+// (stepping.py:298-313 for the directional derivative)
+// ---------------------------------------------------------------------------
+__global__ void k_sigma(const double* vv_qq, double* sigma, double* out_zero_flag) {
+  const double vn = sqrt(vv_qq[0]);
+  const double qn = sqrt(vv_qq[1]);
+  *sigma = vn == 0.0 ? 0.0 : sqrt(2.220446049250313e-16) * (1.0 + qn) / vn;
+  if (out_zero_flag) *out_zero_flag = vn == 0.0 ? 1.0 : 0.0;
+}
+
+__global__ void k_perturb(int64_t n, const double* __restrict__ q, const double* __restrict__ v,
+                          const double* sigma, double* __restrict__ out, const int* gate) {
+  if (gate && !*gate) return;
+  const double s = *sigma;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = q[i] + s * v[i];
+}
+
+// mode 0: out = (r1 - r0) / s ; mode 1: out = V/dt v - (r1 - r0) / s  (s == 0 -> derivative 0)
+__global__ void k_frechet_combine(int64_t nc, const double* __restrict__ r1, const double* __restrict__ r0,
+                                  const double* sigma, const double* __restrict__ v, const double* __restrict__ vol,
+                                  const double* __restrict__ dt, int mode, double* __restrict__ out, const int* gate) {
+  if (gate && !*gate) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nc * 5) return;
+  const double s = *sigma;
+  const double d = s == 0.0 ? 0.0 : (r1[i] - r0[i]) / s;
+  out[i] = mode ? (vol[i / 5] / dt[i / 5]) * v[i] - d : d;
+}
+
+}  // namespace gks
+

@@ -1,0 +1,78 @@
+// Block systems, Krylov work space and device-side GMRES state.
+#pragma once
+#include <functional>
+
+#include "gks_solver.cuh"
+
+namespace gks {
+
+constexpr int GM_MMAX = 64;  // max Krylov dimension
+constexpr int GM_RMAX = 64;  // max restarts
+
+// Device-resident GMRES scalars (krylov.py:55-140 state).
+struct GmresDev {
+  int m, restarts;
+  double rtol, atol;
+  int done, notdone, active, reorth, reorth_gate;
+  int j_used, breakdown, breakdown_any, err, ncycles, matvecs, ny, target_set;
+  double target, beta2, beta, wscale2, wscale, hnext2, hdiv;
+  double dots[GM_MMAX + 1];
+  double corr[GM_MMAX + 1];
+  double h[(GM_MMAX + 1) * GM_MMAX];
+  double cs[GM_MMAX], sn[GM_MMAX], gv[GM_MMAX + 1], y[GM_MMAX];
+  double norms[GM_RMAX * (GM_MMAX + 1)];
+  int nnorms[GM_RMAX];
+};
+
+struct KrylovWS {
+  int64_t n = 0;
+  int m = 0;
+  int grid = 0;
+  double* V = nullptr;
+  double* bufs = nullptr;
+  double *w = nullptr, *r = nullptr, *t = nullptr, *z = nullptr, *b = nullptr, *x = nullptr;
+  double* partial = nullptr;
+  unsigned int* counter = nullptr;
+  GmresDev* g = nullptr;
+};
+
+// Block-row matrix: diagonal blocks + CSR off-diagonal blocks (jacobian.py:74-126)
+struct BlockSys {
+  int64_t nc = 0, nnz = 0;
+  int *rowptr = nullptr, *col = nullptr;
+  double *off = nullptr, *diag = nullptr, *dinv = nullptr;
+  int* status = nullptr;
+  int dinv_ok = 0;
+  cudaStream_t stream = nullptr;
+  KrylovWS ws;
+};
+
+struct GmresParams {
+  int m = 10, restarts = 3, kmax = 2;
+  double rtol = 0.0, atol = 0.0;
+  int check_ortho = 0;
+};
+
+struct GmresHost {
+  int ncycles = 0, matvecs = 0, breakdown = 0, err = 0;
+  double ortho_error = 0.0;
+  int cycle_len[GM_RMAX];
+  double norms[GM_RMAX * (GM_MMAX + 1)];
+};
+
+// out = A v on the device, gated by *gate (matrix-free operators)
+using MatvecFn = std::function<void(const double* v, double* out, const int* gate)>;
+
+int blocksys_alloc(BlockSys* A, int64_t nc, int64_t nnz, cudaStream_t stream);
+void blocksys_free(BlockSys* A);
+void krylov_free(KrylovWS* W);
+int krylov_ensure(KrylovWS* W, int64_t n, int m);
+int blocksys_invert_diag(BlockSys* A);
+void bs_spmv(BlockSys* A, const double* x, double* y, const int* gate);
+void bs_offdiag(BlockSys* A, const double* x, double* y, const int* gate);
+void bs_jacobi(BlockSys* A, const double* b, double* z, double* tmp, int kmax, const int* gate);
+int gmres_device(BlockSys* A, const double* b_dev, double* x_dev, const GmresParams& P, GmresHost* out,
+                 const MatvecFn* matvec);
+int jacobian_assemble(Handle* H, BlockSys* A, const double* ghosts_dev);
+
+}  // namespace gks

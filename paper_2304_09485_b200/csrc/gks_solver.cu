@@ -1,0 +1,524 @@
+// Solver handle + residual pipeline (K1 local dt, K2 reconstruction,
+// K3 fused face flux, K4 deterministic cell assembly).
+//
+// Reference path (gks3d, /root/reference/pkg/src/gks3d):
+//   Solver.local_time_step   stepping.py:135-157
+//   Solver.residual          stepping.py:212-238
+//     _reconstruct           stepping.py:161-178  (recon.py:276-314, hweno.py:139-169,
+//                                                   boundary.py:66-171)
+//     interface_batch        stepping.py:187-208  (flux.py:69-107, 211-243)
+//     evolve_flux / scatter  stepping.py:219-228  (flux.py:162-179)
+//     compact gradients      stepping.py:230-237  (flux.py:182-188, hweno.py:172-194)
+//
+// Data layout in HBM (AoS per entity so one cell's / face's record is one
+// contiguous run): q (nc,5), grad (nc,3,5), coefficients (nc,9,5), face
+// contributions (nfq,5).  Assembly is a cell-centric gather over a CSR list
+// in the reference's np.add.at order (owner entries, then neighbour
+// entries, ascending), so results are deterministic and atomics-free.
+#include <algorithm>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "gks_solver.cuh"
+
+namespace gks {
+
+static constexpr int TPB = 128;
+
+// ---------------------------------------------------------------------------
+// K1: local time step
+// ---------------------------------------------------------------------------
+__global__ void k_local_dt(int64_t nc, const double* __restrict__ q, const int* __restrict__ cdt_start,
+                           const int* __restrict__ cdt, const double* __restrict__ f_normal,
+                           const double* __restrict__ f_area, const double* __restrict__ vol, int viscous,
+                           double mu, double cfl, KinConst kc, double* __restrict__ dt, int* status) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  double qc[5], w[5];
+  for (int k = 0; k < 5; ++k) qc[k] = q[c * 5 + k];
+  if (!cons_to_prim(qc, kc, w)) {
+    raise_dev(status, GKS_ERR_UNPHYSICAL, (int)c);
+    return;
+  }
+  const double a = sqrt(kc.gamma / (2.0 * w[4]));
+  const double V = vol[c];
+  double speed = 0.0;
+  for (int e = cdt_start[c]; e < cdt_start[c + 1]; ++e) {
+    const int f = cdt[e] >> 1;
+    const double* n = f_normal + 3 * f;
+    double un = w[1] * n[0];
+    un += w[2] * n[1];
+    un += w[3] * n[2];
+    const double S = f_area[f];
+    double sig = (fabs(un) + a) * S;
+    if (viscous) sig += (mu / w[0]) * (S * S) / V;
+    speed += sig;
+  }
+  dt[c] = cfl * V / speed;
+}
+
+// deterministic min-reduction for the global time step (single block)
+__global__ void k_min_broadcast(int64_t n, double* __restrict__ dt) {
+  __shared__ double sm[1024];
+  double m = INFINITY;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmin(m, dt[i]);
+  sm[threadIdx.x] = m;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sm[threadIdx.x] = fmin(sm[threadIdx.x], sm[threadIdx.x + s]);
+    __syncthreads();
+  }
+  const double g = sm[0];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dt[i] = g;
+}
+
+// ---------------------------------------------------------------------------
+// K2: reconstruction -> combined coefficients (nc, 9, 5); one thread per
+// (cell, component) because the WENO weights are per cell per component
+// (recon.py:167-195).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void combine(double cb[9], const double (&b)[8][3], const int8_t* act, int M,
+                                        const double* __restrict__ B, double eps, double lw) {
+  double beta0 = 0.0;
+#pragma unroll
+  for (int d = 0; d < 9; ++d) {
+    double t = 0.0;
+#pragma unroll
+    for (int e = 0; e < 9; ++e) t += B[d * 9 + e] * cb[e];
+    beta0 += cb[d] * t;
+  }
+  int nact = 0;
+  double bs[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    bs[m] = b[m][0] * b[m][0] + b[m][1] * b[m][1] + b[m][2] * b[m][2];
+    if (m < M && act[m]) ++nact;
+  }
+  const double g0 = 1.0 - lw * nact;
+  double tau = 0.0;
+#pragma unroll
+  for (int m = 0; m < 8; ++m)
+    if (m < M && act[m]) tau += fabs(beta0 - bs[m]);
+  tau /= (double)(nact > 1 ? nact : 1);
+  const double w0 = g0 * (1.0 + tau / (beta0 + eps));
+  double wm[8];
+  double total = w0;
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    wm[m] = (m < M && act[m]) ? lw * (1.0 + tau / (bs[m] + eps)) : 0.0;
+    total += wm[m];
+  }
+  const double w0n = w0 / total;
+  const double c0 = w0n / g0;
+  const double sub0 = w0n * lw / g0;
+#pragma unroll
+  for (int d = 0; d < 9; ++d) cb[d] *= c0;
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    if (m < M && act[m]) {
+      const double f = wm[m] / total - sub0;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) cb[d] += f * b[m][d];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(TPB) k_recon_weno(int64_t nc, const double* __restrict__ q,
+                                                    const double* __restrict__ big_op, const int* __restrict__ big_gather,
+                                                    int K, const double* __restrict__ sub_op,
+                                                    const int* __restrict__ sub_gather, const int8_t* __restrict__ sub_active,
+                                                    int M, int S, const double* __restrict__ beta, int linear,
+                                                    double eps, double lw, double* __restrict__ coef, const int* gate) {
+  if (gate && !*gate) return;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nc * 5) return;
+  const int64_t c = t / 5;
+  const int k = (int)(t - c * 5);
+  const double qc = q[c * 5 + k];
+  double cb[9];
+#pragma unroll
+  for (int d = 0; d < 9; ++d) cb[d] = 0.0;
+  const double* op = big_op + c * 9 * K;
+  const int* gi = big_gather + c * K;
+  for (int j = 0; j < K; ++j) {
+    const double r = q[(int64_t)gi[j] * 5 + k] - qc;
+#pragma unroll
+    for (int d = 0; d < 9; ++d) cb[d] += op[d * K + j] * r;
+  }
+  if (!linear) {
+    double b[8][3];
+    const int8_t* act = sub_active + c * M;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      b[m][0] = b[m][1] = b[m][2] = 0.0;
+      if (m < M) {
+        const double* so = sub_op + (c * M + m) * 3 * S;
+        const int* sg = sub_gather + (c * M + m) * S;
+        for (int s = 0; s < S; ++s) {
+          const double r = q[(int64_t)sg[s] * 5 + k] - qc;
+          b[m][0] += so[s] * r;
+          b[m][1] += so[S + s] * r;
+          b[m][2] += so[2 * S + s] * r;
+        }
+      }
+    }
+    combine(cb, b, act, M, beta + c * 81, eps, lw);
+  }
+  double* out = coef + c * 45 + k;
+#pragma unroll
+  for (int d = 0; d < 9; ++d) out[d * 5] = cb[d];
+}
+
+__global__ void __launch_bounds__(TPB) k_recon_hweno(int64_t nc, const double* __restrict__ q,
+                                                     const double* __restrict__ grad, const double* __restrict__ h,
+                                                     const double* __restrict__ big_op, const int* __restrict__ avg_gather,
+                                                     const int* __restrict__ grad_gather,
+                                                     const double* __restrict__ grad_scale, int HA, int HG,
+                                                     const double* __restrict__ sub_op, const int* __restrict__ sub_gather,
+                                                     const int8_t* __restrict__ sub_active, int M,
+                                                     const double* __restrict__ beta, int linear, double eps, double lw,
+                                                     double* __restrict__ coef, const int* gate) {
+  if (gate && !*gate) return;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nc * 5) return;
+  const int64_t c = t / 5;
+  const int k = (int)(t - c * 5);
+  const double qc = q[c * 5 + k];
+  const int W = HA + 3 * HG;
+  const double* op = big_op + c * 9 * W;
+  double cb[9];
+#pragma unroll
+  for (int d = 0; d < 9; ++d) cb[d] = 0.0;
+  for (int j = 0; j < HA; ++j) {
+    const double r = q[(int64_t)avg_gather[c * HA + j] * 5 + k] - qc;
+#pragma unroll
+    for (int d = 0; d < 9; ++d) cb[d] += op[d * W + j] * r;
+  }
+  for (int g = 0; g < HG; ++g) {
+    const int64_t m = grad_gather[c * HG + g];
+    const double sc = grad_scale[c * HG + g];
+#pragma unroll
+    for (int x = 0; x < 3; ++x) {
+      const double r = sc * grad[(m * 3 + x) * 5 + k];
+      const int j = HA + 3 * g + x;
+#pragma unroll
+      for (int d = 0; d < 9; ++d) cb[d] += op[d * W + j] * r;
+    }
+  }
+  if (!linear) {
+    double b[8][3];
+    const int8_t* act = sub_active + c * M;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      b[m][0] = b[m][1] = b[m][2] = 0.0;
+      if (m < M) {
+        const double* so = sub_op + (c * M + m) * 21;
+        const int64_t s0 = sub_gather[(c * M + m) * 2 + 0];
+        const int64_t s1 = sub_gather[(c * M + m) * 2 + 1];
+        double rhs[7];
+        rhs[0] = q[s1 * 5 + k] - qc;
+        const double h0 = h[s0], h1 = h[s1];
+#pragma unroll
+        for (int x = 0; x < 3; ++x) {
+          rhs[1 + x] = h0 * grad[(s0 * 3 + x) * 5 + k];
+          rhs[4 + x] = h1 * grad[(s1 * 3 + x) * 5 + k];
+        }
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int s = 0; s < 7; ++s) b[m][d] += so[d * 7 + s] * rhs[s];
+      }
+    }
+    combine(cb, b, act, M, beta + c * 81, eps, lw);
+  }
+  double* out = coef + c * 45 + k;
+#pragma unroll
+  for (int d = 0; d < 9; ++d) out[d * 5] = cb[d];
+}
+
+// ---------------------------------------------------------------------------
+// K3: fused face kernel, one thread per face quadrature point
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void eval_side(const double* __restrict__ q, const double* __restrict__ coef,
+                                          const double* __restrict__ cen, const double* __restrict__ h,
+                                          const double* __restrict__ avg0, int64_t c, const double x[3],
+                                          double val[5], double g[3][5]) {
+  const double hc = h[c];
+  const double xt[3] = {(x[0] - cen[3 * c]) / hc, (x[1] - cen[3 * c + 1]) / hc, (x[2] - cen[3 * c + 2]) / hc};
+  const double mono[9] = {xt[0], xt[1], xt[2], xt[0] * xt[0], xt[0] * xt[1],
+                          xt[0] * xt[2], xt[1] * xt[1], xt[1] * xt[2], xt[2] * xt[2]};
+  double phi[9];
+#pragma unroll
+  for (int d = 0; d < 9; ++d) phi[d] = mono[d] - avg0[c * 9 + d];
+  const double ih = 1.0 / hc;
+  // d mono / d xt (recon.py:48-57) divided by h
+  const double gx[9] = {1, 0, 0, 2 * xt[0], xt[1], xt[2], 0, 0, 0};
+  const double gy[9] = {0, 1, 0, 0, xt[0], 0, 2 * xt[1], xt[2], 0};
+  const double gz[9] = {0, 0, 1, 0, 0, xt[0], 0, xt[1], 2 * xt[2]};
+  const double* C = coef + c * 45;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    double v = 0.0, a = 0.0, b = 0.0, e = 0.0;
+#pragma unroll
+    for (int d = 0; d < 9; ++d) {
+      const double cd = C[d * 5 + k];
+      v += phi[d] * cd;
+      a += (gx[d] / hc) * cd;
+      b += (gy[d] / hc) * cd;
+      e += (gz[d] / hc) * cd;
+    }
+    val[k] = q[c * 5 + k] + v;
+    g[0][k] = a;
+    g[1][k] = b;
+    g[2][k] = e;
+  }
+  (void)ih;
+}
+
+__device__ __forceinline__ void to_local_state(const double qv[5], const double* F, double out[5]) {
+  out[0] = qv[0];
+  out[4] = qv[4];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) out[1 + i] = F[3 * i] * qv[1] + F[3 * i + 1] * qv[2] + F[3 * i + 2] * qv[3];
+}
+
+// slopes along (n, t1, t2), momentum block rotated (stepping.py:180-185)
+__device__ __forceinline__ void local_slopes(const double g[3][5], const double* F, double s[3][5]) {
+  double t[3][5];
+#pragma unroll
+  for (int kk = 0; kk < 3; ++kk)
+#pragma unroll
+    for (int m = 0; m < 5; ++m) t[kk][m] = F[3 * kk] * g[0][m] + F[3 * kk + 1] * g[1][m] + F[3 * kk + 2] * g[2][m];
+#pragma unroll
+  for (int kk = 0; kk < 3; ++kk) {
+    s[kk][0] = t[kk][0];
+    s[kk][4] = t[kk][4];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) s[kk][1 + i] = F[3 * i] * t[kk][1] + F[3 * i + 1] * t[kk][2] + F[3 * i + 2] * t[kk][3];
+  }
+}
+
+struct FaceArgs {
+  int64_t nfq;
+  const double *q, *coef, *cen, *h, *avg0, *dt;
+  const int *fq_face, *f_own, *f_nbr, *f_patch;
+  const double *fq_point, *fq_ws, *f_frame, *f_normal, *f_shift;
+  const DevPatch* patches;
+  int model;
+  double mu;
+  KinConst kc;
+  int want_point;
+  double* contrib;
+  double* qpt;
+  int* status;
+  const int* gate;
+};
+
+__global__ void __launch_bounds__(128) k_face(FaceArgs A) {
+  if (A.gate && !*A.gate) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.nfq) return;
+  const int f = A.fq_face[i];
+  const int64_t o = A.f_own[f];
+  const int64_t nb = A.f_nbr[f];
+  const double x[3] = {A.fq_point[3 * i], A.fq_point[3 * i + 1], A.fq_point[3 * i + 2]};
+  double F[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) F[k] = A.f_frame[9 * f + k];
+  FluxIn in;
+  bool wall = false;
+  double dtf;
+  {
+    double vo[5], go[3][5], vn[5], gn[3][5];
+    eval_side(A.q, A.coef, A.cen, A.h, A.avg0, o, x, vo, go);
+    if (nb >= 0) {
+      const double xs[3] = {x[0] - A.f_shift[3 * f], x[1] - A.f_shift[3 * f + 1], x[2] - A.f_shift[3 * f + 2]};
+      eval_side(A.q, A.coef, A.cen, A.h, A.avg0, nb, xs, vn, gn);
+      dtf = fmin(A.dt[o], A.dt[nb]);
+    } else {
+      const int p = A.f_patch[f];
+      const DevPatch P = A.patches[p];
+      const double nrm[3] = {A.f_normal[3 * f], A.f_normal[3 * f + 1], A.f_normal[3 * f + 2]};
+      if (!ghost_state(vo, P, nrm, A.kc, vn)) {
+        atomicCAS(A.status, 0, GKS_ERR_UNPHYSICAL);
+        atomicMin(A.status + 1, (int)i);
+        A.status[2] = p + 1;
+        return;
+      }
+      ghost_gradients(go, P, nrm, gn);
+      wall = P.wall != 0;
+      dtf = A.dt[o];
+    }
+    double ql[5], qr[5];
+    to_local_state(vo, F, ql);
+    to_local_state(vn, F, qr);
+    if (!cons_to_prim(ql, A.kc, in.wl) || !cons_to_prim(qr, A.kc, in.wr)) {
+      raise_dev(A.status, GKS_ERR_UNPHYSICAL, (int)i);
+      return;
+    }
+    local_slopes(go, F, in.sl);
+    local_slopes(gn, F, in.sr);
+  }
+  double fl[5], pv[5];
+  const int rc = interface_flux(in, -1.0, dtf, A.model, A.mu, A.kc, fl, A.want_point != 0, 0.0, pv, nullptr);
+  if (rc) {
+    raise_dev(A.status, GKS_ERR_UNPHYSICAL, (int)i);
+    return;
+  }
+  if (wall) fl[0] = 0.0;
+  const double ws = A.fq_ws[i];
+  double* out = A.contrib + i * 5;
+  out[0] = ws * fl[0];
+  out[4] = ws * fl[4];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) out[1 + d] = ws * (F[d] * fl[1] + F[3 + d] * fl[2] + F[6 + d] * fl[3]);
+  if (A.want_point) {
+    double* qp = A.qpt + i * 5;
+    qp[0] = pv[0];
+    qp[4] = pv[4];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) qp[1 + d] = F[d] * pv[1] + F[3 + d] * pv[2] + F[6 + d] * pv[3];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: deterministic cell assembly (stepping.py:225-228, hweno.py:172-194)
+// ---------------------------------------------------------------------------
+__global__ void k_assemble(int64_t nc, const int* __restrict__ cfq_start, const int* __restrict__ cfq,
+                           const double* __restrict__ contrib, const double* __restrict__ qpt,
+                           const int* __restrict__ fq_face, const double* __restrict__ fq_ws,
+                           const double* __restrict__ f_normal, const double* __restrict__ vol,
+                           double* __restrict__ res, double* __restrict__ grad_new, const int* gate) {
+  if (gate && !*gate) return;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  double r[5] = {0, 0, 0, 0, 0};
+  double g[3][5] = {};
+  const bool wantg = grad_new != nullptr;
+  for (int e = cfq_start[c]; e < cfq_start[c + 1]; ++e) {
+    const int64_t i = cfq[e] >> 1;
+    const bool is_nbr = cfq[e] & 1;
+    const double* cc = contrib + i * 5;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) r[k] = is_nbr ? r[k] + cc[k] : r[k] - cc[k];
+    if (wantg) {
+      const int f = fq_face[i];
+      const double ws = fq_ws[i];
+      const double* pv = qpt + i * 5;
+#pragma unroll
+      for (int x = 0; x < 3; ++x) {
+        const double wn = ws * f_normal[3 * f + x];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const double t = wn * pv[k];
+          g[x][k] = is_nbr ? g[x][k] - t : g[x][k] + t;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 5; ++k) res[c * 5 + k] = r[k];
+  if (wantg) {
+    const double V = vol[c];
+#pragma unroll
+    for (int x = 0; x < 3; ++x)
+#pragma unroll
+      for (int k = 0; k < 5; ++k) grad_new[(c * 3 + x) * 5 + k] = g[x][k] / V;
+  }
+}
+
+// ghost of the cell-average owner state per boundary face (stepping.py:242-249)
+__global__ void k_boundary_ghosts(int64_t nbf, const int* __restrict__ bfaces, const int* __restrict__ f_own,
+                                  const int* __restrict__ f_patch, const double* __restrict__ f_normal,
+                                  const DevPatch* __restrict__ patches, const double* __restrict__ q, KinConst kc,
+                                  double* __restrict__ ghosts, int* status) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nbf) return;
+  const int f = bfaces[b];
+  const int64_t o = f_own[f];
+  double qc[5], g[5];
+  for (int k = 0; k < 5; ++k) qc[k] = q[o * 5 + k];
+  const double n[3] = {f_normal[3 * f], f_normal[3 * f + 1], f_normal[3 * f + 2]};
+  if (!ghost_state(qc, patches[f_patch[f]], n, kc, g)) {
+    raise_dev(status, GKS_ERR_UNPHYSICAL, (int)o);
+    return;
+  }
+  for (int k = 0; k < 5; ++k) ghosts[b * 5 + k] = g[k];
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+void reset_status(Handle* H) {
+  const int st0[4] = {0, 0x7fffffff, 0, 0};
+  cudaMemcpyAsync(H->status, st0, sizeof(st0), cudaMemcpyHostToDevice, H->stream);
+}
+
+int check_status(Handle* H, const char* what) {
+  int st[4];
+  GKS_CUDA(cudaMemcpyAsync(st, H->status, sizeof(st), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaStreamSynchronize(H->stream));
+  if (st[0] == 0) return GKS_OK;
+  set_error_index(st[1]);
+  if (st[0] == GKS_ERR_UNPHYSICAL && st[2] > 0 && st[2] - 1 < (int)H->patch_names.size())
+    set_error("%s: unphysical reconstructed state at patch '%s' (point %d)", what,
+              H->patch_names[st[2] - 1].c_str(), st[1]);
+  else
+    set_error("%s: error %d at index %d", what, st[0], st[1]);
+  return st[0];
+}
+
+int local_dt_device(Handle* H) {
+  k_local_dt<<<blocks_for(H->nc, TPB), TPB, 0, H->stream>>>(H->nc, H->q, H->cdt_start, H->cdt, H->f_normal,
+                                                             H->f_area, H->vol, H->model == 1 && H->mu > 0.0,
+                                                             H->mu, H->cfl, H->kc, H->dt, H->status);
+  count_launch(1);
+  if (H->global_dt) {
+    k_min_broadcast<<<1, 1024, 0, H->stream>>>(H->nc, H->dt);
+    count_launch(1);
+  }
+  GKS_CUDA(cudaGetLastError());
+  return GKS_OK;
+}
+
+int residual_device(Handle* H, const double* q, double* res, bool with_gradients, const int* gate) {
+  const int64_t n5 = H->nc * 5;
+  if (H->compact) {
+    k_recon_hweno<<<blocks_for(n5, TPB), TPB, 0, H->stream>>>(
+        H->nc, q, H->grad, H->h, H->big_op, H->avg_gather, H->grad_gather, H->grad_scale, H->HA, H->HG,
+        H->sub_op, H->sub_gather, H->sub_active, H->HM, H->beta, H->linear_weights, H->eps, H->lw, H->coef, gate);
+  } else {
+    k_recon_weno<<<blocks_for(n5, TPB), TPB, 0, H->stream>>>(H->nc, q, H->big_op, H->big_gather, H->K,
+                                                              H->sub_op, H->sub_gather, H->sub_active, H->M, H->S,
+                                                              H->beta, H->linear_weights, H->eps, H->lw, H->coef,
+                                                              gate);
+  }
+  FaceArgs A;
+  A.nfq = H->nfq;
+  A.q = q; A.coef = H->coef; A.cen = H->cen; A.h = H->h; A.avg0 = H->avg0; A.dt = H->dt;
+  A.fq_face = H->fq_face; A.f_own = H->f_own; A.f_nbr = H->f_nbr; A.f_patch = H->f_patch;
+  A.fq_point = H->fq_point; A.fq_ws = H->fq_ws; A.f_frame = H->f_frame; A.f_normal = H->f_normal;
+  A.f_shift = H->f_shift; A.patches = H->patches; A.model = H->model; A.mu = H->mu; A.kc = H->kc;
+  A.want_point = with_gradients ? 1 : 0;
+  A.contrib = H->contrib; A.qpt = H->qpt; A.status = H->status; A.gate = gate;
+  k_face<<<blocks_for(H->nfq, 128), 128, 0, H->stream>>>(A);
+  k_assemble<<<blocks_for(H->nc, TPB), TPB, 0, H->stream>>>(H->nc, H->cfq_start, H->cfq, H->contrib, H->qpt,
+                                                             H->fq_face, H->fq_ws, H->f_normal, H->vol, res,
+                                                             with_gradients ? H->grad_new : nullptr, gate);
+  count_launch(3);
+  GKS_CUDA(cudaGetLastError());
+  return GKS_OK;
+}
+
+int boundary_ghosts_device(Handle* H, const double* q) {
+  if (H->nbf == 0) return GKS_OK;
+  k_boundary_ghosts<<<blocks_for(H->nbf, TPB), TPB, 0, H->stream>>>(H->nbf, H->boundary_faces, H->f_own,
+                                                                     H->f_patch, H->f_normal, H->patches, q,
+                                                                     H->kc, H->ghosts, H->status);
+  count_launch(1);
+  GKS_CUDA(cudaGetLastError());
+  return GKS_OK;
+}
+
+}  // namespace gks
