@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""Benchmark: cell-residual evals/s of the implicit HGKS step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c1] [--n 64] [--scheme weno_gmres] [--jacobian roe|frechet]
+
+A step is one backward-Euler step of Solver.advance (residual pipeline ->
+Roe Jacobian -> Jacobi-preconditioned GMRES(10) x 3 restarts -> update) on a
+synthetic mesh (BASELINE.json metric).  `value` counts
+ncells x residual-pipeline evaluations per step (1 in Roe-Jacobian mode,
+1 + #JVPs in Frechet mode) over the device-timed region with the state
+resident in HBM; `e2e` repeats the measurement through the public
+Solver.advance_inplace call with the field in pinned host memory (H2D + D2H
+every step).  `--impl reference` times the CPU oracle (numpy restatement of
+the reference) on a bounded sample of the same workload.
+
+Multi-GPU (torchrun): each rank currently runs an independent replica on
+its GPU (weak scaling, "replicas"); rank 0 prints the max-over-ranks line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+GAMMA = 1.4
+METRIC = "cell-residual evals/sec (1/2/4/8 B200); wall time to 1e-10 residual drop"
+UNIT = "cell-residual evals/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    p.add_argument("--workload", default="c1", choices=("c1",))
+    p.add_argument("--n", type=int, default=64, help="box divisions per axis (6 n^3 Kuhn tets)")
+    p.add_argument("--scheme", default="weno_gmres", choices=("weno_gmres", "hweno_gmres"))
+    p.add_argument("--jacobian", default="roe", choices=("roe", "frechet"))
+    p.add_argument("--cpu-n", type=int, default=10, help="bounded CPU sample size (box divisions)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+# -- workload ---------------------------------------------------------------------
+
+def c1_mesh(n, host_mesh_module):
+    """C1: periodic 6 n^3 Kuhn-tet box."""
+    return host_mesh_module.generate_box_mesh((1.0, 1.0, 1.0), (n, n, n), split="tet", periodic=("x", "y", "z"))
+
+
+def c1_field(mesh, compact):
+    """Smooth density wave advected by the flow: rho = 1 + 0.2 sin(2 pi x), U = 1."""
+    x = mesh.cell_centroid
+    tp = 2 * np.pi
+    rho = 1.0 + 0.2 * np.sin(tp * x[:, 0])
+    q = np.zeros((mesh.ncells, 5))
+    q[:, 0] = rho
+    q[:, 1] = rho
+    q[:, 4] = 1.0 / (GAMMA - 1.0) + 0.5 * rho
+    grad = None
+    if compact:
+        grad = np.zeros((mesh.ncells, 3, 5))
+        g = 0.2 * tp * np.cos(tp * x[:, 0])
+        grad[:, 0, 0] = g
+        grad[:, 0, 1] = g
+        grad[:, 0, 4] = 0.5 * g
+    return q, grad
+
+
+# -- clocks -------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) >= 7:
+                    self.rows.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# -- distributed plumbing ------------------------------------------------------------
+
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as td
+
+        torch.cuda.set_device(local)
+        td.init_process_group("nccl")
+        dist = td
+    return world, rank, local, dist
+
+
+def max_over_ranks(dist, value, local):
+    if dist is None:
+        return value
+    import torch
+
+    t = torch.tensor([value], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+# -- algorithmic traffic / flops per launch --------------------
+
+def kernel_model(solver, compact):
+    from paper_2304_09485_b200 import _native as N
+
+    lib = N.load()
+    info = [int(lib.gks_handle_info(solver._handle, k)) for k in range(9)]
+    nc, nf, nfq, nfi, nbf, nnz, K, M, S = info
+    per_row = nnz / nc
+    model = {
+        # bytes per launch (HBM-bound kernels), unique compulsory traffic
+        "spmv_dinv": nc * (4 + per_row * 204 + 200 + 200 + 40 + 80),
+        "jacobi_sweep": nc * (4 + per_row * 204 + 200 + 40 + 40 + 40),
+        "assemble": nfq * 40 + nc * (4 + 40) + (nfq * 2) * 4,
+        "recon": nc * ((9 * K * 8 + K * 4 + M * 3 * S * 8 + M * S * 4 + M + 648 + 40 + 360) if not compact else
+                       (9 * K * 8 + M * 21 * 8 + M * 8 + 648 + 40 + 120 + 360)),
+        "jac_faces": nfi * (8 + 2 * 40 + 32 + 2 * 200),
+        "jac_diag": nc * (4 + 40 + 8 + 8 + 400) + nnz * 200,
+    }
+    # FP64 flops per launch of the fused face kernel: reference-model count
+    # (build_interface 3,042 + evolve_flux 1,606 + face values ~720)
+    flops = {"face_flux": nfq * (4648 + 720 + (1239 if compact else 0))}
+    return model, flops, dict(nc=nc, nf=nf, nfq=nfq, nfi=nfi, nbf=nbf, nnz=nnz)
+
+
+# -- CPU baseline (oracle) -------------------------------------------------------------
+
+def cpu_baseline(args, steps, label):
+    from oracle.solver import OracleSolver
+    from paper_2304_09485_b200 import mesh as M
+
+    n = args.cpu_n
+    mesh = c1_mesh(n, M)
+    q, grad = c1_field(mesh, args.scheme.startswith("hweno"))
+    t0 = time.perf_counter()
+    s = OracleSolver(mesh, scheme=args.scheme, patches={}, jacobian=args.jacobian)
+    setup = time.perf_counter() - t0
+    q, grad, info = s.advance(q, grad)  # warm-up
+    evals = 0
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        q, grad, info = s.advance(q, grad)
+        evals += 1 + (info["matvecs"] - 1 if args.jacobian == "frechet" else 0)
+    el = time.perf_counter() - t0
+    return {"value": mesh.ncells * evals / el, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{label}: oracle OracleSolver.advance x{steps} on C1 n={n} ({mesh.ncells} cells), "
+                      f"{args.scheme}/{args.jacobian}, numpy single-thread; setup {setup:.1f}s not timed",
+            "seconds": el}
+
+
+def run_reference(args):
+    world, rank, local, dist = dist_init(args)
+    if rank != 0:
+        return 0
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+    steps = max(1, min(args.steps, 5))
+    cb = cpu_baseline(args, steps, "reference arm")
+    line = {
+        "metric": METRIC, "value": cb["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+        "steps": steps, "warmup": 1, "ms_per_step": cb["seconds"] * 1000.0 / steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C1 periodic Kuhn-tet box (bounded CPU sample n={args.cpu_n})",
+                   "scheme": args.scheme, "jacobian": args.jacobian},
+        "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# -- our arm ----------------------------------------------------------------------------
+
+def run_ours(args):
+    world, rank, local, dist = dist_init(args)
+    from paper_2304_09485_b200 import _native as N
+    from paper_2304_09485_b200 import mesh as M
+    from paper_2304_09485_b200.stepping import SolutionField, Solver, SolverOptions
+
+    lib = N.load()
+    compact = args.scheme.startswith("hweno")
+    t0 = time.perf_counter()
+    mesh = c1_mesh(args.n, M)
+    t_mesh = time.perf_counter() - t0
+    q0, g0 = c1_field(mesh, compact)
+    t0 = time.perf_counter()
+    solver = Solver(mesh, SolverOptions(scheme=args.scheme, patches={}, jacobian=args.jacobian, device=local))
+    t_setup = time.perf_counter() - t0
+    nc = mesh.ncells
+    import ctypes as C
+
+    v = C.c_double()
+    N.check(lib.gks_fp64_peak(C.byref(v)))
+    fp64 = v.value
+
+    # ---- device-resident timed region --------------------------------------------
+    solver.upload(SolutionField(q0, g0))
+    for _ in range(args.warmup):
+        solver.advance_resident()
+    prof = N.Profiler()
+    barrier(dist)
+    launches0 = N.kernel_launches()
+    evals = 0
+    with ClockSampler(local) as clk:
+        prof.start()
+        N.check(lib.gks_event_record(solver._handle, 0))
+        infos = []
+        for _ in range(args.steps):
+            infos.append(solver.advance_resident())
+        N.check(lib.gks_event_record(solver._handle, 1))
+        ms = C.c_double()
+        N.check(lib.gks_event_elapsed(solver._handle, 0, 1, C.byref(ms)))
+        kern = prof.stop()
+    launches = N.kernel_launches() - launches0
+    ms_total = max_over_ranks(dist, ms.value, local)
+    barrier(dist)
+    if args.jacobian == "frechet":
+        # one residual for L(Q) + one per Frechet JVP (the matvec count)
+        evals = sum(1 + i.matvecs for i in infos)
+    else:
+        evals = args.steps
+    value = world * nc * evals / (ms_total / 1000.0)
+
+    # ---- end-to-end through the public API (pinned host field) --------------------
+    fld = SolutionField(np.ascontiguousarray(q0.copy()), None if g0 is None else np.ascontiguousarray(g0.copy()))
+    N.check(lib.gks_host_pin(fld.q.ctypes.data_as(C.c_void_p), fld.q.nbytes))
+    if compact:
+        N.check(lib.gks_host_pin(fld.grad.ctypes.data_as(C.c_void_p), fld.grad.nbytes))
+    solver.advance_inplace(fld)
+    barrier(dist)
+    N.check(lib.gks_event_record(solver._handle, 2))
+    e2e_steps = args.steps
+    for _ in range(e2e_steps):
+        solver.advance_inplace(fld)
+    N.check(lib.gks_event_record(solver._handle, 3))
+    ms2 = C.c_double()
+    N.check(lib.gks_event_elapsed(solver._handle, 2, 3, C.byref(ms2)))
+    ms_e2e = max_over_ranks(dist, ms2.value, local)
+    e2e_evals = e2e_steps if args.jacobian == "roe" else int(round(e2e_steps * evals / args.steps))
+    bytes_h2d = fld.q.nbytes + (fld.grad.nbytes if compact else 0)
+    e2e = {"value": world * nc * e2e_evals / (ms_e2e / 1000.0), "unit": UNIT,
+           "h2d_bytes_per_step": bytes_h2d, "d2h_bytes_per_step": bytes_h2d,
+           "api": "Solver.advance_inplace (C ABI gks_advance), pinned numpy field"}
+
+    if rank != 0:
+        return 0
+
+    # ---- roofline of the dominant kernel ----------------------------------------------
+    model_bytes, model_flops, sizes = kernel_model(solver, compact)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    ranked = sorted(((t, name, n) for name, (t, n) in kern.items() if n), reverse=True)
+    kernels = {name: {"ms_total": round(t, 4), "launches": n, "ms_per_launch": round(t / n, 5),
+                      "share": round(t / max(sum(x for x, _, _ in ranked), 1e-9), 4)} for t, name, n in ranked}
+    roof = None
+    for t, name, n in ranked:
+        avg_s = t / n / 1000.0
+        if name in model_bytes:
+            ach = model_bytes[name] / avg_s / 1e9
+            roof = {"kernel": name, "bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                    "frac": round(ach / hbm_peak, 4), "traffic": None,
+                    "algorithmic_bytes_per_launch": model_bytes[name],
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
+            break
+        if name in model_flops:
+            ach = model_flops[name] / avg_s / 1e12
+            roof = {"kernel": name, "bound": "fp64", "achieved": round(ach, 3), "peak": round(fp64, 2),
+                    "unit": "TFLOP/s", "frac": round(ach / fp64, 4), "traffic": None,
+                    "algorithmic_flops_per_launch": model_flops[name],
+                    "peak_source": "live DFMA probe gks_fp64_peak (FP64 absent from MEASURED_PEAKS.json)"}
+            break
+    for name in kernels:
+        if name in model_bytes:
+            kernels[name]["GBps"] = round(model_bytes[name] / (kernels[name]["ms_per_launch"] / 1000) / 1e9, 1)
+        if name in model_flops:
+            kernels[name]["TFLOPs_fp64"] = round(model_flops[name] / (kernels[name]["ms_per_launch"] / 1000) / 1e12, 3)
+
+    cb = None
+    if not args.no_cpu_baseline:
+        try:
+            cb = cpu_baseline(args, 2, "cpu_baseline")
+        except Exception as exc:  # keep the GPU line even if the CPU leg fails
+            cb = {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C1 periodic 6*{args.n}^3 Kuhn-tet box, smooth density wave (configs[0] shape)",
+                   "cells": nc, "faces": sizes["nf"], "face_points": sizes["nfq"], "scheme": args.scheme,
+                   "jacobian": args.jacobian, "gmres": "m=10, restarts=3, jacobi_sweeps=2, rtol=0",
+                   "residual_evals_per_step": evals / args.steps,
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "inputs > L2 (operators %.1f GB)" % (sum(model_bytes[k] for k in ("recon",)) / 1e9),
+                   "setup_s": round(t_setup, 2), "mesh_s": round(t_mesh, 2)},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "roofline": roof,
+        "kernels": kernels,
+        "fp64_peak_tflops": round(fp64, 2),
+        "clocks": clk.summary(),
+        "cpu_baseline": cb,
+        "step_info": {"res_rho_l1": infos[-1].res_rho_l1, "res_l2": infos[-1].res_l2,
+                      "solver_cycles": infos[-1].solver_cycles},
+        "paper_gpu_derived": {"value": 1.60e5, "unit": UNIT, "note": "Quadro RTX 8000, cavity 48k tets (BASELINE.md)"},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

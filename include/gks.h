@@ -226,6 +226,22 @@ int gks_advance_resident(GksHandle* h, GksStepInfo* info);
 int gks_frechet_matvec(GksHandle* h, const double* q, const double* grad, const double* dt, const double* v,
                        double sigma, double* out);
 
+/* ------------------------------------------------------------------ */
+/* Measurement hooks (not reference APIs): CUDA events on the handle's   */
+/* stream, handle sizes, and the per-kernel-class profiler (events on    */
+/* the launching stream around every launch while enabled).              */
+/* ------------------------------------------------------------------ */
+int gks_event_record(GksHandle* h, int slot);                 /* slot 0..7 */
+int gks_event_elapsed(GksHandle* h, int a, int b, double* ms);
+int64_t gks_handle_info(const GksHandle* h, int what);        /* 0 nc 1 nf 2 nfq 3 nfi 4 nbf 5 nnz 6 K 7 M 8 S */
+int gks_fp64_peak(double* tflops);                          /* DFMA throughput probe */
+int gks_host_pin(void* p, int64_t nbytes);                  /* cudaHostRegister a host buffer */
+int gks_host_unpin(void* p);
+int gks_profile_enable(int on);
+int gks_profile_reset(void);
+int gks_profile_read(double* ms_out, int64_t* count_out, int ncls);  /* returns number of classes */
+const char* gks_profile_class_name(int k);
+
 /* measurement hook: kernel-only time of the fused flux on n random
    device-resident interfaces (not a reference API) */
 int gks_flux_bench(int64_t n, int reps, double gamma, double* ms_per_launch);

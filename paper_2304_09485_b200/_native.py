@@ -174,6 +174,16 @@ SIGNATURES = [
     ("gks_state_upload", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
     ("gks_state_download", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
     ("gks_advance_resident", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("gks_event_record", C.c_int, [C.c_void_p, C.c_int]),
+    ("gks_event_elapsed", C.c_int, [C.c_void_p, C.c_int, C.c_int, c_double_p]),
+    ("gks_handle_info", C.c_int64, [C.c_void_p, C.c_int]),
+    ("gks_fp64_peak", C.c_int, [c_double_p]),
+    ("gks_host_pin", C.c_int, [C.c_void_p, C.c_int64]),
+    ("gks_host_unpin", C.c_int, [C.c_void_p]),
+    ("gks_profile_enable", C.c_int, [C.c_int]),
+    ("gks_profile_reset", C.c_int, []),
+    ("gks_profile_read", C.c_int, [c_double_p, c_int64_p, C.c_int]),
+    ("gks_profile_class_name", C.c_char_p, [C.c_int]),
     ("gks_frechet_matvec", C.c_int, [C.c_void_p, c_double_p, c_double_p, c_double_p, c_double_p, C.c_double,
                                      c_double_p]),
 ]
@@ -236,3 +246,22 @@ def f64(a, shape=None):
 
 def kernel_launches():
     return int(load().gks_kernel_launches())
+
+
+class Profiler:
+    """Per-kernel-class device time (CUDA events on the launching stream)."""
+
+    def __init__(self):
+        self.lib = load()
+
+    def start(self):
+        check(self.lib.gks_profile_reset())
+        check(self.lib.gks_profile_enable(1))
+
+    def stop(self):
+        check(self.lib.gks_profile_enable(0))
+        n = 32
+        ms = np.zeros(n)
+        cnt = np.zeros(n, dtype=np.int64)
+        k = self.lib.gks_profile_read(dptr(ms), iptr(cnt), n)
+        return {self.lib.gks_profile_class_name(i).decode(): (float(ms[i]), int(cnt[i])) for i in range(k)}

@@ -453,16 +453,14 @@ static void frechet_apply(Handle* H, BlockSys* A, const double* v, double* out, 
   double* sig = &H->scal->sigma;
   if (!fixed_sigma) {
     dot2(&A->ws, H->stream, n, v, v, H->q, H->q, &H->scal->red[0], &H->scal->red[1], gate);
-    k_sigma<<<1, 1, 0, H->stream>>>(H->scal->red, sig, nullptr);
-    count_launch(1);
+    GKS_LAUNCH(KC_SCALAR, k_sigma, 1, 1, 0, H->stream, H->scal->red, sig, nullptr);
   } else {
     sig = const_cast<double*>(fixed_sigma);
   }
-  k_perturb<<<blocks_for(n, 256), 256, 0, H->stream>>>(n, H->q, v, sig, H->qtmp, gate);
+  GKS_LAUNCH(KC_VEC, k_perturb, blocks_for(n, 256), 256, 0, H->stream, n, H->q, v, sig, H->qtmp, gate);
   residual_device(H, H->qtmp, H->res2, false, gate);
-  k_frechet_combine<<<blocks_for(n, 256), 256, 0, H->stream>>>(H->nc, H->res2, H->res, sig, v, H->vol, H->dt, mode,
+  GKS_LAUNCH(KC_VEC, k_frechet_combine, blocks_for(n, 256), 256, 0, H->stream, H->nc, H->res2, H->res, sig, v, H->vol, H->dt, mode,
                                                                 out, gate);
-  count_launch(2);
 }
 
 static int advance_device(GksHandle* G, GksStepInfo* info) {
@@ -496,9 +494,8 @@ static int advance_device(GksHandle* G, GksStepInfo* info) {
       frechet_apply(H, A, v, out, 1, gate, nullptr);
     };
     TRY(gmres_device(A, H->res, H->dq, P, &gh, H->jac_mode == GKS_JAC_FRECHET ? &mf : nullptr));
-    k_update<<<blocks_for(H->nc, 256), 256, 0, H->stream>>>(H->nc, H->q, H->dq, H->q_new, H->bad);
-    k_stats<<<H->red_blocks, 256, 0, H->stream>>>(H->nc, H->res, H->dt, H->bad, H->partial, H->counter, H->scal);
-    count_launch(2);
+    GKS_LAUNCH(KC_UPDATE, k_update, blocks_for(H->nc, 256), 256, 0, H->stream, H->nc, H->q, H->dq, H->q_new, H->bad);
+    GKS_LAUNCH(KC_UPDATE, k_stats, H->red_blocks, 256, 0, H->stream, H->nc, H->res, H->dt, H->bad, H->partial, H->counter, H->scal);
     DevScalars sc;
     GKS_CUDA(cudaMemcpyAsync(&sc, H->scal, sizeof(sc), cudaMemcpyDeviceToHost, H->stream));
     GKS_CUDA(cudaStreamSynchronize(H->stream));
@@ -511,12 +508,12 @@ static int advance_device(GksHandle* G, GksStepInfo* info) {
       info->dt_min = sc.dt_min;
       info->solver_cycles = gh.ncycles;
       info->retried = retried;
+      if (g_prof_on) prof_harvest();
       return GKS_OK;
     }
     info->nbad = sc.nbad;
     if (attempt == 0) {
-      k_halve_dt<<<blocks_for(H->nc, 256), 256, 0, H->stream>>>(H->nc, H->bad, H->dt);
-      count_launch(1);
+      GKS_LAUNCH(KC_UPDATE, k_halve_dt, blocks_for(H->nc, 256), 256, 0, H->stream, H->nc, H->bad, H->dt);
       retried = 1;
     }
   }
@@ -696,6 +693,43 @@ int gks_gmres(GksBlockSystem* a, const double* b, double* x_out, int m, int rest
   cudaFree(db);
   cudaFree(dx);
   return rc;
+}
+
+int gks_event_record(GksHandle* G, int slot) {
+  Handle* H = &G->H;
+  if (slot < 0 || slot >= 8) return GKS_ERR_BAD_ARG;
+  if (!H->ev_ready) {
+    for (int k = 0; k < 8; ++k) GKS_CUDA(cudaEventCreate(&H->ev[k]));
+    H->ev_ready = 1;
+  }
+  GKS_CUDA(cudaEventRecord(H->ev[slot], H->stream));
+  return GKS_OK;
+}
+
+int gks_event_elapsed(GksHandle* G, int a, int b, double* ms) {
+  Handle* H = &G->H;
+  if (!H->ev_ready || a < 0 || b < 0 || a >= 8 || b >= 8) return GKS_ERR_BAD_ARG;
+  GKS_CUDA(cudaEventSynchronize(H->ev[b]));
+  float f = 0.f;
+  GKS_CUDA(cudaEventElapsedTime(&f, H->ev[a], H->ev[b]));
+  *ms = f;
+  return GKS_OK;
+}
+
+int64_t gks_handle_info(const GksHandle* G, int what) {
+  const Handle* H = &G->H;
+  switch (what) {
+    case 0: return H->nc;
+    case 1: return H->nf;
+    case 2: return H->nfq;
+    case 3: return H->nfi;
+    case 4: return H->nbf;
+    case 5: return H->nnz;
+    case 6: return H->compact ? H->HA + 3 * H->HG : H->K;   /* big-op width */
+    case 7: return H->compact ? H->HM : H->M;               /* sub-stencil slots */
+    case 8: return H->compact ? 7 : H->S;                   /* sub-stencil width */
+    default: return -1;
+  }
 }
 
 int gks_state_upload(GksHandle* G, const double* q, const double* grad) {

@@ -32,4 +32,24 @@ __device__ __forceinline__ void raise_dev(int* status, int code, int index) {
 
 inline int blocks_for(int64_t n, int threads) { return (int)((n + threads - 1) / threads); }
 
+// --- launch accounting and the optional per-kernel-class profiler ----------
+// Kernel classes reported by gks_profile_read (names in gks_flux.cu).
+enum KClass : int {
+  KC_DT = 0, KC_RECON, KC_FACE, KC_ASSEMBLE, KC_GHOST, KC_JAC_FACE, KC_JAC_DIAG, KC_SPMV, KC_JACOBI,
+  KC_REDUCE, KC_VEC, KC_SCALAR, KC_UPDATE, KC_FLUXBATCH, KC_COUNT
+};
+void count_launch(int n);
+extern bool g_prof_on;
+cudaEvent_t prof_begin(cudaStream_t s);
+void prof_end(int cls, cudaStream_t s, cudaEvent_t start);
+void prof_harvest();
+
+#define GKS_LAUNCH(cls, kern, grid, block, smem, stream, ...)              \
+  do {                                                                     \
+    cudaEvent_t _pa = ::gks::g_prof_on ? ::gks::prof_begin(stream) : nullptr; \
+    kern<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);              \
+    ::gks::count_launch(1);                                                \
+    if (_pa) ::gks::prof_end((cls), (stream), _pa);                        \
+  } while (0)
+
 }  // namespace gks

@@ -34,6 +34,60 @@ int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// ---------------------------------------------------------------------------
+// per-kernel-class profiler: CUDA events recorded on the launching stream
+// around each launch; harvested at the solver's synchronisation points.
+// ---------------------------------------------------------------------------
+bool g_prof_on = false;
+static std::mutex g_prof_mu;
+static std::vector<cudaEvent_t> g_prof_pool;
+struct ProfRec { int cls; cudaEvent_t a, b; };
+static std::vector<ProfRec> g_prof_pending;
+static double g_prof_ms[KC_COUNT];
+static int64_t g_prof_n[KC_COUNT];
+static const char* g_prof_names[KC_COUNT] = {"local_dt", "recon", "face_flux", "assemble", "ghosts",
+                                             "jac_faces", "jac_diag", "spmv_dinv", "jacobi_sweep",
+                                             "reduce_dot", "vector", "scalar", "update_stats", "flux_batch"};
+
+static cudaEvent_t prof_event() {
+  if (g_prof_pool.empty()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  cudaEvent_t e = g_prof_pool.back();
+  g_prof_pool.pop_back();
+  return e;
+}
+
+cudaEvent_t prof_begin(cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  cudaEvent_t e = prof_event();
+  cudaEventRecord(e, s);
+  return e;
+}
+
+void prof_end(int cls, cudaStream_t s, cudaEvent_t a) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  cudaEvent_t b = prof_event();
+  cudaEventRecord(b, s);
+  g_prof_pending.push_back({cls, a, b});
+}
+
+void prof_harvest() {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& r : g_prof_pending) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    g_prof_ms[r.cls] += ms;
+    g_prof_n[r.cls] += 1;
+    g_prof_pool.push_back(r.a);
+    g_prof_pool.push_back(r.b);
+  }
+  g_prof_pending.clear();
+}
+
 __global__ void __launch_bounds__(128) k_flux_batch(int64_t n, const double* __restrict__ wl,
                                                     const double* __restrict__ wr,
                                                     const double* __restrict__ sl,
@@ -76,6 +130,22 @@ __global__ void __launch_bounds__(128) k_flux_batch(int64_t n, const double* __r
   }
 }
 
+// FP64 DFMA throughput probe (roofline denominator; not in MEASURED_PEAKS.json)
+template <int CH>
+__global__ void k_dfma_probe(double* out, int iters, double a, double b) {
+  double x[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) x[c] = threadIdx.x * 1e-3 + c;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) x[c] = fma(x[c], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s += x[c];
+  if (s == 12345.678) out[0] = s;
+}
+
 }  // namespace gks
 
 using namespace gks;
@@ -83,6 +153,69 @@ using namespace gks;
 extern "C" {
 
 int gks_abi_version(void) { return GKS_ABI_VERSION; }
+
+int gks_fp64_peak(double* tflops) {
+  int dev = 0, sms = 148;
+  GKS_CUDA(cudaGetDevice(&dev));
+  GKS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  double* out;
+  GKS_CUDA(cudaMalloc(&out, 8));
+  const int threads = 256, iters = 4096, blocks = sms * 8;
+  k_dfma_probe<8><<<blocks, threads>>>(out, 64, 0.999999, 1e-7);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(e0);
+    k_dfma_probe<8><<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  count_launch(6);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  GKS_CUDA(cudaGetLastError());
+  *tflops = 2.0 * blocks * threads * (double)iters * 8 / (best * 1e-3) / 1e12;
+  return GKS_OK;
+}
+
+int gks_host_pin(void* p, int64_t nbytes) {
+  GKS_CUDA(cudaHostRegister(p, (size_t)nbytes, cudaHostRegisterDefault));
+  return GKS_OK;
+}
+
+int gks_host_unpin(void* p) {
+  GKS_CUDA(cudaHostUnregister(p));
+  return GKS_OK;
+}
+
+int gks_profile_enable(int on) {
+  prof_harvest();
+  g_prof_on = on != 0;
+  return GKS_OK;
+}
+
+int gks_profile_read(double* ms_out, int64_t* count_out, int ncls) {
+  prof_harvest();
+  for (int k = 0; k < ncls && k < KC_COUNT; ++k) {
+    if (ms_out) ms_out[k] = g_prof_ms[k];
+    if (count_out) count_out[k] = g_prof_n[k];
+  }
+  return KC_COUNT;
+}
+
+int gks_profile_reset(void) {
+  prof_harvest();
+  for (int k = 0; k < KC_COUNT; ++k) { g_prof_ms[k] = 0; g_prof_n[k] = 0; }
+  return GKS_OK;
+}
+
+const char* gks_profile_class_name(int k) { return (k >= 0 && k < KC_COUNT) ? g_prof_names[k] : ""; }
 const char* gks_last_error(void) { return g_err.c_str(); }
 int64_t gks_last_error_index(void) { return g_err_index; }
 int64_t gks_kernel_launches(void) { return g_launches.load(); }
@@ -131,10 +264,8 @@ int gks_flux_batch(int64_t n, const double* wl, const double* wr, const double* 
   if (point_out) GKS_CUDA(cudaMalloc(&d_p, s5));
   const int st0[4] = {0, 0x7fffffff, 0, 0};
   GKS_CUDA(cudaMemcpy(d_status, st0, sizeof(st0), cudaMemcpyHostToDevice));
-  k_flux_batch<<<blocks_for(n, 128), 128>>>(n, d_wl, d_wr, d_sl, d_sr, d_tau, d_dt,
-                                            point_out ? d_tp : nullptr, make_kin(gamma), d_f,
-                                            d_p, d_status);
-  count_launch(1);
+  GKS_LAUNCH(KC_FLUXBATCH, k_flux_batch, blocks_for(n, 128), 128, 0, 0, n, d_wl, d_wr, d_sl, d_sr, d_tau,
+             d_dt, point_out ? d_tp : nullptr, make_kin(gamma), d_f, d_p, d_status);
   GKS_CUDA(cudaGetLastError());
   int st[4];
   GKS_CUDA(cudaMemcpy(st, d_status, sizeof(st), cudaMemcpyDeviceToHost));

@@ -42,9 +42,10 @@ __device__ __forceinline__ double block_sum(double v, double* sm) {
   return sm[0];
 }
 
-// Finish a 2-value reduction: block partials -> out0/out1 by the last block.
-// Returns true in the thread that wrote the final values.
-__device__ __forceinline__ bool finish2(double s0, double s1, double* partial, unsigned int* counter,
+// Finish a 2-value reduction: block partials -> out0/out1 by the last block
+// to arrive.  The last block reduces the partials with a fixed thread
+// assignment and tree, so the result is independent of block scheduling.
+__device__ __forceinline__ void finish2(double s0, double s1, double* partial, unsigned int* counter,
                                         double* out0, double* out1, double* sm) {
   __shared__ bool last;
   double a = block_sum(s0, sm);
@@ -58,34 +59,52 @@ __device__ __forceinline__ bool finish2(double s0, double s1, double* partial, u
     last = (t == gridDim.x - 1);
   }
   __syncthreads();
-  if (!last) return false;
+  if (!last) return;
   __threadfence();
+  double x0 = 0.0, x1 = 0.0;
+  for (unsigned k = threadIdx.x; k < gridDim.x; k += blockDim.x) {
+    x0 += __ldcg(partial + 2 * k);
+    x1 += __ldcg(partial + 2 * k + 1);
+  }
+  __syncthreads();
+  x0 = block_sum(x0, sm);
+  __syncthreads();
+  x1 = block_sum(x1, sm);
   if (threadIdx.x == 0) {
-    double x0 = 0.0, x1 = 0.0;
-    for (unsigned k = 0; k < gridDim.x; ++k) {
-      x0 += ((volatile double*)partial)[2 * k];
-      x1 += ((volatile double*)partial)[2 * k + 1];
-    }
     if (out0) *out0 = x0;
     if (out1) *out1 = x1;
-    return true;
   }
-  return false;
 }
 
-// out0 = a.b, out1 = c.d   (c may be null)
+// out0 = a.b, out1 = c.d   (c may be null); 4-way unrolled streaming loop
 __global__ void __launch_bounds__(RB_THREADS) k_dot2(int64_t n, const double* __restrict__ a,
                                                      const double* __restrict__ b, const double* __restrict__ c,
                                                      const double* __restrict__ d, double* out0, double* out1,
                                                      double* partial, unsigned int* counter, const int* gate) {
   __shared__ double sm[RB_THREADS];
   if (gate && !*gate) return;
-  double s0 = 0.0, s1 = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    s0 += a[i] * b[i];
-    if (c) s1 += c[i] * d[i];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double s0 = 0.0, s1 = 0.0, t0 = 0.0, t1 = 0.0;
+  if (c) {
+    for (; i + stride < n; i += 2 * stride) {
+      s0 += a[i] * b[i];
+      t0 += a[i + stride] * b[i + stride];
+      s1 += c[i] * d[i];
+      t1 += c[i + stride] * d[i + stride];
+    }
+    if (i < n) {
+      s0 += a[i] * b[i];
+      s1 += c[i] * d[i];
+    }
+  } else {
+    for (; i + stride < n; i += 2 * stride) {
+      s0 += a[i] * b[i];
+      t0 += a[i + stride] * b[i + stride];
+    }
+    if (i < n) s0 += a[i] * b[i];
   }
-  finish2(s0, s1, partial, counter, out0, out1, sm);
+  finish2(s0 + t0, s1 + t1, partial, counter, out0, out1, sm);
 }
 
 // w -= (*coef) * v ; out = w . nxt  (nxt == nullptr: out = w . w)
@@ -96,13 +115,24 @@ __global__ void __launch_bounds__(RB_THREADS) k_axpy_dot(int64_t n, double* __re
   __shared__ double sm[RB_THREADS];
   if (gate && !*gate) return;
   const double h = *coef;
-  double s = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double wi = w[i] - h * v[i];
-    w[i] = wi;
-    s += wi * (nxt ? nxt[i] : wi);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double s = 0.0, t = 0.0;
+  const double* x = nxt ? nxt : w;
+  for (; i + stride < n; i += 2 * stride) {
+    const double w0 = w[i] - h * v[i];
+    const double w1 = w[i + stride] - h * v[i + stride];
+    w[i] = w0;
+    w[i + stride] = w1;
+    s += w0 * (nxt ? x[i] : w0);
+    t += w1 * (nxt ? x[i + stride] : w1);
   }
-  finish2(s, 0.0, partial, counter, out, nullptr, sm);
+  if (i < n) {
+    const double w0 = w[i] - h * v[i];
+    w[i] = w0;
+    s += w0 * (nxt ? x[i] : w0);
+  }
+  finish2(s + t, 0.0, partial, counter, out, nullptr, sm);
 }
 
 // out = in / *den
@@ -449,7 +479,7 @@ static int red_grid(int64_t n) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t want = (n + RB_THREADS - 1) / RB_THREADS;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 4));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
 }
 
 int blocksys_alloc(BlockSys* A, int64_t nc, int64_t nnz, cudaStream_t stream) {
@@ -505,62 +535,53 @@ static inline int cblocks(int64_t nc) { return (int)((nc + CELLS_PER_BLOCK - 1) 
 
 // y = A x  (diag + off)
 void bs_spmv(BlockSys* A, const double* x, double* y, const int* gate) {
-  k_block<1><<<cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream>>>(A->nc, A->rowptr, A->col, A->off, A->diag,
+  GKS_LAUNCH(KC_SPMV, k_block<1>, cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream, A->nc, A->rowptr, A->col, A->off, A->diag,
                                                                     A->dinv, x, nullptr, y, nullptr, gate);
-  count_launch(1);
 }
 
 // y = (L+U) x
 void bs_offdiag(BlockSys* A, const double* x, double* y, const int* gate) {
-  k_block<0><<<cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream>>>(A->nc, A->rowptr, A->col, A->off, A->diag,
+  GKS_LAUNCH(KC_SPMV, k_block<0>, cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream, A->nc, A->rowptr, A->col, A->off, A->diag,
                                                                     A->dinv, x, nullptr, y, nullptr, gate);
-  count_launch(1);
 }
 
 // z = P^-1 b : z0 = D^-1 b, then kmax sweeps z <- D^-1 (b - (L+U) z)  (krylov.py:24-34)
 // uses tmp as the ping-pong buffer; result in z
 void bs_jacobi(BlockSys* A, const double* b, double* z, double* tmp, int kmax, const int* gate) {
   const int64_t n5 = A->nc * 5;
-  k_dinv_apply<<<blocks_for(n5, 256), 256, 0, A->stream>>>(A->nc, A->dinv, b, z, gate);
-  count_launch(1);
+  GKS_LAUNCH(KC_VEC, k_dinv_apply, blocks_for(n5, 256), 256, 0, A->stream, A->nc, A->dinv, b, z, gate);
   double* cur = z;
   double* nxt = tmp;
   for (int k = 0; k < kmax; ++k) {
-    k_block<6><<<cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream>>>(A->nc, A->rowptr, A->col, A->off, A->diag,
+    GKS_LAUNCH(KC_JACOBI, k_block<6>, cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream, A->nc, A->rowptr, A->col, A->off, A->diag,
                                                                       A->dinv, cur, b, nxt, nullptr, gate);
-    count_launch(1);
     std::swap(cur, nxt);
   }
   if (cur != z) {
-    k_copy<<<red_grid(n5), RB_THREADS, 0, A->stream>>>(n5, z, cur);
-    count_launch(1);
+    GKS_LAUNCH(KC_VEC, k_copy, red_grid(n5), RB_THREADS, 0, A->stream, n5, z, cur);
   }
 }
 
 // w = P^-1 A v : fused spmv + first D^-1, then sweeps
 void bs_prec_matvec(BlockSys* A, const double* v, double* w, double* t, double* tmp, int kmax, const int* gate) {
-  k_block<5><<<cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream>>>(A->nc, A->rowptr, A->col, A->off, A->diag,
+  GKS_LAUNCH(KC_SPMV, k_block<5>, cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream, A->nc, A->rowptr, A->col, A->off, A->diag,
                                                                     A->dinv, v, nullptr, w, t, gate);
-  count_launch(1);
   double* cur = w;
   double* nxt = tmp;
   for (int k = 0; k < kmax; ++k) {
-    k_block<6><<<cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream>>>(A->nc, A->rowptr, A->col, A->off, A->diag,
+    GKS_LAUNCH(KC_JACOBI, k_block<6>, cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream, A->nc, A->rowptr, A->col, A->off, A->diag,
                                                                       A->dinv, cur, t, nxt, nullptr, gate);
-    count_launch(1);
     std::swap(cur, nxt);
   }
   if (cur != w) {
     const int64_t n5 = A->nc * 5;
-    k_copy<<<red_grid(n5), RB_THREADS, 0, A->stream>>>(n5, w, cur);
-    count_launch(1);
+    GKS_LAUNCH(KC_VEC, k_copy, red_grid(n5), RB_THREADS, 0, A->stream, n5, w, cur);
   }
 }
 
 void dot2(KrylovWS* W, cudaStream_t s, int64_t n, const double* a, const double* b, const double* c,
           const double* d, double* o0, double* o1, const int* gate) {
-  k_dot2<<<W->grid, RB_THREADS, 0, s>>>(n, a, b, c, d, o0, o1, W->partial, W->counter, gate);
-  count_launch(1);
+  GKS_LAUNCH(KC_REDUCE, k_dot2, W->grid, RB_THREADS, 0, s, n, a, b, c, d, o0, o1, W->partial, W->counter, gate);
 }
 
 // Restarted left-preconditioned GMRES (krylov.py:55-140) on device vectors;
@@ -603,17 +624,14 @@ int gmres_device(BlockSys* A, const double* b_dev, double* x_dev, const GmresPar
     else bs_spmv(A, v, dst, gate);
   };
   for (int cyc = 0; cyc < P.restarts; ++cyc) {
-    k_gm_cycle_begin<<<1, 1, 0, s>>>(g);
-    count_launch(1);
+    GKS_LAUNCH(KC_SCALAR, k_gm_cycle_begin, 1, 1, 0, s, g);
     // r = b - A x ; rh = P r ; beta = ||rh||
     Av(x_dev, W->t, notdone);
-    k_sub<<<grid, RB_THREADS, 0, s>>>(n, W->r, b_dev, W->t, notdone);
-    count_launch(1);
+    GKS_LAUNCH(KC_VEC, k_sub, grid, RB_THREADS, 0, s, n, W->r, b_dev, W->t, notdone);
     bs_jacobi(A, W->r, W->z, W->w, kmax, notdone);
     dot2(W, s, n, W->z, W->z, nullptr, nullptr, &g->beta2, nullptr, notdone);
-    k_gm_cycle_start<<<1, 1, 0, s>>>(g, cyc);
-    k_div<<<grid, RB_THREADS, 0, s>>>(n, W->V, W->z, &g->beta, act);
-    count_launch(2);
+    GKS_LAUNCH(KC_SCALAR, k_gm_cycle_start, 1, 1, 0, s, g, cyc);
+    GKS_LAUNCH(KC_VEC, k_div, grid, RB_THREADS, 0, s, n, W->V, W->z, &g->beta, act);
     for (int j = 0; j < m; ++j) {
       const double* vj = W->V + (int64_t)j * n;
       // w = P^-1 A v_j
@@ -628,28 +646,23 @@ int gmres_device(BlockSys* A, const double* b_dev, double* x_dev, const GmresPar
       for (int i = 0; i <= j; ++i) {
         const double* nxt = i < j ? W->V + (int64_t)(i + 1) * n : nullptr;
         double* dst = i < j ? &g->dots[i + 1] : &g->hnext2;
-        k_axpy_dot<<<W->grid, RB_THREADS, 0, s>>>(n, W->w, W->V + (int64_t)i * n, &g->dots[i], nxt, dst,
+        GKS_LAUNCH(KC_REDUCE, k_axpy_dot, W->grid, RB_THREADS, 0, s, n, W->w, W->V + (int64_t)i * n, &g->dots[i], nxt, dst,
                                                   W->partial, W->counter, act);
-        count_launch(1);
       }
-      k_gm_reorth_check<<<1, 1, 0, s>>>(g, j);
-      count_launch(1);
+      GKS_LAUNCH(KC_SCALAR, k_gm_reorth_check, 1, 1, 0, s, g, j);
       // conditional second pass (krylov.py:97-104)
       dot2(W, s, n, W->w, W->V, nullptr, nullptr, &g->corr[0], nullptr, rgate);
       for (int i = 0; i <= j; ++i) {
         const double* nxt = i < j ? W->V + (int64_t)(i + 1) * n : nullptr;
         double* dst = i < j ? &g->corr[i + 1] : &g->hnext2;
-        k_axpy_dot<<<W->grid, RB_THREADS, 0, s>>>(n, W->w, W->V + (int64_t)i * n, &g->corr[i], nxt, dst,
+        GKS_LAUNCH(KC_REDUCE, k_axpy_dot, W->grid, RB_THREADS, 0, s, n, W->w, W->V + (int64_t)i * n, &g->corr[i], nxt, dst,
                                                   W->partial, W->counter, rgate);
-        count_launch(1);
       }
-      k_gm_givens<<<1, 1, 0, s>>>(g, j, cyc);
-      k_div<<<grid, RB_THREADS, 0, s>>>(n, W->V + (int64_t)(j + 1) * n, W->w, &g->hdiv, act);
-      count_launch(2);
+      GKS_LAUNCH(KC_SCALAR, k_gm_givens, 1, 1, 0, s, g, j, cyc);
+      GKS_LAUNCH(KC_VEC, k_div, grid, RB_THREADS, 0, s, n, W->V + (int64_t)(j + 1) * n, W->w, &g->hdiv, act);
     }
-    k_gm_cycle_end<<<1, 1, 0, s>>>(g, cyc);
-    k_gm_update_x<<<grid, RB_THREADS, 0, s>>>(n, x_dev, W->V, g);
-    count_launch(2);
+    GKS_LAUNCH(KC_SCALAR, k_gm_cycle_end, 1, 1, 0, s, g, cyc);
+    GKS_LAUNCH(KC_VEC, k_gm_update_x, grid, RB_THREADS, 0, s, n, x_dev, W->V, g);
     if (P.check_ortho && out) {
       // Gram matrix of the cycle's basis (krylov.py:778-782), host-side check
       GmresDev gh;
@@ -699,14 +712,13 @@ int jacobian_assemble(Handle* H, BlockSys* A, const double* ghosts_dev) {
   const int st0[4] = {0, 0x7fffffff, 0, 0};
   GKS_CUDA(cudaMemcpyAsync(A->status, st0, sizeof(st0), cudaMemcpyHostToDevice, H->stream));
   if (H->nfi)
-    k_jac_faces<<<blocks_for(H->nfi, 128), 128, 0, H->stream>>>(H->nfi, H->interior_faces, H->f_own, H->f_nbr,
+    GKS_LAUNCH(KC_JAC_FACE, k_jac_faces, blocks_for(H->nfi, 128), 128, 0, H->stream, H->nfi, H->interior_faces, H->f_own, H->f_nbr,
                                                                  H->f_normal, H->f_area, H->q, H->face_slot,
                                                                  H->gamma, A->off);
-  k_jac_diag<<<blocks_for(H->nc, 128), 128, 0, H->stream>>>(H->nc, H->cjd_start, H->cjd, H->face_slot, A->off,
+  GKS_LAUNCH(KC_JAC_DIAG, k_jac_diag, blocks_for(H->nc, 128), 128, 0, H->stream, H->nc, H->cjd_start, H->cjd, H->face_slot, A->off,
                                                              H->f_own, H->f_normal, H->f_area, H->bidx, ghosts_dev,
                                                              H->q, H->vol, H->dt, H->gamma, A->diag, A->dinv,
                                                              A->status);
-  count_launch(2);
   GKS_CUDA(cudaGetLastError());
   int st[4];
   GKS_CUDA(cudaMemcpyAsync(st, A->status, sizeof(st), cudaMemcpyDeviceToHost, H->stream));
@@ -718,8 +730,7 @@ int jacobian_assemble(Handle* H, BlockSys* A, const double* ghosts_dev) {
 int blocksys_invert_diag(BlockSys* A) {
   const int st0[4] = {0, 0x7fffffff, 0, 0};
   GKS_CUDA(cudaMemcpyAsync(A->status, st0, sizeof(st0), cudaMemcpyHostToDevice, A->stream));
-  k_dinv_only<<<blocks_for(A->nc, 128), 128, 0, A->stream>>>(A->nc, A->diag, A->dinv, A->status);
-  count_launch(1);
+  GKS_LAUNCH(KC_JAC_DIAG, k_dinv_only, blocks_for(A->nc, 128), 128, 0, A->stream, A->nc, A->diag, A->dinv, A->status);
   int st[4];
   GKS_CUDA(cudaMemcpyAsync(st, A->status, sizeof(st), cudaMemcpyDeviceToHost, A->stream));
   GKS_CUDA(cudaStreamSynchronize(A->stream));
@@ -780,16 +791,32 @@ __global__ void __launch_bounds__(RB_THREADS) k_stats(int64_t nc, const double* 
     last = atomicInc(counter, gridDim.x - 1) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    double x0 = 0, x1 = 0, x2 = INFINITY, x3 = 0;
-    volatile double* p = partial;
-    for (unsigned k = 0; k < gridDim.x; ++k) {
-      x0 += p[4 * k]; x1 += p[4 * k + 1]; x2 = fmin(x2, p[4 * k + 2]); x3 += p[4 * k + 3];
-    }
+  if (!last) return;
+  __threadfence();
+  double x0 = 0, x1 = 0, x2 = INFINITY, x3 = 0;
+  for (unsigned k = threadIdx.x; k < gridDim.x; k += blockDim.x) {
+    x0 += __ldcg(partial + 4 * k);
+    x1 += __ldcg(partial + 4 * k + 1);
+    x2 = fmin(x2, __ldcg(partial + 4 * k + 2));
+    x3 += __ldcg(partial + 4 * k + 3);
+  }
+  __syncthreads();
+  x0 = block_sum(x0, sm);
+  __syncthreads();
+  x1 = block_sum(x1, sm);
+  __syncthreads();
+  x3 = block_sum(x3, sm);
+  __syncthreads();
+  sm[threadIdx.x] = x2;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sm[threadIdx.x] = fmin(sm[threadIdx.x], sm[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
     out->res_rho_l1 = x0 / (double)nc;
     out->res_l2 = sqrt(x1 / (double)(5 * nc));
-    out->dt_min = x2;
+    out->dt_min = sm[0];
     out->nbad = (int)x3;
   }
 }

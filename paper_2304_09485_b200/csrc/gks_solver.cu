@@ -470,13 +470,11 @@ int check_status(Handle* H, const char* what) {
 }
 
 int local_dt_device(Handle* H) {
-  k_local_dt<<<blocks_for(H->nc, TPB), TPB, 0, H->stream>>>(H->nc, H->q, H->cdt_start, H->cdt, H->f_normal,
+  GKS_LAUNCH(KC_DT, k_local_dt, blocks_for(H->nc, TPB), TPB, 0, H->stream, H->nc, H->q, H->cdt_start, H->cdt, H->f_normal,
                                                              H->f_area, H->vol, H->model == 1 && H->mu > 0.0,
                                                              H->mu, H->cfl, H->kc, H->dt, H->status);
-  count_launch(1);
   if (H->global_dt) {
-    k_min_broadcast<<<1, 1024, 0, H->stream>>>(H->nc, H->dt);
-    count_launch(1);
+    GKS_LAUNCH(KC_DT, k_min_broadcast, 1, 1024, 0, H->stream, H->nc, H->dt);
   }
   GKS_CUDA(cudaGetLastError());
   return GKS_OK;
@@ -485,11 +483,11 @@ int local_dt_device(Handle* H) {
 int residual_device(Handle* H, const double* q, double* res, bool with_gradients, const int* gate) {
   const int64_t n5 = H->nc * 5;
   if (H->compact) {
-    k_recon_hweno<<<blocks_for(n5, TPB), TPB, 0, H->stream>>>(
+    GKS_LAUNCH(KC_RECON, k_recon_hweno, blocks_for(n5, TPB), TPB, 0, H->stream, 
         H->nc, q, H->grad, H->h, H->big_op, H->avg_gather, H->grad_gather, H->grad_scale, H->HA, H->HG,
         H->sub_op, H->sub_gather, H->sub_active, H->HM, H->beta, H->linear_weights, H->eps, H->lw, H->coef, gate);
   } else {
-    k_recon_weno<<<blocks_for(n5, TPB), TPB, 0, H->stream>>>(H->nc, q, H->big_op, H->big_gather, H->K,
+    GKS_LAUNCH(KC_RECON, k_recon_weno, blocks_for(n5, TPB), TPB, 0, H->stream, H->nc, q, H->big_op, H->big_gather, H->K,
                                                               H->sub_op, H->sub_gather, H->sub_active, H->M, H->S,
                                                               H->beta, H->linear_weights, H->eps, H->lw, H->coef,
                                                               gate);
@@ -502,21 +500,19 @@ int residual_device(Handle* H, const double* q, double* res, bool with_gradients
   A.f_shift = H->f_shift; A.patches = H->patches; A.model = H->model; A.mu = H->mu; A.kc = H->kc;
   A.want_point = with_gradients ? 1 : 0;
   A.contrib = H->contrib; A.qpt = H->qpt; A.status = H->status; A.gate = gate;
-  k_face<<<blocks_for(H->nfq, 128), 128, 0, H->stream>>>(A);
-  k_assemble<<<blocks_for(H->nc, TPB), TPB, 0, H->stream>>>(H->nc, H->cfq_start, H->cfq, H->contrib, H->qpt,
+  GKS_LAUNCH(KC_FACE, k_face, blocks_for(H->nfq, 128), 128, 0, H->stream, A);
+  GKS_LAUNCH(KC_ASSEMBLE, k_assemble, blocks_for(H->nc, TPB), TPB, 0, H->stream, H->nc, H->cfq_start, H->cfq, H->contrib, H->qpt,
                                                              H->fq_face, H->fq_ws, H->f_normal, H->vol, res,
                                                              with_gradients ? H->grad_new : nullptr, gate);
-  count_launch(3);
   GKS_CUDA(cudaGetLastError());
   return GKS_OK;
 }
 
 int boundary_ghosts_device(Handle* H, const double* q) {
   if (H->nbf == 0) return GKS_OK;
-  k_boundary_ghosts<<<blocks_for(H->nbf, TPB), TPB, 0, H->stream>>>(H->nbf, H->boundary_faces, H->f_own,
+  GKS_LAUNCH(KC_GHOST, k_boundary_ghosts, blocks_for(H->nbf, TPB), TPB, 0, H->stream, H->nbf, H->boundary_faces, H->f_own,
                                                                      H->f_patch, H->f_normal, H->patches, q,
                                                                      H->kc, H->ghosts, H->status);
-  count_launch(1);
   GKS_CUDA(cudaGetLastError());
   return GKS_OK;
 }

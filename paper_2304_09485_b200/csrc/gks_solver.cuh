@@ -102,6 +102,7 @@ struct Handle {
   // timing / evidence
   int64_t launches = 0;
   cudaEvent_t ev[8];
+  int ev_ready = 0;
   std::vector<void*> allocs;
 };
 

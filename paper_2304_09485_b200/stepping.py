@@ -54,6 +54,7 @@ class StepInfo:
     dt_min: float
     solver_cycles: int = 0
     retried: bool = False
+    matvecs: int = 0  # B200 build: GMRES operator applications (Frechet mode: residual evals)
 
 
 @dataclass
@@ -282,9 +283,7 @@ class Solver:
             rc = N.load().gks_advance(self._handle, N.dptr(q), N.dptr(grad), C.byref(info))
             if rc:
                 self._raise(rc, "advance")
-            return SolutionField(q, grad if self.compact else None), StepInfo(
-                float(info.res_rho_l1), float(info.res_l2), float(info.dt_min), int(info.solver_cycles),
-                bool(info.retried))
+            return SolutionField(q, grad if self.compact else None), _info(info)
         # composed path (reference structure, stepping.py:270-296) with device calls
         dt = self.local_time_step(fld)
         retried = False
@@ -304,6 +303,24 @@ class Solver:
                 retried = True
         raise SteppingError(
             f"unphysical update persists after dt halving at cells {np.flatnonzero(bad)[:8].tolist()}")
+
+    def advance_inplace(self, fld: SolutionField) -> StepInfo:
+        """advance() writing the new state into fld.q / fld.grad (no host copies).
+
+        Lets callers keep the field in pinned host buffers (gks_host_pin) so the
+        per-step H2D/D2H copies run at full PCIe bandwidth.
+        """
+        nc = self.mesh.ncells
+        if fld.q.dtype != np.float64 or not fld.q.flags.c_contiguous or fld.q.shape != (nc, 5):
+            raise ValueError("advance_inplace needs a C-contiguous float64 (nc, 5) field")
+        if self.compact and (fld.grad is None or not fld.grad.flags.c_contiguous):
+            raise SteppingError("compact scheme needs a C-contiguous gradient field")
+        info = N.GksStepInfo()
+        rc = N.load().gks_advance(self._handle, N.dptr(fld.q), N.dptr(fld.grad) if self.compact else None,
+                                  C.byref(info))
+        if rc:
+            self._raise(rc, "advance")
+        return _info(info)
 
     def frechet_matvec(self, fld: SolutionField, v, dt_cells, sigma=None):
         """Directional residual derivative (L(Q + s v) - L(Q)) / s, gradients frozen."""
@@ -349,8 +366,12 @@ class Solver:
         rc = N.load().gks_advance_resident(self._handle, C.byref(info))
         if rc:
             self._raise(rc, "advance")
-        return StepInfo(float(info.res_rho_l1), float(info.res_l2), float(info.dt_min), int(info.solver_cycles),
-                        bool(info.retried))
+        return _info(info)
+
+
+def _info(ci):
+    return StepInfo(float(ci.res_rho_l1), float(ci.res_l2), float(ci.dt_min), int(ci.solver_cycles),
+                    bool(ci.retried), int(ci.matvecs))
 
 
 _JAC_HANDLES = {}
