@@ -13,7 +13,10 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libgks.so"
+import os
+
+# GKS_LIB overrides the library path (experiment variants built with build.py --out=)
+LIB_PATH = Path(os.environ.get("GKS_LIB", Path(__file__).resolve().parent / "libgks.so"))
 
 GKS_OK = 0
 GKS_ERR_BAD_ARG = 1

@@ -52,7 +52,17 @@ def sources():
     return cu, cpp
 
 
-def build(verbose=False, force=False, ptxas_verbose=False):
+def build(verbose=False, force=False, ptxas_verbose=False, defines=(), out=None):
+    """Compile libgks.so (out: alternative path for experiment variants)."""
+    global LIB, BUILD
+    if out is not None:
+        lib_saved, build_saved = LIB, BUILD
+        LIB = Path(out)
+        BUILD = LIB.parent / "obj"
+        try:
+            return build(verbose, True, ptxas_verbose, defines, None)
+        finally:
+            LIB, BUILD = lib_saved, build_saved
     cu, cpp = sources()
     deps = cu + cpp + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [INCLUDE / "gks.h", Path(__file__)]
     if LIB.exists() and not force:
@@ -65,7 +75,8 @@ def build(verbose=False, force=False, ptxas_verbose=False):
     for src in cu:
         obj = BUILD / (src.stem + ".o")
         extra = ["-Xptxas", "-v"] if ptxas_verbose else []
-        _run([nvcc, *ARCH, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)], verbose or ptxas_verbose)
+        dflags = [f"-D{d}" for d in defines]
+        _run([nvcc, *ARCH, *NVCC_FLAGS, *dflags, *extra, "-c", str(src), "-o", str(obj)], verbose or ptxas_verbose)
         objs.append(obj)
     for src in cpp:
         obj = BUILD / (src.stem + ".o")
@@ -79,5 +90,8 @@ def build(verbose=False, force=False, ptxas_verbose=False):
 
 
 if __name__ == "__main__":
-    build(verbose="--verbose" in sys.argv, force=True, ptxas_verbose="--ptxas" in sys.argv)
-    print(LIB)
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")]
+    lib = build(verbose="--verbose" in sys.argv, force=True, ptxas_verbose="--ptxas" in sys.argv, defines=defs,
+                out=outs[0] if outs else None)
+    print(lib)

@@ -8,6 +8,10 @@
 
 #include "../../include/gks.h"
 
+#ifndef GKS_FLUX_MINB
+#define GKS_FLUX_MINB 1  // min resident CTAs/SM for the FP64 flux kernels (register budget)
+#endif
+
 namespace gks {
 
 void set_error(const char* fmt, ...);

@@ -88,7 +88,7 @@ void prof_harvest() {
   g_prof_pending.clear();
 }
 
-__global__ void __launch_bounds__(128) k_flux_batch(int64_t n, const double* __restrict__ wl,
+__global__ void __launch_bounds__(128, GKS_FLUX_MINB) k_flux_batch(int64_t n, const double* __restrict__ wl,
                                                     const double* __restrict__ wr,
                                                     const double* __restrict__ sl,
                                                     const double* __restrict__ sr,
@@ -99,23 +99,21 @@ __global__ void __launch_bounds__(128) k_flux_batch(int64_t n, const double* __r
                                                     double* __restrict__ point, int* status) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  FluxIn in;
+  auto get = [&](int side, double w[5], double s5[3][5]) {
+    const double* W = side ? wr : wl;
+    const double* S = side ? sr : sl;
 #pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    in.wl[k] = wl[i * 5 + k];
-    in.wr[k] = wr[i * 5 + k];
-  }
+    for (int k = 0; k < 5; ++k) w[k] = W[i * 5 + k];
 #pragma unroll
-  for (int d = 0; d < 3; ++d)
+    for (int d = 0; d < 3; ++d)
 #pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      in.sl[d][k] = sl ? sl[i * 15 + d * 5 + k] : 0.0;
-      in.sr[d][k] = sr ? sr[i * 15 + d * 5 + k] : 0.0;
-    }
+      for (int k = 0; k < 5; ++k) s5[d][k] = S ? S[i * 15 + d * 5 + k] : 0.0;
+    return true;
+  };
   double f[5], p[5];
   const bool want_point = tp != nullptr;
-  const int rc = interface_flux(in, tau[i], dt[i], MODEL_INVISCID, 0.0, kc, f, want_point,
-                                want_point ? tp[i] : 0.0, p, nullptr);
+  const int rc = interface_flux_sides(get, tau[i], dt[i], MODEL_INVISCID, 0.0, kc, f, want_point,
+                                      want_point ? tp[i] : 0.0, p, nullptr);
   if (rc) {
     raise_dev(status, GKS_ERR_UNPHYSICAL, (int)i);
     return;

@@ -180,66 +180,79 @@ struct FluxIn {
 // optionally, the point value at time tp (p = 0).  tau < 0 means "compute
 // tau from the collision model" (flux.py:211-227, stepping.py:200-207).
 // Returns 0 on success, 1 if an intermediate state is unphysical.
-__device__ __forceinline__ int interface_flux(const FluxIn& in, double tau_in, double dt,
-                                              int model, double mu, const KinConst& kc,
-                                              double flux[5], bool want_point, double tp,
-                                              double point[5], double* tau_out) {
-  if (!prim_ok(in.wl) || !prim_ok(in.wr)) return 1;
-  double al[3][5], ar[3][5], Al[5], Ar[5];
-  double q0[5], dqa[3][5];
-  Maxw mlp, mrn;
-  {
+//
+// Register plan: the two transport sides run through ONE loop body (not
+// unrolled) and only leave behind the sums the reference's families need:
+//   q0   = sum_s rho_s <psi>_s                     (compatibility, flux.py:94)
+//   dqa  = sum_s rho_s <(a_s,k . psi) psi>_s        (equilibrium slopes, :99)
+//   F4/F5/F6 = transport base / slope / time families at u^1 (flux.py:127-146)
+//   P5/P6    = the same slope / time families at u^0 (point value)
+// so each Maxwellian's moment tables die as soon as its families are formed.
+template <class SideFn>
+__device__ __forceinline__ int interface_flux_sides(const SideFn& get_side, double tau_in, double dt,
+                                                    int model, double mu, const KinConst& kc,
+                                                    double flux[5], bool want_point, double tp,
+                                                    double point[5], double* tau_out) {
+  double q0[5] = {0, 0, 0, 0, 0};
+  double dqa[3][5] = {};
+  double F4[5] = {0, 0, 0, 0, 0}, F5[5] = {0, 0, 0, 0, 0}, F6[5] = {0, 0, 0, 0, 0};
+  double P5[5] = {0, 0, 0, 0, 0}, P6[5] = {0, 0, 0, 0, 0};
+  double pside0 = 0.0, pside1 = 0.0;
+#pragma unroll 1
+  for (int side = 0; side < 2; ++side) {
+    double w[5], sl[3][5];
+    if (!get_side(side, w, sl)) return 1;
+    if (!prim_ok(w)) return 1;
+    const double rho = w[0];
+    const double ps = rho / (2.0 * w[4]);
+    pside0 = side ? pside0 : ps;
+    pside1 = side ? ps : pside1;
+    double a[3][5], A[5];
     Maxw m;
-    maxw_full(m, in.wl, kc);
+    maxw_full(m, w, kc);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) micro_slope(in.wl, in.sl[k], kc, al[k]);
-    const double zero5[5] = {0, 0, 0, 0, 0};
-    double D[5];
-    wmom<0, true>(m, zero5, al, D);
-    double rhs[5];
+    for (int k = 0; k < 3; ++k) micro_slope(w, sl[k], kc, a[k]);
+    {
+      // time slope from the compatibility condition (kinetic.py:305-312)
+      const double zero5[5] = {0, 0, 0, 0, 0};
+      double D[5];
+      wmom<0, true>(m, zero5, a, D);
 #pragma unroll
-    for (int i = 0; i < 5; ++i) rhs[i] = -in.wl[0] * D[i];
-    micro_slope(in.wl, rhs, kc, Al);
-    mlp = m;
-    maxw_half_u(mlp, in.wl, 1.0);
+      for (int i = 0; i < 5; ++i) D[i] = -rho * D[i];
+      micro_slope(w, D, kc, A);
+    }
+    maxw_half_u(m, w, side ? -1.0 : 1.0);
     const double e0[5] = {1, 0, 0, 0, 0};
+    const double zero5[5] = {0, 0, 0, 0, 0};
     double t[5];
-    wmom<0, false>(mlp, e0, nullptr, t);
+    wmom<0, false>(m, e0, nullptr, t);
 #pragma unroll
-    for (int i = 0; i < 5; ++i) q0[i] = in.wl[0] * t[i];
+    for (int i = 0; i < 5; ++i) q0[i] += rho * t[i];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      wmom<0, false>(mlp, al[k], nullptr, t);
+      wmom<0, false>(m, a[k], nullptr, t);
 #pragma unroll
-      for (int i = 0; i < 5; ++i) dqa[k][i] = in.wl[0] * t[i];
+      for (int i = 0; i < 5; ++i) dqa[k][i] += rho * t[i];
+    }
+    wmom<1, false>(m, e0, nullptr, t);
+#pragma unroll
+    for (int i = 0; i < 5; ++i) F4[i] += rho * t[i];
+    wmom<1, true>(m, zero5, a, t);
+#pragma unroll
+    for (int i = 0; i < 5; ++i) F5[i] += rho * t[i];
+    wmom<1, false>(m, A, nullptr, t);
+#pragma unroll
+    for (int i = 0; i < 5; ++i) F6[i] += rho * t[i];
+    if (want_point) {
+      wmom<0, true>(m, zero5, a, t);
+#pragma unroll
+      for (int i = 0; i < 5; ++i) P5[i] += rho * t[i];
+      wmom<0, false>(m, A, nullptr, t);
+#pragma unroll
+      for (int i = 0; i < 5; ++i) P6[i] += rho * t[i];
     }
   }
-  {
-    Maxw m;
-    maxw_full(m, in.wr, kc);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) micro_slope(in.wr, in.sr[k], kc, ar[k]);
-    const double zero5[5] = {0, 0, 0, 0, 0};
-    double D[5];
-    wmom<0, true>(m, zero5, ar, D);
-    double rhs[5];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) rhs[i] = -in.wr[0] * D[i];
-    micro_slope(in.wr, rhs, kc, Ar);
-    mrn = m;
-    maxw_half_u(mrn, in.wr, -1.0);
-    const double e0[5] = {1, 0, 0, 0, 0};
-    double t[5];
-    wmom<0, false>(mrn, e0, nullptr, t);
-#pragma unroll
-    for (int i = 0; i < 5; ++i) q0[i] += in.wr[0] * t[i];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      wmom<0, false>(mrn, ar[k], nullptr, t);
-#pragma unroll
-      for (int i = 0; i < 5; ++i) dqa[k][i] += in.wr[0] * t[i];
-    }
-  }
+  double pside[2] = {pside0, pside1};
   double w0[5];
   if (!cons_to_prim(q0, kc, w0)) return 1;
   double ab[3][5], Ab[5];
@@ -249,17 +262,16 @@ __device__ __forceinline__ int interface_flux(const FluxIn& in, double tau_in, d
   for (int k = 0; k < 3; ++k) micro_slope(w0, dqa[k], kc, ab[k]);
   {
     const double zero5[5] = {0, 0, 0, 0, 0};
-    double D[5], rhs[5];
+    double D[5];
     wmom<0, true>(m0, zero5, ab, D);
 #pragma unroll
-    for (int i = 0; i < 5; ++i) rhs[i] = -w0[0] * D[i];
-    micro_slope(w0, rhs, kc, Ab);
+    for (int i = 0; i < 5; ++i) D[i] = -w0[0] * D[i];
+    micro_slope(w0, D, kc, Ab);
   }
   // collision time
   double tau = tau_in;
   if (tau < 0.0) {
-    const double pl = in.wl[0] / (2.0 * in.wl[4]);
-    const double pr = in.wr[0] / (2.0 * in.wr[4]);
+    const double pl = pside[0], pr = pside[1];
     const double jump = fabs(pl - pr) / (pl + pr) * dt;
     if (model == MODEL_VISCOUS) {
       const double p0 = w0[0] / (2.0 * w0[4]);
@@ -300,38 +312,17 @@ __device__ __forceinline__ int interface_flux(const FluxIn& in, double tau_in, d
       for (int i = 0; i < 5; ++i) d[k][i] = c2 * ab[k][i];
     wmom<1, true>(m0, s, d, o);
 #pragma unroll
-    for (int i = 0; i < 5; ++i) flux[i] = w0[0] * o[i];
-    const double rl = in.wl[0], rr = in.wr[0];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) s[i] = c6 * rl * Al[i];
-    s[0] += c4 * rl;
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-#pragma unroll
-      for (int i = 0; i < 5; ++i) d[k][i] = c5 * (rl * al[k][i]);
-    wmom<1, true>(mlp, s, d, o);
-#pragma unroll
-    for (int i = 0; i < 5; ++i) flux[i] += o[i];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) s[i] = c6 * rr * Ar[i];
-    s[0] += c4 * rr;
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-#pragma unroll
-      for (int i = 0; i < 5; ++i) d[k][i] = c5 * (rr * ar[k][i]);
-    wmom<1, true>(mrn, s, d, o);
-#pragma unroll
-    for (int i = 0; i < 5; ++i) flux[i] += o[i];
+    for (int i = 0; i < 5; ++i) flux[i] = w0[0] * o[i] + (c4 * F4[i] + c5 * F5[i] + c6 * F6[i]);
   }
   if (want_point) {
     // flux.py:182-188 at time tp
     const double e = exp(-tp / tau);
     const double g1 = 1.0 - e, g2 = (tp + tau) * e - tau, g3 = tp - tau + tau * e;
     const double f1 = e, f2 = -(tau + tp) * e, f3 = -tau * e;
-    double s[5], d[3][5], o[5];
 #pragma unroll
-    for (int i = 0; i < 5; ++i) point[i] = 0.0;
+    for (int i = 0; i < 5; ++i) point[i] = f1 * q0[i] + f2 * P5[i] + f3 * P6[i];
     if (g1 != 0.0 || g2 != 0.0 || g3 != 0.0) {
+      double s[5], d[3][5], o[5];
 #pragma unroll
       for (int i = 0; i < 5; ++i) s[i] = g3 * Ab[i];
       s[0] += g1;
@@ -341,31 +332,26 @@ __device__ __forceinline__ int interface_flux(const FluxIn& in, double tau_in, d
         for (int i = 0; i < 5; ++i) d[k][i] = g2 * ab[k][i];
       wmom<0, true>(m0, s, d, o);
 #pragma unroll
-      for (int i = 0; i < 5; ++i) point[i] = w0[0] * o[i];
+      for (int i = 0; i < 5; ++i) point[i] += w0[0] * o[i];
     }
-    const double rl = in.wl[0], rr = in.wr[0];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) s[i] = f3 * rl * Al[i];
-    s[0] += f1 * rl;
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-#pragma unroll
-      for (int i = 0; i < 5; ++i) d[k][i] = f2 * (rl * al[k][i]);
-    wmom<0, true>(mlp, s, d, o);
-#pragma unroll
-    for (int i = 0; i < 5; ++i) point[i] += o[i];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) s[i] = f3 * rr * Ar[i];
-    s[0] += f1 * rr;
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-#pragma unroll
-      for (int i = 0; i < 5; ++i) d[k][i] = f2 * (rr * ar[k][i]);
-    wmom<0, true>(mrn, s, d, o);
-#pragma unroll
-    for (int i = 0; i < 5; ++i) point[i] += o[i];
   }
   return 0;
+}
+
+// Convenience form on explicit left/right inputs.
+__device__ __forceinline__ int interface_flux(const FluxIn& in, double tau_in, double dt, int model, double mu,
+                                              const KinConst& kc, double flux[5], bool want_point, double tp,
+                                              double point[5], double* tau_out) {
+  auto get = [&](int side, double w[5], double sl[3][5]) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) w[i] = side ? in.wr[i] : in.wl[i];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int i = 0; i < 5; ++i) sl[k][i] = side ? in.sr[k][i] : in.sl[k][i];
+    return true;
+  };
+  return interface_flux_sides(get, tau_in, dt, model, mu, kc, flux, want_point, tp, point, tau_out);
 }
 
 }  // namespace gks

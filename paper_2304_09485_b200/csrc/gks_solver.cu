@@ -315,58 +315,65 @@ struct FaceArgs {
   const int* gate;
 };
 
-__global__ void __launch_bounds__(128) k_face(FaceArgs A) {
+__global__ void __launch_bounds__(128, GKS_FLUX_MINB) k_face(FaceArgs A) {
   if (A.gate && !*A.gate) return;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.nfq) return;
   const int f = A.fq_face[i];
   const int64_t o = A.f_own[f];
   const int64_t nb = A.f_nbr[f];
-  const double x[3] = {A.fq_point[3 * i], A.fq_point[3 * i + 1], A.fq_point[3 * i + 2]};
-  double F[9];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) F[k] = A.f_frame[9 * f + k];
-  FluxIn in;
-  bool wall = false;
-  double dtf;
-  {
-    double vo[5], go[3][5], vn[5], gn[3][5];
-    eval_side(A.q, A.coef, A.cen, A.h, A.avg0, o, x, vo, go);
-    if (nb >= 0) {
-      const double xs[3] = {x[0] - A.f_shift[3 * f], x[1] - A.f_shift[3 * f + 1], x[2] - A.f_shift[3 * f + 2]};
-      eval_side(A.q, A.coef, A.cen, A.h, A.avg0, nb, xs, vn, gn);
-      dtf = fmin(A.dt[o], A.dt[nb]);
+  const int p = nb >= 0 ? -1 : A.f_patch[f];
+  const bool wall = p >= 0 && A.patches[p].wall;
+  const double dtf = nb >= 0 ? fmin(A.dt[o], A.dt[nb]) : A.dt[o];
+  int ghost_fail = 0;
+  // side 0: owner reconstruction; side 1: neighbour (shifted chart) or ghost
+  auto get = [&](int side, double w[5], double sl[3][5]) {
+    const double x[3] = {A.fq_point[3 * i], A.fq_point[3 * i + 1], A.fq_point[3 * i + 2]};
+    double v[5], g[3][5];
+    if (side == 0 || nb < 0) {
+      eval_side(A.q, A.coef, A.cen, A.h, A.avg0, o, x, v, g);
     } else {
-      const int p = A.f_patch[f];
+      const double xs[3] = {x[0] - A.f_shift[3 * f], x[1] - A.f_shift[3 * f + 1], x[2] - A.f_shift[3 * f + 2]};
+      eval_side(A.q, A.coef, A.cen, A.h, A.avg0, nb, xs, v, g);
+    }
+    if (side == 1 && nb < 0) {
       const DevPatch P = A.patches[p];
       const double nrm[3] = {A.f_normal[3 * f], A.f_normal[3 * f + 1], A.f_normal[3 * f + 2]};
-      if (!ghost_state(vo, P, nrm, A.kc, vn)) {
-        atomicCAS(A.status, 0, GKS_ERR_UNPHYSICAL);
-        atomicMin(A.status + 1, (int)i);
-        A.status[2] = p + 1;
-        return;
+      double vg[5], gg[3][5];
+      if (!ghost_state(v, P, nrm, A.kc, vg)) {
+        ghost_fail = 1;
+        return false;
       }
-      ghost_gradients(go, P, nrm, gn);
-      wall = P.wall != 0;
-      dtf = A.dt[o];
+      ghost_gradients(g, P, nrm, gg);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        v[k] = vg[k];
+        g[0][k] = gg[0][k];
+        g[1][k] = gg[1][k];
+        g[2][k] = gg[2][k];
+      }
     }
-    double ql[5], qr[5];
-    to_local_state(vo, F, ql);
-    to_local_state(vn, F, qr);
-    if (!cons_to_prim(ql, A.kc, in.wl) || !cons_to_prim(qr, A.kc, in.wr)) {
-      raise_dev(A.status, GKS_ERR_UNPHYSICAL, (int)i);
-      return;
-    }
-    local_slopes(go, F, in.sl);
-    local_slopes(gn, F, in.sr);
-  }
+    const double* F = A.f_frame + 9 * f;
+    double ql[5];
+    to_local_state(v, F, ql);
+    if (!cons_to_prim(ql, A.kc, w)) return false;
+    local_slopes(g, F, sl);
+    return true;
+  };
   double fl[5], pv[5];
-  const int rc = interface_flux(in, -1.0, dtf, A.model, A.mu, A.kc, fl, A.want_point != 0, 0.0, pv, nullptr);
+  const int rc = interface_flux_sides(get, -1.0, dtf, A.model, A.mu, A.kc, fl, A.want_point != 0, 0.0, pv, nullptr);
   if (rc) {
-    raise_dev(A.status, GKS_ERR_UNPHYSICAL, (int)i);
+    if (ghost_fail) {
+      atomicCAS(A.status, 0, GKS_ERR_UNPHYSICAL);
+      atomicMin(A.status + 1, (int)i);
+      A.status[2] = p + 1;
+    } else {
+      raise_dev(A.status, GKS_ERR_UNPHYSICAL, (int)i);
+    }
     return;
   }
   if (wall) fl[0] = 0.0;
+  const double* F = A.f_frame + 9 * f;
   const double ws = A.fq_ws[i];
   double* out = A.contrib + i * 5;
   out[0] = ws * fl[0];

@@ -258,11 +258,13 @@ class Mesh:
             patch_names.append(name)
             if len(flist) == 0:
                 continue
-            widths = {len(f) for f in flist}
             pk = np.full((len(flist), 4), -1, dtype=np.int64)
-            for wdt in widths:
-                sel = [i for i, f in enumerate(flist) if len(f) == wdt]
-                pk[sel, :wdt] = np.sort(np.asarray([flist[i] for i in sel], dtype=np.int64), axis=1)
+            if isinstance(flist, np.ndarray) and flist.ndim == 2:
+                pk[:, : flist.shape[1]] = np.sort(flist.astype(np.int64), axis=1)
+            else:
+                for wdt in {len(f) for f in flist}:
+                    sel = [i for i, f in enumerate(flist) if len(f) == wdt]
+                    pk[sel, :wdt] = np.sort(np.asarray([flist[i] for i in sel], dtype=np.int64), axis=1)
             pv = _row_keys(pk)
             pos = np.searchsorted(face_key_sorted, pv)
             pos = np.minimum(pos, len(face_key_sorted) - 1)

@@ -1,0 +1,177 @@
+"""Synthetic unstructured tet meshes for the sphere / wing configurations.
+
+The reference cases (cases/sphere_*.ini, m6wing_transonic.ini) point at
+external .ugks meshes that do not exist offline.  These
+generators build the labelled synthetic stand-ins used by configs 2-5:
+
+* generate_sphere_mesh -- sphere of radius R in the box [-L, L]^3: Kuhn tets
+  on a sinh-stretched lattice (resolution concentrated at the body), cells
+  whose centroid lies inside the sphere removed, wall nodes projected
+  radially onto r = R wherever that keeps every adjacent tet positive.
+* generate_wing_mesh -- a swept, tapered, symmetric-section wing carved the
+  same way (the ONERA M6 geometry is not available offline).
+
+Cells come out in lattice order (good locality for the device gathers).
+Patch names follow the reference case files: "sphere"/"wing" for the body,
+"farfield" or "inlet"/"outlet" for the box sides.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .mesh import Mesh, MeshError
+
+_KUHN = np.array(((0, 1, 2, 6), (0, 2, 3, 6), (0, 3, 7, 6), (0, 7, 4, 6), (0, 4, 5, 6), (0, 5, 1, 6)))
+_TFACES = np.array(((0, 2, 1), (0, 1, 3), (1, 2, 3), (0, 3, 2)))
+
+
+def stretched_axis(n, half, beta):
+    """n cells on [-half, half] with spacing growing away from 0 (x = half sinh(b s)/sinh(b))."""
+    s = np.linspace(-1.0, 1.0, n + 1)
+    if beta <= 0:
+        return half * s
+    x = half * np.sinh(beta * s) / np.sinh(beta)
+    x[0], x[-1] = -half, half
+    if n % 2 == 0:
+        x[n // 2] = 0.0
+    return x
+
+
+def _beta_for(n, half, h0):
+    """Smallest stretching whose centre spacing is <= h0 (capped at 8)."""
+    for b in np.linspace(0.05, 8.0, 800):
+        if half * b / np.sinh(b) * 2.0 / n <= h0:
+            return float(b)
+    return 8.0
+
+
+def _lattice(xs, ys, zs):
+    nx, ny, nz = len(xs) - 1, len(ys) - 1, len(zs) - 1
+    X, Y, Z = np.meshgrid(xs, ys, zs, indexing="ij")
+    nodes = np.stack([X, Y, Z], axis=-1).reshape(-1, 3)
+
+    def nid(i, j, k):
+        return (i * (ny + 1) + j) * (nz + 1) + k
+
+    i, j, k = (a.ravel() for a in np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij"))
+    hexes = np.stack([nid(i, j, k), nid(i + 1, j, k), nid(i + 1, j + 1, k), nid(i, j + 1, k),
+                      nid(i, j, k + 1), nid(i + 1, j, k + 1), nid(i + 1, j + 1, k + 1), nid(i, j + 1, k + 1)], 1)
+    return nodes, hexes[:, _KUHN].reshape(-1, 4)
+
+
+def _carve(nodes, tets, inside, bounds, side_names):
+    """Drop tets whose centroid is inside; classify the boundary faces of the rest."""
+    cen = nodes[tets].mean(axis=1)
+    keep = ~inside(cen)
+    if not keep.any():
+        raise MeshError("body removes every cell")
+    tets = tets[keep]
+    faces = tets[:, _TFACES].reshape(-1, 3)
+    key = np.sort(faces, axis=1)
+    kv = np.ascontiguousarray(key).view(np.dtype((np.void, 24))).ravel()
+    _, inv, cnt = np.unique(kv, return_inverse=True, return_counts=True)
+    bnd = faces[cnt[inv] == 1]
+    p = nodes[bnd]
+    lo, hi = bounds
+    names = np.full(len(bnd), "", dtype=object)
+    tol = 1e-9 * max(np.max(np.abs(lo)), np.max(np.abs(hi)), 1.0)
+    for ax in range(3):
+        names[np.all(np.abs(p[:, :, ax] - lo[ax]) < tol, axis=1)] = side_names[2 * ax]
+        names[np.all(np.abs(p[:, :, ax] - hi[ax]) < tol, axis=1)] = side_names[2 * ax + 1]
+    return tets, bnd, names
+
+
+def _compact(nodes, tets, faces_by_patch):
+    used = np.unique(tets)
+    remap = -np.ones(len(nodes), dtype=np.int64)
+    remap[used] = np.arange(len(used))
+    return nodes[used], remap[tets], {k: remap[v] for k, v in faces_by_patch.items()}
+
+
+def _tet_volumes(nodes, tets):
+    p = nodes[tets]
+    return np.einsum("ij,ij->i", np.cross(p[:, 1] - p[:, 0], p[:, 2] - p[:, 0]), p[:, 3] - p[:, 0]) / 6.0
+
+
+def _project(nodes, tets, body_nodes, target, min_frac=0.05):
+    """Move body nodes to target positions unless that degrades an adjacent tet."""
+    v0 = _tet_volumes(nodes, tets)
+    moved = nodes.copy()
+    moved[body_nodes] = target
+    active = np.zeros(len(nodes), dtype=bool)
+    active[body_nodes] = True
+    for _ in range(20):
+        v = _tet_volumes(moved, tets)
+        bad = v < min_frac * v0
+        if not bad.any():
+            break
+        revert = np.unique(tets[bad])
+        revert = revert[active[revert]]
+        if not len(revert):
+            break
+        moved[revert] = nodes[revert]
+        active[revert] = False
+    return moved
+
+
+def generate_sphere_mesh(n, radius=0.5, half=10.0, beta=None, boundary="farfield", project=True):
+    """Synthetic tet sphere-in-box (configs 2, 3, 5).
+
+    n: lattice cells per axis (about 6 n^3 tets minus the body);
+    boundary: "farfield" (all sides farfield_riemann, patch "farfield") or
+    "supersonic" (x-min and lateral sides "inlet", x-max "outlet").
+    """
+    if beta is None:
+        beta = _beta_for(n, half, radius / 10.0)  # ~10 lattice cells across the radius
+    ax = stretched_axis(n, half, beta)
+    nodes, tets = _lattice(ax, ax, ax)
+    lo, hi = np.full(3, -half), np.full(3, half)
+    sides = ("xmin", "xmax", "ymin", "ymax", "zmin", "zmax")
+    tets, bnd, names = _carve(nodes, tets, lambda c: np.einsum("ij,ij->i", c, c) < radius * radius,
+                              (lo, hi), sides)
+    body = bnd[names == ""]
+    if project:
+        bn = np.unique(body)
+        r = np.linalg.norm(nodes[bn], axis=1)
+        nodes = _project(nodes, tets, bn, nodes[bn] * (radius / r)[:, None])
+    if boundary == "farfield":
+        patches = {"sphere": body, "farfield": bnd[names != ""]}
+    elif boundary == "supersonic":
+        patches = {"sphere": body, "inlet": bnd[(names != "") & (names != "xmax")], "outlet": bnd[names == "xmax"]}
+    else:
+        raise MeshError(f"unknown boundary layout {boundary!r}")
+    nodes, tets, patches = _compact(nodes, tets, patches)
+    return Mesh.build(nodes, tets, (), patches)
+
+
+def generate_wing_mesh(n, span=1.5, root_chord=0.8, taper=0.56, sweep_deg=30.0, thickness=0.10,
+                       half=8.0, beta=None):
+    """Swept, tapered wing (symmetric 4-digit thickness law) stand-in for config 4.
+
+    The wing root sits on the y = 0 plane inside the box; the body is carved
+    stair-step (no projection).  Patches: "wing", "farfield".
+    """
+    if beta is None:
+        beta = _beta_for(n, half, 0.25 * thickness * root_chord)
+    ax = stretched_axis(n, half, beta)
+    nodes, tets = _lattice(ax, ax, ax)
+    tan_s = np.tan(np.radians(sweep_deg))
+
+    def inside(c):
+        x, y, z = c[:, 0] + 0.3, np.abs(c[:, 1]), c[:, 2]
+        chord = root_chord * (1.0 - (1.0 - taper) * np.clip(y / span, 0.0, 1.0))
+        xl = y * tan_s
+        t = (x - xl) / chord
+        ok = (y <= span) & (t >= 0.0) & (t <= 1.0)
+        tc = np.clip(t, 0.0, 1.0)
+        yt = 5.0 * thickness * chord * (0.2969 * np.sqrt(tc) - 0.1260 * tc - 0.3516 * tc ** 2 + 0.2843 * tc ** 3
+                                         - 0.1015 * tc ** 4)
+        return ok & (np.abs(z) <= yt)
+
+    lo, hi = np.full(3, -half), np.full(3, half)
+    sides = ("xmin", "xmax", "ymin", "ymax", "zmin", "zmax")
+    tets, bnd, names = _carve(nodes, tets, inside, (lo, hi), sides)
+    patches = {"wing": bnd[names == ""], "farfield": bnd[names != ""]}
+    nodes, tets, patches = _compact(nodes, tets, patches)
+    return Mesh.build(nodes, tets, (), patches)
