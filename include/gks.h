@@ -152,6 +152,35 @@ int gks_create(const GksMeshDesc* mesh, const GksSetup* setup, const GksOptions*
                GksHandle** out);
 void gks_destroy(GksHandle* h);
 
+/* ------------------------------------------------------------------ */
+/* Domain decomposition (multi-GPU; no reference counterpart) */
+/* A local handle holds cells [owned | ghost layer 1 | deeper layers];   */
+/* owned + layer-1 ghosts are reconstructed, owned rows are assembled /   */
+/* solved.  Halo maps list, per peer rank, the local ids to send and the  */
+/* local ids to receive into (q: all ghost layers, x: layer 1).          */
+/* ------------------------------------------------------------------ */
+typedef struct GksHaloDesc {
+  int npeers;
+  const int* peers;              /* (npeers) */
+  const int64_t* send_offsets;   /* (npeers+1) into send_ids */
+  const int64_t* send_ids;
+  const int64_t* recv_offsets;   /* (npeers+1) into recv_ids */
+  const int64_t* recv_ids;
+} GksHaloDesc;
+
+typedef struct GksDomainDesc {
+  int64_t n_owned, n_recon, nc_global;
+  GksHaloDesc q, x;
+} GksDomainDesc;
+
+int gks_create_local(const GksMeshDesc* mesh, const GksSetup* setup, const GksOptions* opt,
+                     const GksDomainDesc* domain, int device, GksHandle** out);
+/* restrict a global setup to local cells (local->global ids; global->local map, -1 = absent) */
+int gks_setup_subset(const GksSetup* global, const int64_t* cells, int64_t n_local, const int64_t* g2l,
+                     int64_t n_global, GksSetup** out);
+int gks_comm_unique_id(void* out, int64_t nbytes);           /* ncclGetUniqueId (128 bytes) */
+int gks_comm_init(GksHandle* h, const void* unique_id, int nranks, int rank);
+
 /* Solver.local_time_step (stepping.py:135-157): q (nc,5) -> dt (nc) */
 int gks_local_dt(GksHandle* h, const double* q, double* dt_out);
 

@@ -129,6 +129,16 @@ class GksStepInfo(C.Structure):
                 ("first_bad", C.c_int64 * 8)]
 
 
+class GksHaloDesc(C.Structure):
+    _fields_ = [("npeers", C.c_int), ("peers", C.c_void_p), ("send_offsets", C.c_void_p),
+                ("send_ids", C.c_void_p), ("recv_offsets", C.c_void_p), ("recv_ids", C.c_void_p)]
+
+
+class GksDomainDesc(C.Structure):
+    _fields_ = [("n_owned", C.c_int64), ("n_recon", C.c_int64), ("nc_global", C.c_int64),
+                ("q", GksHaloDesc), ("x", GksHaloDesc)]
+
+
 class GksError(RuntimeError):
     def __init__(self, code, message, index=-1):
         super().__init__(message)
@@ -153,6 +163,12 @@ SIGNATURES = [
                                   C.POINTER(C.c_int64)]),
     ("gks_setup_copy", C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int64]),
     ("gks_create", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
+    ("gks_create_local", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                   C.POINTER(C.c_void_p)]),
+    ("gks_setup_subset", C.c_int, [C.c_void_p, c_int64_p, C.c_int64, c_int64_p, C.c_int64,
+                                   C.POINTER(C.c_void_p)]),
+    ("gks_comm_unique_id", C.c_int, [C.c_void_p, C.c_int64]),
+    ("gks_comm_init", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
     ("gks_destroy", None, [C.c_void_p]),
     ("gks_local_dt", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
     ("gks_residual", C.c_int, [C.c_void_p, c_double_p, c_double_p, c_double_p, C.c_int, c_double_p,

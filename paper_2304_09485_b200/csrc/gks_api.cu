@@ -73,7 +73,20 @@ static std::vector<int> to_i32(const int64_t* p, size_t n) {
     if (_rc) return _rc;       \
   } while (0)
 
-int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const GksOptions* o, int device) {
+static int upload_halo(Handle* H, HaloMap& X, const GksHaloDesc& d) {
+  X.peers.assign(d.peers, d.peers + d.npeers);
+  X.soff.assign(d.send_offsets, d.send_offsets + d.npeers + 1);
+  X.roff.assign(d.recv_offsets, d.recv_offsets + d.npeers + 1);
+  X.ns = X.soff.back();
+  X.nr = X.roff.back();
+  auto si = to_i32(d.send_ids, X.ns), ri = to_i32(d.recv_ids, X.nr);
+  TRY(upload(H, &X.sids, si.data(), si.size()));
+  TRY(upload(H, &X.rids, ri.data(), ri.size()));
+  return GKS_OK;
+}
+
+int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const GksOptions* o, int device,
+                  const GksDomainDesc* dom) {
   Handle* H = &G->H;
   H->device = device;
   GKS_CUDA(cudaSetDevice(device));
@@ -84,6 +97,14 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
     return GKS_ERR_BAD_ARG;
   }
   H->nc = nc; H->nf = nf; H->nfq = nfq;
+  H->n_owned = dom ? dom->n_owned : nc;
+  H->n_recon = dom ? dom->n_recon : nc;
+  H->nc_global = dom ? dom->nc_global : nc;
+  if (H->n_owned < 1 || H->n_owned > H->n_recon || H->n_recon > nc) {
+    set_error("bad domain sizes (owned %lld, recon %lld, local %lld)", (long long)H->n_owned,
+              (long long)H->n_recon, (long long)nc);
+    return GKS_ERR_BAD_ARG;
+  }
   H->scheme = o->scheme;
   H->compact = o->scheme == GKS_SCHEME_HWENO_GMRES;
   H->model = o->model;
@@ -222,14 +243,18 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
       erow[2 * k] = m->face_owner[f]; ecol[2 * k] = m->face_neighbor[f];
       erow[2 * k + 1] = m->face_neighbor[f]; ecol[2 * k + 1] = m->face_owner[f];
     }
-    std::vector<int64_t> order(nnz);
-    std::iota(order.begin(), order.end(), 0);
+    std::vector<int64_t> order;
+    order.reserve(nnz);
+    for (int64_t e = 0; e < nnz; ++e)
+      if (erow[e] < H->n_owned) order.push_back(e);  // rows of ghost cells live on their owner rank
     std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
       if (erow[a] != erow[b]) return erow[a] < erow[b];
       return ecol[a] < ecol[b];
     });
-    std::vector<int> rowptr(nc + 1, 0), col(nnz), fslot(2 * nf, -1);
-    for (int64_t p = 0; p < nnz; ++p) {
+    const int64_t nkept = order.size();
+    H->nnz = nkept;
+    std::vector<int> rowptr(H->n_owned + 1, 0), col(nkept), fslot(2 * nf, -1);
+    for (int64_t p = 0; p < nkept; ++p) {
       const int64_t e = order[p];
       col[p] = (int)ecol[e];
       rowptr[erow[e] + 1]++;
@@ -241,9 +266,10 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
     TRY(upload(H, &H->face_slot, fslot.data(), fslot.size()));
     TRY(upload(H, &H->bidx, bidx.data(), bidx.size()));
     BlockSys* A = &G->jac.sys;
-    TRY(blocksys_alloc(A, nc, nnz, H->stream));
-    GKS_CUDA(cudaMemcpy(A->rowptr, rowptr.data(), (nc + 1) * sizeof(int), cudaMemcpyHostToDevice));
-    if (nnz) GKS_CUDA(cudaMemcpy(A->col, col.data(), nnz * sizeof(int), cudaMemcpyHostToDevice));
+    TRY(blocksys_alloc(A, H->n_owned, nkept, H->stream));
+    A->n_ext = H->n_recon;
+    GKS_CUDA(cudaMemcpy(A->rowptr, rowptr.data(), (H->n_owned + 1) * sizeof(int), cudaMemcpyHostToDevice));
+    if (nkept) GKS_CUDA(cudaMemcpy(A->col, col.data(), nkept * sizeof(int), cudaMemcpyHostToDevice));
     G->jac.owned = false;
   }
 
@@ -312,12 +338,20 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   TRY(alloc(H, &H->counter, 1));
   GKS_CUDA(cudaMemset(H->counter, 0, sizeof(unsigned int)));
   GKS_CUDA(cudaMemset(H->grad, 0, nc * 15 * sizeof(double)));
+  if (dom) {
+    TRY(upload_halo(H, H->hq, dom->q));
+    TRY(upload_halo(H, H->hx, dom->x));
+    const int64_t mx = std::max(std::max(H->hq.ns, H->hq.nr), std::max(H->hx.ns, H->hx.nr));
+    TRY(alloc(H, &H->hsend, std::max<int64_t>(mx, 1) * 15));
+    TRY(alloc(H, &H->hrecv, std::max<int64_t>(mx, 1) * 15));
+  }
   return GKS_OK;
 }
 
 void destroy_handle(GksHandle* G) {
   Handle* H = &G->H;
   cudaSetDevice(H->device);
+  comm_destroy(H);
   if (H->stream) cudaStreamSynchronize(H->stream);
   for (void* p : H->allocs) cudaFree(p);
   blocksys_free(&G->jac.sys);
@@ -358,7 +392,7 @@ int gks_create(const GksMeshDesc* mesh, const GksSetup* setup, const GksOptions*
     setup = own;
   }
   GksHandle* G = new GksHandle();
-  int rc = create_handle(G, mesh, setup, opt, device);
+  int rc = create_handle(G, mesh, setup, opt, device, nullptr);
   if (own) gks_setup_free(own);
   if (rc) {
     destroy_handle(G);
@@ -366,6 +400,37 @@ int gks_create(const GksMeshDesc* mesh, const GksSetup* setup, const GksOptions*
     return rc;
   }
   *out = G;
+  return GKS_OK;
+}
+
+int gks_create_local(const GksMeshDesc* mesh, const GksSetup* setup, const GksOptions* opt,
+                     const GksDomainDesc* domain, int device, GksHandle** out) {
+  set_error_index(-1);
+  if (!mesh || !opt || !out || !setup || !domain) {
+    set_error("gks_create_local: bad arguments");
+    return GKS_ERR_BAD_ARG;
+  }
+  if (int rc = no_device()) return rc;
+  GksHandle* G = new GksHandle();
+  int rc = create_handle(G, mesh, setup, opt, device, domain);
+  if (rc) {
+    destroy_handle(G);
+    delete G;
+    return rc;
+  }
+  *out = G;
+  return GKS_OK;
+}
+
+int gks_comm_init(GksHandle* G, const void* unique_id, int nranks, int rank) {
+  Handle* H = &G->H;
+  TRY(comm_init(H, unique_id, nranks, rank));
+  BlockSys* A = &G->jac.sys;
+  A->halo_x = [H](double* x) { halo_exchange(H, H->hx, x, 5, H->stream); };
+  A->red2 = [H](double* a, double* b) {
+    if (a) allreduce(H, a, 1, 0, 0, H->stream);
+    if (b) allreduce(H, b, 1, 0, 0, H->stream);
+  };
   return GKS_OK;
 }
 
@@ -442,25 +507,26 @@ __global__ void k_perturb(int64_t n, const double* q, const double* v, const dou
 __global__ void k_frechet_combine(int64_t nc, const double* r1, const double* r0, const double* sigma,
                                   const double* v, const double* vol, const double* dt, int mode, double* out,
                                   const int* gate);
-void dot2(KrylovWS* W, cudaStream_t s, int64_t n, const double* a, const double* b, const double* c,
-          const double* d, double* o0, double* o1, const int* gate);
+void dot2(BlockSys* A, int64_t n, const double* a, const double* b, const double* c, const double* d, double* o0,
+          double* o1, const int* gate);
 
 // J v (mode 0: Frechet derivative; mode 1: V/dt v - derivative) with the step
 // residual H->res as the base point; q_base = H->q, dt = H->dt.
 static void frechet_apply(Handle* H, BlockSys* A, const double* v, double* out, int mode, const int* gate,
                           const double* fixed_sigma) {
-  const int64_t n = H->nc * 5;
+  const int64_t n = H->n_owned * 5;
   double* sig = &H->scal->sigma;
   if (!fixed_sigma) {
-    dot2(&A->ws, H->stream, n, v, v, H->q, H->q, &H->scal->red[0], &H->scal->red[1], gate);
+    dot2(A, n, v, v, H->q, H->q, &H->scal->red[0], &H->scal->red[1], gate);
     GKS_LAUNCH(KC_SCALAR, k_sigma, 1, 1, 0, H->stream, H->scal->red, sig, nullptr);
   } else {
     sig = const_cast<double*>(fixed_sigma);
   }
   GKS_LAUNCH(KC_VEC, k_perturb, blocks_for(n, 256), 256, 0, H->stream, n, H->q, v, sig, H->qtmp, gate);
+  halo_exchange(H, H->hq, H->qtmp, 5, H->stream);
   residual_device(H, H->qtmp, H->res2, false, gate);
-  GKS_LAUNCH(KC_VEC, k_frechet_combine, blocks_for(n, 256), 256, 0, H->stream, H->nc, H->res2, H->res, sig, v, H->vol, H->dt, mode,
-                                                                out, gate);
+  GKS_LAUNCH(KC_VEC, k_frechet_combine, blocks_for(n, 256), 256, 0, H->stream, H->n_owned, H->res2, H->res, sig, v,
+             H->vol, H->dt, mode, out, gate);
 }
 
 static int advance_device(GksHandle* G, GksStepInfo* info) {
@@ -471,6 +537,9 @@ static int advance_device(GksHandle* G, GksStepInfo* info) {
     set_error("scheme 'weno_lusgs' (sequential LUSGS sweep) is not part of the device path");
     return GKS_ERR_BAD_ARG;
   }
+  // ghost layers are stale after the previous update: refresh Q (+grad)
+  TRY(halo_exchange(H, H->hq, H->q, 5, H->stream));
+  if (H->compact) TRY(halo_exchange(H, H->hq, H->grad, 15, H->stream));
   reset_status(H);
   TRY(local_dt_device(H));
   TRY(check_status(H, "local_time_step"));
@@ -494,34 +563,40 @@ static int advance_device(GksHandle* G, GksStepInfo* info) {
       frechet_apply(H, A, v, out, 1, gate, nullptr);
     };
     TRY(gmres_device(A, H->res, H->dq, P, &gh, H->jac_mode == GKS_JAC_FRECHET ? &mf : nullptr));
-    GKS_LAUNCH(KC_UPDATE, k_update, blocks_for(H->nc, 256), 256, 0, H->stream, H->nc, H->q, H->dq, H->q_new, H->bad);
-    GKS_LAUNCH(KC_UPDATE, k_stats, H->red_blocks, 256, 0, H->stream, H->nc, H->res, H->dt, H->bad, H->partial, H->counter, H->scal);
+    GKS_LAUNCH(KC_UPDATE, k_update, blocks_for(H->n_owned, 256), 256, 0, H->stream, H->n_owned, H->q, H->dq,
+               H->q_new, H->bad);
+    GKS_LAUNCH(KC_UPDATE, k_stats, H->red_blocks, 256, 0, H->stream, H->n_owned, H->res, H->dt, H->bad, H->partial,
+               H->counter, H->scal);
+    TRY(allreduce(H, H->scal->stat, 3, 0, 0, H->stream));
+    TRY(allreduce(H, H->scal->stat + 3, 1, 0, 1, H->stream));
     DevScalars sc;
     GKS_CUDA(cudaMemcpyAsync(&sc, H->scal, sizeof(sc), cudaMemcpyDeviceToHost, H->stream));
     GKS_CUDA(cudaStreamSynchronize(H->stream));
     info->matvecs += gh.matvecs;
-    if (sc.nbad == 0) {
+    const int nbad = (int)sc.stat[2];
+    if (nbad == 0) {
       std::swap(H->q, H->q_new);
       if (H->compact) std::swap(H->grad, H->grad_new);
-      info->res_rho_l1 = sc.res_rho_l1;
-      info->res_l2 = sc.res_l2;
-      info->dt_min = sc.dt_min;
+      info->res_rho_l1 = sc.stat[0] / (double)H->nc_global;
+      info->res_l2 = sqrt(sc.stat[1] / (double)(5 * H->nc_global));
+      info->dt_min = sc.stat[3];
       info->solver_cycles = gh.ncycles;
       info->retried = retried;
       if (g_prof_on) prof_harvest();
       return GKS_OK;
     }
-    info->nbad = sc.nbad;
+    info->nbad = nbad;
     if (attempt == 0) {
-      GKS_LAUNCH(KC_UPDATE, k_halve_dt, blocks_for(H->nc, 256), 256, 0, H->stream, H->nc, H->bad, H->dt);
+      GKS_LAUNCH(KC_UPDATE, k_halve_dt, blocks_for(H->n_owned, 256), 256, 0, H->stream, H->n_owned, H->bad, H->dt);
+      TRY(halo_exchange(H, H->hx, H->dt, 1, H->stream));
       retried = 1;
     }
   }
-  std::vector<int8_t> bad(H->nc);
-  GKS_CUDA(cudaMemcpy(bad.data(), H->bad, H->nc, cudaMemcpyDeviceToHost));
+  std::vector<int8_t> bad(H->n_owned);
+  GKS_CUDA(cudaMemcpy(bad.data(), H->bad, H->n_owned, cudaMemcpyDeviceToHost));
   int k = 0;
   std::string lst;
-  for (int64_t c = 0; c < H->nc && k < 8; ++c)
+  for (int64_t c = 0; c < H->n_owned && k < 8; ++c)
     if (bad[c]) {
       info->first_bad[k++] = c;
       lst += (lst.empty() ? "" : ", ") + std::to_string(c);
@@ -619,7 +694,7 @@ static int bs_vec_op(GksBlockSystem* a, const double* x, double* y, int which) {
   TRY(bs_check_size(a));
   BlockSys* A = &a->sys;
   const int64_t n = A->nc * 5;
-  TRY(krylov_ensure(&A->ws, n, 1));
+  TRY(krylov_ensure(&A->ws, n, 5 * std::max<int64_t>(A->n_ext, A->nc), 1));
   GKS_CUDA(cudaMemcpyAsync(A->ws.x, x, n * sizeof(double), cudaMemcpyHostToDevice, A->stream));
   if (which == 0) bs_spmv(A, A->ws.x, A->ws.b, nullptr);
   else bs_offdiag(A, A->ws.x, A->ws.b, nullptr);
@@ -648,7 +723,7 @@ int gks_blocksys_jacobi(GksBlockSystem* a, const double* b, int k_max, double* z
     return GKS_ERR_SINGULAR;
   }
   const int64_t n = A->nc * 5;
-  TRY(krylov_ensure(&A->ws, n, 1));
+  TRY(krylov_ensure(&A->ws, n, 5 * std::max<int64_t>(A->n_ext, A->nc), 1));
   GKS_CUDA(cudaMemcpyAsync(A->ws.b, b, n * sizeof(double), cudaMemcpyHostToDevice, A->stream));
   bs_jacobi(A, A->ws.b, A->ws.z, A->ws.w, k_max, nullptr);
   GKS_CUDA(cudaGetLastError());
@@ -663,7 +738,7 @@ int gks_gmres(GksBlockSystem* a, const double* b, double* x_out, int m, int rest
   set_error_index(-1);
   BlockSys* A = &a->sys;
   const int64_t n = A->nc * 5;
-  TRY(krylov_ensure(&A->ws, n, m));
+  TRY(krylov_ensure(&A->ws, n, 5 * std::max<int64_t>(A->n_ext, A->nc), m));
   double* db;
   double* dx;
   GKS_CUDA(cudaMalloc(&db, n * sizeof(double)));
@@ -774,7 +849,7 @@ int gks_frechet_matvec(GksHandle* G, const double* q, const double* grad, const 
   GKS_CUDA(cudaSetDevice(H->device));
   const int64_t n = H->nc * 5;
   BlockSys* A = &G->jac.sys;
-  TRY(krylov_ensure(&A->ws, n, 1));
+  TRY(krylov_ensure(&A->ws, n, 5 * std::max<int64_t>(A->n_ext, A->nc), 1));
   GKS_CUDA(cudaMemcpyAsync(H->q, q, n * sizeof(double), cudaMemcpyHostToDevice, H->stream));
   if (grad) GKS_CUDA(cudaMemcpyAsync(H->grad, grad, H->nc * 15 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
   GKS_CUDA(cudaMemcpyAsync(H->dt, dt, H->nc * sizeof(double), cudaMemcpyHostToDevice, H->stream));

@@ -170,14 +170,19 @@ __global__ void k_jac_faces(int64_t nfi, const int* __restrict__ ifaces, const i
   const double lam = spectral_radius(qm, n, gam);
   const double hs = 0.5 * f_area[f];
   double J[5][5];
-  euler_jacobian(qn, n, gam, J);
-  double* B = off + (int64_t)fslot[2 * f] * 25;  // row own, col nbr
-  for (int i = 0; i < 5; ++i)
-    for (int j = 0; j < 5; ++j) B[i * 5 + j] = hs * (J[i][j] - (i == j ? lam : 0.0));
-  euler_jacobian(qo, n, gam, J);
-  B = off + (int64_t)fslot[2 * f + 1] * 25;  // row nbr, col own
-  for (int i = 0; i < 5; ++i)
-    for (int j = 0; j < 5; ++j) B[i * 5 + j] = hs * (-J[i][j] - (i == j ? lam : 0.0));
+  // rows of ghost cells (cut faces on a partitioned mesh) have no slot
+  if (fslot[2 * f] >= 0) {
+    euler_jacobian(qn, n, gam, J);
+    double* B = off + (int64_t)fslot[2 * f] * 25;  // row own, col nbr
+    for (int i = 0; i < 5; ++i)
+      for (int j = 0; j < 5; ++j) B[i * 5 + j] = hs * (J[i][j] - (i == j ? lam : 0.0));
+  }
+  if (fslot[2 * f + 1] >= 0) {
+    euler_jacobian(qo, n, gam, J);
+    double* B = off + (int64_t)fslot[2 * f + 1] * 25;  // row nbr, col own
+    for (int i = 0; i < 5; ++i)
+      for (int j = 0; j < 5; ++j) B[i * 5 + j] = hs * (-J[i][j] - (i == j ? lam : 0.0));
+  }
 }
 
 // 5x5 inverse by LU with partial pivoting (numpy.linalg.inv: LAPACK gesv on I)
@@ -220,13 +225,15 @@ __device__ __forceinline__ bool inv5(const double A[25], double X[25]) {
 }
 
 // diagonal blocks: V/dt I + interior(own) + interior(nbr) + boundary(own), then D^-1
+// (jacobian.py:567-610, np.add.at order: interior faces as owner, interior
+// faces as neighbour, boundary faces; ascending face id within each group)
 __global__ void k_jac_diag(int64_t nc, const int* __restrict__ cjd_start, const int* __restrict__ cjd,
-                           const int* __restrict__ face_slot_of_face, const double* __restrict__ off,
-                           const int* __restrict__ f_own, const double* __restrict__ f_normal,
-                           const double* __restrict__ f_area, const int* __restrict__ bidx_of_face,
-                           const double* __restrict__ ghosts, const double* __restrict__ q,
-                           const double* __restrict__ vol, const double* __restrict__ dt, double gam,
-                           double* __restrict__ diag, double* __restrict__ dinv, int* status) {
+                           const int* __restrict__ f_own, const int* __restrict__ f_nbr,
+                           const double* __restrict__ f_normal, const double* __restrict__ f_area,
+                           const int* __restrict__ bidx_of_face, const double* __restrict__ ghosts,
+                           const double* __restrict__ q, const double* __restrict__ vol,
+                           const double* __restrict__ dt, double gam, double* __restrict__ diag,
+                           double* __restrict__ dinv, int* status) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nc) return;
   double D[25];
@@ -238,29 +245,27 @@ __global__ void k_jac_diag(int64_t nc, const int* __restrict__ cjd_start, const 
   for (int e = cjd_start[c]; e < cjd_start[c + 1]; ++e) {
     const int f = cjd[e] >> 1;
     const int side = cjd[e] & 1;
-    const int slot = face_slot_of_face[2 * f + (side ^ 1)];
-    if (slot >= 0) {
-      // interior face: the diagonal contribution equals minus the opposite
-      // off-diagonal block (exactly: hs*(J + lam I) = -(hs*(-J - lam I)))
-      const double* B = off + (int64_t)slot * 25;
-      for (int i = 0; i < 25; ++i) D[i] += -B[i];
-    } else {
+    const double n[3] = {f_normal[3 * f], f_normal[3 * f + 1], f_normal[3 * f + 2]};
+    const double hs = 0.5 * f_area[f];
+    const int64_t nb = f_nbr[f];
+    double qm[5];
+    if (nb >= 0) {
+      const int64_t o = f_own[f];
+      for (int k = 0; k < 5; ++k) qm[k] = 0.5 * (q[o * 5 + k] + q[nb * 5 + k]);
+    } else if (ghosts) {
       // boundary face, frozen ghost sharpens |lambda| (jacobian.py:597-610)
-      const double n[3] = {f_normal[3 * f], f_normal[3 * f + 1], f_normal[3 * f + 2]};
-      double qb[5];
-      if (ghosts) {
-        const int64_t b = bidx_of_face[f];
-        for (int k = 0; k < 5; ++k) qb[k] = 0.5 * (qc[k] + ghosts[b * 5 + k]);
-      } else {
-        for (int k = 0; k < 5; ++k) qb[k] = qc[k];
-      }
-      const double lb = spectral_radius(qb, n, gam);
-      double J[5][5];
-      euler_jacobian(qc, n, gam, J);
-      const double hs = 0.5 * f_area[f];
-      for (int i = 0; i < 5; ++i)
-        for (int j = 0; j < 5; ++j) D[i * 5 + j] += hs * (J[i][j] + (i == j ? lb : 0.0));
+      const int64_t b = bidx_of_face[f];
+      for (int k = 0; k < 5; ++k) qm[k] = 0.5 * (qc[k] + ghosts[b * 5 + k]);
+    } else {
+      for (int k = 0; k < 5; ++k) qm[k] = qc[k];
     }
+    const double lam = spectral_radius(qm, n, gam);
+    double J[5][5];
+    euler_jacobian(qc, n, gam, J);
+    const double sg = side ? -1.0 : 1.0;  // neighbour side: -J(Q_j, n)
+    for (int i = 0; i < 5; ++i)
+      for (int j = 0; j < 5; ++j) D[i * 5 + j] += hs * ((side ? -J[i][j] : J[i][j]) + (i == j ? lam : 0.0));
+    (void)sg;
   }
   for (int i = 0; i < 25; ++i) diag[c * 25 + i] = D[i];
   double X[25];
@@ -453,12 +458,13 @@ __global__ void k_gm_cycle_end(GmresDev* g, int cyc) {
 #undef GH
 
 // x += y @ V[:ny]  (the combination is formed first, then added)
-__global__ void k_gm_update_x(int64_t n, double* __restrict__ x, const double* __restrict__ V, const GmresDev* g) {
+__global__ void k_gm_update_x(int64_t n, int64_t ld, double* __restrict__ x, const double* __restrict__ V,
+                              const GmresDev* g) {
   const int ny = g->ny;
   if (ny == 0) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int k = 0; k < ny; ++k) s += g->y[k] * V[k * n + i];
+    for (int k = 0; k < ny; ++k) s += g->y[k] * V[k * ld + i];
     x[i] = x[i] + s;
   }
 }
@@ -510,19 +516,23 @@ void krylov_free(KrylovWS* W) {
   *W = KrylovWS{};
 }
 
-int krylov_ensure(KrylovWS* W, int64_t n, int m) {
-  if (W->V && W->n == n && W->m >= m) return GKS_OK;
+int krylov_ensure(KrylovWS* W, int64_t n, int64_t ld, int m) {
+  if (ld < n) ld = n;
+  if (W->V && W->n == n && W->ld == ld && W->m >= m) return GKS_OK;
   krylov_free(W);
   W->n = n;
+  W->ld = ld;
   W->m = m;
-  GKS_CUDA(cudaMalloc(&W->V, (size_t)(m + 1) * n * sizeof(double)));
-  GKS_CUDA(cudaMalloc(&W->bufs, (size_t)6 * n * sizeof(double)));
+  GKS_CUDA(cudaMalloc(&W->V, (size_t)(m + 1) * ld * sizeof(double)));
+  GKS_CUDA(cudaMemset(W->V, 0, (size_t)(m + 1) * ld * sizeof(double)));
+  GKS_CUDA(cudaMalloc(&W->bufs, (size_t)6 * ld * sizeof(double)));
+  GKS_CUDA(cudaMemset(W->bufs, 0, (size_t)6 * ld * sizeof(double)));
   W->w = W->bufs;
-  W->r = W->bufs + n;
-  W->t = W->bufs + 2 * n;
-  W->z = W->bufs + 3 * n;
-  W->b = W->bufs + 4 * n;
-  W->x = W->bufs + 5 * n;
+  W->r = W->bufs + ld;
+  W->t = W->bufs + 2 * ld;
+  W->z = W->bufs + 3 * ld;
+  W->b = W->bufs + 4 * ld;
+  W->x = W->bufs + 5 * ld;
   W->grid = red_grid(n);
   GKS_CUDA(cudaMalloc(&W->partial, (size_t)W->grid * 2 * sizeof(double)));
   GKS_CUDA(cudaMalloc(&W->counter, sizeof(unsigned int)));
@@ -533,14 +543,20 @@ int krylov_ensure(KrylovWS* W, int64_t n, int m) {
 
 static inline int cblocks(int64_t nc) { return (int)((nc + CELLS_PER_BLOCK - 1) / CELLS_PER_BLOCK); }
 
+static inline void halo(BlockSys* A, const double* x) {
+  if (A->halo_x) A->halo_x(const_cast<double*>(x));
+}
+
 // y = A x  (diag + off)
 void bs_spmv(BlockSys* A, const double* x, double* y, const int* gate) {
+  halo(A, x);
   GKS_LAUNCH(KC_SPMV, k_block<1>, cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream, A->nc, A->rowptr, A->col, A->off, A->diag,
                                                                     A->dinv, x, nullptr, y, nullptr, gate);
 }
 
 // y = (L+U) x
 void bs_offdiag(BlockSys* A, const double* x, double* y, const int* gate) {
+  halo(A, x);
   GKS_LAUNCH(KC_SPMV, k_block<0>, cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream, A->nc, A->rowptr, A->col, A->off, A->diag,
                                                                     A->dinv, x, nullptr, y, nullptr, gate);
 }
@@ -553,6 +569,7 @@ void bs_jacobi(BlockSys* A, const double* b, double* z, double* tmp, int kmax, c
   double* cur = z;
   double* nxt = tmp;
   for (int k = 0; k < kmax; ++k) {
+    halo(A, cur);
     GKS_LAUNCH(KC_JACOBI, k_block<6>, cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream, A->nc, A->rowptr, A->col, A->off, A->diag,
                                                                       A->dinv, cur, b, nxt, nullptr, gate);
     std::swap(cur, nxt);
@@ -564,11 +581,13 @@ void bs_jacobi(BlockSys* A, const double* b, double* z, double* tmp, int kmax, c
 
 // w = P^-1 A v : fused spmv + first D^-1, then sweeps
 void bs_prec_matvec(BlockSys* A, const double* v, double* w, double* t, double* tmp, int kmax, const int* gate) {
+  halo(A, v);
   GKS_LAUNCH(KC_SPMV, k_block<5>, cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream, A->nc, A->rowptr, A->col, A->off, A->diag,
                                                                     A->dinv, v, nullptr, w, t, gate);
   double* cur = w;
   double* nxt = tmp;
   for (int k = 0; k < kmax; ++k) {
+    halo(A, cur);
     GKS_LAUNCH(KC_JACOBI, k_block<6>, cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream, A->nc, A->rowptr, A->col, A->off, A->diag,
                                                                       A->dinv, cur, t, nxt, nullptr, gate);
     std::swap(cur, nxt);
@@ -579,9 +598,20 @@ void bs_prec_matvec(BlockSys* A, const double* v, double* w, double* t, double* 
   }
 }
 
-void dot2(KrylovWS* W, cudaStream_t s, int64_t n, const double* a, const double* b, const double* c,
-          const double* d, double* o0, double* o1, const int* gate) {
-  GKS_LAUNCH(KC_REDUCE, k_dot2, W->grid, RB_THREADS, 0, s, n, a, b, c, d, o0, o1, W->partial, W->counter, gate);
+void dot2(BlockSys* A, int64_t n, const double* a, const double* b, const double* c, const double* d, double* o0,
+          double* o1, const int* gate) {
+  KrylovWS* W = &A->ws;
+  GKS_LAUNCH(KC_REDUCE, k_dot2, W->grid, RB_THREADS, 0, A->stream, n, a, b, c, d, o0, o1, W->partial, W->counter,
+             gate);
+  if (A->red2) A->red2(o0, o1);
+}
+
+void axpy_dot(BlockSys* A, int64_t n, double* w, const double* v, const double* coef, const double* nxt, double* out,
+              const int* gate) {
+  KrylovWS* W = &A->ws;
+  GKS_LAUNCH(KC_REDUCE, k_axpy_dot, W->grid, RB_THREADS, 0, A->stream, n, w, v, coef, nxt, out, W->partial,
+             W->counter, gate);
+  if (A->red2) A->red2(out, nullptr);
 }
 
 // Restarted left-preconditioned GMRES (krylov.py:55-140) on device vectors;
@@ -599,7 +629,8 @@ int gmres_device(BlockSys* A, const double* b_dev, double* x_dev, const GmresPar
     return GKS_ERR_SINGULAR;
   }
   KrylovWS* W = &A->ws;
-  int rc = krylov_ensure(W, n, m);
+  const int64_t ld = 5 * std::max<int64_t>(A->n_ext, A->nc);
+  int rc = krylov_ensure(W, n, ld, m);
   if (rc) return rc;
   cudaStream_t s = A->stream;
   GmresDev* g = W->g;
@@ -613,7 +644,7 @@ int gmres_device(BlockSys* A, const double* b_dev, double* x_dev, const GmresPar
     g0.atol = P.atol;
     GKS_CUDA(cudaMemcpyAsync(g, &g0, offsetof(GmresDev, dots), cudaMemcpyHostToDevice, s));
   }
-  GKS_CUDA(cudaMemsetAsync(x_dev, 0, n * sizeof(double), s));
+  GKS_CUDA(cudaMemsetAsync(x_dev, 0, ld * sizeof(double), s));
   const int* act = &g->active;
   const int* notdone = &g->notdone;
   const int* rgate = &g->reorth_gate;
@@ -629,11 +660,11 @@ int gmres_device(BlockSys* A, const double* b_dev, double* x_dev, const GmresPar
     Av(x_dev, W->t, notdone);
     GKS_LAUNCH(KC_VEC, k_sub, grid, RB_THREADS, 0, s, n, W->r, b_dev, W->t, notdone);
     bs_jacobi(A, W->r, W->z, W->w, kmax, notdone);
-    dot2(W, s, n, W->z, W->z, nullptr, nullptr, &g->beta2, nullptr, notdone);
+    dot2(A, n, W->z, W->z, nullptr, nullptr, &g->beta2, nullptr, notdone);
     GKS_LAUNCH(KC_SCALAR, k_gm_cycle_start, 1, 1, 0, s, g, cyc);
     GKS_LAUNCH(KC_VEC, k_div, grid, RB_THREADS, 0, s, n, W->V, W->z, &g->beta, act);
     for (int j = 0; j < m; ++j) {
-      const double* vj = W->V + (int64_t)j * n;
+      const double* vj = W->V + (int64_t)j * ld;
       // w = P^-1 A v_j
       if (matvec) {
         Av(vj, W->t, act);
@@ -642,27 +673,25 @@ int gmres_device(BlockSys* A, const double* b_dev, double* x_dev, const GmresPar
         bs_prec_matvec(A, vj, W->w, W->t, W->r, kmax, act);
       }
       // ||w||^2 and w.v_0 in one pass, then fused axpy + next dot (MGS)
-      dot2(W, s, n, W->w, W->w, W->w, W->V, &g->wscale2, &g->dots[0], act);
+      dot2(A, n, W->w, W->w, W->w, W->V, &g->wscale2, &g->dots[0], act);
       for (int i = 0; i <= j; ++i) {
-        const double* nxt = i < j ? W->V + (int64_t)(i + 1) * n : nullptr;
+        const double* nxt = i < j ? W->V + (int64_t)(i + 1) * ld : nullptr;
         double* dst = i < j ? &g->dots[i + 1] : &g->hnext2;
-        GKS_LAUNCH(KC_REDUCE, k_axpy_dot, W->grid, RB_THREADS, 0, s, n, W->w, W->V + (int64_t)i * n, &g->dots[i], nxt, dst,
-                                                  W->partial, W->counter, act);
+        axpy_dot(A, n, W->w, W->V + (int64_t)i * ld, &g->dots[i], nxt, dst, act);
       }
       GKS_LAUNCH(KC_SCALAR, k_gm_reorth_check, 1, 1, 0, s, g, j);
       // conditional second pass (krylov.py:97-104)
-      dot2(W, s, n, W->w, W->V, nullptr, nullptr, &g->corr[0], nullptr, rgate);
+      dot2(A, n, W->w, W->V, nullptr, nullptr, &g->corr[0], nullptr, rgate);
       for (int i = 0; i <= j; ++i) {
-        const double* nxt = i < j ? W->V + (int64_t)(i + 1) * n : nullptr;
+        const double* nxt = i < j ? W->V + (int64_t)(i + 1) * ld : nullptr;
         double* dst = i < j ? &g->corr[i + 1] : &g->hnext2;
-        GKS_LAUNCH(KC_REDUCE, k_axpy_dot, W->grid, RB_THREADS, 0, s, n, W->w, W->V + (int64_t)i * n, &g->corr[i], nxt, dst,
-                                                  W->partial, W->counter, rgate);
+        axpy_dot(A, n, W->w, W->V + (int64_t)i * ld, &g->corr[i], nxt, dst, rgate);
       }
       GKS_LAUNCH(KC_SCALAR, k_gm_givens, 1, 1, 0, s, g, j, cyc);
-      GKS_LAUNCH(KC_VEC, k_div, grid, RB_THREADS, 0, s, n, W->V + (int64_t)(j + 1) * n, W->w, &g->hdiv, act);
+      GKS_LAUNCH(KC_VEC, k_div, grid, RB_THREADS, 0, s, n, W->V + (int64_t)(j + 1) * ld, W->w, &g->hdiv, act);
     }
     GKS_LAUNCH(KC_SCALAR, k_gm_cycle_end, 1, 1, 0, s, g, cyc);
-    GKS_LAUNCH(KC_VEC, k_gm_update_x, grid, RB_THREADS, 0, s, n, x_dev, W->V, g);
+    GKS_LAUNCH(KC_VEC, k_gm_update_x, grid, RB_THREADS, 0, s, n, ld, x_dev, W->V, g);
     if (P.check_ortho && out) {
       // Gram matrix of the cycle's basis (krylov.py:778-782), host-side check
       GmresDev gh;
@@ -670,12 +699,12 @@ int gmres_device(BlockSys* A, const double* b_dev, double* x_dev, const GmresPar
       GKS_CUDA(cudaStreamSynchronize(s));
       const int ju = gh.ny;
       if (ju > 1) {
-        std::vector<double> hv((size_t)ju * n);
+        std::vector<double> hv((size_t)ju * ld);
         GKS_CUDA(cudaMemcpy(hv.data(), W->V, hv.size() * sizeof(double), cudaMemcpyDeviceToHost));
         for (int a = 0; a < ju; ++a)
           for (int b = 0; b < ju; ++b) {
             double acc = 0.0;
-            for (int64_t i = 0; i < n; ++i) acc += hv[a * n + i] * hv[b * n + i];
+            for (int64_t i = 0; i < n; ++i) acc += hv[a * ld + i] * hv[b * ld + i];
             out->ortho_error = std::max(out->ortho_error, fabs(acc - (a == b ? 1.0 : 0.0)));
           }
       }
@@ -715,10 +744,9 @@ int jacobian_assemble(Handle* H, BlockSys* A, const double* ghosts_dev) {
     GKS_LAUNCH(KC_JAC_FACE, k_jac_faces, blocks_for(H->nfi, 128), 128, 0, H->stream, H->nfi, H->interior_faces, H->f_own, H->f_nbr,
                                                                  H->f_normal, H->f_area, H->q, H->face_slot,
                                                                  H->gamma, A->off);
-  GKS_LAUNCH(KC_JAC_DIAG, k_jac_diag, blocks_for(H->nc, 128), 128, 0, H->stream, H->nc, H->cjd_start, H->cjd, H->face_slot, A->off,
-                                                             H->f_own, H->f_normal, H->f_area, H->bidx, ghosts_dev,
-                                                             H->q, H->vol, H->dt, H->gamma, A->diag, A->dinv,
-                                                             A->status);
+  GKS_LAUNCH(KC_JAC_DIAG, k_jac_diag, blocks_for(H->n_owned, 128), 128, 0, H->stream, H->n_owned, H->cjd_start,
+             H->cjd, H->f_own, H->f_nbr, H->f_normal, H->f_area, H->bidx, ghosts_dev, H->q, H->vol, H->dt, H->gamma,
+             A->diag, A->dinv, A->status);
   GKS_CUDA(cudaGetLastError());
   int st[4];
   GKS_CUDA(cudaMemcpyAsync(st, A->status, sizeof(st), cudaMemcpyDeviceToHost, H->stream));
@@ -757,7 +785,8 @@ __global__ void k_update(int64_t nc, const double* __restrict__ q, const double*
   bad[c] = (rho <= 0.0) || (e <= 0.0) || !fin;
 }
 
-// sum|res_rho|, sum res^2, min dt, bad count -> DevScalars (deterministic)
+// sum|res_rho|, sum res^2, bad count, min dt -> DevScalars.stat (deterministic,
+// raw sums so ranks can allreduce before the host normalises)
 __global__ void __launch_bounds__(RB_THREADS) k_stats(int64_t nc, const double* __restrict__ res,
                                                       const double* __restrict__ dt, const int8_t* __restrict__ bad,
                                                       double* partial, unsigned int* counter, DevScalars* out) {
@@ -785,39 +814,39 @@ __global__ void __launch_bounds__(RB_THREADS) k_stats(int64_t nc, const double* 
   if (threadIdx.x == 0) {
     partial[4 * blockIdx.x] = A;
     partial[4 * blockIdx.x + 1] = B;
-    partial[4 * blockIdx.x + 2] = sm[0];
-    partial[4 * blockIdx.x + 3] = NB;
+    partial[4 * blockIdx.x + 2] = NB;
+    partial[4 * blockIdx.x + 3] = sm[0];
     __threadfence();
     last = atomicInc(counter, gridDim.x - 1) == gridDim.x - 1;
   }
   __syncthreads();
   if (!last) return;
   __threadfence();
-  double x0 = 0, x1 = 0, x2 = INFINITY, x3 = 0;
+  double x0 = 0, x1 = 0, x2 = 0, x3 = INFINITY;
   for (unsigned k = threadIdx.x; k < gridDim.x; k += blockDim.x) {
     x0 += __ldcg(partial + 4 * k);
     x1 += __ldcg(partial + 4 * k + 1);
-    x2 = fmin(x2, __ldcg(partial + 4 * k + 2));
-    x3 += __ldcg(partial + 4 * k + 3);
+    x2 += __ldcg(partial + 4 * k + 2);
+    x3 = fmin(x3, __ldcg(partial + 4 * k + 3));
   }
   __syncthreads();
   x0 = block_sum(x0, sm);
   __syncthreads();
   x1 = block_sum(x1, sm);
   __syncthreads();
-  x3 = block_sum(x3, sm);
+  x2 = block_sum(x2, sm);
   __syncthreads();
-  sm[threadIdx.x] = x2;
+  sm[threadIdx.x] = x3;
   __syncthreads();
   for (int s = blockDim.x / 2; s > 0; s >>= 1) {
     if (threadIdx.x < s) sm[threadIdx.x] = fmin(sm[threadIdx.x], sm[threadIdx.x + s]);
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    out->res_rho_l1 = x0 / (double)nc;
-    out->res_l2 = sqrt(x1 / (double)(5 * nc));
-    out->dt_min = sm[0];
-    out->nbad = (int)x3;
+    out->stat[0] = x0;
+    out->stat[1] = x1;
+    out->stat[2] = x2;
+    out->stat[3] = sm[0];
   }
 }
 

@@ -25,7 +25,8 @@ struct GmresDev {
 };
 
 struct KrylovWS {
-  int64_t n = 0;
+  int64_t n = 0;     // reduction length (5 * owned rows)
+  int64_t ld = 0;    // allocation length per vector (5 * (owned + layer-1 ghosts))
   int m = 0;
   int grid = 0;
   double* V = nullptr;
@@ -39,6 +40,9 @@ struct KrylovWS {
 // Block-row matrix: diagonal blocks + CSR off-diagonal blocks (jacobian.py:74-126)
 struct BlockSys {
   int64_t nc = 0, nnz = 0;
+  int64_t n_ext = 0;                                  // rows + layer-1 ghost columns
+  std::function<void(double*)> halo_x;                // fill ghost entries of x before (L+U) x
+  std::function<void(double*, double*)> red2;         // allreduce two device scalars (null ok)
   int *rowptr = nullptr, *col = nullptr;
   double *off = nullptr, *diag = nullptr, *dinv = nullptr;
   int* status = nullptr;
@@ -66,7 +70,7 @@ using MatvecFn = std::function<void(const double* v, double* out, const int* gat
 int blocksys_alloc(BlockSys* A, int64_t nc, int64_t nnz, cudaStream_t stream);
 void blocksys_free(BlockSys* A);
 void krylov_free(KrylovWS* W);
-int krylov_ensure(KrylovWS* W, int64_t n, int m);
+int krylov_ensure(KrylovWS* W, int64_t n, int64_t ld, int m);
 int blocksys_invert_diag(BlockSys* A);
 void bs_spmv(BlockSys* A, const double* x, double* y, const int* gate);
 void bs_offdiag(BlockSys* A, const double* x, double* y, const int* gate);

@@ -214,6 +214,7 @@ struct GksSetup {
     int64_t shape[4];
   };
   std::map<std::string, Arr> arrays;
+  std::vector<std::vector<char>> owned_storage;  // backing store of subset setups
   template <class T>
   void reg(const char* name, const std::vector<T>& v, int dtype, std::initializer_list<int64_t> shp) {
     Arr a{v.data(), dtype, (int)shp.size(), {0, 0, 0, 0}};
@@ -724,6 +725,50 @@ int gks_setup_build(const GksMeshDesc* m, int schemes, int nthreads, GksSetup** 
 }
 
 void gks_setup_free(GksSetup* s) { delete s; }
+
+// Restrict a global setup to local cells: rows of every per-cell array are
+// gathered in local order and cell-id gathers are renumbered to local ids
+// (ids outside the local set map to 0 -- only rows of cells that are not
+// reconstructed locally can contain them).
+int gks_setup_subset(const GksSetup* g, const int64_t* cells, int64_t n_local, const int64_t* g2l,
+                     int64_t n_global, GksSetup** out) {
+  if (!g || !cells || !g2l || !out || n_local <= 0 || n_global != g->nc) {
+    gks::set_error("gks_setup_subset: bad arguments");
+    return GKS_ERR_BAD_ARG;
+  }
+  static const char* gathers[] = {"weno_big_gather", "weno_sub_gather", "hweno_big_avg_gather",
+                                  "hweno_big_grad_gather", "hweno_sub_gather"};
+  GksSetup* S = new GksSetup();
+  S->nc = n_local;
+  S->nfpc = g->nfpc;
+  for (const auto& kv : g->arrays) {
+    const auto& a = kv.second;
+    if (a.ndim < 1 || a.shape[0] != g->nc) continue;  // CSR stencil tables are not per-cell arrays
+    const int esz = a.dtype == 2 ? 1 : 8;
+    int64_t row = esz;
+    for (int d = 1; d < a.ndim; ++d) row *= a.shape[d];
+    S->owned_storage.emplace_back((size_t)(n_local * row));
+    std::vector<char>& buf = S->owned_storage.back();
+    const char* src = static_cast<const char*>(a.p);
+    for (int64_t c = 0; c < n_local; ++c) memcpy(buf.data() + c * row, src + cells[c] * row, row);
+    bool is_gather = false;
+    for (const char* nm : gathers) is_gather |= kv.first == nm;
+    if (is_gather) {
+      int64_t* v = reinterpret_cast<int64_t*>(buf.data());
+      const int64_t n = n_local * row / 8;
+      for (int64_t k = 0; k < n; ++k) {
+        const int64_t l = (v[k] >= 0 && v[k] < n_global) ? g2l[v[k]] : -1;
+        v[k] = l >= 0 ? l : 0;
+      }
+    }
+    GksSetup::Arr b = a;
+    b.p = buf.data();
+    b.shape[0] = n_local;
+    S->arrays[kv.first] = b;
+  }
+  *out = S;
+  return GKS_OK;
+}
 
 int gks_setup_query(const GksSetup* s, const char* name, int* dtype, int* ndim, int64_t* shape) {
   if (!s || !name) return GKS_ERR_BAD_ARG;

@@ -59,7 +59,7 @@ __global__ void k_local_dt(int64_t nc, const double* __restrict__ q, const int* 
 }
 
 // deterministic min-reduction for the global time step (single block)
-__global__ void k_min_broadcast(int64_t n, double* __restrict__ dt) {
+__global__ void k_min_reduce(int64_t n, const double* __restrict__ dt, double* out) {
   __shared__ double sm[1024];
   double m = INFINITY;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmin(m, dt[i]);
@@ -69,8 +69,13 @@ __global__ void k_min_broadcast(int64_t n, double* __restrict__ dt) {
     if (threadIdx.x < s) sm[threadIdx.x] = fmin(sm[threadIdx.x], sm[threadIdx.x + s]);
     __syncthreads();
   }
-  const double g = sm[0];
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dt[i] = g;
+  if (threadIdx.x == 0) *out = sm[0];
+}
+
+__global__ void k_fill(int64_t n, double* __restrict__ dt, const double* val) {
+  const double g = *val;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dt[i] = g;
 }
 
 // ---------------------------------------------------------------------------
@@ -462,8 +467,16 @@ void reset_status(Handle* H) {
   cudaMemcpyAsync(H->status, st0, sizeof(st0), cudaMemcpyHostToDevice, H->stream);
 }
 
+#define TRY_STATUS(x)     \
+  do {                     \
+    int _r = (x);          \
+    if (_r) return _r;     \
+  } while (0)
+
 int check_status(Handle* H, const char* what) {
   int st[4];
+  // every rank must agree on failure: the error code is max-reduced first
+  if (H->comm) TRY_STATUS(allreduce(H, H->status, 1, 1, 2, H->stream));
   GKS_CUDA(cudaMemcpyAsync(st, H->status, sizeof(st), cudaMemcpyDeviceToHost, H->stream));
   GKS_CUDA(cudaStreamSynchronize(H->stream));
   if (st[0] == 0) return GKS_OK;
@@ -477,24 +490,29 @@ int check_status(Handle* H, const char* what) {
 }
 
 int local_dt_device(Handle* H) {
-  GKS_LAUNCH(KC_DT, k_local_dt, blocks_for(H->nc, TPB), TPB, 0, H->stream, H->nc, H->q, H->cdt_start, H->cdt, H->f_normal,
-                                                             H->f_area, H->vol, H->model == 1 && H->mu > 0.0,
-                                                             H->mu, H->cfl, H->kc, H->dt, H->status);
+  GKS_LAUNCH(KC_DT, k_local_dt, blocks_for(H->n_owned, TPB), TPB, 0, H->stream, H->n_owned, H->q, H->cdt_start,
+             H->cdt, H->f_normal, H->f_area, H->vol, H->model == 1 && H->mu > 0.0, H->mu, H->cfl, H->kc, H->dt,
+             H->status);
   if (H->global_dt) {
-    GKS_LAUNCH(KC_DT, k_min_broadcast, 1, 1024, 0, H->stream, H->nc, H->dt);
+    GKS_LAUNCH(KC_DT, k_min_reduce, 1, 1024, 0, H->stream, H->n_owned, H->dt, &H->scal->red[6]);
+    TRY_STATUS(allreduce(H, &H->scal->red[6], 1, 0, 1, H->stream));
+    GKS_LAUNCH(KC_DT, k_fill, blocks_for(H->nc, 256), 256, 0, H->stream, H->nc, H->dt, &H->scal->red[6]);
+  } else {
+    // face windows min(dt_owner, dt_nbr) on cut faces need the layer-1 ghosts' dt
+    TRY_STATUS(halo_exchange(H, H->hx, H->dt, 1, H->stream));
   }
   GKS_CUDA(cudaGetLastError());
   return GKS_OK;
 }
 
 int residual_device(Handle* H, const double* q, double* res, bool with_gradients, const int* gate) {
-  const int64_t n5 = H->nc * 5;
+  const int64_t n5 = H->n_recon * 5;  // owned + layer-1 ghosts (redundant reconstruction)
   if (H->compact) {
     GKS_LAUNCH(KC_RECON, k_recon_hweno, blocks_for(n5, TPB), TPB, 0, H->stream, 
-        H->nc, q, H->grad, H->h, H->big_op, H->avg_gather, H->grad_gather, H->grad_scale, H->HA, H->HG,
+        H->n_recon, q, H->grad, H->h, H->big_op, H->avg_gather, H->grad_gather, H->grad_scale, H->HA, H->HG,
         H->sub_op, H->sub_gather, H->sub_active, H->HM, H->beta, H->linear_weights, H->eps, H->lw, H->coef, gate);
   } else {
-    GKS_LAUNCH(KC_RECON, k_recon_weno, blocks_for(n5, TPB), TPB, 0, H->stream, H->nc, q, H->big_op, H->big_gather, H->K,
+    GKS_LAUNCH(KC_RECON, k_recon_weno, blocks_for(n5, TPB), TPB, 0, H->stream, H->n_recon, q, H->big_op, H->big_gather, H->K,
                                                               H->sub_op, H->sub_gather, H->sub_active, H->M, H->S,
                                                               H->beta, H->linear_weights, H->eps, H->lw, H->coef,
                                                               gate);
@@ -508,7 +526,7 @@ int residual_device(Handle* H, const double* q, double* res, bool with_gradients
   A.want_point = with_gradients ? 1 : 0;
   A.contrib = H->contrib; A.qpt = H->qpt; A.status = H->status; A.gate = gate;
   GKS_LAUNCH(KC_FACE, k_face, blocks_for(H->nfq, 128), 128, 0, H->stream, A);
-  GKS_LAUNCH(KC_ASSEMBLE, k_assemble, blocks_for(H->nc, TPB), TPB, 0, H->stream, H->nc, H->cfq_start, H->cfq, H->contrib, H->qpt,
+  GKS_LAUNCH(KC_ASSEMBLE, k_assemble, blocks_for(H->n_owned, TPB), TPB, 0, H->stream, H->n_owned, H->cfq_start, H->cfq, H->contrib, H->qpt,
                                                              H->fq_face, H->fq_ws, H->f_normal, H->vol, res,
                                                              with_gradients ? H->grad_new : nullptr, gate);
   GKS_CUDA(cudaGetLastError());

@@ -33,8 +33,17 @@ struct DevPatch {
 // Scalars shared between kernels without host round trips.
 struct DevScalars {
   double red[8];        // reduction results (norms, dots)
-  double res_rho_l1, res_l2, dt_min, sigma;
-  int nbad, pad;
+  double stat[4];       // sum|res_rho|, sum res^2, #bad cells, min dt (allreduced)
+  double sigma;
+};
+
+// Halo exchange map: per peer, local ids sent (owned cells) / received (ghosts)
+struct HaloMap {
+  std::vector<int> peers;
+  std::vector<int64_t> soff{0}, roff{0};
+  int* sids = nullptr;  // device
+  int* rids = nullptr;  // device
+  int64_t ns = 0, nr = 0;
 };
 
 template <class T>
@@ -48,6 +57,12 @@ struct Handle {
   cudaStream_t stream = nullptr;
   // sizes
   int64_t nc = 0, nf = 0, nfq = 0, nfi = 0, nbf = 0, nnz = 0;
+  // domain decomposition: local cells = [owned | layer-1 ghosts | deeper ghosts]
+  int64_t n_owned = 0, n_recon = 0, nc_global = 0;
+  HaloMap hq, hx;                    // Q(+grad) halo (all layers), x/dt halo (layer 1)
+  double *hsend = nullptr, *hrecv = nullptr;
+  void* comm = nullptr;              // ncclComm_t
+  int nranks = 1, rank = 0;
   int nfpc = 4;
   // options
   int scheme = 0, model = 0, compact = 0, linear_weights = 0, global_dt = 0, jac_mode = 0;
@@ -257,6 +272,10 @@ __device__ __forceinline__ double spectral_radius(const double q[5], const doubl
 // host-side entry points shared across translation units
 int residual_device(Handle* H, const double* q, double* res, bool with_gradients, const int* gate);
 void reset_status(Handle* H);
+int halo_exchange(Handle* H, HaloMap& X, double* arr, int width, cudaStream_t s);
+int allreduce(Handle* H, void* dev, int64_t count, int dtype, int op, cudaStream_t s);  // dtype 0 f64 1 i32; op 0 sum 1 min 2 max
+int comm_init(Handle* H, const void* uid, int nranks, int rank);
+void comm_destroy(Handle* H);
 int local_dt_device(Handle* H);
 int boundary_ghosts_device(Handle* H, const double* q);
 int jacobian_device(Handle* H, const double* q, bool ghosts_given);
