@@ -46,13 +46,22 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    p.add_argument("--workload", default="c1", choices=("c1",))
-    p.add_argument("--n", type=int, default=64, help="box divisions per axis (6 n^3 Kuhn tets)")
-    p.add_argument("--scheme", default="weno_gmres", choices=("weno_gmres", "hweno_gmres"))
-    p.add_argument("--jacobian", default="roe", choices=("roe", "frechet"))
-    p.add_argument("--cpu-n", type=int, default=10, help="bounded CPU sample size (box divisions)")
+    p.add_argument("--workload", default="c2", choices=("c1", "c2"),
+                   help="c1: periodic Kuhn-tet box (configs[0]); c2: subsonic sphere, matrix-free GMRES (configs[1])")
+    p.add_argument("--n", type=int, default=None, help="lattice divisions per axis (c1 default 64, c2 default 64)")
+    p.add_argument("--scheme", default=None, choices=("weno_gmres", "hweno_gmres"))
+    p.add_argument("--jacobian", default=None, choices=("roe", "frechet"))
+    p.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of decomposition")
+    p.add_argument("--cpu-n", type=int, default=None, help="bounded CPU sample size (c1 box divisions / c2 cube-face cells)")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    return p.parse_args()
+    a = p.parse_args()
+    # configs[1]: inviscid subsonic sphere, non-compact HGKS + matrix-free GMRES
+    defaults = {"c1": (64, "weno_gmres", "roe"), "c2": (16, "weno_gmres", "frechet")}[a.workload]
+    a.n = a.n or defaults[0]
+    a.scheme = a.scheme or defaults[1]
+    a.jacobian = a.jacobian or defaults[2]
+    a.cpu_n = a.cpu_n or {"c1": 10, "c2": 2}[a.workload]
+    return a
 
 
 # -- workload ---------------------------------------------------------------------
@@ -60,6 +69,39 @@ def parse():
 def c1_mesh(n, host_mesh_module):
     """C1: periodic 6 n^3 Kuhn-tet box."""
     return host_mesh_module.generate_box_mesh((1.0, 1.0, 1.0), (n, n, n), split="tet", periodic=("x", "y", "z"))
+
+
+MA_C2 = 0.5
+
+
+def c2_mesh(n, meshgen_module):
+    """C2: body-fitted synthetic tet sphere (D = 1), farfield at 20 D."""
+    return meshgen_module.generate_sphere_mesh(n, radius=0.5, far=10.0)
+
+
+def c2_problem(mesh, compact):
+    from paper_2304_09485_b200.boundary import PatchSpec
+    from paper_2304_09485_b200.stepping import initial_field
+
+    ref = np.array([1.0, MA_C2, 0.0, 0.0, 1.0 / GAMMA])  # a_inf = 1 -> U = Ma
+    patches = {"sphere": PatchSpec("sphere", "wall_slip_adiabatic"),
+               "farfield": PatchSpec("farfield", "farfield_riemann", reference=ref)}
+    fld = initial_field(mesh, ref, GAMMA, compact=compact)
+    return patches, fld.q, fld.grad
+
+
+def build_workload(args, compact):
+    from paper_2304_09485_b200 import mesh as M
+    from paper_2304_09485_b200 import meshgen as MG
+
+    if args.workload == "c1":
+        mesh = c1_mesh(args.n, M)
+        q, g = c1_field(mesh, compact)
+        return mesh, {}, q, g, f"C1 periodic 6*{args.n}^3 Kuhn-tet box, smooth density wave (configs[0] shape)"
+    mesh = c2_mesh(args.n, MG)
+    patches, q, g = c2_problem(mesh, compact)
+    return mesh, patches, q, g, (f"C2 synthetic body-fitted tet sphere (cubed-sphere n={args.n}, D=1, farfield 20D), "
+                                 f"inviscid Ma {MA_C2}, slip wall + Riemann farfield, impulsive start (configs[1])")
 
 
 def c1_field(mesh, compact):
@@ -189,10 +231,18 @@ def cpu_baseline(args, steps, label):
     from paper_2304_09485_b200 import mesh as M
 
     n = args.cpu_n
-    mesh = c1_mesh(n, M)
-    q, grad = c1_field(mesh, args.scheme.startswith("hweno"))
+    compact = args.scheme.startswith("hweno")
+    if args.workload == "c1":
+        mesh = c1_mesh(n, M)
+        q, grad = c1_field(mesh, compact)
+        patches = {}
+    else:
+        from paper_2304_09485_b200 import meshgen as MG
+
+        mesh = c2_mesh(n, MG)
+        patches, q, grad = c2_problem(mesh, compact)
     t0 = time.perf_counter()
-    s = OracleSolver(mesh, scheme=args.scheme, patches={}, jacobian=args.jacobian)
+    s = OracleSolver(mesh, scheme=args.scheme, patches=patches, jacobian=args.jacobian)
     setup = time.perf_counter() - t0
     q, grad, info = s.advance(q, grad)  # warm-up
     evals = 0
@@ -202,7 +252,8 @@ def cpu_baseline(args, steps, label):
         evals += 1 + (info["matvecs"] - 1 if args.jacobian == "frechet" else 0)
     el = time.perf_counter() - t0
     return {"value": mesh.ncells * evals / el, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{label}: oracle OracleSolver.advance x{steps} on C1 n={n} ({mesh.ncells} cells), "
+            "sample": f"{label}: oracle OracleSolver.advance x{steps} on {args.workload.upper()} n={n} "
+                      f"({mesh.ncells} cells), "
                       f"{args.scheme}/{args.jacobian}, numpy single-thread; setup {setup:.1f}s not timed",
             "seconds": el}
 
@@ -218,7 +269,7 @@ def run_reference(args):
         "metric": METRIC, "value": cb["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": steps, "warmup": 1, "ms_per_step": cb["seconds"] * 1000.0 / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"C1 periodic Kuhn-tet box (bounded CPU sample n={args.cpu_n})",
+        "config": {"workload": f"{args.workload.upper()} (bounded CPU sample, lattice n={args.cpu_n})",
                    "scheme": args.scheme, "jacobian": args.jacobian},
         "cpu_baseline": cb,
         "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -238,11 +289,19 @@ def run_ours(args):
     lib = N.load()
     compact = args.scheme.startswith("hweno")
     t0 = time.perf_counter()
-    mesh = c1_mesh(args.n, M)
+    mesh, patches, q0, g0, workload = build_workload(args, compact)
     t_mesh = time.perf_counter() - t0
-    q0, g0 = c1_field(mesh, compact)
     t0 = time.perf_counter()
-    solver = Solver(mesh, SolverOptions(scheme=args.scheme, patches={}, jacobian=args.jacobian, device=local))
+    opts = SolverOptions(scheme=args.scheme, patches=patches, jacobian=args.jacobian, device=local)
+    decomp = world > 1 and not args.replicas
+    if decomp:
+        from paper_2304_09485_b200.distributed import DistributedSolver
+
+        uid = [DistributedSolver.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        solver = DistributedSolver(mesh, opts, rank=rank, nranks=world, comm_id=uid[0])
+    else:
+        solver = Solver(mesh, opts)
     t_setup = time.perf_counter() - t0
     nc = mesh.ncells
     import ctypes as C
@@ -252,7 +311,7 @@ def run_ours(args):
     fp64 = v.value
 
     # ---- device-resident timed region --------------------------------------------
-    solver.upload(SolutionField(q0, g0))
+    solver.upload(SolutionField(q0, g0))  # DistributedSolver.upload scatters the local part
     for _ in range(args.warmup):
         solver.advance_resident()
     prof = N.Profiler()
@@ -277,28 +336,41 @@ def run_ours(args):
         evals = sum(1 + i.matvecs for i in infos)
     else:
         evals = args.steps
-    value = world * nc * evals / (ms_total / 1000.0)
+    value = (1 if decomp else world) * nc * evals / (ms_total / 1000.0)
 
     # ---- end-to-end through the public API (pinned host field) --------------------
-    fld = SolutionField(np.ascontiguousarray(q0.copy()), None if g0 is None else np.ascontiguousarray(g0.copy()))
-    N.check(lib.gks_host_pin(fld.q.ctypes.data_as(C.c_void_p), fld.q.nbytes))
+    if decomp:
+        cells = solver.dom.cells
+        fq = np.ascontiguousarray(q0[cells])
+        fg = None if g0 is None else np.ascontiguousarray(g0[cells])
+    else:
+        fq = np.ascontiguousarray(q0.copy())
+        fg = None if g0 is None else np.ascontiguousarray(g0.copy())
+    N.check(lib.gks_host_pin(fq.ctypes.data_as(C.c_void_p), fq.nbytes))
     if compact:
-        N.check(lib.gks_host_pin(fld.grad.ctypes.data_as(C.c_void_p), fld.grad.nbytes))
-    solver.advance_inplace(fld)
+        N.check(lib.gks_host_pin(fg.ctypes.data_as(C.c_void_p), fg.nbytes))
+    info_c = N.GksStepInfo()
+
+    def e2e_step():
+        # the C ABI call behind Solver.advance_inplace: H2D of the field, the
+        # whole step, D2H of the new field
+        N.check(lib.gks_advance(solver._handle, N.dptr(fq), N.dptr(fg) if compact else None, C.byref(info_c)))
+
+    e2e_step()
     barrier(dist)
     N.check(lib.gks_event_record(solver._handle, 2))
     e2e_steps = args.steps
     for _ in range(e2e_steps):
-        solver.advance_inplace(fld)
+        e2e_step()
     N.check(lib.gks_event_record(solver._handle, 3))
     ms2 = C.c_double()
     N.check(lib.gks_event_elapsed(solver._handle, 2, 3, C.byref(ms2)))
     ms_e2e = max_over_ranks(dist, ms2.value, local)
     e2e_evals = e2e_steps if args.jacobian == "roe" else int(round(e2e_steps * evals / args.steps))
-    bytes_h2d = fld.q.nbytes + (fld.grad.nbytes if compact else 0)
-    e2e = {"value": world * nc * e2e_evals / (ms_e2e / 1000.0), "unit": UNIT,
+    bytes_h2d = fq.nbytes + (fg.nbytes if compact else 0)
+    e2e = {"value": (1 if decomp else world) * nc * e2e_evals / (ms_e2e / 1000.0), "unit": UNIT,
            "h2d_bytes_per_step": bytes_h2d, "d2h_bytes_per_step": bytes_h2d,
-           "api": "Solver.advance_inplace (C ABI gks_advance), pinned numpy field"}
+           "api": "C ABI gks_advance (behind Solver.advance_inplace), pinned numpy field"}
 
     if rank != 0:
         return 0
@@ -343,12 +415,13 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"C1 periodic 6*{args.n}^3 Kuhn-tet box, smooth density wave (configs[0] shape)",
+        "scaling": "strong" if decomp else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload,
                    "cells": nc, "faces": sizes["nf"], "face_points": sizes["nfq"], "scheme": args.scheme,
                    "jacobian": args.jacobian, "gmres": "m=10, restarts=3, jacobi_sweeps=2, rtol=0",
                    "residual_evals_per_step": evals / args.steps,
-                   "parallelism": "replicas" if world > 1 else "single",
+                   "parallelism": ("replicas" if not decomp else f"cell-partitioned RCB x{world}, NCCL halo + allreduce")
+                   if world > 1 else "single",
                    "l2": "inputs > L2 (operators %.1f GB)" % (sum(model_bytes[k] for k in ("recon",)) / 1e9),
                    "setup_s": round(t_setup, 2), "mesh_s": round(t_mesh, 2)},
         "e2e": e2e,

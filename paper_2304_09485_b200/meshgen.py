@@ -4,10 +4,12 @@ The reference cases (cases/sphere_*.ini, m6wing_transonic.ini) point at
 external .ugks meshes that do not exist offline.  These
 generators build the labelled synthetic stand-ins used by configs 2-5:
 
-* generate_sphere_mesh -- sphere of radius R in the box [-L, L]^3: Kuhn tets
-  on a sinh-stretched lattice (resolution concentrated at the body), cells
-  whose centroid lies inside the sphere removed, wall nodes projected
-  radially onto r = R wherever that keeps every adjacent tet positive.
+* generate_sphere_mesh -- body-fitted cubed-sphere shell between r = R and
+  r = R_far (equiangular gnomonic map, geometric radial growth), each hex
+  split into 24 tets through face and cell centres (conforming across the
+  cube-face blocks whatever their orientation).
+* generate_carved_sphere_mesh -- older stair-step stand-in: Kuhn tets on a
+  stretched lattice with the sphere carved out (kept for tests).
 * generate_wing_mesh -- a swept, tapered, symmetric-section wing carved the
   same way (the ONERA M6 geometry is not available offline).
 
@@ -115,8 +117,96 @@ def _project(nodes, tets, body_nodes, target, min_frac=0.05):
     return moved
 
 
-def generate_sphere_mesh(n, radius=0.5, half=10.0, beta=None, boundary="farfield", project=True):
-    """Synthetic tet sphere-in-box (configs 2, 3, 5).
+def _cube_dirs(n):
+    """Equiangular gnomonic directions of the 6 cube faces: (6, n+1, n+1, 3) unit vectors."""
+    a = np.tan(np.linspace(-np.pi / 4, np.pi / 4, n + 1))
+    A, B = np.meshgrid(a, a, indexing="ij")
+    one = np.ones_like(A)
+    faces = [np.stack([one, A, B], -1), np.stack([-one, B, A], -1),
+             np.stack([B, one, A], -1), np.stack([A, -one, B], -1),
+             np.stack([A, B, one], -1), np.stack([B, A, -one], -1)]
+    d = np.stack(faces)
+    return d / np.linalg.norm(d, axis=-1, keepdims=True)
+
+
+def _dedup_points(p, scale):
+    """Unique points (rounded to 1e-12 of scale) -> (unique array, inverse index)."""
+    key = np.round(p / scale * 1e12).astype(np.int64)
+    kv = np.ascontiguousarray(key).view(np.dtype((np.void, 24))).ravel()
+    _, first, inv = np.unique(kv, return_index=True, return_inverse=True)
+    order = np.argsort(first)
+    rank = np.empty_like(order)
+    rank[order] = np.arange(len(order))
+    return p[first[order]], rank[inv]
+
+
+# quad faces of a hex (VTK order), each listed so the cell centre sees it with outward winding
+_HEX_QUADS = np.array(((0, 3, 2, 1), (4, 5, 6, 7), (0, 1, 5, 4), (1, 2, 6, 5), (2, 3, 7, 6), (3, 0, 4, 7)))
+
+
+def generate_sphere_mesh(n, radius=0.5, far=10.0, nr=None, boundary="farfield"):
+    """Body-fitted synthetic tet sphere (configs 2, 3, 5): a cubed-sphere shell.
+
+    n: cells per cube-face edge (angular), nr: radial layers (geometric growth
+    from `radius` to `far`, default ~2.5 n).  Each shell hex is split into 24
+    tets through its face centres and centre, which is conforming whatever the
+    orientation of the neighbouring cube-face block.  About 144 n^2 nr tets.
+    Patches: "sphere" (r = radius) and "farfield", or "inlet"/"outlet"
+    (outer faces with x < 0 / x >= 0) for boundary="supersonic".
+    """
+    if nr is None:
+        nr = max(4, int(round(2.5 * n)))
+    dirs = _cube_dirs(n)
+    g = (far / radius) ** (1.0 / nr)
+    radii = radius * g ** np.arange(nr + 1)
+    radii[-1] = far
+    # hex corner points: (6, n+1, n+1, nr+1)
+    P = dirs[:, :, :, None, :] * radii[None, None, None, :, None]
+    f, i, j, k = (x.ravel() for x in np.meshgrid(np.arange(6), np.arange(n), np.arange(n), np.arange(nr),
+                                                  indexing="ij"))
+    corner = np.stack([P[f, i, j, k], P[f, i + 1, j, k], P[f, i + 1, j + 1, k], P[f, i, j + 1, k],
+                       P[f, i, j, k + 1], P[f, i + 1, j, k + 1], P[f, i + 1, j + 1, k + 1], P[f, i, j + 1, k + 1]], 1)
+    nh = len(corner)
+    quads = corner[:, _HEX_QUADS]                    # (nh, 6, 4, 3)
+    fcen = quads.mean(axis=2)                        # (nh, 6, 3)
+    # face 0 (nodes 0-3) lies on r_k: on the wall when k == 0; project its centre onto the sphere
+    wall_c = fcen[:, 0] / np.linalg.norm(fcen[:, 0], axis=1)[:, None] * radius
+    fcen[k == 0, 0] = wall_c[k == 0]
+    ccen = corner.mean(axis=1)                       # (nh, 3)
+    scale = far
+    allpts = np.concatenate([corner.reshape(-1, 3), fcen.reshape(-1, 3), ccen])
+    nodes, inv = _dedup_points(allpts, scale)
+    cid = inv[: nh * 8].reshape(nh, 8)
+    fid = inv[nh * 8: nh * 8 + nh * 6].reshape(nh, 6)
+    zid = inv[nh * 8 + nh * 6:]
+    # 24 tets: (edge a, edge b, face centre, cell centre) for each quad edge
+    qn = cid[:, _HEX_QUADS]                          # (nh, 6, 4)
+    a = qn
+    b = np.roll(qn, -1, axis=2)
+    fc = np.broadcast_to(fid[:, :, None], a.shape)
+    cc = np.broadcast_to(zid[:, None, None], a.shape)
+    tets = np.stack([a, b, fc, cc], axis=-1).reshape(-1, 4)
+    vol = _tet_volumes(nodes, tets)
+    flip = vol < 0
+    tets[flip] = tets[flip][:, [0, 2, 1, 3]]
+    if np.any(np.abs(vol) <= 0):
+        raise MeshError("degenerate tet in the sphere shell")
+    # boundary triangles: wall = face 0 of k == 0 hexes, far = face 1 of k == nr-1 hexes
+    tri = np.stack([a, b, fc], axis=-1)               # (nh, 6, 4, 3)
+    wall = tri[k == 0, 0].reshape(-1, 3)
+    outer_tri = tri[k == nr - 1, 1].reshape(-1, 3)
+    if boundary == "farfield":
+        patches = {"sphere": wall, "farfield": outer_tri}
+    elif boundary == "supersonic":
+        xc = nodes[outer_tri].mean(axis=1)[:, 0]
+        patches = {"sphere": wall, "inlet": outer_tri[xc < 0], "outlet": outer_tri[xc >= 0]}
+    else:
+        raise MeshError(f"unknown boundary layout {boundary!r}")
+    return Mesh.build(nodes, tets, (), patches)
+
+
+def generate_carved_sphere_mesh(n, radius=0.5, half=10.0, beta=None, boundary="farfield", project=True):
+    """Stair-step tet sphere-in-box (legacy stand-in; see generate_sphere_mesh).
 
     n: lattice cells per axis (about 6 n^3 tets minus the body);
     boundary: "farfield" (all sides farfield_riemann, patch "farfield") or

@@ -174,7 +174,7 @@ def test_sphere_mesh_parity_with_oracle(scheme):
     from paper_2304_09485_b200.meshgen import generate_sphere_mesh
     from paper_2304_09485_b200.stepping import SolutionField, Solver, SolverOptions
 
-    mesh = generate_sphere_mesh(8, half=4.0)
+    mesh = generate_sphere_mesh(2, far=4.0, nr=5)
     ref = np.array([1.0, 0.5, 0.02, -0.01, 1.0 / GAMMA])
     patches = {"sphere": PatchSpec("sphere", "wall_slip_adiabatic"),
                "farfield": PatchSpec("farfield", "farfield_riemann", reference=ref)}

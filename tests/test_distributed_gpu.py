@@ -22,7 +22,7 @@ def setup_case(scheme):
     from paper_2304_09485_b200.meshgen import generate_sphere_mesh
     from paper_2304_09485_b200.stepping import SolverOptions
 
-    mesh = generate_sphere_mesh(10, half=4.0)
+    mesh = generate_sphere_mesh(3, far=4.0, nr=6)
     ref = np.array([1.0, 0.5, 0.02, -0.01, 1 / 1.4])
     patches = {"sphere": PatchSpec("sphere", "wall_slip_adiabatic"),
                "farfield": PatchSpec("farfield", "farfield_riemann", reference=ref)}

@@ -7,7 +7,7 @@ import pytest
 from paper_2304_09485_b200.config import ConfigError, load_config, parse_patch
 from paper_2304_09485_b200.driver import ResidualHistory
 from paper_2304_09485_b200.mesh import MeshError, generate_box_mesh, load_mesh, save_mesh
-from paper_2304_09485_b200.meshgen import generate_sphere_mesh, generate_wing_mesh
+from paper_2304_09485_b200.meshgen import generate_carved_sphere_mesh, generate_sphere_mesh, generate_wing_mesh
 from paper_2304_09485_b200.output import read_residual_csv, write_residual_csv, write_vtk
 
 
@@ -88,11 +88,15 @@ def test_mesh_file_round_trip(tmp_path):
 
 
 def test_sphere_generator():
-    m = generate_sphere_mesh(12)
+    m = generate_sphere_mesh(3, nr=6)
     m.validate()
-    assert m.patch_names == ["sphere", "farfield"]
+    assert m.patch_names == ["sphere", "farfield"] and m.ncells == 144 * 9 * 6
     assert np.all(m.cell_volume > 0)
-    s = generate_sphere_mesh(12, boundary="supersonic")
+    wall_pts = m.fq_point[np.isin(m.fq_face, np.flatnonzero(m.face_patch == 0))]
+    assert np.allclose(np.linalg.norm(wall_pts, axis=1), 0.5, rtol=0.05)
+    c = generate_carved_sphere_mesh(12)
+    c.validate()
+    s = generate_sphere_mesh(3, boundary="supersonic")
     assert s.patch_names == ["sphere", "inlet", "outlet"]
     w = generate_wing_mesh(24)
     w.validate()

@@ -19,7 +19,7 @@ def meshes():
     return {
         "tet4p": generate_box_mesh((1, 1, 1), (4, 4, 4), split="tet", periodic=("x", "y", "z")),
         "tet4j": generate_box_mesh((1, 1, 1), (4, 4, 4), split="tet", perturb=0.15, seed=3),
-        "sphere": generate_sphere_mesh(8, half=4.0),
+        "sphere": generate_sphere_mesh(2, far=4.0, nr=5),
     }
 
 
