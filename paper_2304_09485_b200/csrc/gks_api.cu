@@ -160,7 +160,16 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   TRY(setup_array(S, "avg0", &hf, &hi, &hb, &shp));
   TRY(upload(H, &H->avg0, hf.data(), hf.size()));
   TRY(setup_array(S, "beta_mat", &hf, &hi, &hb, &shp));
-  TRY(upload(H, &H->beta, hf.data(), hf.size()));
+  {
+    // symmetric smoothness-indicator matrices: keep the upper triangle (45 of 81)
+    std::vector<double> packed(nc * 45);
+    for (int64_t c = 0; c < nc; ++c) {
+      int idx = 0;
+      for (int d = 0; d < 9; ++d)
+        for (int e = d; e < 9; ++e) packed[c * 45 + idx++] = hf[c * 81 + d * 9 + e];
+    }
+    TRY(upload(H, &H->beta, packed.data(), packed.size()));
+  }
 
   // faces
   {

@@ -8,8 +8,17 @@
 
 #include "../../include/gks.h"
 
+// Minimum resident 128-thread CTAs per SM (register budgets) for the FP64
+// flux kernels, chosen by measurement (profiles/r01): the face kernel runs
+// best at 128 regs/thread (4 CTAs), the batch kernel at 168 (3 CTAs).
+#ifndef GKS_FACE_MINB
+#define GKS_FACE_MINB 4
+#endif
 #ifndef GKS_FLUX_MINB
-#define GKS_FLUX_MINB 1  // min resident CTAs/SM for the FP64 flux kernels (register budget)
+#define GKS_FLUX_MINB 3
+#endif
+#ifndef GKS_RECON_MINB
+#define GKS_RECON_MINB 4
 #endif
 
 namespace gks {

@@ -110,10 +110,14 @@ __global__ void __launch_bounds__(128, GKS_FLUX_MINB) k_flux_batch(int64_t n, co
       for (int k = 0; k < 5; ++k) s5[d][k] = S ? S[i * 15 + d * 5 + k] : 0.0;
     return true;
   };
+  auto press = [&](double& pl, double& pr) {
+    pl = wl[i * 5] / (2.0 * wl[i * 5 + 4]);
+    pr = wr[i * 5] / (2.0 * wr[i * 5 + 4]);
+    return true;
+  };
   double f[5], p[5];
-  const bool want_point = tp != nullptr;
-  const int rc = interface_flux_sides(get, tau[i], dt[i], MODEL_INVISCID, 0.0, kc, f, want_point,
-                                      want_point ? tp[i] : 0.0, p, nullptr);
+  const int rc = tp ? interface_flux_t<false, true>(get, press, tau[i], dt[i], 0.0, kc, f, tp[i], p)
+                    : interface_flux_t<false, false>(get, press, tau[i], dt[i], 0.0, kc, f, 0.0, p);
   if (rc) {
     raise_dev(status, GKS_ERR_UNPHYSICAL, (int)i);
     return;

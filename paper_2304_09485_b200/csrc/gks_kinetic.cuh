@@ -176,42 +176,103 @@ struct FluxIn {
   double sl[3][5], sr[3][5];  // local-frame conserved slopes along (n, t1, t2)
 };
 
+// time coefficients of flux.py:162-179 (divided by dt) and of the point
+// value at time tp (flux.py:182-188)
+struct TimeCoef {
+  double c1, c2, c3, c4, c5, c6;  // flux families (g base/slope/time, f base/slope/time)
+  double g1, g2, g3, f1, f2, f3;  // point-value families
+};
+
+__device__ __forceinline__ TimeCoef time_coefficients(double tau, double dt, double tp) {
+  TimeCoef t;
+  if (isinf(tau)) {
+    // collisionless limit with slopes dropped: the KFVS split flux
+    t.c1 = t.c2 = t.c3 = t.c5 = t.c6 = 0.0;
+    t.c4 = 1.0;
+  } else {
+    const double x = dt / tau;
+    const double em1 = -expm1(-x);
+    const double e = exp(-x);
+    const double idt = 1.0 / dt;
+    t.c1 = (dt - tau * em1) * idt;
+    t.c2 = (2.0 * tau * tau * em1 - tau * dt * e - tau * dt) * idt;
+    t.c3 = (0.5 * dt * dt - tau * dt + tau * tau * em1) * idt;
+    const double c4r = tau * em1;
+    const double c5r = tau * tau * em1 - tau * dt * e;
+    t.c4 = c4r * idt;
+    t.c5 = -(tau * c4r + c5r) * idt;
+    t.c6 = -tau * c4r * idt;
+  }
+  const double e = exp(-tp / tau);
+  t.g1 = 1.0 - e;
+  t.g2 = (tp + tau) * e - tau;
+  t.g3 = tp - tau + tau * e;
+  t.f1 = e;
+  t.f2 = -(tau + tp) * e;
+  t.f3 = -tau * e;
+  return t;
+}
+
+__device__ __forceinline__ double collision_tau(double pl, double pr, double dt, bool viscous, double mu,
+                                                const double w0[5]) {
+  const double jump = fabs(pl - pr) / (pl + pr) * dt;
+  if (viscous) return mu / (w0[0] / (2.0 * w0[4])) + jump;
+  return 0.1 * dt + jump;
+}
+
 // Interface distribution -> time-averaged flux over [0, dt] (p = 1) and,
-// optionally, the point value at time tp (p = 0).  tau < 0 means "compute
-// tau from the collision model" (flux.py:211-227, stepping.py:200-207).
+// optionally (POINT), the point value at time tp (p = 0).
+//   get_side(side, w, s)   : local primitive state and conserved slopes of side 0 (left) / 1 (right)
+//   get_pressures(pl, pr)  : both side pressures, needed before the side loop when tau_in < 0
 // Returns 0 on success, 1 if an intermediate state is unphysical.
 //
 // Register plan: the two transport sides run through ONE loop body (not
-// unrolled) and only leave behind the sums the reference's families need:
-//   q0   = sum_s rho_s <psi>_s                     (compatibility, flux.py:94)
-//   dqa  = sum_s rho_s <(a_s,k . psi) psi>_s        (equilibrium slopes, :99)
-//   F4/F5/F6 = transport base / slope / time families at u^1 (flux.py:127-146)
-//   P5/P6    = the same slope / time families at u^0 (point value)
-// so each Maxwellian's moment tables die as soon as its families are formed.
-template <class SideFn>
-__device__ __forceinline__ int interface_flux_sides(const SideFn& get_side, double tau_in, double dt,
-                                                    int model, double mu, const KinConst& kc,
-                                                    double flux[5], bool want_point, double tp,
-                                                    double point[5], double* tau_out) {
+// unrolled).  When tau is known before the loop (inviscid, or given) the
+// six families of flux.py:110-159 are folded per side into one polynomial
+// weight, so a side leaves behind only
+//   q0  = sum_s rho_s <psi>_s                     (compatibility, flux.py:94)
+//   dqa = sum_s rho_s <(a_s,k . psi) psi>_s        (equilibrium slopes, :99)
+//   F   = sum_s rho_s <u (c4 + c5 a_s.c + c6 A_s) psi>_s  (transport part of the flux)
+// (+ the point-value analogue).  Viscous tau needs W0, so that path keeps
+// the three transport families separate until tau is known.
+template <bool VISCOUS, bool POINT, class SideFn, class PressFn>
+__device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const PressFn& get_pressures, double tau_in,
+                                                double dt, double mu, const KinConst& kc, double flux[5], double tp,
+                                                double point[5]) {
   double q0[5] = {0, 0, 0, 0, 0};
   double dqa[3][5] = {};
-  double F4[5] = {0, 0, 0, 0, 0}, F5[5] = {0, 0, 0, 0, 0}, F6[5] = {0, 0, 0, 0, 0};
-  double P5[5] = {0, 0, 0, 0, 0}, P6[5] = {0, 0, 0, 0, 0};
-  double pside0 = 0.0, pside1 = 0.0;
+  double F[5] = {0, 0, 0, 0, 0};   // folded transport flux (known tau) / base family (viscous)
+  double F5[5] = {0, 0, 0, 0, 0};  // viscous only: slope family
+  double F6[5] = {0, 0, 0, 0, 0};  // viscous only: time family
+  double P[5] = {0, 0, 0, 0, 0};   // point value transport part (known tau) / slope family (viscous)
+  double P6[5] = {0, 0, 0, 0, 0};  // viscous only
+  double pl = 0.0, pr = 0.0;
+  TimeCoef tc;
+  double tau = tau_in;
+  const bool tau_known = !VISCOUS || tau_in >= 0.0;
+  if (!VISCOUS) {
+    if (tau < 0.0) {
+      if (!get_pressures(pl, pr)) return 1;
+      tau = collision_tau(pl, pr, dt, false, mu, nullptr);
+    }
+    tc = time_coefficients(tau, dt, tp);
+  }
 #pragma unroll 1
   for (int side = 0; side < 2; ++side) {
-    double w[5], sl[3][5];
-    if (!get_side(side, w, sl)) return 1;
+    double w[5], a[3][5];
+    if (!get_side(side, w, a)) return 1;
     if (!prim_ok(w)) return 1;
     const double rho = w[0];
-    const double ps = rho / (2.0 * w[4]);
-    pside0 = side ? pside0 : ps;
-    pside1 = side ? ps : pside1;
-    double a[3][5], A[5];
+    if (VISCOUS) {
+      const double ps = rho / (2.0 * w[4]);
+      pl = side ? pl : ps;
+      pr = side ? ps : pr;
+    }
+    double A[5];
     Maxw m;
     maxw_full(m, w, kc);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) micro_slope(w, sl[k], kc, a[k]);
+    for (int k = 0; k < 3; ++k) micro_slope(w, a[k], kc, a[k]);  // slopes -> micro-slopes in place
     {
       // time slope from the compatibility condition (kinetic.py:305-312)
       const double zero5[5] = {0, 0, 0, 0, 0};
@@ -223,7 +284,6 @@ __device__ __forceinline__ int interface_flux_sides(const SideFn& get_side, doub
     }
     maxw_half_u(m, w, side ? -1.0 : 1.0);
     const double e0[5] = {1, 0, 0, 0, 0};
-    const double zero5[5] = {0, 0, 0, 0, 0};
     double t[5];
     wmom<0, false>(m, e0, nullptr, t);
 #pragma unroll
@@ -234,25 +294,50 @@ __device__ __forceinline__ int interface_flux_sides(const SideFn& get_side, doub
 #pragma unroll
       for (int i = 0; i < 5; ++i) dqa[k][i] += rho * t[i];
     }
-    wmom<1, false>(m, e0, nullptr, t);
+    if (tau_known && !VISCOUS) {
+      double sw[5], dw[3][5];
 #pragma unroll
-    for (int i = 0; i < 5; ++i) F4[i] += rho * t[i];
-    wmom<1, true>(m, zero5, a, t);
+      for (int i = 0; i < 5; ++i) sw[i] = tc.c6 * A[i];
+      sw[0] += tc.c4;
 #pragma unroll
-    for (int i = 0; i < 5; ++i) F5[i] += rho * t[i];
-    wmom<1, false>(m, A, nullptr, t);
+      for (int k = 0; k < 3; ++k)
 #pragma unroll
-    for (int i = 0; i < 5; ++i) F6[i] += rho * t[i];
-    if (want_point) {
-      wmom<0, true>(m, zero5, a, t);
+        for (int i = 0; i < 5; ++i) dw[k][i] = tc.c5 * a[k][i];
+      wmom<1, true>(m, sw, dw, t);
 #pragma unroll
-      for (int i = 0; i < 5; ++i) P5[i] += rho * t[i];
-      wmom<0, false>(m, A, nullptr, t);
+      for (int i = 0; i < 5; ++i) F[i] += rho * t[i];
+      if (POINT) {
 #pragma unroll
-      for (int i = 0; i < 5; ++i) P6[i] += rho * t[i];
+        for (int i = 0; i < 5; ++i) sw[i] = tc.f3 * A[i];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+#pragma unroll
+          for (int i = 0; i < 5; ++i) dw[k][i] = tc.f2 * a[k][i];
+        wmom<0, true>(m, sw, dw, t);
+#pragma unroll
+        for (int i = 0; i < 5; ++i) P[i] += rho * t[i];
+      }
+    } else {
+      const double zero5[5] = {0, 0, 0, 0, 0};
+      wmom<1, false>(m, e0, nullptr, t);
+#pragma unroll
+      for (int i = 0; i < 5; ++i) F[i] += rho * t[i];
+      wmom<1, true>(m, zero5, a, t);
+#pragma unroll
+      for (int i = 0; i < 5; ++i) F5[i] += rho * t[i];
+      wmom<1, false>(m, A, nullptr, t);
+#pragma unroll
+      for (int i = 0; i < 5; ++i) F6[i] += rho * t[i];
+      if (POINT) {
+        wmom<0, true>(m, zero5, a, t);
+#pragma unroll
+        for (int i = 0; i < 5; ++i) P[i] += rho * t[i];
+        wmom<0, false>(m, A, nullptr, t);
+#pragma unroll
+        for (int i = 0; i < 5; ++i) P6[i] += rho * t[i];
+      }
     }
   }
-  double pside[2] = {pside0, pside1};
   double w0[5];
   if (!cons_to_prim(q0, kc, w0)) return 1;
   double ab[3][5], Ab[5];
@@ -268,68 +353,40 @@ __device__ __forceinline__ int interface_flux_sides(const SideFn& get_side, doub
     for (int i = 0; i < 5; ++i) D[i] = -w0[0] * D[i];
     micro_slope(w0, D, kc, Ab);
   }
-  // collision time
-  double tau = tau_in;
-  if (tau < 0.0) {
-    const double pl = pside[0], pr = pside[1];
-    const double jump = fabs(pl - pr) / (pl + pr) * dt;
-    if (model == MODEL_VISCOUS) {
-      const double p0 = w0[0] / (2.0 * w0[4]);
-      tau = mu / p0 + jump;
-    } else {
-      tau = 0.1 * dt + jump;
+  if (VISCOUS) {
+    if (tau < 0.0) tau = collision_tau(pl, pr, dt, true, mu, w0);
+    tc = time_coefficients(tau, dt, tp);
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      F[i] = tc.c4 * F[i] + tc.c5 * F5[i] + tc.c6 * F6[i];
+      if (POINT) P[i] = tc.f2 * P[i] + tc.f3 * P6[i];
     }
   }
-  if (tau_out) *tau_out = tau;
-  // time-integrated coefficients (flux.py:162-179)
   {
-    double c1, c2, c3, c4, c5, c6;
-    if (isinf(tau)) {
-      // collisionless limit with slopes dropped: the KFVS split flux
-      c1 = c2 = c3 = c5 = c6 = 0.0;
-      c4 = 1.0;
-    } else {
-      const double x = dt / tau;
-      const double em1 = -expm1(-x);
-      const double e = exp(-x);
-      const double idt = 1.0 / dt;
-      c1 = (dt - tau * em1) * idt;
-      c2 = (2.0 * tau * tau * em1 - tau * dt * e - tau * dt) * idt;
-      c3 = (0.5 * dt * dt - tau * dt + tau * tau * em1) * idt;
-      const double c4r = tau * em1;
-      const double c5r = tau * tau * em1 - tau * dt * e;
-      c4 = c4r * idt;
-      c5 = -(tau * c4r + c5r) * idt;
-      c6 = -tau * c4r * idt;
-    }
     double s[5], d[3][5], o[5];
 #pragma unroll
-    for (int i = 0; i < 5; ++i) s[i] = c3 * Ab[i];
-    s[0] += c1;
+    for (int i = 0; i < 5; ++i) s[i] = tc.c3 * Ab[i];
+    s[0] += tc.c1;
 #pragma unroll
     for (int k = 0; k < 3; ++k)
 #pragma unroll
-      for (int i = 0; i < 5; ++i) d[k][i] = c2 * ab[k][i];
+      for (int i = 0; i < 5; ++i) d[k][i] = tc.c2 * ab[k][i];
     wmom<1, true>(m0, s, d, o);
 #pragma unroll
-    for (int i = 0; i < 5; ++i) flux[i] = w0[0] * o[i] + (c4 * F4[i] + c5 * F5[i] + c6 * F6[i]);
+    for (int i = 0; i < 5; ++i) flux[i] = w0[0] * o[i] + F[i];
   }
-  if (want_point) {
-    // flux.py:182-188 at time tp
-    const double e = exp(-tp / tau);
-    const double g1 = 1.0 - e, g2 = (tp + tau) * e - tau, g3 = tp - tau + tau * e;
-    const double f1 = e, f2 = -(tau + tp) * e, f3 = -tau * e;
+  if (POINT) {
 #pragma unroll
-    for (int i = 0; i < 5; ++i) point[i] = f1 * q0[i] + f2 * P5[i] + f3 * P6[i];
-    if (g1 != 0.0 || g2 != 0.0 || g3 != 0.0) {
+    for (int i = 0; i < 5; ++i) point[i] = tc.f1 * q0[i] + P[i];
+    if (tc.g1 != 0.0 || tc.g2 != 0.0 || tc.g3 != 0.0) {
       double s[5], d[3][5], o[5];
 #pragma unroll
-      for (int i = 0; i < 5; ++i) s[i] = g3 * Ab[i];
-      s[0] += g1;
+      for (int i = 0; i < 5; ++i) s[i] = tc.g3 * Ab[i];
+      s[0] += tc.g1;
 #pragma unroll
       for (int k = 0; k < 3; ++k)
 #pragma unroll
-        for (int i = 0; i < 5; ++i) d[k][i] = g2 * ab[k][i];
+        for (int i = 0; i < 5; ++i) d[k][i] = tc.g2 * ab[k][i];
       wmom<0, true>(m0, s, d, o);
 #pragma unroll
       for (int i = 0; i < 5; ++i) point[i] += w0[0] * o[i];
@@ -338,7 +395,7 @@ __device__ __forceinline__ int interface_flux_sides(const SideFn& get_side, doub
   return 0;
 }
 
-// Convenience form on explicit left/right inputs.
+// Convenience form on explicit left/right inputs (inviscid or given tau).
 __device__ __forceinline__ int interface_flux(const FluxIn& in, double tau_in, double dt, int model, double mu,
                                               const KinConst& kc, double flux[5], bool want_point, double tp,
                                               double point[5], double* tau_out) {
@@ -351,7 +408,18 @@ __device__ __forceinline__ int interface_flux(const FluxIn& in, double tau_in, d
       for (int i = 0; i < 5; ++i) sl[k][i] = side ? in.sr[k][i] : in.sl[k][i];
     return true;
   };
-  return interface_flux_sides(get, tau_in, dt, model, mu, kc, flux, want_point, tp, point, tau_out);
+  auto press = [&](double& pl, double& pr) {
+    pl = in.wl[0] / (2.0 * in.wl[4]);
+    pr = in.wr[0] / (2.0 * in.wr[4]);
+    return true;
+  };
+  if (!prim_ok(in.wl) || !prim_ok(in.wr)) return 1;
+  (void)tau_out;
+  if (model == MODEL_VISCOUS)
+    return want_point ? interface_flux_t<true, true>(get, press, tau_in, dt, mu, kc, flux, tp, point)
+                      : interface_flux_t<true, false>(get, press, tau_in, dt, mu, kc, flux, tp, point);
+  return want_point ? interface_flux_t<false, true>(get, press, tau_in, dt, mu, kc, flux, tp, point)
+                    : interface_flux_t<false, false>(get, press, tau_in, dt, mu, kc, flux, tp, point);
 }
 
 }  // namespace gks

@@ -85,13 +85,17 @@ __global__ void k_fill(int64_t n, double* __restrict__ dt, const double* val) {
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void combine(double cb[9], const double (&b)[8][3], const int8_t* act, int M,
                                         const double* __restrict__ B, double eps, double lw) {
+  // beta0 = c^T B c with B packed as its upper triangle (45 entries, row-major)
   double beta0 = 0.0;
+  {
+    int idx = 0;
 #pragma unroll
-  for (int d = 0; d < 9; ++d) {
-    double t = 0.0;
+    for (int d = 0; d < 9; ++d) {
+      double t = B[idx++] * cb[d];
 #pragma unroll
-    for (int e = 0; e < 9; ++e) t += B[d * 9 + e] * cb[e];
-    beta0 += cb[d] * t;
+      for (int e = d + 1; e < 9; ++e) t += 2.0 * B[idx++] * cb[e];
+      beta0 += cb[d] * t;
+    }
   }
   int nact = 0;
   double bs[8];
@@ -129,7 +133,11 @@ __device__ __forceinline__ void combine(double cb[9], const double (&b)[8][3], c
   }
 }
 
-__global__ void __launch_bounds__(TPB) k_recon_weno(int64_t nc, const double* __restrict__ q,
+// KM / SM: compile-time upper bounds of the big-stencil and sub-stencil widths
+// (loops fully unrolled with a predicate, so every gather of a thread is in
+// flight at once instead of one dependent gather chain per member).
+template <int KM, int SM>
+__global__ void __launch_bounds__(TPB, GKS_RECON_MINB) k_recon_weno(int64_t nc, const double* __restrict__ q,
                                                     const double* __restrict__ big_op, const int* __restrict__ big_gather,
                                                     int K, const double* __restrict__ sub_op,
                                                     const int* __restrict__ sub_gather, const int8_t* __restrict__ sub_active,
@@ -141,15 +149,19 @@ __global__ void __launch_bounds__(TPB) k_recon_weno(int64_t nc, const double* __
   const int64_t c = t / 5;
   const int k = (int)(t - c * 5);
   const double qc = q[c * 5 + k];
-  double cb[9];
-#pragma unroll
-  for (int d = 0; d < 9; ++d) cb[d] = 0.0;
   const double* op = big_op + c * 9 * K;
   const int* gi = big_gather + c * K;
-  for (int j = 0; j < K; ++j) {
-    const double r = q[(int64_t)gi[j] * 5 + k] - qc;
+  double r[KM];
 #pragma unroll
-    for (int d = 0; d < 9; ++d) cb[d] += op[d * K + j] * r;
+  for (int j = 0; j < KM; ++j) r[j] = j < K ? __ldg(q + (int64_t)__ldg(gi + j) * 5 + k) - qc : 0.0;
+  double cb[9];
+#pragma unroll
+  for (int d = 0; d < 9; ++d) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < KM; ++j)
+      if (j < K) acc += __ldg(op + d * K + j) * r[j];
+    cb[d] = acc;
   }
   if (!linear) {
     double b[8][3];
@@ -160,22 +172,28 @@ __global__ void __launch_bounds__(TPB) k_recon_weno(int64_t nc, const double* __
       if (m < M) {
         const double* so = sub_op + (c * M + m) * 3 * S;
         const int* sg = sub_gather + (c * M + m) * S;
-        for (int s = 0; s < S; ++s) {
-          const double r = q[(int64_t)sg[s] * 5 + k] - qc;
-          b[m][0] += so[s] * r;
-          b[m][1] += so[S + s] * r;
-          b[m][2] += so[2 * S + s] * r;
+        double rs[SM];
+#pragma unroll
+        for (int s2 = 0; s2 < SM; ++s2) rs[s2] = s2 < S ? __ldg(q + (int64_t)__ldg(sg + s2) * 5 + k) - qc : 0.0;
+#pragma unroll
+        for (int s2 = 0; s2 < SM; ++s2) {
+          if (s2 < S) {
+            b[m][0] += __ldg(so + s2) * rs[s2];
+            b[m][1] += __ldg(so + S + s2) * rs[s2];
+            b[m][2] += __ldg(so + 2 * S + s2) * rs[s2];
+          }
         }
       }
     }
-    combine(cb, b, act, M, beta + c * 81, eps, lw);
+    combine(cb, b, act, M, beta + c * 45, eps, lw);
   }
   double* out = coef + c * 45 + k;
 #pragma unroll
   for (int d = 0; d < 9; ++d) out[d * 5] = cb[d];
 }
 
-__global__ void __launch_bounds__(TPB) k_recon_hweno(int64_t nc, const double* __restrict__ q,
+template <int HAM, int HGM>
+__global__ void __launch_bounds__(TPB, GKS_RECON_MINB) k_recon_hweno(int64_t nc, const double* __restrict__ q,
                                                      const double* __restrict__ grad, const double* __restrict__ h,
                                                      const double* __restrict__ big_op, const int* __restrict__ avg_gather,
                                                      const int* __restrict__ grad_gather,
@@ -192,24 +210,35 @@ __global__ void __launch_bounds__(TPB) k_recon_hweno(int64_t nc, const double* _
   const double qc = q[c * 5 + k];
   const int W = HA + 3 * HG;
   const double* op = big_op + c * 9 * W;
+  // right-hand side: neighbour averages, then h-scaled gradients (hweno.py:147-151)
+  double ra[HAM], rg[HGM][3];
+#pragma unroll
+  for (int j = 0; j < HAM; ++j) ra[j] = j < HA ? __ldg(q + (int64_t)__ldg(avg_gather + c * HA + j) * 5 + k) - qc : 0.0;
+#pragma unroll
+  for (int g = 0; g < HGM; ++g) {
+    if (g < HG) {
+      const int64_t m = __ldg(grad_gather + c * HG + g);
+      const double sc = __ldg(grad_scale + c * HG + g);
+#pragma unroll
+      for (int x = 0; x < 3; ++x) rg[g][x] = sc * __ldg(grad + (m * 3 + x) * 5 + k);
+    } else {
+      rg[g][0] = rg[g][1] = rg[g][2] = 0.0;
+    }
+  }
   double cb[9];
 #pragma unroll
-  for (int d = 0; d < 9; ++d) cb[d] = 0.0;
-  for (int j = 0; j < HA; ++j) {
-    const double r = q[(int64_t)avg_gather[c * HA + j] * 5 + k] - qc;
+  for (int d = 0; d < 9; ++d) {
+    double acc = 0.0;
 #pragma unroll
-    for (int d = 0; d < 9; ++d) cb[d] += op[d * W + j] * r;
-  }
-  for (int g = 0; g < HG; ++g) {
-    const int64_t m = grad_gather[c * HG + g];
-    const double sc = grad_scale[c * HG + g];
+    for (int j = 0; j < HAM; ++j)
+      if (j < HA) acc += __ldg(op + d * W + j) * ra[j];
 #pragma unroll
-    for (int x = 0; x < 3; ++x) {
-      const double r = sc * grad[(m * 3 + x) * 5 + k];
-      const int j = HA + 3 * g + x;
+    for (int g = 0; g < HGM; ++g)
+      if (g < HG) {
 #pragma unroll
-      for (int d = 0; d < 9; ++d) cb[d] += op[d * W + j] * r;
-    }
+        for (int x = 0; x < 3; ++x) acc += __ldg(op + d * W + HA + 3 * g + x) * rg[g][x];
+      }
+    cb[d] = acc;
   }
   if (!linear) {
     double b[8][3];
@@ -232,10 +261,10 @@ __global__ void __launch_bounds__(TPB) k_recon_hweno(int64_t nc, const double* _
 #pragma unroll
         for (int d = 0; d < 3; ++d)
 #pragma unroll
-          for (int s = 0; s < 7; ++s) b[m][d] += so[d * 7 + s] * rhs[s];
+          for (int s2 = 0; s2 < 7; ++s2) b[m][d] += so[d * 7 + s2] * rhs[s2];
       }
     }
-    combine(cb, b, act, M, beta + c * 81, eps, lw);
+    combine(cb, b, act, M, beta + c * 45, eps, lw);
   }
   double* out = coef + c * 45 + k;
 #pragma unroll
@@ -281,6 +310,28 @@ __device__ __forceinline__ void eval_side(const double* __restrict__ q, const do
   (void)ih;
 }
 
+// value only (no gradients): the pre-loop pressures of the inviscid collision time
+__device__ __forceinline__ void eval_value(const double* __restrict__ q, const double* __restrict__ coef,
+                                           const double* __restrict__ cen, const double* __restrict__ h,
+                                           const double* __restrict__ avg0, int64_t c, const double x[3],
+                                           double val[5]) {
+  const double hc = h[c];
+  const double xt[3] = {(x[0] - cen[3 * c]) / hc, (x[1] - cen[3 * c + 1]) / hc, (x[2] - cen[3 * c + 2]) / hc};
+  const double mono[9] = {xt[0], xt[1], xt[2], xt[0] * xt[0], xt[0] * xt[1],
+                          xt[0] * xt[2], xt[1] * xt[1], xt[1] * xt[2], xt[2] * xt[2]};
+  double phi[9];
+#pragma unroll
+  for (int d = 0; d < 9; ++d) phi[d] = mono[d] - avg0[c * 9 + d];
+  const double* C = coef + c * 45;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    double v = 0.0;
+#pragma unroll
+    for (int d = 0; d < 9; ++d) v += phi[d] * C[d * 5 + k];
+    val[k] = q[c * 5 + k] + v;
+  }
+}
+
 __device__ __forceinline__ void to_local_state(const double qv[5], const double* F, double out[5]) {
   out[0] = qv[0];
   out[4] = qv[4];
@@ -320,7 +371,8 @@ struct FaceArgs {
   const int* gate;
 };
 
-__global__ void __launch_bounds__(128, GKS_FLUX_MINB) k_face(FaceArgs A) {
+template <bool VISC, bool POINT>
+__global__ void __launch_bounds__(128, GKS_FACE_MINB) k_face(FaceArgs A) {
   if (A.gate && !*A.gate) return;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.nfq) return;
@@ -365,8 +417,33 @@ __global__ void __launch_bounds__(128, GKS_FLUX_MINB) k_face(FaceArgs A) {
     local_slopes(g, F, sl);
     return true;
   };
+  // both side pressures first (inviscid tau is then known before the side loop)
+  auto press = [&](double& pl, double& pr) {
+    const double x[3] = {A.fq_point[3 * i], A.fq_point[3 * i + 1], A.fq_point[3 * i + 2]};
+    double v[5], w[5];
+    eval_value(A.q, A.coef, A.cen, A.h, A.avg0, o, x, v);
+    if (!cons_to_prim(v, A.kc, w)) return false;
+    pl = w[0] / (2.0 * w[4]);
+    if (nb >= 0) {
+      const double xs[3] = {x[0] - A.f_shift[3 * f], x[1] - A.f_shift[3 * f + 1], x[2] - A.f_shift[3 * f + 2]};
+      eval_value(A.q, A.coef, A.cen, A.h, A.avg0, nb, xs, v);
+    } else {
+      const DevPatch P = A.patches[p];
+      const double nrm[3] = {A.f_normal[3 * f], A.f_normal[3 * f + 1], A.f_normal[3 * f + 2]};
+      double vg[5];
+      if (!ghost_state(v, P, nrm, A.kc, vg)) {
+        ghost_fail = 1;
+        return false;
+      }
+#pragma unroll
+      for (int k = 0; k < 5; ++k) v[k] = vg[k];
+    }
+    if (!cons_to_prim(v, A.kc, w)) return false;
+    pr = w[0] / (2.0 * w[4]);
+    return true;
+  };
   double fl[5], pv[5];
-  const int rc = interface_flux_sides(get, -1.0, dtf, A.model, A.mu, A.kc, fl, A.want_point != 0, 0.0, pv, nullptr);
+  const int rc = interface_flux_t<VISC, POINT>(get, press, -1.0, dtf, A.mu, A.kc, fl, 0.0, pv);
   if (rc) {
     if (ghost_fail) {
       atomicCAS(A.status, 0, GKS_ERR_UNPHYSICAL);
@@ -385,7 +462,7 @@ __global__ void __launch_bounds__(128, GKS_FLUX_MINB) k_face(FaceArgs A) {
   out[4] = ws * fl[4];
 #pragma unroll
   for (int d = 0; d < 3; ++d) out[1 + d] = ws * (F[d] * fl[1] + F[3 + d] * fl[2] + F[6 + d] * fl[3]);
-  if (A.want_point) {
+  if (POINT) {
     double* qp = A.qpt + i * 5;
     qp[0] = pv[0];
     qp[4] = pv[4];
@@ -508,14 +585,26 @@ int local_dt_device(Handle* H) {
 int residual_device(Handle* H, const double* q, double* res, bool with_gradients, const int* gate) {
   const int64_t n5 = H->n_recon * 5;  // owned + layer-1 ghosts (redundant reconstruction)
   if (H->compact) {
-    GKS_LAUNCH(KC_RECON, k_recon_hweno, blocks_for(n5, TPB), TPB, 0, H->stream, 
-        H->n_recon, q, H->grad, H->h, H->big_op, H->avg_gather, H->grad_gather, H->grad_scale, H->HA, H->HG,
-        H->sub_op, H->sub_gather, H->sub_active, H->HM, H->beta, H->linear_weights, H->eps, H->lw, H->coef, gate);
+    const int nb5 = blocks_for(n5, TPB);
+#define GKS_HWENO(HAM, HGM)                                                                                       \
+  GKS_LAUNCH(KC_RECON, (k_recon_hweno<HAM, HGM>), nb5, TPB, 0, H->stream, H->n_recon, q, H->grad, H->h, H->big_op, \
+             H->avg_gather, H->grad_gather, H->grad_scale, H->HA, H->HG, H->sub_op, H->sub_gather, H->sub_active,   \
+             H->HM, H->beta, H->linear_weights, H->eps, H->lw, H->coef, gate)
+    if (H->HA <= 4 && H->HG <= 5) GKS_HWENO(4, 5);
+    else if (H->HA <= 6 && H->HG <= 7) GKS_HWENO(6, 7);
+    else GKS_HWENO(16, 17);
+#undef GKS_HWENO
   } else {
-    GKS_LAUNCH(KC_RECON, k_recon_weno, blocks_for(n5, TPB), TPB, 0, H->stream, H->n_recon, q, H->big_op, H->big_gather, H->K,
-                                                              H->sub_op, H->sub_gather, H->sub_active, H->M, H->S,
-                                                              H->beta, H->linear_weights, H->eps, H->lw, H->coef,
-                                                              gate);
+    const int nb5 = blocks_for(n5, TPB);
+#define GKS_WENO(KM, SM)                                                                                        \
+  GKS_LAUNCH(KC_RECON, (k_recon_weno<KM, SM>), nb5, TPB, 0, H->stream, H->n_recon, q, H->big_op, H->big_gather,  \
+             H->K, H->sub_op, H->sub_gather, H->sub_active, H->M, H->S, H->beta, H->linear_weights, H->eps, H->lw, \
+             H->coef, gate)
+    if (H->K <= 16 && H->S <= 6) GKS_WENO(16, 6);
+    else if (H->K <= 24 && H->S <= 6) GKS_WENO(24, 6);
+    else if (H->K <= 32 && H->S <= 8) GKS_WENO(32, 8);
+    else GKS_WENO(64, 16);
+#undef GKS_WENO
   }
   FaceArgs A;
   A.nfq = H->nfq;
@@ -525,7 +614,14 @@ int residual_device(Handle* H, const double* q, double* res, bool with_gradients
   A.f_shift = H->f_shift; A.patches = H->patches; A.model = H->model; A.mu = H->mu; A.kc = H->kc;
   A.want_point = with_gradients ? 1 : 0;
   A.contrib = H->contrib; A.qpt = H->qpt; A.status = H->status; A.gate = gate;
-  GKS_LAUNCH(KC_FACE, k_face, blocks_for(H->nfq, 128), 128, 0, H->stream, A);
+  const int fb = blocks_for(H->nfq, 128);
+  if (H->model == 1) {
+    if (with_gradients) GKS_LAUNCH(KC_FACE, (k_face<true, true>), fb, 128, 0, H->stream, A);
+    else GKS_LAUNCH(KC_FACE, (k_face<true, false>), fb, 128, 0, H->stream, A);
+  } else {
+    if (with_gradients) GKS_LAUNCH(KC_FACE, (k_face<false, true>), fb, 128, 0, H->stream, A);
+    else GKS_LAUNCH(KC_FACE, (k_face<false, false>), fb, 128, 0, H->stream, A);
+  }
   GKS_LAUNCH(KC_ASSEMBLE, k_assemble, blocks_for(H->n_owned, TPB), TPB, 0, H->stream, H->n_owned, H->cfq_start, H->cfq, H->contrib, H->qpt,
                                                              H->fq_face, H->fq_ws, H->f_normal, H->vol, res,
                                                              with_gradients ? H->grad_new : nullptr, gate);
