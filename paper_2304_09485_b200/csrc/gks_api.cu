@@ -3,6 +3,7 @@
 // copies host arrays in, runs the device path and copies results out; the
 // *_device variants keep the state resident for the benchmark loop.
 #include <stddef.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -262,10 +263,11 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
     });
     const int64_t nkept = order.size();
     H->nnz = nkept;
-    std::vector<int> rowptr(H->n_owned + 1, 0), col(nkept), fslot(2 * nf, -1);
+    std::vector<int> rowptr(H->n_owned + 1, 0), col(nkept), fslot(2 * nf, -1), ent(std::max<int64_t>(nkept, 1));
     for (int64_t p = 0; p < nkept; ++p) {
       const int64_t e = order[p];
       col[p] = (int)ecol[e];
+      ent[p] = (ifaces[e / 2] << 1) | (int)(e & 1);
       rowptr[erow[e] + 1]++;
       fslot[2 * ifaces[e / 2] + (e & 1)] = (int)p;
     }
@@ -280,6 +282,13 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
     GKS_CUDA(cudaMemcpy(A->rowptr, rowptr.data(), (H->n_owned + 1) * sizeof(int), cudaMemcpyHostToDevice));
     if (nkept) GKS_CUDA(cudaMemcpy(A->col, col.data(), nkept * sizeof(int), cudaMemcpyHostToDevice));
     G->jac.owned = false;
+    // matrix-free Roe products for the handle's Jacobian (GKS_ROE_MF=0 streams the stored blocks)
+    const char* mf = getenv("GKS_ROE_MF");
+    A->mf = (mf && mf[0] == '0') ? 0 : 1;
+    A->gm1 = o->gamma - 1.0;
+    TRY(upload(H, &A->ent, ent.data(), ent.size()));
+    TRY(alloc(H, &A->fdat, (size_t)std::max<int64_t>(nf, 1) * 5));
+    TRY(alloc(H, &A->prim, (size_t)nc * 5));
   }
 
   // reconstruction operators

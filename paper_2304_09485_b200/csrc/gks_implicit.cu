@@ -155,7 +155,8 @@ __global__ void k_copy(int64_t n, double* __restrict__ out, const double* __rest
 __global__ void k_jac_faces(int64_t nfi, const int* __restrict__ ifaces, const int* __restrict__ f_own,
                             const int* __restrict__ f_nbr, const double* __restrict__ f_normal,
                             const double* __restrict__ f_area, const double* __restrict__ q,
-                            const int* __restrict__ fslot, double gam, double* __restrict__ off) {
+                            const int* __restrict__ fslot, double gam, double* __restrict__ off,
+                            double* __restrict__ fdat) {
   const int64_t fi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (fi >= nfi) return;
   const int f = ifaces[fi];
@@ -169,6 +170,10 @@ __global__ void k_jac_faces(int64_t nfi, const int* __restrict__ ifaces, const i
   const double n[3] = {f_normal[3 * f], f_normal[3 * f + 1], f_normal[3 * f + 2]};
   const double lam = spectral_radius(qm, n, gam);
   const double hs = 0.5 * f_area[f];
+  if (fdat) {
+    double* fd = fdat + (int64_t)f * 5;
+    fd[0] = n[0]; fd[1] = n[1]; fd[2] = n[2]; fd[3] = hs; fd[4] = lam;
+  }
   double J[5][5];
   // rows of ghost cells (cut faces on a partitioned mesh) have no slot
   if (fslot[2 * f] >= 0) {
@@ -477,6 +482,80 @@ __global__ void k_sub(int64_t n, double* __restrict__ r, const double* __restric
     r[i] = b[i] - t[i];
 }
 
+// per-cell primitives for the matrix-free Roe products (jacobian.py:37-61 inputs)
+__global__ void k_roe_prim(int64_t n, const double* __restrict__ q, double gm1, double* __restrict__ prim) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const double rho = q[c * 5];
+  const double vx = q[c * 5 + 1] / rho, vy = q[c * 5 + 2] / rho, vz = q[c * 5 + 3] / rho;
+  const double ke = 0.5 * (vx * vx + vy * vy + vz * vz);
+  const double p = gm1 * (q[c * 5 + 4] - rho * ke);
+  double* P = prim + c * 5;
+  P[0] = vx; P[1] = vy; P[2] = vz; P[3] = (q[c * 5 + 4] + p) / rho; P[4] = ke;
+}
+
+// Same MODE bits as k_block, one thread per cell: the off-diagonal sum is
+// recomputed entry by entry (in the CSR order of the stored path)
+//   J(Q,n) x = (mx, v a + un x_m + n b, H a + un (b + x4)),
+//   a = mx - un x0,  b = (gamma-1)(ke x0 - v.x_m + x4),  mx = n.x_m
+template <int MODE>
+__global__ void __launch_bounds__(128) k_roe_mf(int64_t nc, const int* __restrict__ rowptr,
+                                                const int* __restrict__ col, const int* __restrict__ ent,
+                                                const double* __restrict__ fdat, const double* __restrict__ prim,
+                                                double gm1, const double* __restrict__ diag,
+                                                const double* __restrict__ dinv, const double* __restrict__ x,
+                                                const double* __restrict__ b, double* __restrict__ out,
+                                                double* __restrict__ out_pre, const int* gate) {
+  if (gate && !*gate) return;
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  double o[5] = {0, 0, 0, 0, 0};
+  for (int e = rowptr[c]; e < rowptr[c + 1]; ++e) {
+    const int64_t j = col[e];
+    const int en = __ldg(ent + e);
+    const double* fd = fdat + (int64_t)(en >> 1) * 5;
+    const double sg = (en & 1) ? -1.0 : 1.0;
+    const double nx = fd[0], ny = fd[1], nz = fd[2], hs = fd[3], lam = fd[4];
+    const double* P = prim + j * 5;
+    const double vx = P[0], vy = P[1], vz = P[2], H = P[3], ke = P[4];
+    const double* xj = x + j * 5;
+    const double x0 = xj[0], x1 = xj[1], x2 = xj[2], x3 = xj[3], x4 = xj[4];
+    const double mx = nx * x1 + ny * x2 + nz * x3;
+    const double un = nx * vx + ny * vy + nz * vz;
+    const double a = mx - un * x0;
+    const double bb = gm1 * (ke * x0 - (vx * x1 + vy * x2 + vz * x3) + x4);
+    const double sh = sg * hs, lh = lam * hs;
+    o[0] += sh * mx - lh * x0;
+    o[1] += sh * (vx * a + un * x1 + nx * bb) - lh * x1;
+    o[2] += sh * (vy * a + un * x2 + ny * bb) - lh * x2;
+    o[3] += sh * (vz * a + un * x3 + nz * bb) - lh * x3;
+    o[4] += sh * (H * a + un * (bb + x4)) - lh * x4;
+  }
+  double r[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    double acc = o[i];
+    if (MODE & 1) {
+      const double* Dr = diag + c * 25 + i * 5;
+      const double* xc = x + c * 5;
+      acc = (Dr[0] * xc[0] + Dr[1] * xc[1] + Dr[2] * xc[2] + Dr[3] * xc[3] + Dr[4] * xc[4]) + acc;
+    }
+    if (MODE & 2) acc = b[c * 5 + i] - acc;
+    r[i] = acc;
+    if (out_pre) out_pre[c * 5 + i] = acc;
+  }
+  if (MODE & 4) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const double* Xr = dinv + c * 25 + i * 5;
+      out[c * 5 + i] = Xr[0] * r[0] + Xr[1] * r[1] + Xr[2] * r[2] + Xr[3] * r[3] + Xr[4] * r[4];
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) out[c * 5 + i] = r[i];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -547,18 +626,30 @@ static inline void halo(BlockSys* A, const double* x) {
   if (A->halo_x) A->halo_x(const_cast<double*>(x));
 }
 
+// one block product of kind MODE: stored blocks (cell x row threads) or the
+// matrix-free Roe form (one thread per cell)
+template <int MODE>
+static void block_product(BlockSys* A, const double* x, const double* b, double* out, double* pre, const int* gate) {
+  const int kc = (MODE == 6) ? KC_JACOBI : KC_SPMV;
+  if (A->mf) {
+    GKS_LAUNCH(kc, k_roe_mf<MODE>, blocks_for(A->nc, 128), 128, 0, A->stream, A->nc, A->rowptr, A->col, A->ent,
+               A->fdat, A->prim, A->gm1, A->diag, A->dinv, x, b, out, pre, gate);
+  } else {
+    GKS_LAUNCH(kc, k_block<MODE>, cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream, A->nc, A->rowptr, A->col, A->off,
+               A->diag, A->dinv, x, b, out, pre, gate);
+  }
+}
+
 // y = A x  (diag + off)
 void bs_spmv(BlockSys* A, const double* x, double* y, const int* gate) {
   halo(A, x);
-  GKS_LAUNCH(KC_SPMV, k_block<1>, cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream, A->nc, A->rowptr, A->col, A->off, A->diag,
-                                                                    A->dinv, x, nullptr, y, nullptr, gate);
+  block_product<1>(A, x, nullptr, y, nullptr, gate);
 }
 
 // y = (L+U) x
 void bs_offdiag(BlockSys* A, const double* x, double* y, const int* gate) {
   halo(A, x);
-  GKS_LAUNCH(KC_SPMV, k_block<0>, cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream, A->nc, A->rowptr, A->col, A->off, A->diag,
-                                                                    A->dinv, x, nullptr, y, nullptr, gate);
+  block_product<0>(A, x, nullptr, y, nullptr, gate);
 }
 
 // z = P^-1 b : z0 = D^-1 b, then kmax sweeps z <- D^-1 (b - (L+U) z)  (krylov.py:24-34)
@@ -570,8 +661,7 @@ void bs_jacobi(BlockSys* A, const double* b, double* z, double* tmp, int kmax, c
   double* nxt = tmp;
   for (int k = 0; k < kmax; ++k) {
     halo(A, cur);
-    GKS_LAUNCH(KC_JACOBI, k_block<6>, cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream, A->nc, A->rowptr, A->col, A->off, A->diag,
-                                                                      A->dinv, cur, b, nxt, nullptr, gate);
+    block_product<6>(A, cur, b, nxt, nullptr, gate);
     std::swap(cur, nxt);
   }
   if (cur != z) {
@@ -582,14 +672,12 @@ void bs_jacobi(BlockSys* A, const double* b, double* z, double* tmp, int kmax, c
 // w = P^-1 A v : fused spmv + first D^-1, then sweeps
 void bs_prec_matvec(BlockSys* A, const double* v, double* w, double* t, double* tmp, int kmax, const int* gate) {
   halo(A, v);
-  GKS_LAUNCH(KC_SPMV, k_block<5>, cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream, A->nc, A->rowptr, A->col, A->off, A->diag,
-                                                                    A->dinv, v, nullptr, w, t, gate);
+  block_product<5>(A, v, nullptr, w, t, gate);
   double* cur = w;
   double* nxt = tmp;
   for (int k = 0; k < kmax; ++k) {
     halo(A, cur);
-    GKS_LAUNCH(KC_JACOBI, k_block<6>, cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream, A->nc, A->rowptr, A->col, A->off, A->diag,
-                                                                      A->dinv, cur, t, nxt, nullptr, gate);
+    block_product<6>(A, cur, t, nxt, nullptr, gate);
     std::swap(cur, nxt);
   }
   if (cur != w) {
@@ -743,7 +831,10 @@ int jacobian_assemble(Handle* H, BlockSys* A, const double* ghosts_dev) {
   if (H->nfi)
     GKS_LAUNCH(KC_JAC_FACE, k_jac_faces, blocks_for(H->nfi, 128), 128, 0, H->stream, H->nfi, H->interior_faces, H->f_own, H->f_nbr,
                                                                  H->f_normal, H->f_area, H->q, H->face_slot,
-                                                                 H->gamma, A->off);
+                                                                 H->gamma, A->off, A->fdat);
+  if (A->mf)
+    GKS_LAUNCH(KC_JAC_FACE, k_roe_prim, blocks_for(H->n_recon, 128), 128, 0, H->stream, H->n_recon, H->q,
+               H->gamma - 1.0, A->prim);
   GKS_LAUNCH(KC_JAC_DIAG, k_jac_diag, blocks_for(H->n_owned, 128), 128, 0, H->stream, H->n_owned, H->cjd_start,
              H->cjd, H->f_own, H->f_nbr, H->f_normal, H->f_area, H->bidx, ghosts_dev, H->q, H->vol, H->dt, H->gamma,
              A->diag, A->dinv, A->status);

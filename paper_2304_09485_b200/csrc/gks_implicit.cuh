@@ -49,6 +49,14 @@ struct BlockSys {
   int dinv_ok = 0;
   cudaStream_t stream = nullptr;
   KrylovWS ws;
+  // matrix-free Roe off-diagonal products (handle-owned Jacobians): instead of
+  // streaming the stored 5x5 blocks, recompute hs*(+-J(Q_j,n) x_j - lam x_j)
+  // from per-face (n, hs, lam) and per-cell primitives (v, H, ke)
+  int mf = 0;
+  int* ent = nullptr;      // per CSR slot: face << 1 | side (side 0: the row is the face owner)
+  double* fdat = nullptr;  // per local face: nx, ny, nz, hs = S/2, lam
+  double* prim = nullptr;  // per local cell: vx, vy, vz, H, ke
+  double gm1 = 0.4;
 };
 
 struct GmresParams {

@@ -86,9 +86,15 @@ __device__ __forceinline__ void mono_acc(const Maxw& m, double k, double o[5]) {
 }
 
 // <u^P W(c) psi> with W(c) = s.psi(c) + DIR * sum_k c_k d_k.psi(c).
+// GKS_WMOM_NOINLINE keeps one out-of-line copy per (P, DIR) instead of one
+// per call site (instruction-cache pressure of the fused flux kernel).
+#ifdef GKS_WMOM_NOINLINE
+#define GKS_WMOM_ATTR __device__ __noinline__
+#else
+#define GKS_WMOM_ATTR __device__ __forceinline__
+#endif
 template <int P, bool DIR>
-__device__ __forceinline__ void wmom(const Maxw& m, const double s[5], const double (*d)[5],
-                                     double o[5]) {
+GKS_WMOM_ATTR void wmom(const Maxw& m, const double s[5], const double (*d)[5], double o[5]) {
   o[0] = o[1] = o[2] = o[3] = o[4] = 0.0;
   const double hs = 0.5 * s[4];
   if (!DIR) {
