@@ -399,6 +399,10 @@ struct Geo {
 
 extern "C" {
 
+// Memory-lean build (10^7-cell meshes): a sizing pass, then every cell
+// rebuilds its stencil and writes its operators straight into the final
+// padded arrays; per-cell stencil objects are never kept.  The CSR stencil
+// tables are only exported when asked for (schemes == 0 or bit 2).
 int gks_setup_build(const GksMeshDesc* m, int schemes, int nthreads, GksSetup** out) {
   if (!m || !out || m->ncells <= 0) {
     gks::set_error("gks_setup_build: bad arguments");
@@ -413,62 +417,83 @@ int gks_setup_build(const GksMeshDesc* m, int schemes, int nthreads, GksSetup** 
     nfpc = std::max<int>(nfpc, (int)(m->cell_face_start[c + 1] - m->cell_face_start[c]));
   S->nfpc = nfpc;
   MeshView mv{m};
-  std::vector<CellStencil> cs(nc);
+  const bool want_weno = schemes & 1, want_hweno = schemes & 2;
+  const bool want_stencils = schemes == 0 || (schemes & 4);
+
+  // ---- pass A: sizes ------------------------------------------------------
+  std::vector<int32_t> big_n(nc), sub_n(nc), nbr_n(nc);
+  std::vector<int8_t> wfb(nc), hfb(nc);
+  int64_t sub_len_max = 0;
+#pragma omp parallel for schedule(dynamic, 256) reduction(max : sub_len_max)
+  for (int64_t c = 0; c < nc; ++c) {
+    CellStencil st;
+    build_cell_stencil(m, mv, c, st);
+    big_n[c] = (int32_t)st.big.size();
+    sub_n[c] = (int32_t)st.subs.size();
+    int present = 0;
+    for (int64_t id : st.nbr) present += id >= 0;
+    nbr_n[c] = present;
+    wfb[c] = st.weno_fallback;
+    hfb[c] = st.hweno_fallback;
+    for (auto& sub : st.subs) sub_len_max = std::max<int64_t>(sub_len_max, (int64_t)sub.size() - 1);
+  }
+  S->weno_fallback = wfb;
+  S->hweno_fallback = hfb;
+
+  // ---- optional stencil export (CSR) ---------------------------------------
+  if (want_stencils) {
+    S->nbr_ids.assign(nc * nfpc, -1);
+    S->nbr_shift.assign(nc * nfpc * 3, 0.0);
+    S->big_start.assign(nc + 1, 0);
+    S->sub_cell_start.assign(nc + 1, 0);
+    for (int64_t c = 0; c < nc; ++c) {
+      S->big_start[c + 1] = S->big_start[c] + big_n[c];
+      S->sub_cell_start[c + 1] = S->sub_cell_start[c] + sub_n[c];
+    }
+    S->big_ids.resize(S->big_start[nc]);
+    S->big_shift.resize(S->big_start[nc] * 3);
+    std::vector<int64_t> sub_len(S->sub_cell_start[nc], 0);
+    // member counts per sub need the stencils: one more pass
 #pragma omp parallel for schedule(dynamic, 256)
-  for (int64_t c = 0; c < nc; ++c) build_cell_stencil(m, mv, c, cs[c]);
-
-  // flatten stencils
-  S->nbr_ids.assign(nc * nfpc, -1);
-  S->nbr_shift.assign(nc * nfpc * 3, 0.0);
-  S->big_start.assign(nc + 1, 0);
-  S->sub_cell_start.assign(nc + 1, 0);
-  S->weno_fallback.assign(nc, 0);
-  S->hweno_fallback.assign(nc, 0);
-  for (int64_t c = 0; c < nc; ++c) {
-    S->big_start[c + 1] = S->big_start[c] + (int64_t)cs[c].big.size();
-    S->sub_cell_start[c + 1] = S->sub_cell_start[c] + (int64_t)cs[c].subs.size();
-    S->weno_fallback[c] = cs[c].weno_fallback;
-    S->hweno_fallback[c] = cs[c].hweno_fallback;
-    for (size_t k = 0; k < cs[c].nbr.size(); ++k) {
-      S->nbr_ids[c * nfpc + k] = cs[c].nbr[k];
-      S->nbr_shift[(c * nfpc + k) * 3 + 0] = cs[c].nbr_s[k].x;
-      S->nbr_shift[(c * nfpc + k) * 3 + 1] = cs[c].nbr_s[k].y;
-      S->nbr_shift[(c * nfpc + k) * 3 + 2] = cs[c].nbr_s[k].z;
+    for (int64_t c = 0; c < nc; ++c) {
+      CellStencil st;
+      build_cell_stencil(m, mv, c, st);
+      int64_t si = S->sub_cell_start[c];
+      for (auto& sub : st.subs) sub_len[si++] = (int64_t)sub.size();
     }
-  }
-  S->big_ids.resize(S->big_start[nc]);
-  S->big_shift.resize(S->big_start[nc] * 3);
-  S->sub_member_start.assign(S->sub_cell_start[nc] + 1, 0);
-  {
-    int64_t si = 0;
-    for (int64_t c = 0; c < nc; ++c)
-      for (auto& sub : cs[c].subs) {
-        S->sub_member_start[si + 1] = S->sub_member_start[si] + (int64_t)sub.size();
-        ++si;
+    S->sub_member_start.assign(sub_len.size() + 1, 0);
+    for (size_t k = 0; k < sub_len.size(); ++k) S->sub_member_start[k + 1] = S->sub_member_start[k] + sub_len[k];
+    S->sub_ids.resize(S->sub_member_start.back());
+    S->sub_shift.resize(S->sub_member_start.back() * 3);
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int64_t c = 0; c < nc; ++c) {
+      CellStencil st;
+      build_cell_stencil(m, mv, c, st);
+      for (size_t k = 0; k < st.nbr.size(); ++k) {
+        S->nbr_ids[c * nfpc + k] = st.nbr[k];
+        S->nbr_shift[(c * nfpc + k) * 3 + 0] = st.nbr_s[k].x;
+        S->nbr_shift[(c * nfpc + k) * 3 + 1] = st.nbr_s[k].y;
+        S->nbr_shift[(c * nfpc + k) * 3 + 2] = st.nbr_s[k].z;
       }
-  }
-  S->sub_ids.resize(S->sub_member_start.back());
-  S->sub_shift.resize(S->sub_member_start.back() * 3);
-#pragma omp parallel for schedule(static)
-  for (int64_t c = 0; c < nc; ++c) {
-    int64_t b = S->big_start[c];
-    for (auto& mb : cs[c].big) {
-      S->big_ids[b] = mb.id;
-      S->big_shift[3 * b] = mb.s.x; S->big_shift[3 * b + 1] = mb.s.y; S->big_shift[3 * b + 2] = mb.s.z;
-      ++b;
-    }
-    int64_t si = S->sub_cell_start[c];
-    for (auto& sub : cs[c].subs) {
-      int64_t q = S->sub_member_start[si++];
-      for (auto& mb : sub) {
-        S->sub_ids[q] = mb.id;
-        S->sub_shift[3 * q] = mb.s.x; S->sub_shift[3 * q + 1] = mb.s.y; S->sub_shift[3 * q + 2] = mb.s.z;
-        ++q;
+      int64_t b = S->big_start[c];
+      for (auto& mb : st.big) {
+        S->big_ids[b] = mb.id;
+        S->big_shift[3 * b] = mb.s.x; S->big_shift[3 * b + 1] = mb.s.y; S->big_shift[3 * b + 2] = mb.s.z;
+        ++b;
+      }
+      int64_t si = S->sub_cell_start[c];
+      for (auto& sub : st.subs) {
+        int64_t q = S->sub_member_start[si++];
+        for (auto& mb : sub) {
+          S->sub_ids[q] = mb.id;
+          S->sub_shift[3 * q] = mb.s.x; S->sub_shift[3 * q + 1] = mb.s.y; S->sub_shift[3 * q + 2] = mb.s.z;
+          ++q;
+        }
       }
     }
   }
 
-  // recon geometry (recon.py:104-146)
+  // ---- recon geometry (recon.py:104-146) ----------------------------------
   Geo geo{m};
   S->avg0.assign(nc * NCOEF, 0.0);
   S->beta.assign(nc * NCOEF * NCOEF, 0.0);
@@ -496,43 +521,65 @@ int gks_setup_build(const GksMeshDesc* m, int schemes, int nthreads, GksSetup** 
     for (int d = 0; d < NCOEF; ++d) row[d] -= S->avg0[c * NCOEF + d];
   };
 
-  if (schemes & 1) {
-    // WENO operators (recon.py:216-274)
-    std::vector<std::vector<double>> bops(nc);
-    std::vector<int> bcols(nc);
-    std::vector<std::vector<std::vector<double>>> sops(nc);
-    std::vector<std::vector<std::vector<int64_t>>> sids(nc);
+  if (want_weno) {
+    // WENO operators (recon.py:216-274) written in place with upper-bound widths
+    int64_t kmax = 1, mup = 1;
+    for (int64_t c = 0; c < nc; ++c) {
+      kmax = std::max<int64_t>(kmax, std::max(big_n[c] - 1, 1));
+      mup = std::max<int64_t>(mup, sub_n[c]);
+    }
+    const int64_t sup = std::max<int64_t>(sub_len_max, 1);
+    S->w_big_op.assign(nc * NCOEF * kmax, 0.0);
+    S->w_big_gather.assign(nc * kmax, 0);
+    S->w_sub_op.assign(nc * mup * 3 * sup, 0.0);
+    S->w_sub_gather.assign(nc * mup * sup, 0);
+    S->w_sub_active.assign(nc * mup, 0);
     S->w_big_degree.assign(nc, 2);
+    std::vector<int32_t> msurv(nc, 0), ssurv(nc, 0);
 #pragma omp parallel for schedule(dynamic, 64)
     for (int64_t c = 0; c < nc; ++c) {
-      const CellStencil& st = cs[c];
+      CellStencil st;
+      build_cell_stencil(m, mv, c, st);
+      int nsurv = 0, scols = 0;
       for (auto& sub : st.subs) {
         const int S1 = (int)sub.size() - 1;
-        std::vector<double> rows(S1 * 3), full(NCOEF);
+        std::vector<double> rows(S1 * 3), full(NCOEF), op(3 * S1);
         for (int k = 1; k <= S1; ++k) {
           member_row(c, sub[k], full.data());
           for (int d = 0; d < 3; ++d) rows[(k - 1) * 3 + d] = full[d];
         }
-        std::vector<double> op(3 * S1);
         if (!pinv(S1, 3, rows.data(), 3, op.data())) continue;
-        sops[c].push_back(op);
-        std::vector<int64_t> ids;
-        for (int k = 1; k <= S1; ++k) ids.push_back(sub[k].id);
-        sids[c].push_back(ids);
+        for (int d = 0; d < 3; ++d)
+          for (int k = 0; k < S1; ++k) S->w_sub_op[((c * mup + nsurv) * 3 + d) * sup + k] = op[d * S1 + k];
+        for (int k = 0; k < S1; ++k) S->w_sub_gather[(c * mup + nsurv) * sup + k] = sub[k + 1].id;
+        S->w_sub_active[c * mup + nsurv] = 1;
+        scols = std::max(scols, S1);
+        ++nsurv;
       }
-      if (sops[c].size() < 2) { sops[c].clear(); sids[c].clear(); }
+      if (nsurv < 2) {  // fewer than two candidates: drop them all
+        for (int mm = 0; mm < nsurv; ++mm) {
+          S->w_sub_active[c * mup + mm] = 0;
+          for (int64_t k = 0; k < 3 * sup; ++k) S->w_sub_op[(c * mup + mm) * 3 * sup + k] = 0.0;
+          for (int64_t k = 0; k < sup; ++k) S->w_sub_gather[(c * mup + mm) * sup + k] = 0;
+        }
+        nsurv = 0;
+        scols = 0;
+      }
+      msurv[c] = nsurv;
+      ssurv[c] = scols;
       const int R = (int)st.big.size() - 1;
       std::vector<double> rows((size_t)std::max(R, 0) * NCOEF);
       for (int k = 1; k <= R; ++k) member_row(c, st.big[k], &rows[(k - 1) * NCOEF]);
       std::vector<double> op;
       bool ok = false;
-      if (!sops[c].empty() && R >= NCOEF) {
+      if (nsurv && R >= NCOEF) {
         op.assign((size_t)NCOEF * R, 0.0);
         ok = pinv(R, NCOEF, rows.data(), NCOEF, op.data());
       }
+      int cols = R;
       if (!ok) {
         S->w_big_degree[c] = 1;
-        const int cols = std::max(R, 1);
+        cols = std::max(R, 1);
         op.assign((size_t)NCOEF * cols, 0.0);
         if (R >= 3) {
           std::vector<double> lr(R * 3), lin(3 * R);
@@ -542,52 +589,64 @@ int gks_setup_build(const GksMeshDesc* m, int schemes, int nthreads, GksSetup** 
             for (int d = 0; d < 3; ++d)
               for (int k = 0; k < R; ++k) op[d * cols + k] = lin[d * R + k];
         }
-        bcols[c] = cols;
-      } else {
-        bcols[c] = R;
       }
-      bops[c] = op;
-    }
-    int64_t kmax = 1, mmax = 0, smax = 1;
-    for (int64_t c = 0; c < nc; ++c) {
-      kmax = std::max<int64_t>(kmax, bcols[c]);
-      mmax = std::max<int64_t>(mmax, (int64_t)sops[c].size());
-      for (auto& op : sops[c]) smax = std::max<int64_t>(smax, (int64_t)op.size() / 3);
-    }
-    // reference: kmax = max op columns (>= 1); mmax = max(mmax, 1)
-    mmax = std::max<int64_t>(mmax, 1);
-    S->w_kmax = kmax; S->w_mmax = mmax; S->w_smax = smax;
-    S->w_big_op.assign(nc * NCOEF * kmax, 0.0);
-    S->w_big_gather.assign(nc * kmax, 0);
-    S->w_sub_op.assign(nc * mmax * 3 * smax, 0.0);
-    S->w_sub_gather.assign(nc * mmax * smax, 0);
-    S->w_sub_active.assign(nc * mmax, 0);
-#pragma omp parallel for schedule(static)
-    for (int64_t c = 0; c < nc; ++c) {
-      const int cols = bcols[c];
       for (int d = 0; d < NCOEF; ++d)
-        for (int k = 0; k < cols; ++k) S->w_big_op[(c * NCOEF + d) * kmax + k] = bops[c][d * cols + k];
-      for (int64_t k = 1; k < (int64_t)cs[c].big.size(); ++k) S->w_big_gather[c * kmax + k - 1] = cs[c].big[k].id;
-      for (size_t mm = 0; mm < sops[c].size(); ++mm) {
-        const int sc = (int)sops[c][mm].size() / 3;
-        for (int d = 0; d < 3; ++d)
-          for (int k = 0; k < sc; ++k) S->w_sub_op[((c * mmax + mm) * 3 + d) * smax + k] = sops[c][mm][d * sc + k];
-        for (int k = 0; k < sc; ++k) S->w_sub_gather[(c * mmax + mm) * smax + k] = sids[c][mm][k];
-        S->w_sub_active[c * mmax + mm] = 1;
-      }
+        for (int k = 0; k < cols; ++k) S->w_big_op[(c * NCOEF + d) * kmax + k] = op[d * cols + k];
+      for (int k = 1; k <= R; ++k) S->w_big_gather[c * kmax + k - 1] = st.big[k].id;
     }
+    // reference widths: mmax = max(surviving subs, 1), smax = max surviving sub columns (default 1)
+    int64_t mmax = 0, smax = 0;
+    for (int64_t c = 0; c < nc; ++c) {
+      mmax = std::max<int64_t>(mmax, msurv[c]);
+      smax = std::max<int64_t>(smax, ssurv[c]);
+    }
+    mmax = std::max<int64_t>(mmax, 1);
+    smax = std::max<int64_t>(smax, 1);
+    if (mmax != mup || smax != sup) {
+      std::vector<double> op2(nc * mmax * 3 * smax, 0.0);
+      std::vector<int64_t> g2(nc * mmax * smax, 0);
+      std::vector<int8_t> a2(nc * mmax, 0);
+      for (int64_t c = 0; c < nc; ++c)
+        for (int64_t mm = 0; mm < mmax; ++mm) {
+          a2[c * mmax + mm] = S->w_sub_active[c * mup + mm];
+          for (int64_t d = 0; d < 3; ++d)
+            for (int64_t k = 0; k < smax; ++k)
+              op2[((c * mmax + mm) * 3 + d) * smax + k] = S->w_sub_op[((c * mup + mm) * 3 + d) * sup + k];
+          for (int64_t k = 0; k < smax; ++k) g2[(c * mmax + mm) * smax + k] = S->w_sub_gather[(c * mup + mm) * sup + k];
+        }
+      S->w_sub_op.swap(op2);
+      S->w_sub_gather.swap(g2);
+      S->w_sub_active.swap(a2);
+    }
+    S->w_kmax = kmax;
+    S->w_mmax = mmax;
+    S->w_smax = smax;
   }
 
-  if (schemes & 2) {
+  if (want_hweno) {
     // HWENO operators (hweno.py:62-137)
-    std::vector<std::vector<double>> bops(nc);
-    std::vector<int> bcols(nc), nas(nc);
-    std::vector<std::vector<std::vector<double>>> sops(nc);
-    std::vector<std::vector<int64_t>> snbr(nc);
+    int64_t amax = 0, gmax = 0;
+    for (int64_t c = 0; c < nc; ++c) {
+      amax = std::max<int64_t>(amax, nbr_n[c]);
+      gmax = std::max<int64_t>(gmax, nbr_n[c] + 1);
+    }
+    amax = std::max<int64_t>(amax, 1);
+    const int64_t mup = std::max<int64_t>(nfpc, 1);
+    const int64_t W = amax + 3 * gmax;
+    S->h_big_op.assign(nc * NCOEF * W, 0.0);
+    S->h_big_avg_gather.assign(nc * amax, 0);
+    S->h_big_grad_gather.assign(nc * gmax, 0);
+    S->h_big_grad_scale.assign(nc * gmax, 0.0);
+    S->h_big_ncols.assign(nc, 0);
     S->h_big_degree.assign(nc, 2);
+    S->h_sub_op.assign(nc * mup * 21, 0.0);
+    S->h_sub_gather.assign(nc * mup * 2, 0);
+    S->h_sub_active.assign(nc * mup, 0);
+    std::vector<int32_t> msurv(nc, 0);
 #pragma omp parallel for schedule(dynamic, 64)
     for (int64_t c = 0; c < nc; ++c) {
-      const CellStencil& st = cs[c];
+      CellStencil st;
+      build_cell_stencil(m, mv, c, st);
       std::vector<Member> ids = {{c, {0, 0, 0}}};
       for (size_t k = 0; k < st.nbr.size(); ++k)
         if (st.nbr[k] >= 0) ids.push_back({st.nbr[k], st.nbr_s[k]});
@@ -614,93 +673,94 @@ int gks_setup_build(const GksMeshDesc* m, int schemes, int nthreads, GksSetup** 
           for (int d = 0; d < 3; ++d)
             for (int k = 0; k < R; ++k) op[d * R + k] = lin[d * R + k];
       }
-      bops[c] = op;
-      bcols[c] = R;
-      nas[c] = na;
+      S->h_big_ncols[c] = R;
+      for (int d = 0; d < NCOEF; ++d) {
+        for (int k = 0; k < na; ++k) S->h_big_op[(c * NCOEF + d) * W + k] = op[d * R + k];
+        for (int k = na; k < R; ++k) S->h_big_op[(c * NCOEF + d) * W + amax + (k - na)] = op[d * R + k];
+      }
+      S->h_big_grad_gather[c * gmax] = c;
+      S->h_big_grad_scale[c * gmax] = m->cell_h[c];
+      for (int k = 1; k <= na; ++k) {
+        S->h_big_avg_gather[c * amax + k - 1] = ids[k].id;
+        S->h_big_grad_gather[c * gmax + k] = ids[k].id;
+        S->h_big_grad_scale[c * gmax + k] = m->cell_h[ids[k].id];
+      }
+      int nsurv = 0;
       if (!st.hweno_fallback) {
+        double g0[3][NCOEF];
+        geo.grad_rows(c, c, V3{0, 0, 0}, g0);
         for (int k = 1; k <= na; ++k) {
           // rows: [avg row of the neighbour (3 cols); grad rows of target; grad rows of neighbour]
           double srows[7 * 3];
           double full[NCOEF];
           member_row(c, ids[k], full);
           for (int d = 0; d < 3; ++d) srows[d] = full[d];
-          double g[3][NCOEF];
-          geo.grad_rows(c, c, V3{0, 0, 0}, g);
           for (int x = 0; x < 3; ++x)
-            for (int d = 0; d < 3; ++d) srows[(1 + x) * 3 + d] = g[x][d];
+            for (int d = 0; d < 3; ++d) srows[(1 + x) * 3 + d] = g0[x][d];
+          double g[3][NCOEF];
           geo.grad_rows(c, ids[k].id, ids[k].s, g);
           for (int x = 0; x < 3; ++x)
             for (int d = 0; d < 3; ++d) srows[(4 + x) * 3 + d] = g[x][d];
-          std::vector<double> sop(3 * 7);
-          if (!pinv(7, 3, srows, 3, sop.data())) continue;
-          sops[c].push_back(sop);
-          snbr[c].push_back(ids[k].id);
+          double sop[21];
+          if (!pinv(7, 3, srows, 3, sop)) continue;
+          for (int i = 0; i < 21; ++i) S->h_sub_op[(c * mup + nsurv) * 21 + i] = sop[i];
+          S->h_sub_gather[(c * mup + nsurv) * 2 + 0] = c;
+          S->h_sub_gather[(c * mup + nsurv) * 2 + 1] = ids[k].id;
+          S->h_sub_active[c * mup + nsurv] = 1;
+          ++nsurv;
         }
-        if (sops[c].size() < 2) { sops[c].clear(); snbr[c].clear(); }
+        if (nsurv < 2) {
+          for (int mm = 0; mm < nsurv; ++mm) {
+            S->h_sub_active[c * mup + mm] = 0;
+            for (int i = 0; i < 21; ++i) S->h_sub_op[(c * mup + mm) * 21 + i] = 0.0;
+            S->h_sub_gather[(c * mup + mm) * 2] = 0;
+            S->h_sub_gather[(c * mup + mm) * 2 + 1] = 0;
+          }
+          nsurv = 0;
+        }
       }
+      msurv[c] = nsurv;
     }
-    int64_t amax = 0, gmax = 0, mmax = 0;
-    for (int64_t c = 0; c < nc; ++c) {
-      amax = std::max<int64_t>(amax, nas[c]);
-      gmax = std::max<int64_t>(gmax, nas[c] + 1);
-      mmax = std::max<int64_t>(mmax, (int64_t)sops[c].size());
-    }
-    amax = std::max<int64_t>(amax, 1);
+    int64_t mmax = 0;
+    for (int64_t c = 0; c < nc; ++c) mmax = std::max<int64_t>(mmax, msurv[c]);
     mmax = std::max<int64_t>(mmax, 1);
-    S->h_amax = amax; S->h_gmax = gmax; S->h_mmax = mmax;
-    const int64_t W = amax + 3 * gmax;
-    S->h_big_op.assign(nc * NCOEF * W, 0.0);
-    S->h_big_avg_gather.assign(nc * amax, 0);
-    S->h_big_grad_gather.assign(nc * gmax, 0);
-    S->h_big_grad_scale.assign(nc * gmax, 0.0);
-    S->h_big_ncols.assign(nc, 0);
-    S->h_sub_op.assign(nc * mmax * 3 * 7, 0.0);
-    S->h_sub_gather.assign(nc * mmax * 2, 0);
-    S->h_sub_active.assign(nc * mmax, 0);
-#pragma omp parallel for schedule(static)
-    for (int64_t c = 0; c < nc; ++c) {
-      const int na = nas[c], R = bcols[c];
-      S->h_big_ncols[c] = R;
-      for (int d = 0; d < NCOEF; ++d) {
-        for (int k = 0; k < na; ++k) S->h_big_op[(c * NCOEF + d) * W + k] = bops[c][d * R + k];
-        for (int k = na; k < R; ++k) S->h_big_op[(c * NCOEF + d) * W + amax + (k - na)] = bops[c][d * R + k];
-      }
-      int a = 0;
-      S->h_big_grad_gather[c * gmax + 0] = c;
-      S->h_big_grad_scale[c * gmax + 0] = m->cell_h[c];
-      int gi = 1;
-      for (size_t k = 0; k < cs[c].nbr.size(); ++k) {
-        const int64_t j = cs[c].nbr[k];
-        if (j < 0) continue;
-        S->h_big_avg_gather[c * amax + a++] = j;
-        S->h_big_grad_gather[c * gmax + gi] = j;
-        S->h_big_grad_scale[c * gmax + gi] = m->cell_h[j];
-        ++gi;
-      }
-      for (size_t mm = 0; mm < sops[c].size(); ++mm) {
-        for (int i = 0; i < 21; ++i) S->h_sub_op[(c * mmax + mm) * 21 + i] = sops[c][mm][i];
-        S->h_sub_gather[(c * mmax + mm) * 2 + 0] = c;
-        S->h_sub_gather[(c * mmax + mm) * 2 + 1] = snbr[c][mm];
-        S->h_sub_active[c * mmax + mm] = 1;
-      }
+    if (mmax != mup) {
+      std::vector<double> op2(nc * mmax * 21, 0.0);
+      std::vector<int64_t> g2(nc * mmax * 2, 0);
+      std::vector<int8_t> a2(nc * mmax, 0);
+      for (int64_t c = 0; c < nc; ++c)
+        for (int64_t mm = 0; mm < mmax; ++mm) {
+          a2[c * mmax + mm] = S->h_sub_active[c * mup + mm];
+          for (int i = 0; i < 21; ++i) op2[(c * mmax + mm) * 21 + i] = S->h_sub_op[(c * mup + mm) * 21 + i];
+          g2[(c * mmax + mm) * 2] = S->h_sub_gather[(c * mup + mm) * 2];
+          g2[(c * mmax + mm) * 2 + 1] = S->h_sub_gather[(c * mup + mm) * 2 + 1];
+        }
+      S->h_sub_op.swap(op2);
+      S->h_sub_gather.swap(g2);
+      S->h_sub_active.swap(a2);
     }
+    S->h_amax = amax;
+    S->h_gmax = gmax;
+    S->h_mmax = mmax;
   }
 
   // register exports
-  S->reg("nbr_ids", S->nbr_ids, 1, {nc, nfpc});
-  S->reg("nbr_shift", S->nbr_shift, 0, {nc, nfpc, 3});
-  S->reg("big_start", S->big_start, 1, {nc + 1});
-  S->reg("big_ids", S->big_ids, 1, {(int64_t)S->big_ids.size()});
-  S->reg("big_shift", S->big_shift, 0, {(int64_t)S->big_ids.size(), 3});
-  S->reg("sub_cell_start", S->sub_cell_start, 1, {nc + 1});
-  S->reg("sub_member_start", S->sub_member_start, 1, {(int64_t)S->sub_member_start.size()});
-  S->reg("sub_ids", S->sub_ids, 1, {(int64_t)S->sub_ids.size()});
-  S->reg("sub_shift", S->sub_shift, 0, {(int64_t)S->sub_ids.size(), 3});
+  if (want_stencils) {
+    S->reg("nbr_ids", S->nbr_ids, 1, {nc, nfpc});
+    S->reg("nbr_shift", S->nbr_shift, 0, {nc, nfpc, 3});
+    S->reg("big_start", S->big_start, 1, {nc + 1});
+    S->reg("big_ids", S->big_ids, 1, {(int64_t)S->big_ids.size()});
+    S->reg("big_shift", S->big_shift, 0, {(int64_t)S->big_ids.size(), 3});
+    S->reg("sub_cell_start", S->sub_cell_start, 1, {nc + 1});
+    S->reg("sub_member_start", S->sub_member_start, 1, {(int64_t)S->sub_member_start.size()});
+    S->reg("sub_ids", S->sub_ids, 1, {(int64_t)S->sub_ids.size()});
+    S->reg("sub_shift", S->sub_shift, 0, {(int64_t)S->sub_ids.size(), 3});
+  }
   S->reg("weno_fallback", S->weno_fallback, 2, {nc});
   S->reg("hweno_fallback", S->hweno_fallback, 2, {nc});
   S->reg("avg0", S->avg0, 0, {nc, NCOEF});
   S->reg("beta_mat", S->beta, 0, {nc, NCOEF, NCOEF});
-  if (schemes & 1) {
+  if (want_weno) {
     S->reg("weno_big_op", S->w_big_op, 0, {nc, NCOEF, S->w_kmax});
     S->reg("weno_big_gather", S->w_big_gather, 1, {nc, S->w_kmax});
     S->reg("weno_big_degree", S->w_big_degree, 2, {nc});
@@ -708,7 +768,7 @@ int gks_setup_build(const GksMeshDesc* m, int schemes, int nthreads, GksSetup** 
     S->reg("weno_sub_gather", S->w_sub_gather, 1, {nc, S->w_mmax, S->w_smax});
     S->reg("weno_sub_active", S->w_sub_active, 2, {nc, S->w_mmax});
   }
-  if (schemes & 2) {
+  if (want_hweno) {
     const int64_t W = S->h_amax + 3 * S->h_gmax;
     S->reg("hweno_big_op", S->h_big_op, 0, {nc, NCOEF, W});
     S->reg("hweno_big_avg_gather", S->h_big_avg_gather, 1, {nc, S->h_amax});

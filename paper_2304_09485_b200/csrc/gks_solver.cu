@@ -15,6 +15,8 @@
 // contributions (nfq,5).  Assembly is a cell-centric gather over a CSR list
 // in the reference's np.add.at order (owner entries, then neighbour
 // entries, ascending), so results are deterministic and atomics-free.
+#include <stdlib.h>
+
 #include <algorithm>
 #include <numeric>
 #include <string>

@@ -93,4 +93,4 @@ class _Cells:
 
 def build_stencils(mesh, nthreads=0) -> StencilTable:
     """Select big and sub-candidate stencils for every cell (stencils.py:119-192)."""
-    return StencilTable(N.NativeSetup(mesh, schemes=0, nthreads=nthreads), mesh)
+    return StencilTable(N.NativeSetup(mesh, schemes=0, nthreads=nthreads), mesh)  # schemes 0: stencils only

@@ -174,7 +174,8 @@ class Solver:
     @property
     def stencils(self):
         if self._stencils is None:
-            self._stencils = StencilTable(self._setup, self.mesh)
+            # the operator setup does not keep the stencil tables: build them on demand
+            self._stencils = StencilTable(N.NativeSetup(self.mesh, schemes=0), self.mesh)
         return self._stencils
 
     # -- helpers ----------------------------------------------------------------
