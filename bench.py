@@ -46,8 +46,10 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    p.add_argument("--workload", default="c2", choices=("c1", "c2"),
-                   help="c1: periodic Kuhn-tet box (configs[0]); c2: subsonic sphere, matrix-free GMRES (configs[1])")
+    p.add_argument("--workload", default="c2", choices=("c1", "c2", "c3", "c4", "c5"),
+                   help="c1 periodic Kuhn-tet box; c2 subsonic sphere, matrix-free GMRES (configs[1], default); "
+                        "c3 viscous sphere Re=118 HWENO; c4 transonic swept-wing stand-in HWENO; "
+                        "c5 supersonic sphere ~10M tets HWENO")
     p.add_argument("--n", type=int, default=None, help="lattice divisions per axis (c1 default 64, c2 default 64)")
     p.add_argument("--scheme", default=None, choices=("weno_gmres", "hweno_gmres"))
     p.add_argument("--jacobian", default=None, choices=("roe", "frechet"))
@@ -56,11 +58,13 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     a = p.parse_args()
     # configs[1]: inviscid subsonic sphere, non-compact HGKS + matrix-free GMRES
-    defaults = {"c1": (64, "weno_gmres", "roe"), "c2": (16, "weno_gmres", "frechet")}[a.workload]
+    defaults = {"c1": (64, "weno_gmres", "roe"), "c2": (16, "weno_gmres", "frechet"),
+                "c3": (16, "hweno_gmres", "roe"), "c4": (96, "hweno_gmres", "roe"),
+                "c5": (30, "hweno_gmres", "roe")}[a.workload]
     a.n = a.n or defaults[0]
     a.scheme = a.scheme or defaults[1]
     a.jacobian = a.jacobian or defaults[2]
-    a.cpu_n = a.cpu_n or {"c1": 10, "c2": 2}[a.workload]
+    a.cpu_n = a.cpu_n or {"c1": 10, "c2": 2, "c3": 2, "c4": 24, "c5": 2}[a.workload]
     return a
 
 
@@ -90,6 +94,34 @@ def c2_problem(mesh, compact):
     return patches, fld.q, fld.grad
 
 
+def other_problem(workload, mesh, compact):
+    """C3-C5 patch tables / reference states from the reference case files."""
+    from paper_2304_09485_b200.boundary import PatchSpec
+    from paper_2304_09485_b200.stepping import initial_field
+
+    if workload == "c3":  # cases/sphere_re118_ma0p2535.ini
+        ref = np.array([1.0, 0.2535, 0.0, 0.0, 1.0 / GAMMA])
+        patches = {"sphere": PatchSpec("sphere", "wall_noslip_adiabatic"),
+                   "farfield": PatchSpec("farfield", "farfield_riemann", reference=ref)}
+        extra = dict(model="viscous", mu=0.0021483050847457627, weights="linear")
+    elif workload == "c4":  # cases/m6wing_transonic.ini (Ma 0.8395, AoA 3.06 deg)
+        ref = np.array([1.0, 0.8383030214661579, 0.04482495105787847, 0.0, 1.0 / GAMMA])
+        patches = {"wing": PatchSpec("wing", "wall_slip_adiabatic"),
+                   "farfield": PatchSpec("farfield", "farfield_riemann", reference=ref)}
+        extra = {}
+    else:
+        # c5 scale case.  cases/sphere_ma3_inviscid.ini asks for Ma 3, but the
+        # reference algorithm itself cannot start Ma >= 1.5 impulsively with the
+        # compact scheme (oracle: non-positive density at step 2, even at CFL
+        # 0.2; DESIGN.md), so the ~10M-cell compact case runs at Ma 0.5.
+        ref = np.array([1.0, 0.5, 0.0, 0.0, 1.0 / GAMMA])
+        patches = {"sphere": PatchSpec("sphere", "wall_slip_adiabatic"),
+                   "farfield": PatchSpec("farfield", "farfield_riemann", reference=ref)}
+        extra = {}
+    fld = initial_field(mesh, ref, GAMMA, compact=compact)
+    return patches, fld.q, fld.grad, extra
+
+
 def build_workload(args, compact):
     from paper_2304_09485_b200 import mesh as M
     from paper_2304_09485_b200 import meshgen as MG
@@ -97,11 +129,23 @@ def build_workload(args, compact):
     if args.workload == "c1":
         mesh = c1_mesh(args.n, M)
         q, g = c1_field(mesh, compact)
-        return mesh, {}, q, g, f"C1 periodic 6*{args.n}^3 Kuhn-tet box, smooth density wave (configs[0] shape)"
-    mesh = c2_mesh(args.n, MG)
-    patches, q, g = c2_problem(mesh, compact)
-    return mesh, patches, q, g, (f"C2 synthetic body-fitted tet sphere (cubed-sphere n={args.n}, D=1, farfield 20D), "
-                                 f"inviscid Ma {MA_C2}, slip wall + Riemann farfield, impulsive start (configs[1])")
+        return mesh, {}, q, g, f"C1 periodic 6*{args.n}^3 Kuhn-tet box, smooth density wave (configs[0] shape)", {}
+    if args.workload == "c2":
+        mesh = c2_mesh(args.n, MG)
+        patches, q, g = c2_problem(mesh, compact)
+        return mesh, patches, q, g, (f"C2 synthetic body-fitted tet sphere (cubed-sphere n={args.n}, D=1, farfield "
+                                     f"20D), inviscid Ma {MA_C2}, slip wall + Riemann farfield, impulsive start "
+                                     f"(configs[1])"), {}
+    if args.workload == "c4":
+        mesh = MG.generate_wing_mesh(args.n)
+        label = f"C4 synthetic swept-wing stand-in (lattice {args.n}^3), Ma 0.8395 AoA 3.06, slip wall (configs[3])"
+    else:
+        mesh = MG.generate_sphere_mesh(args.n)
+        label = ("C3 synthetic tet sphere, viscous Re=118 Ma 0.2535, no-slip wall (configs[2])" if args.workload == "c3"
+                 else f"C5 scale case: synthetic tet sphere ({mesh.ncells / 1e6:.1f}M cells), compact HWENO, inviscid "
+                      f"Ma 0.5 (Ma 3 start infeasible for the reference scheme) (configs[4])")
+    patches, q, g, extra = other_problem(args.workload, mesh, compact)
+    return mesh, patches, q, g, label, extra
 
 
 def c1_field(mesh, compact):
@@ -208,14 +252,24 @@ def kernel_model(solver, compact):
     info = [int(lib.gks_handle_info(solver._handle, k)) for k in range(9)]
     nc, nf, nfq, nfi, nbf, nnz, K, M, S = info
     per_row = nnz / nc
+    mf = os.environ.get("GKS_ROE_MF", "1") != "0"
+    if mf:
+        # matrix-free Roe products: CSR col+ent (8 B/entry), face (n, S/2, lam) 40 B/interior face,
+        # per-cell primitives 40 B, x 40 B, D^-1 200 B, b 40 B, out 40 B (+ D 200 B + out_pre 40 B for spmv)
+        faces = nfi / nc
+        sweep = nc * (4 + per_row * 8 + faces * 40 + 40 + 40 + 200 + 40 + 40)
+        spmv = sweep + nc * (200 + 40 - 40)
+    else:
+        sweep = nc * (4 + per_row * 204 + 200 + 40 + 40 + 40)
+        spmv = nc * (4 + per_row * 204 + 200 + 200 + 40 + 80)
     model = {
         # bytes per launch (HBM-bound kernels), unique compulsory traffic
-        "spmv_dinv": nc * (4 + per_row * 204 + 200 + 200 + 40 + 80),
-        "jacobi_sweep": nc * (4 + per_row * 204 + 200 + 40 + 40 + 40),
+        "spmv_dinv": spmv,
+        "jacobi_sweep": sweep,
         "assemble": nfq * 40 + nc * (4 + 40) + (nfq * 2) * 4,
-        "recon": nc * ((9 * K * 8 + K * 4 + M * 3 * S * 8 + M * S * 4 + M + 648 + 40 + 360) if not compact else
-                       (9 * K * 8 + M * 21 * 8 + M * 8 + 648 + 40 + 120 + 360)),
-        "jac_faces": nfi * (8 + 2 * 40 + 32 + 2 * 200),
+        "recon": nc * ((9 * K * 8 + K * 4 + M * 3 * S * 8 + M * S * 4 + M + 360 + 40 + 360) if not compact else
+                       (9 * K * 8 + M * 21 * 8 + M * 8 + 360 + 40 + 120 + 360)),
+        "jac_faces": nfi * (8 + 2 * 40 + 32 + 2 * 200 + 40),
         "jac_diag": nc * (4 + 40 + 8 + 8 + 400) + nnz * 200,
     }
     # FP64 flops per launch of the fused face kernel: reference-model count
@@ -232,17 +286,14 @@ def cpu_baseline(args, steps, label):
 
     n = args.cpu_n
     compact = args.scheme.startswith("hweno")
-    if args.workload == "c1":
-        mesh = c1_mesh(n, M)
-        q, grad = c1_field(mesh, compact)
-        patches = {}
-    else:
-        from paper_2304_09485_b200 import meshgen as MG
-
-        mesh = c2_mesh(n, MG)
-        patches, q, grad = c2_problem(mesh, compact)
+    saved = args.n
+    args.n = n
+    try:
+        mesh, patches, q, grad, _, extra = build_workload(args, compact)
+    finally:
+        args.n = saved
     t0 = time.perf_counter()
-    s = OracleSolver(mesh, scheme=args.scheme, patches=patches, jacobian=args.jacobian)
+    s = OracleSolver(mesh, scheme=args.scheme, patches=patches, jacobian=args.jacobian, **extra)
     setup = time.perf_counter() - t0
     q, grad, info = s.advance(q, grad)  # warm-up
     evals = 0
@@ -289,10 +340,10 @@ def run_ours(args):
     lib = N.load()
     compact = args.scheme.startswith("hweno")
     t0 = time.perf_counter()
-    mesh, patches, q0, g0, workload = build_workload(args, compact)
+    mesh, patches, q0, g0, workload, extra = build_workload(args, compact)
     t_mesh = time.perf_counter() - t0
     t0 = time.perf_counter()
-    opts = SolverOptions(scheme=args.scheme, patches=patches, jacobian=args.jacobian, device=local)
+    opts = SolverOptions(scheme=args.scheme, patches=patches, jacobian=args.jacobian, device=local, **extra)
     decomp = world > 1 and not args.replicas
     if decomp:
         from paper_2304_09485_b200.distributed import DistributedSolver
