@@ -24,11 +24,12 @@ p.add_argument("--threshold", type=float, default=1e-10)
 p.add_argument("--scheme", default="weno_gmres")
 p.add_argument("--jacobian", default="roe")
 p.add_argument("--cfl", type=float, default=2.0)
+p.add_argument("--weights", default="nonlinear")
 a = p.parse_args()
 mesh = c2_mesh(a.n, MG)
 compact = a.scheme.startswith("hweno")
 patches, q, g = c2_problem(mesh, compact)
-s = Solver(mesh, SolverOptions(scheme=a.scheme, patches=patches, jacobian=a.jacobian, cfl=a.cfl))
+s = Solver(mesh, SolverOptions(scheme=a.scheme, patches=patches, jacobian=a.jacobian, cfl=a.cfl, weights=a.weights))
 s.upload(SolutionField(q, g))
 hist = []
 t0 = time.perf_counter()
