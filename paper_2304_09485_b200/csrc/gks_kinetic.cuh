@@ -70,68 +70,57 @@ __device__ __forceinline__ void maxw_half_u(Maxw& m, const double w[5], double s
   recur<7>(m.U, u, 0.5 / lam);
 }
 
-// One weight monomial u^a v^b w^c xi^2s (coefficient k) against u^P psi.
-template <int P, int A, int B, int C, int S>
-__device__ __forceinline__ void mono_acc(const Maxw& m, double k, double o[5]) {
+// One group of weight monomials sharing the factor v^B w^C xi^2S, with a
+// polynomial sum_a k[a] u^a in u, integrated against u^P psi.  Grouping by
+// the (v, w, xi) part lets each group's u-sums be formed once (the compiler
+// may not reassociate FP sums by itself).
+template <int P, int B, int C, int S, int NA>
+__device__ __forceinline__ void group_acc(const Maxw& m, const double (&k)[NA], double o[5]) {
+  double s0 = k[0] * m.U[P], s1 = k[0] * m.U[P + 1], s2 = k[0] * m.U[P + 2];
+#pragma unroll
+  for (int a = 1; a < NA; ++a) {
+    s0 += k[a] * m.U[a + P];
+    s1 += k[a] * m.U[a + P + 1];
+    s2 += k[a] * m.U[a + P + 2];
+  }
   const double vw = m.V[B] * m.W[C];
   const double vwx = vw * m.X[S];
-  const double ua = m.U[A + P];
-  const double kua = k * ua;
-  o[0] += kua * vwx;
-  o[1] += k * m.U[A + P + 1] * vwx;
-  o[2] += kua * (m.V[B + 1] * m.W[C] * m.X[S]);
-  o[3] += kua * (m.V[B] * m.W[C + 1] * m.X[S]);
-  o[4] += 0.5 * k * (m.U[A + P + 2] * vwx +
-                     ua * (m.X[S] * (m.V[B + 2] * m.W[C] + m.V[B] * m.W[C + 2]) + vw * m.X[S + 1]));
+  o[0] += s0 * vwx;
+  o[1] += s1 * vwx;
+  o[2] += s0 * (m.V[B + 1] * m.W[C] * m.X[S]);
+  o[3] += s0 * (m.V[B] * m.W[C + 1] * m.X[S]);
+  o[4] += 0.5 * (s2 * vwx + s0 * (m.X[S] * (m.V[B + 2] * m.W[C] + m.V[B] * m.W[C + 2]) + vw * m.X[S + 1]));
 }
 
 // <u^P W(c) psi> with W(c) = s.psi(c) + DIR * sum_k c_k d_k.psi(c).
-// GKS_WMOM_NOINLINE keeps one out-of-line copy per (P, DIR) instead of one
-// per call site (instruction-cache pressure of the fused flux kernel).
-#ifdef GKS_WMOM_NOINLINE
-#define GKS_WMOM_ATTR __device__ __noinline__
-#else
-#define GKS_WMOM_ATTR __device__ __forceinline__
-#endif
+// The 23 weight monomials (8 without DIR) fall into 13 (6) groups.
 template <int P, bool DIR>
-GKS_WMOM_ATTR void wmom(const Maxw& m, const double s[5], const double (*d)[5], double o[5]) {
+__device__ __forceinline__ void wmom(const Maxw& m, const double s[5], const double (*d)[5], double o[5]) {
   o[0] = o[1] = o[2] = o[3] = o[4] = 0.0;
   const double hs = 0.5 * s[4];
   if (!DIR) {
-    mono_acc<P, 0, 0, 0, 0>(m, s[0], o);
-    mono_acc<P, 1, 0, 0, 0>(m, s[1], o);
-    mono_acc<P, 0, 1, 0, 0>(m, s[2], o);
-    mono_acc<P, 0, 0, 1, 0>(m, s[3], o);
-    mono_acc<P, 2, 0, 0, 0>(m, hs, o);
-    mono_acc<P, 0, 2, 0, 0>(m, hs, o);
-    mono_acc<P, 0, 0, 2, 0>(m, hs, o);
-    mono_acc<P, 0, 0, 0, 1>(m, hs, o);
+    group_acc<P, 0, 0, 0, 3>(m, {s[0], s[1], hs}, o);  // 1, u, u^2
+    group_acc<P, 1, 0, 0, 1>(m, {s[2]}, o);            // v
+    group_acc<P, 0, 1, 0, 1>(m, {s[3]}, o);            // w
+    group_acc<P, 2, 0, 0, 1>(m, {hs}, o);              // v^2
+    group_acc<P, 0, 2, 0, 1>(m, {hs}, o);              // w^2
+    group_acc<P, 0, 0, 1, 1>(m, {hs}, o);              // xi^2
     return;
   }
-  mono_acc<P, 0, 0, 0, 0>(m, s[0], o);
-  mono_acc<P, 1, 0, 0, 0>(m, s[1] + d[0][0], o);
-  mono_acc<P, 0, 1, 0, 0>(m, s[2] + d[1][0], o);
-  mono_acc<P, 0, 0, 1, 0>(m, s[3] + d[2][0], o);
-  mono_acc<P, 2, 0, 0, 0>(m, hs + d[0][1], o);
-  mono_acc<P, 0, 2, 0, 0>(m, hs + d[1][2], o);
-  mono_acc<P, 0, 0, 2, 0>(m, hs + d[2][3], o);
-  mono_acc<P, 0, 0, 0, 1>(m, hs, o);
-  mono_acc<P, 1, 1, 0, 0>(m, d[0][2] + d[1][1], o);
-  mono_acc<P, 1, 0, 1, 0>(m, d[0][3] + d[2][1], o);
-  mono_acc<P, 0, 1, 1, 0>(m, d[1][3] + d[2][2], o);
   const double hu = 0.5 * d[0][4], hv = 0.5 * d[1][4], hw = 0.5 * d[2][4];
-  mono_acc<P, 3, 0, 0, 0>(m, hu, o);
-  mono_acc<P, 1, 2, 0, 0>(m, hu, o);
-  mono_acc<P, 1, 0, 2, 0>(m, hu, o);
-  mono_acc<P, 1, 0, 0, 1>(m, hu, o);
-  mono_acc<P, 2, 1, 0, 0>(m, hv, o);
-  mono_acc<P, 0, 3, 0, 0>(m, hv, o);
-  mono_acc<P, 0, 1, 2, 0>(m, hv, o);
-  mono_acc<P, 0, 1, 0, 1>(m, hv, o);
-  mono_acc<P, 2, 0, 1, 0>(m, hw, o);
-  mono_acc<P, 0, 2, 1, 0>(m, hw, o);
-  mono_acc<P, 0, 0, 3, 0>(m, hw, o);
-  mono_acc<P, 0, 0, 1, 1>(m, hw, o);
+  group_acc<P, 0, 0, 0, 4>(m, {s[0], s[1] + d[0][0], hs + d[0][1], hu}, o);  // 1, u, u^2, u^3
+  group_acc<P, 1, 0, 0, 3>(m, {s[2] + d[1][0], d[0][2] + d[1][1], hv}, o);   // v, uv, u^2 v
+  group_acc<P, 0, 1, 0, 3>(m, {s[3] + d[2][0], d[0][3] + d[2][1], hw}, o);   // w, uw, u^2 w
+  group_acc<P, 2, 0, 0, 2>(m, {hs + d[1][2], hu}, o);                       // v^2, u v^2
+  group_acc<P, 0, 2, 0, 2>(m, {hs + d[2][3], hu}, o);                       // w^2, u w^2
+  group_acc<P, 0, 0, 1, 2>(m, {hs, hu}, o);                                 // xi^2, u xi^2
+  group_acc<P, 1, 1, 0, 1>(m, {d[1][3] + d[2][2]}, o);                      // vw
+  group_acc<P, 3, 0, 0, 1>(m, {hv}, o);                                     // v^3
+  group_acc<P, 0, 3, 0, 1>(m, {hw}, o);                                     // w^3
+  group_acc<P, 1, 2, 0, 1>(m, {hv}, o);                                     // v w^2
+  group_acc<P, 2, 1, 0, 1>(m, {hw}, o);                                     // v^2 w
+  group_acc<P, 1, 0, 1, 1>(m, {hv}, o);                                     // v xi^2
+  group_acc<P, 0, 1, 1, 1>(m, {hw}, o);                                     // w xi^2
 }
 
 // kinetic.py:271-302 closed-form solve of <a psi> = dq / rho.
