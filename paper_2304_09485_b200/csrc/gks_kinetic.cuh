@@ -123,6 +123,45 @@ __device__ __forceinline__ void wmom(const Maxw& m, const double s[5], const dou
   group_acc<P, 0, 1, 1, 1>(m, {hw}, o);                                     // w xi^2
 }
 
+// Gram matrix G_ij = <u^P psi_i psi_j> of one Maxwellian.  Every weight
+// without the directional part is a product with it: wmom<P,false>(m, s) = G s,
+// so the several such weights of one Maxwellian share one G.
+template <int P>
+__device__ __forceinline__ void gram(const Maxw& m, double G[5][5]) {
+  const double* U = m.U + P;
+  const double* V = m.V;
+  const double* W = m.W;
+  const double x1 = m.X[1];
+  const double r = V[2] + W[2] + x1;  // <v^2 + w^2 + xi^2>
+  G[0][0] = U[0];
+  G[0][1] = U[1];
+  G[0][2] = U[0] * V[1];
+  G[0][3] = U[0] * W[1];
+  G[0][4] = 0.5 * (U[2] + U[0] * r);
+  G[1][1] = U[2];
+  G[1][2] = U[1] * V[1];
+  G[1][3] = U[1] * W[1];
+  G[1][4] = 0.5 * (U[3] + U[1] * r);
+  G[2][2] = U[0] * V[2];
+  G[2][3] = U[0] * V[1] * W[1];
+  G[2][4] = 0.5 * (U[2] * V[1] + U[0] * (V[3] + V[1] * (W[2] + x1)));
+  G[3][3] = U[0] * W[2];
+  G[3][4] = 0.5 * (U[2] * W[1] + U[0] * (W[3] + W[1] * (V[2] + x1)));
+  G[4][4] = 0.25 * (U[4] + 2.0 * U[2] * r +
+                    U[0] * (V[4] + W[4] + m.X[2] + 2.0 * (V[2] * W[2] + (V[2] + W[2]) * x1)));
+#pragma unroll
+  for (int i = 1; i < 5; ++i)
+#pragma unroll
+    for (int j = 0; j < i; ++j) G[i][j] = G[j][i];
+}
+
+// acc += scale * G s
+__device__ __forceinline__ void gram_acc(const double G[5][5], const double s[5], double scale, double acc[5]) {
+#pragma unroll
+  for (int i = 0; i < 5; ++i)
+    acc[i] += scale * (G[i][0] * s[0] + G[i][1] * s[1] + G[i][2] * s[2] + G[i][3] * s[3] + G[i][4] * s[4]);
+}
+
 // kinetic.py:271-302 closed-form solve of <a psi> = dq / rho.
 __device__ __forceinline__ void micro_slope(const double w[5], const double dq[5],
                                             const KinConst& kc, double a[5]) {
@@ -278,16 +317,15 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
       micro_slope(w, D, kc, A);
     }
     maxw_half_u(m, w, side ? -1.0 : 1.0);
-    const double e0[5] = {1, 0, 0, 0, 0};
     double t[5];
-    wmom<0, false>(m, e0, nullptr, t);
+    {
+      double G[5][5];
+      gram<0>(m, G);
 #pragma unroll
-    for (int i = 0; i < 5; ++i) q0[i] += rho * t[i];
+      for (int i = 0; i < 5; ++i) q0[i] += rho * G[i][0];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      wmom<0, false>(m, a[k], nullptr, t);
-#pragma unroll
-      for (int i = 0; i < 5; ++i) dqa[k][i] += rho * t[i];
+      for (int k = 0; k < 3; ++k) gram_acc(G, a[k], rho, dqa[k]);
+      if (VISCOUS && POINT) gram_acc(G, A, rho, P6);
     }
     if (tau_known && !VISCOUS) {
       double sw[5], dw[3][5];
@@ -314,22 +352,20 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
       }
     } else {
       const double zero5[5] = {0, 0, 0, 0, 0};
-      wmom<1, false>(m, e0, nullptr, t);
+      {
+        double Gu[5][5];
+        gram<1>(m, Gu);
 #pragma unroll
-      for (int i = 0; i < 5; ++i) F[i] += rho * t[i];
+        for (int i = 0; i < 5; ++i) F[i] += rho * Gu[i][0];
+        gram_acc(Gu, A, rho, F6);
+      }
       wmom<1, true>(m, zero5, a, t);
 #pragma unroll
       for (int i = 0; i < 5; ++i) F5[i] += rho * t[i];
-      wmom<1, false>(m, A, nullptr, t);
-#pragma unroll
-      for (int i = 0; i < 5; ++i) F6[i] += rho * t[i];
       if (POINT) {
         wmom<0, true>(m, zero5, a, t);
 #pragma unroll
         for (int i = 0; i < 5; ++i) P[i] += rho * t[i];
-        wmom<0, false>(m, A, nullptr, t);
-#pragma unroll
-        for (int i = 0; i < 5; ++i) P6[i] += rho * t[i];
       }
     }
   }
