@@ -47,9 +47,14 @@ static int setup_array(const GksSetup* S, const char* name, std::vector<double>*
   return gks_setup_copy(S, name, b->data(), n);
 }
 
+// Every device array carries 64 bytes of tail padding: the bulk-copy staging
+// of the reconstruction kernels rounds a tile's chunk up to 16 bytes and may
+// read up to 15 bytes past the last record (gks_stage.cuh).
+static constexpr size_t kTailPad = 64;
+
 template <class T>
 static int upload(Handle* H, T** dst, const T* src, size_t n) {
-  GKS_CUDA(cudaMalloc(dst, std::max<size_t>(n, 1) * sizeof(T)));
+  GKS_CUDA(cudaMalloc(dst, std::max<size_t>(n, 1) * sizeof(T) + kTailPad));
   H->allocs.push_back(*dst);
   if (n) GKS_CUDA(cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice));
   return GKS_OK;
@@ -57,7 +62,7 @@ static int upload(Handle* H, T** dst, const T* src, size_t n) {
 
 template <class T>
 static int alloc(Handle* H, T** dst, size_t n) {
-  GKS_CUDA(cudaMalloc(dst, std::max<size_t>(n, 1) * sizeof(T)));
+  GKS_CUDA(cudaMalloc(dst, std::max<size_t>(n, 1) * sizeof(T) + kTailPad));
   H->allocs.push_back(*dst);
   return GKS_OK;
 }
@@ -84,6 +89,37 @@ static int upload_halo(Handle* H, HaloMap& X, const GksHaloDesc& d) {
   TRY(upload(H, &X.sids, si.data(), si.size()));
   TRY(upload(H, &X.rids, ri.data(), ri.size()));
   return GKS_OK;
+}
+
+// Reconstruction records are padded per cell to a compile-time stencil
+// shape of the K2 kernels (gks_solver.cu recon_device): extra operator
+// columns are zero, extra gather slots point at the cell itself (so the
+// right-hand side entry is Q_c - Q_c = 0 exactly), extra sub-stencils are
+// inactive.  (rows, cols) -> (rows, cols_t) per cell.
+template <class T, class Fill>
+static std::vector<T> pad_records(const std::vector<T>& src, int64_t nc, int64_t rows, int64_t cols, int64_t rows_t,
+                                  int64_t cols_t, Fill fill) {
+  std::vector<T> out((size_t)nc * rows_t * cols_t);
+  for (int64_t c = 0; c < nc; ++c)
+    for (int64_t r = 0; r < rows_t; ++r)
+      for (int64_t j = 0; j < cols_t; ++j)
+        out[(c * rows_t + r) * cols_t + j] =
+            (r < rows && j < cols) ? src[(c * rows + r) * cols + j] : fill(c);
+  return out;
+}
+
+static bool weno_shape(int K, int M, int S, int* Kt, int* Mt, int* St) {
+  if (M <= 4 && S <= 6 && K <= 16) { *Kt = std::max(K, 13); *Mt = 4; *St = 6; return true; }
+  if (M <= 8 && S <= 3 && K <= 24) { *Kt = 24; *Mt = 8; *St = 3; return true; }
+  if (M <= 8 && S <= 8 && K <= 32) { *Kt = 32; *Mt = 8; *St = 8; return true; }
+  return false;
+}
+
+static bool hweno_shape(int HA, int HG, int M, int* At, int* Gt, int* Mt) {
+  if (HA <= 4 && HG <= 5 && M <= 4) { *At = 4; *Gt = 5; *Mt = 4; return true; }
+  if (HA <= 6 && HG <= 7 && M <= 6) { *At = 6; *Gt = 7; *Mt = 6; return true; }
+  if (HA <= 16 && HG <= 17 && M <= 8) { *At = 16; *Gt = 17; *Mt = 8; return true; }
+  return false;
 }
 
 int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const GksOptions* o, int device,
@@ -292,41 +328,89 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   }
 
   // reconstruction operators
+  // (records padded to the kernel's stencil shape, see pad_records)
+  auto zero_d = [](int64_t) { return 0.0; };
+  auto self_i = [](int64_t c) { return (int)c; };
+  auto zero_b = [](int64_t) { return (int8_t)0; };
   if (H->compact) {
-    TRY(setup_array(S, "hweno_big_op", &hf, &hi, &hb, &shp));
-    H->HA = 0;
-    TRY(upload(H, &H->big_op, hf.data(), hf.size()));
+    std::vector<double> op, gs, so;
+    std::vector<int> ag, gg, sg;
+    std::vector<int8_t> act;
+    TRY(setup_array(S, "hweno_big_op", &op, &hi, &hb, &shp));
     TRY(setup_array(S, "hweno_big_avg_gather", &hf, &hi, &hb, &shp));
     H->HA = (int)shp[1];
-    { auto v = to_i32(hi.data(), hi.size()); TRY(upload(H, &H->avg_gather, v.data(), v.size())); }
+    ag = to_i32(hi.data(), hi.size());
     TRY(setup_array(S, "hweno_big_grad_gather", &hf, &hi, &hb, &shp));
     H->HG = (int)shp[1];
-    { auto v = to_i32(hi.data(), hi.size()); TRY(upload(H, &H->grad_gather, v.data(), v.size())); }
-    TRY(setup_array(S, "hweno_big_grad_scale", &hf, &hi, &hb, &shp));
-    TRY(upload(H, &H->grad_scale, hf.data(), hf.size()));
-    TRY(setup_array(S, "hweno_sub_op", &hf, &hi, &hb, &shp));
+    gg = to_i32(hi.data(), hi.size());
+    TRY(setup_array(S, "hweno_big_grad_scale", &gs, &hi, &hb, &shp));
+    TRY(setup_array(S, "hweno_sub_op", &so, &hi, &hb, &shp));
     H->HM = (int)shp[1];
-    TRY(upload(H, &H->sub_op, hf.data(), hf.size()));
     TRY(setup_array(S, "hweno_sub_gather", &hf, &hi, &hb, &shp));
-    { auto v = to_i32(hi.data(), hi.size()); TRY(upload(H, &H->sub_gather, v.data(), v.size())); }
-    TRY(setup_array(S, "hweno_sub_active", &hf, &hi, &hb, &shp));
-    TRY(upload(H, &H->sub_active, hb.data(), hb.size()));
-    if (H->HM > 8) { set_error("HWENO: more than 8 sub-stencils per cell"); return GKS_ERR_BAD_ARG; }
+    sg = to_i32(hi.data(), hi.size());
+    TRY(setup_array(S, "hweno_sub_active", &hf, &hi, &act, &shp));
+    int At, Gt, Mt;
+    if (!hweno_shape(H->HA, H->HG, H->HM, &At, &Gt, &Mt)) {
+      set_error("HWENO stencil shape (%d, %d, %d) exceeds the reconstruction kernels", H->HA, H->HG, H->HM);
+      return GKS_ERR_BAD_ARG;
+    }
+    H->Kt = At; H->St = Gt; H->Mt = Mt;
+    // big operator columns: [averages HA | gradients 3 HG] -> [At | 3 Gt]
+    {
+      const int W = H->HA + 3 * H->HG, Wt = At + 3 * Gt;
+      std::vector<double> opt((size_t)nc * 9 * Wt, 0.0);
+      for (int64_t c = 0; c < nc; ++c)
+        for (int d = 0; d < 9; ++d) {
+          const double* src = &op[(c * 9 + d) * W];
+          double* dst = &opt[(c * 9 + d) * Wt];
+          for (int j = 0; j < H->HA; ++j) dst[j] = src[j];
+          for (int j = 0; j < 3 * H->HG; ++j) dst[At + j] = src[H->HA + j];
+        }
+      TRY(upload(H, &H->big_op, opt.data(), opt.size()));
+    }
+    { auto v = pad_records(ag, nc, 1, H->HA, 1, At, self_i); TRY(upload(H, &H->avg_gather, v.data(), v.size())); }
+    { auto v = pad_records(gg, nc, 1, H->HG, 1, Gt, self_i); TRY(upload(H, &H->grad_gather, v.data(), v.size())); }
+    { auto v = pad_records(gs, nc, 1, H->HG, 1, Gt, zero_d); TRY(upload(H, &H->grad_scale, v.data(), v.size())); }
+    { auto v = pad_records(so, nc, H->HM, 21, Mt, 21, zero_d); TRY(upload(H, &H->sub_op, v.data(), v.size())); }
+    { auto v = pad_records(sg, nc, H->HM, 2, Mt, 2, self_i); TRY(upload(H, &H->sub_gather, v.data(), v.size())); }
+    { auto v = pad_records(act, nc, 1, H->HM, 1, Mt, zero_b); TRY(upload(H, &H->sub_active, v.data(), v.size())); }
   } else {
-    TRY(setup_array(S, "weno_big_op", &hf, &hi, &hb, &shp));
+    std::vector<double> op, so;
+    std::vector<int> bg, sg;
+    std::vector<int8_t> act;
+    TRY(setup_array(S, "weno_big_op", &op, &hi, &hb, &shp));
     H->K = (int)shp[2];
-    TRY(upload(H, &H->big_op, hf.data(), hf.size()));
     TRY(setup_array(S, "weno_big_gather", &hf, &hi, &hb, &shp));
-    { auto v = to_i32(hi.data(), hi.size()); TRY(upload(H, &H->big_gather, v.data(), v.size())); }
-    TRY(setup_array(S, "weno_sub_op", &hf, &hi, &hb, &shp));
+    bg = to_i32(hi.data(), hi.size());
+    TRY(setup_array(S, "weno_sub_op", &so, &hi, &hb, &shp));
     H->M = (int)shp[1];
     H->S = (int)shp[3];
-    TRY(upload(H, &H->sub_op, hf.data(), hf.size()));
     TRY(setup_array(S, "weno_sub_gather", &hf, &hi, &hb, &shp));
-    { auto v = to_i32(hi.data(), hi.size()); TRY(upload(H, &H->sub_gather, v.data(), v.size())); }
-    TRY(setup_array(S, "weno_sub_active", &hf, &hi, &hb, &shp));
-    TRY(upload(H, &H->sub_active, hb.data(), hb.size()));
-    if (H->M > 8) { set_error("WENO: more than 8 sub-stencils per cell"); return GKS_ERR_BAD_ARG; }
+    sg = to_i32(hi.data(), hi.size());
+    TRY(setup_array(S, "weno_sub_active", &hf, &hi, &act, &shp));
+    int Kt, Mt, St;
+    if (!weno_shape(H->K, H->M, H->S, &Kt, &Mt, &St)) {
+      set_error("WENO stencil shape (%d, %d, %d) exceeds the reconstruction kernels", H->K, H->M, H->S);
+      return GKS_ERR_BAD_ARG;
+    }
+    H->Kt = Kt; H->Mt = Mt; H->St = St;
+    { auto v = pad_records(op, nc, 9, H->K, 9, Kt, zero_d); TRY(upload(H, &H->big_op, v.data(), v.size())); }
+    { auto v = pad_records(bg, nc, 1, H->K, 1, Kt, self_i); TRY(upload(H, &H->big_gather, v.data(), v.size())); }
+    {
+      // sub operator (M, 3, S) -> (Mt, 3, St)
+      auto v = pad_records(so, nc * H->M, 3, H->S, 3, St, zero_d);  // pad S
+      auto w = pad_records(v, nc, H->M, 3 * St, Mt, 3 * St, zero_d);  // pad M
+      TRY(upload(H, &H->sub_op, w.data(), w.size()));
+    }
+    {
+      std::vector<int> v((size_t)nc * Mt * St);
+      for (int64_t c = 0; c < nc; ++c)
+        for (int mm = 0; mm < Mt; ++mm)
+          for (int s2 = 0; s2 < St; ++s2)
+            v[(c * Mt + mm) * St + s2] = (mm < H->M && s2 < H->S) ? sg[(c * H->M + mm) * H->S + s2] : (int)c;
+      TRY(upload(H, &H->sub_gather, v.data(), v.size()));
+    }
+    { auto v = pad_records(act, nc, 1, H->M, 1, Mt, zero_b); TRY(upload(H, &H->sub_active, v.data(), v.size())); }
   }
 
   // state and work buffers

@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "gks_solver.cuh"
+#include "gks_stage.cuh"
 
 namespace gks {
 
@@ -85,9 +86,24 @@ __global__ void k_fill(int64_t n, double* __restrict__ dt, const double* val) {
 // (cell, component) because the WENO weights are per cell per component
 // (recon.py:167-195).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void combine(double cb[9], const double (&b)[8][3], const int8_t* act, int M,
-                                        const double* __restrict__ B, double eps, double lw) {
-  // beta0 = c^T B c with B packed as its upper triangle (45 entries, row-major)
+// K2 kernels run on tiles of RT cells per CTA (RT x 5 threads: thread =
+// (cell, component)).  Warp 0 stages the tile's per-cell operator records
+// into shared memory with bulk copies (gks_stage.cuh); every thread then
+// gathers its stencil's Q from L2 and contracts against the staged records.
+//
+// Stencil shapes are compile-time (K, M, S) / (HA, HG, M): the handle pads
+// every cell's records to the instantiated shape at upload (zero operator
+// columns, the cell itself as padded gather index, inactive padded
+// sub-stencils), so the kernels carry no runtime bounds: ncu r01 measured
+// 45 % of all instructions in the runtime-bound version as ISETP/IMAD/BRA.
+static constexpr int RT = 32;
+static constexpr int RT_THREADS = RT * 5;
+
+// recon.py:167-195 on one (cell, component); beta packed as the upper
+// triangle (45 entries, row-major).
+template <int M>
+__device__ __forceinline__ void combine(double cb[9], const double (&b)[M][3], const int8_t* act,
+                                        const double* B, double eps, double lw) {
   double beta0 = 0.0;
   {
     int idx = 0;
@@ -100,24 +116,24 @@ __device__ __forceinline__ void combine(double cb[9], const double (&b)[8][3], c
     }
   }
   int nact = 0;
-  double bs[8];
+  double bs[M];
 #pragma unroll
-  for (int m = 0; m < 8; ++m) {
+  for (int m = 0; m < M; ++m) {
     bs[m] = b[m][0] * b[m][0] + b[m][1] * b[m][1] + b[m][2] * b[m][2];
-    if (m < M && act[m]) ++nact;
+    if (act[m]) ++nact;
   }
   const double g0 = 1.0 - lw * nact;
   double tau = 0.0;
 #pragma unroll
-  for (int m = 0; m < 8; ++m)
-    if (m < M && act[m]) tau += fabs(beta0 - bs[m]);
+  for (int m = 0; m < M; ++m)
+    if (act[m]) tau += fabs(beta0 - bs[m]);
   tau /= (double)(nact > 1 ? nact : 1);
   const double w0 = g0 * (1.0 + tau / (beta0 + eps));
-  double wm[8];
+  double wm[M];
   double total = w0;
 #pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    wm[m] = (m < M && act[m]) ? lw * (1.0 + tau / (bs[m] + eps)) : 0.0;
+  for (int m = 0; m < M; ++m) {
+    wm[m] = act[m] ? lw * (1.0 + tau / (bs[m] + eps)) : 0.0;
     total += wm[m];
   }
   const double w0n = w0 / total;
@@ -126,8 +142,8 @@ __device__ __forceinline__ void combine(double cb[9], const double (&b)[8][3], c
 #pragma unroll
   for (int d = 0; d < 9; ++d) cb[d] *= c0;
 #pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    if (m < M && act[m]) {
+  for (int m = 0; m < M; ++m) {
+    if (act[m]) {
       const double f = wm[m] / total - sub0;
 #pragma unroll
       for (int d = 0; d < 3; ++d) cb[d] += f * b[m][d];
@@ -135,138 +151,170 @@ __device__ __forceinline__ void combine(double cb[9], const double (&b)[8][3], c
   }
 }
 
-// KM / SM: compile-time upper bounds of the big-stencil and sub-stencil widths
-// (loops fully unrolled with a predicate, so every gather of a thread is in
-// flight at once instead of one dependent gather chain per member).
-template <int KM, int SM>
-__global__ void __launch_bounds__(TPB, GKS_RECON_MINB) k_recon_weno(int64_t nc, const double* __restrict__ q,
-                                                    const double* __restrict__ big_op, const int* __restrict__ big_gather,
-                                                    int K, const double* __restrict__ sub_op,
-                                                    const int* __restrict__ sub_gather, const int8_t* __restrict__ sub_active,
-                                                    int M, int S, const double* __restrict__ beta, int linear,
-                                                    double eps, double lw, double* __restrict__ coef, const int* gate) {
+// staged arrays of the two schemes
+enum : int { WT_OP = 0, WT_GI, WT_SO, WT_SG, WT_ACT, WT_BETA, WT_N };
+enum : int { HT_OP = 0, HT_AG, HT_GG, HT_GS, HT_SO, HT_SG, HT_ACT, HT_BETA, HT_N };
+using WenoTile = Tile<WT_N>;
+using HwenoTile = Tile<HT_N>;
+
+inline WenoTile weno_tile(int K, int M, int S, const double* big_op, const int* big_gather, const double* sub_op,
+                          const int* sub_gather, const int8_t* sub_active, const double* beta, bool linear) {
+  TileBuilder<WT_N> b(RT);
+  b.add(WT_OP, big_op, 9u * K * 8u);
+  b.add(WT_GI, big_gather, (uint32_t)K * 4u);
+  b.add(WT_SO, sub_op, 3u * M * S * 8u, !linear);
+  b.add(WT_SG, sub_gather, (uint32_t)(M * S) * 4u, !linear);
+  b.add(WT_ACT, sub_active, (uint32_t)M, !linear);
+  b.add(WT_BETA, beta, 45u * 8u, !linear);
+  return b.t;
+}
+
+inline HwenoTile hweno_tile(int HA, int HG, int M, const double* big_op, const int* avg_gather,
+                            const int* grad_gather, const double* grad_scale, const double* sub_op,
+                            const int* sub_gather, const int8_t* sub_active, const double* beta, bool linear) {
+  TileBuilder<HT_N> b(RT);
+  b.add(HT_OP, big_op, 9u * (HA + 3 * HG) * 8u);
+  b.add(HT_AG, avg_gather, (uint32_t)HA * 4u);
+  b.add(HT_GG, grad_gather, (uint32_t)HG * 4u);
+  b.add(HT_GS, grad_scale, (uint32_t)HG * 8u);
+  b.add(HT_SO, sub_op, (uint32_t)M * 21u * 8u, !linear);
+  b.add(HT_SG, sub_gather, (uint32_t)M * 2u * 4u, !linear);
+  b.add(HT_ACT, sub_active, (uint32_t)M, !linear);
+  b.add(HT_BETA, beta, 45u * 8u, !linear);
+  return b.t;
+}
+
+template <class T, int N>
+__device__ __forceinline__ const T* staged(const unsigned char* sm, const Tile<N>& t, int i, int cl) {
+  return (const T*)(sm + t.a[i].off + cl * t.a[i].stride);
+}
+
+template <int K, int M, int S>
+__global__ void __launch_bounds__(RT_THREADS, GKS_RECON_MINB) k_recon_weno(int64_t nc, const double* __restrict__ q,
+                                                                           WenoTile T, int linear, double eps,
+                                                                           double lw, double* __restrict__ coef,
+                                                                           const int* gate) {
   if (gate && !*gate) return;
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nc * 5) return;
-  const int64_t c = t / 5;
-  const int k = (int)(t - c * 5);
-  const double qc = q[c * 5 + k];
-  const double* op = big_op + c * 9 * K;
-  const int* gi = big_gather + c * K;
-  double r[KM];
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ uint64_t bar;
+  const int64_t c0 = (int64_t)blockIdx.x * RT;
+  const int n = (int)(nc - c0 < RT ? nc - c0 : RT);
+  stage_tile(sm, &bar, T, c0, n);
+  const int cl = threadIdx.x / 5;
+  const int k = threadIdx.x - cl * 5;
+  const int64_t c = c0 + cl;
+  const double qc = cl < n ? __ldg(q + c * 5 + k) : 0.0;
+  mbar_wait(&bar, 0);
+  if (cl >= n) return;
+  const double* op = staged<double>(sm, T, WT_OP, cl);
+  const int* gi = staged<int>(sm, T, WT_GI, cl);
+  double r[K];
 #pragma unroll
-  for (int j = 0; j < KM; ++j) r[j] = j < K ? __ldg(q + (int64_t)__ldg(gi + j) * 5 + k) - qc : 0.0;
+  for (int j = 0; j < K; ++j) r[j] = __ldg(q + (int64_t)gi[j] * 5 + k) - qc;
   double cb[9];
 #pragma unroll
   for (int d = 0; d < 9; ++d) {
     double acc = 0.0;
 #pragma unroll
-    for (int j = 0; j < KM; ++j)
-      if (j < K) acc += __ldg(op + d * K + j) * r[j];
+    for (int j = 0; j < K; ++j) acc += op[d * K + j] * r[j];
     cb[d] = acc;
   }
   if (!linear) {
-    double b[8][3];
-    const int8_t* act = sub_active + c * M;
+    const double* so = staged<double>(sm, T, WT_SO, cl);
+    const int* sg = staged<int>(sm, T, WT_SG, cl);
+    double b[M][3];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) {
-      b[m][0] = b[m][1] = b[m][2] = 0.0;
-      if (m < M) {
-        const double* so = sub_op + (c * M + m) * 3 * S;
-        const int* sg = sub_gather + (c * M + m) * S;
-        double rs[SM];
+    for (int m = 0; m < M; ++m) {
+      double rs[S];
 #pragma unroll
-        for (int s2 = 0; s2 < SM; ++s2) rs[s2] = s2 < S ? __ldg(q + (int64_t)__ldg(sg + s2) * 5 + k) - qc : 0.0;
+      for (int s2 = 0; s2 < S; ++s2) rs[s2] = __ldg(q + (int64_t)sg[m * S + s2] * 5 + k) - qc;
 #pragma unroll
-        for (int s2 = 0; s2 < SM; ++s2) {
-          if (s2 < S) {
-            b[m][0] += __ldg(so + s2) * rs[s2];
-            b[m][1] += __ldg(so + S + s2) * rs[s2];
-            b[m][2] += __ldg(so + 2 * S + s2) * rs[s2];
-          }
-        }
+      for (int d = 0; d < 3; ++d) {
+        double acc = 0.0;
+#pragma unroll
+        for (int s2 = 0; s2 < S; ++s2) acc += so[(m * 3 + d) * S + s2] * rs[s2];
+        b[m][d] = acc;
       }
     }
-    combine(cb, b, act, M, beta + c * 45, eps, lw);
+    combine<M>(cb, b, staged<int8_t>(sm, T, WT_ACT, cl), staged<double>(sm, T, WT_BETA, cl), eps, lw);
   }
   double* out = coef + c * 45 + k;
 #pragma unroll
   for (int d = 0; d < 9; ++d) out[d * 5] = cb[d];
 }
 
-template <int HAM, int HGM>
-__global__ void __launch_bounds__(TPB, GKS_RECON_MINB) k_recon_hweno(int64_t nc, const double* __restrict__ q,
-                                                     const double* __restrict__ grad, const double* __restrict__ h,
-                                                     const double* __restrict__ big_op, const int* __restrict__ avg_gather,
-                                                     const int* __restrict__ grad_gather,
-                                                     const double* __restrict__ grad_scale, int HA, int HG,
-                                                     const double* __restrict__ sub_op, const int* __restrict__ sub_gather,
-                                                     const int8_t* __restrict__ sub_active, int M,
-                                                     const double* __restrict__ beta, int linear, double eps, double lw,
-                                                     double* __restrict__ coef, const int* gate) {
+template <int HA, int HG, int M>
+__global__ void __launch_bounds__(RT_THREADS, GKS_RECON_MINB) k_recon_hweno(int64_t nc, const double* __restrict__ q,
+                                                                            const double* __restrict__ grad,
+                                                                            const double* __restrict__ h,
+                                                                            HwenoTile T, int linear, double eps,
+                                                                            double lw, double* __restrict__ coef,
+                                                                            const int* gate) {
   if (gate && !*gate) return;
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nc * 5) return;
-  const int64_t c = t / 5;
-  const int k = (int)(t - c * 5);
-  const double qc = q[c * 5 + k];
-  const int W = HA + 3 * HG;
-  const double* op = big_op + c * 9 * W;
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ uint64_t bar;
+  const int64_t c0 = (int64_t)blockIdx.x * RT;
+  const int n = (int)(nc - c0 < RT ? nc - c0 : RT);
+  stage_tile(sm, &bar, T, c0, n);
+  const int cl = threadIdx.x / 5;
+  const int k = threadIdx.x - cl * 5;
+  const int64_t c = c0 + cl;
+  const double qc = cl < n ? __ldg(q + c * 5 + k) : 0.0;
+  mbar_wait(&bar, 0);
+  if (cl >= n) return;
+  constexpr int W = HA + 3 * HG;
+  const double* op = staged<double>(sm, T, HT_OP, cl);
+  const int* ag = staged<int>(sm, T, HT_AG, cl);
+  const int* gg = staged<int>(sm, T, HT_GG, cl);
+  const double* gs = staged<double>(sm, T, HT_GS, cl);
   // right-hand side: neighbour averages, then h-scaled gradients (hweno.py:147-151)
-  double ra[HAM], rg[HGM][3];
+  double ra[HA], rg[HG][3];
 #pragma unroll
-  for (int j = 0; j < HAM; ++j) ra[j] = j < HA ? __ldg(q + (int64_t)__ldg(avg_gather + c * HA + j) * 5 + k) - qc : 0.0;
+  for (int j = 0; j < HA; ++j) ra[j] = __ldg(q + (int64_t)ag[j] * 5 + k) - qc;
 #pragma unroll
-  for (int g = 0; g < HGM; ++g) {
-    if (g < HG) {
-      const int64_t m = __ldg(grad_gather + c * HG + g);
-      const double sc = __ldg(grad_scale + c * HG + g);
+  for (int g = 0; g < HG; ++g) {
+    const int64_t m = gg[g];
+    const double sc = gs[g];
 #pragma unroll
-      for (int x = 0; x < 3; ++x) rg[g][x] = sc * __ldg(grad + (m * 3 + x) * 5 + k);
-    } else {
-      rg[g][0] = rg[g][1] = rg[g][2] = 0.0;
-    }
+    for (int x = 0; x < 3; ++x) rg[g][x] = sc * __ldg(grad + (m * 3 + x) * 5 + k);
   }
   double cb[9];
 #pragma unroll
   for (int d = 0; d < 9; ++d) {
     double acc = 0.0;
 #pragma unroll
-    for (int j = 0; j < HAM; ++j)
-      if (j < HA) acc += __ldg(op + d * W + j) * ra[j];
+    for (int j = 0; j < HA; ++j) acc += op[d * W + j] * ra[j];
 #pragma unroll
-    for (int g = 0; g < HGM; ++g)
-      if (g < HG) {
+    for (int g = 0; g < HG; ++g)
 #pragma unroll
-        for (int x = 0; x < 3; ++x) acc += __ldg(op + d * W + HA + 3 * g + x) * rg[g][x];
-      }
+      for (int x = 0; x < 3; ++x) acc += op[d * W + HA + 3 * g + x] * rg[g][x];
     cb[d] = acc;
   }
   if (!linear) {
-    double b[8][3];
-    const int8_t* act = sub_active + c * M;
+    const double* so = staged<double>(sm, T, HT_SO, cl);
+    const int* sg = staged<int>(sm, T, HT_SG, cl);
+    double b[M][3];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) {
-      b[m][0] = b[m][1] = b[m][2] = 0.0;
-      if (m < M) {
-        const double* so = sub_op + (c * M + m) * 21;
-        const int64_t s0 = sub_gather[(c * M + m) * 2 + 0];
-        const int64_t s1 = sub_gather[(c * M + m) * 2 + 1];
-        double rhs[7];
-        rhs[0] = q[s1 * 5 + k] - qc;
-        const double h0 = h[s0], h1 = h[s1];
+    for (int m = 0; m < M; ++m) {
+      const int64_t s0 = sg[m * 2 + 0];
+      const int64_t s1 = sg[m * 2 + 1];
+      double rhs[7];
+      rhs[0] = __ldg(q + s1 * 5 + k) - qc;
+      const double h0 = __ldg(h + s0), h1 = __ldg(h + s1);
 #pragma unroll
-        for (int x = 0; x < 3; ++x) {
-          rhs[1 + x] = h0 * grad[(s0 * 3 + x) * 5 + k];
-          rhs[4 + x] = h1 * grad[(s1 * 3 + x) * 5 + k];
-        }
+      for (int x = 0; x < 3; ++x) {
+        rhs[1 + x] = h0 * __ldg(grad + (s0 * 3 + x) * 5 + k);
+        rhs[4 + x] = h1 * __ldg(grad + (s1 * 3 + x) * 5 + k);
+      }
 #pragma unroll
-        for (int d = 0; d < 3; ++d)
+      for (int d = 0; d < 3; ++d) {
+        double acc = 0.0;
 #pragma unroll
-          for (int s2 = 0; s2 < 7; ++s2) b[m][d] += so[d * 7 + s2] * rhs[s2];
+        for (int s2 = 0; s2 < 7; ++s2) acc += so[(m * 3 + d) * 7 + s2] * rhs[s2];
+        b[m][d] = acc;
       }
     }
-    combine(cb, b, act, M, beta + c * 45, eps, lw);
+    combine<M>(cb, b, staged<int8_t>(sm, T, HT_ACT, cl), staged<double>(sm, T, HT_BETA, cl), eps, lw);
   }
   double* out = coef + c * 45 + k;
 #pragma unroll
@@ -584,30 +632,62 @@ int local_dt_device(Handle* H) {
   return GKS_OK;
 }
 
-int residual_device(Handle* H, const double* q, double* res, bool with_gradients, const int* gate) {
-  const int64_t n5 = H->n_recon * 5;  // owned + layer-1 ghosts (redundant reconstruction)
+// Instantiated stencil shapes; the handle pads its records to one of them
+// (gks_api.cu recon_shape).
+static int recon_device(Handle* H, const double* q, const int* gate) {
+  const int nbt = blocks_for(H->n_recon, RT);
+  const bool lin = H->linear_weights != 0;
+  constexpr uint32_t kMaxSmem = 227 * 1024;
+  const int Kt = H->Kt, Mt = H->Mt, St = H->St;
   if (H->compact) {
-    const int nb5 = blocks_for(n5, TPB);
-#define GKS_HWENO(HAM, HGM)                                                                                       \
-  GKS_LAUNCH(KC_RECON, (k_recon_hweno<HAM, HGM>), nb5, TPB, 0, H->stream, H->n_recon, q, H->grad, H->h, H->big_op, \
-             H->avg_gather, H->grad_gather, H->grad_scale, H->HA, H->HG, H->sub_op, H->sub_gather, H->sub_active,   \
-             H->HM, H->beta, H->linear_weights, H->eps, H->lw, H->coef, gate)
-    if (H->HA <= 4 && H->HG <= 5) GKS_HWENO(4, 5);
-    else if (H->HA <= 6 && H->HG <= 7) GKS_HWENO(6, 7);
-    else GKS_HWENO(16, 17);
+    const HwenoTile T = hweno_tile(Kt, St, Mt, H->big_op, H->avg_gather, H->grad_gather, H->grad_scale, H->sub_op,
+                                   H->sub_gather, H->sub_active, H->beta, lin);
+    if (T.smem > kMaxSmem) {
+      set_error("reconstruction tile needs %u B of shared memory (stencil too wide)", T.smem);
+      return GKS_ERR_BAD_ARG;
+    }
+#define GKS_HWENO(HA, HG, M)                                                                                      \
+  if (Kt == HA && St == HG && Mt == M) {                                                                          \
+    GKS_CUDA(cudaFuncSetAttribute(k_recon_hweno<HA, HG, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
+                                  (int)T.smem));                                                                  \
+    GKS_LAUNCH(KC_RECON, (k_recon_hweno<HA, HG, M>), nbt, RT_THREADS, T.smem, H->stream, H->n_recon, q, H->grad,   \
+               H->h, T, H->linear_weights, H->eps, H->lw, H->coef, gate);                                         \
+    return GKS_OK;                                                                                                \
+  }
+    GKS_HWENO(4, 5, 4)
+    GKS_HWENO(6, 7, 6)
+    GKS_HWENO(16, 17, 8)
 #undef GKS_HWENO
   } else {
-    const int nb5 = blocks_for(n5, TPB);
-#define GKS_WENO(KM, SM)                                                                                        \
-  GKS_LAUNCH(KC_RECON, (k_recon_weno<KM, SM>), nb5, TPB, 0, H->stream, H->n_recon, q, H->big_op, H->big_gather,  \
-             H->K, H->sub_op, H->sub_gather, H->sub_active, H->M, H->S, H->beta, H->linear_weights, H->eps, H->lw, \
-             H->coef, gate)
-    if (H->K <= 16 && H->S <= 6) GKS_WENO(16, 6);
-    else if (H->K <= 24 && H->S <= 6) GKS_WENO(24, 6);
-    else if (H->K <= 32 && H->S <= 8) GKS_WENO(32, 8);
-    else GKS_WENO(64, 16);
+    const WenoTile T = weno_tile(Kt, Mt, St, H->big_op, H->big_gather, H->sub_op, H->sub_gather, H->sub_active,
+                                 H->beta, lin);
+    if (T.smem > kMaxSmem) {
+      set_error("reconstruction tile needs %u B of shared memory (stencil too wide)", T.smem);
+      return GKS_ERR_BAD_ARG;
+    }
+#define GKS_WENO(K, M, S)                                                                                         \
+  if (Kt == K && Mt == M && St == S) {                                                                            \
+    GKS_CUDA(cudaFuncSetAttribute(k_recon_weno<K, M, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,             \
+                                  (int)T.smem));                                                                  \
+    GKS_LAUNCH(KC_RECON, (k_recon_weno<K, M, S>), nbt, RT_THREADS, T.smem, H->stream, H->n_recon, q, T,            \
+               H->linear_weights, H->eps, H->lw, H->coef, gate);                                                  \
+    return GKS_OK;                                                                                                \
+  }
+    GKS_WENO(13, 4, 6)
+    GKS_WENO(14, 4, 6)
+    GKS_WENO(15, 4, 6)
+    GKS_WENO(16, 4, 6)
+    GKS_WENO(24, 8, 3)
+    GKS_WENO(32, 8, 8)
 #undef GKS_WENO
   }
+  set_error("no reconstruction kernel for padded stencil shape (%d, %d, %d)", Kt, Mt, St);
+  return GKS_ERR_BAD_ARG;
+}
+
+int residual_device(Handle* H, const double* q, double* res, bool with_gradients, const int* gate) {
+  // owned + layer-1 ghosts (redundant reconstruction), RT cells per CTA
+  if (int rc = recon_device(H, q, gate)) return rc;
   FaceArgs A;
   A.nfq = H->nfq;
   A.q = q; A.coef = H->coef; A.cen = H->cen; A.h = H->h; A.avg0 = H->avg0; A.dt = H->dt;

@@ -96,6 +96,7 @@ struct Handle {
   // reconstruction operators
   int K = 0, M = 0, S = 0;          // WENO widths
   int HA = 0, HG = 0, HM = 0;       // HWENO widths
+  int Kt = 0, Mt = 0, St = 0;       // padded record shape of the K2 kernel (K,M,S) / (HA,HG,M)
   double *big_op = nullptr, *sub_op = nullptr, *beta = nullptr, *grad_scale = nullptr;
   int *big_gather = nullptr, *sub_gather = nullptr, *avg_gather = nullptr, *grad_gather = nullptr;
   int8_t* sub_active = nullptr;
