@@ -250,6 +250,10 @@ int gks_advance(GksHandle* h, double* q_inout, double* grad_inout, GksStepInfo* 
 int gks_state_upload(GksHandle* h, const double* q, const double* grad);
 int gks_state_download(GksHandle* h, double* q, double* grad);
 int gks_advance_resident(GksHandle* h, GksStepInfo* info);
+/* Steps after a handle's first replay one captured CUDA graph of the whole
+   step (no host synchronisation inside it).  enable = 0 runs every step
+   uncaptured (default: on unless the environment sets GKS_GRAPH=0). */
+int gks_set_graph(GksHandle* h, int enable);
 /* Solver.frechet_matvec (stepping.py:298-313); sigma <= 0 selects the
    reference's automatic step.  out = (L(q + s v) - L(q)) / s */
 int gks_frechet_matvec(GksHandle* h, const double* q, const double* grad, const double* dt, const double* v,

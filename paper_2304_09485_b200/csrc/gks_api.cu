@@ -24,10 +24,37 @@ struct GksBlockSystem {
   bool owned = true;  // false for the handle's Jacobian view
 };
 
+// Phases of one implicit step with their own device error words, read back
+// once after the step (so the step needs no host synchronisation inside and
+// can be captured in a CUDA graph).
+enum : int { PH_DT = 0, PH_RES, PH_GHOST, PH_N };
+
+// Host mirror of everything the host needs after a step (pinned memory).
+struct StepHost {
+  int st[4 * PH_N];
+  int jst[4];
+  gks::DevScalars sc;
+  gks::GmresDev g;
+};
+
+// One captured implicit step.  The graph bakes in the state buffers, and
+// the step swaps q/q_new (grad/grad_new), so two executables alternate.
+struct StepGraph {
+  cudaGraphExec_t exec = nullptr;
+  const double* q = nullptr;
+  const double* grad = nullptr;
+  int64_t launches = 0;  // kernel nodes (launch accounting on replay)
+};
+
 struct GksHandle {
   gks::Handle H;
   GksBlockSystem jac;
   bool jac_valid = false;
+  int* phase_status = nullptr;  // device, 4 * PH_N ints
+  StepHost* sh = nullptr;       // pinned
+  StepGraph graphs[2];
+  int64_t steps = 0;            // steps advanced through this handle
+  int graph = -1;               // CUDA-graph steps: -1 env default (GKS_GRAPH), 0 off, 1 on
 };
 
 namespace gks {
@@ -430,6 +457,8 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   TRY(alloc(H, &H->bad, nc));
   TRY(alloc(H, &H->scal, 1));
   TRY(alloc(H, &H->status, 4));
+  TRY(alloc(H, &G->phase_status, 4 * PH_N));
+  GKS_CUDA(cudaMallocHost(&G->sh, sizeof(StepHost)));
   {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -455,6 +484,9 @@ void destroy_handle(GksHandle* G) {
   cudaSetDevice(H->device);
   comm_destroy(H);
   if (H->stream) cudaStreamSynchronize(H->stream);
+  for (StepGraph& g : G->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (G->sh) cudaFreeHost(G->sh);
   for (void* p : H->allocs) cudaFree(p);
   blocksys_free(&G->jac.sys);
   if (H->stream) cudaStreamDestroy(H->stream);
@@ -527,6 +559,11 @@ int gks_create_local(const GksMeshDesc* mesh, const GksSetup* setup, const GksOp
 int gks_comm_init(GksHandle* G, const void* unique_id, int nranks, int rank) {
   Handle* H = &G->H;
   TRY(comm_init(H, unique_id, nranks, rank));
+  // captured steps predate the communicator: re-capture with the exchanges
+  for (StepGraph& g : G->graphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g = StepGraph();
+  }
   BlockSys* A = &G->jac.sys;
   A->halo_x = [H](double* x) { halo_exchange(H, H->hx, x, 5, H->stream); };
   A->red2 = [H](double* a, double* b) {
@@ -631,49 +668,145 @@ static void frechet_apply(Handle* H, BlockSys* A, const double* v, double* out, 
              H->vol, H->dt, mode, out, gate);
 }
 
-static int advance_device(GksHandle* G, GksStepInfo* info) {
+// One attempt of the step on the current dt: residual -> Roe Jacobian ->
+// GMRES -> update -> norms (stepping.py:270-296).  Launch-only.
+static int enqueue_attempt(GksHandle* G) {
   Handle* H = &G->H;
   BlockSys* A = &G->jac.sys;
+  // residual-pipeline errors (including those of the Frechet JVPs' residual
+  // evaluations inside GMRES, stepping.py:298-313) land in the PH_RES word
+  struct StatusScope {
+    Handle* H;
+    int* saved;
+    ~StatusScope() { H->status = saved; }
+  } scope{H, H->status};
+  H->status = G->phase_status + 4 * PH_RES;
+  TRY(residual_device(H, H->q, H->res, H->compact != 0, nullptr));
+  if (H->nbf) {
+    H->status = G->phase_status + 4 * PH_GHOST;
+    TRY(boundary_ghosts_device(H, H->q));
+    H->status = G->phase_status + 4 * PH_RES;
+  }
+  TRY(jacobian_enqueue(H, A, H->nbf ? H->ghosts : nullptr));
+  GmresParams P;
+  P.m = H->krylov_dim;
+  P.restarts = H->restarts;
+  P.kmax = H->jacobi_sweeps;
+  P.rtol = H->gmres_rtol;
+  MatvecFn mf = [H, A](const double* v, double* out, const int* gate) {
+    frechet_apply(H, A, v, out, 1, gate, nullptr);
+  };
+  TRY(gmres_enqueue(A, H->res, H->dq, P, H->jac_mode == GKS_JAC_FRECHET ? &mf : nullptr, false));
+  GKS_LAUNCH(KC_UPDATE, k_update, blocks_for(H->n_owned, 256), 256, 0, H->stream, H->n_owned, H->q, H->dq, H->q_new,
+             H->bad);
+  GKS_LAUNCH(KC_UPDATE, k_stats, H->red_blocks, 256, 0, H->stream, H->n_owned, H->res, H->dt, H->bad, H->partial,
+             H->counter, H->scal);
+  TRY(allreduce(H, H->scal->stat, 3, 0, 0, H->stream));
+  TRY(allreduce(H, H->scal->stat + 3, 1, 0, 1, H->stream));
+  if (H->comm) {
+    // every rank must agree on failure: error codes are max-reduced
+    for (int ph = 0; ph < PH_N; ++ph) TRY(allreduce(H, G->phase_status + 4 * ph, 1, 1, 2, H->stream));
+    TRY(allreduce(H, A->status, 1, 1, 2, H->stream));
+  }
+  return GKS_OK;
+}
+
+// The whole step up to the first attempt's norms.
+static int enqueue_step(GksHandle* G) {
+  Handle* H = &G->H;
+  GKS_LAUNCH(KC_SCALAR, k_status_init, 1, 1, 0, H->stream, G->phase_status, PH_N);
+  // ghost layers are stale after the previous update: refresh Q (+grad)
+  TRY(halo_exchange(H, H->hq, H->q, 5, H->stream));
+  if (H->compact) TRY(halo_exchange(H, H->hq, H->grad, 15, H->stream));
+  int* const status = H->status;
+  H->status = G->phase_status + 4 * PH_DT;
+  const int rc = local_dt_device(H);
+  H->status = status;
+  TRY(rc);
+  return enqueue_attempt(G);
+}
+
+// Read the step's device records back (one synchronisation) and report the
+// first error in program order, as the reference raises it.
+static int collect_step(GksHandle* G, GmresHost* gh) {
+  Handle* H = &G->H;
+  BlockSys* A = &G->jac.sys;
+  StepHost* sh = G->sh;
+  GKS_CUDA(cudaMemcpyAsync(sh->st, G->phase_status, sizeof(sh->st), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaMemcpyAsync(sh->jst, A->status, sizeof(sh->jst), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaMemcpyAsync(&sh->sc, H->scal, sizeof(DevScalars), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaMemcpyAsync(&sh->g, A->ws.g, sizeof(GmresDev), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaStreamSynchronize(H->stream));
+  static const char* what[PH_N] = {"local_time_step", "residual", "boundary_ghosts"};
+  for (int ph = 0; ph < PH_N; ++ph) TRY(status_report(H, what[ph], sh->st + 4 * ph));
+  A->dinv_ok = sh->jst[0] == 0;
+  if (!A->dinv_ok) {
+    set_error("singular diagonal block in Jacobi preconditioner");
+    return GKS_ERR_SINGULAR;
+  }
+  return gmres_result(&sh->g, gh);
+}
+
+// CUDA graphs for the step (GKS_GRAPH=0 disables; the per-launch profiler
+// runs uncaptured).  The first step of a handle runs uncaptured so every
+// lazily allocated workspace exists before capture.
+static bool graph_enabled(const GksHandle* G) {
+  static const bool env_on = [] {
+    const char* e = getenv("GKS_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  const bool on = G->graph < 0 ? env_on : G->graph != 0;
+  return on && !g_prof_on && G->steps > 0;
+}
+
+static int run_step_graph(GksHandle* G) {
+  Handle* H = &G->H;
+  StepGraph* slot = nullptr;
+  for (StepGraph& g : G->graphs)
+    if (g.exec && g.q == H->q && g.grad == H->grad) slot = &g;
+  if (!slot) {
+    slot = !G->graphs[0].exec ? &G->graphs[0] : &G->graphs[1];
+    if (slot->exec) {
+      cudaGraphExecDestroy(slot->exec);
+      slot->exec = nullptr;
+    }
+    cudaGraph_t graph = nullptr;
+    const int64_t l0 = gks_kernel_launches();
+    GKS_CUDA(cudaStreamBeginCapture(H->stream, cudaStreamCaptureModeRelaxed));
+    const int rc = enqueue_step(G);
+    const cudaError_t e = cudaStreamEndCapture(H->stream, &graph);
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    GKS_CUDA(e);
+    const cudaError_t ei = cudaGraphInstantiate(&slot->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    GKS_CUDA(ei);
+    slot->q = H->q;
+    slot->grad = H->grad;
+    slot->launches = gks_kernel_launches() - l0;
+    count_launch((int)-slot->launches);  // captured, not launched
+  }
+  GKS_CUDA(cudaGraphLaunch(slot->exec, H->stream));
+  count_launch((int)slot->launches);
+  return GKS_OK;
+}
+
+static int advance_device(GksHandle* G, GksStepInfo* info) {
+  Handle* H = &G->H;
   memset(info, 0, sizeof(*info));
   if (H->scheme == GKS_SCHEME_WENO_LUSGS) {
     set_error("scheme 'weno_lusgs' (sequential LUSGS sweep) is not part of the device path");
     return GKS_ERR_BAD_ARG;
   }
-  // ghost layers are stale after the previous update: refresh Q (+grad)
-  TRY(halo_exchange(H, H->hq, H->q, 5, H->stream));
-  if (H->compact) TRY(halo_exchange(H, H->hq, H->grad, 15, H->stream));
-  reset_status(H);
-  TRY(local_dt_device(H));
-  TRY(check_status(H, "local_time_step"));
+  if (graph_enabled(G)) TRY(run_step_graph(G));
+  else TRY(enqueue_step(G));
   int retried = 0;
   for (int attempt = 0; attempt < 2; ++attempt) {
-    reset_status(H);
-    TRY(residual_device(H, H->q, H->res, H->compact != 0, nullptr));
-    TRY(check_status(H, "residual"));
-    if (H->nbf) {
-      TRY(boundary_ghosts_device(H, H->q));
-      TRY(check_status(H, "boundary_ghosts"));
-    }
-    TRY(jacobian_assemble(H, A, H->nbf ? H->ghosts : nullptr));
-    GmresParams P;
-    P.m = H->krylov_dim;
-    P.restarts = H->restarts;
-    P.kmax = H->jacobi_sweeps;
-    P.rtol = H->gmres_rtol;
     GmresHost gh;
-    MatvecFn mf = [H, A](const double* v, double* out, const int* gate) {
-      frechet_apply(H, A, v, out, 1, gate, nullptr);
-    };
-    TRY(gmres_device(A, H->res, H->dq, P, &gh, H->jac_mode == GKS_JAC_FRECHET ? &mf : nullptr));
-    GKS_LAUNCH(KC_UPDATE, k_update, blocks_for(H->n_owned, 256), 256, 0, H->stream, H->n_owned, H->q, H->dq,
-               H->q_new, H->bad);
-    GKS_LAUNCH(KC_UPDATE, k_stats, H->red_blocks, 256, 0, H->stream, H->n_owned, H->res, H->dt, H->bad, H->partial,
-               H->counter, H->scal);
-    TRY(allreduce(H, H->scal->stat, 3, 0, 0, H->stream));
-    TRY(allreduce(H, H->scal->stat + 3, 1, 0, 1, H->stream));
-    DevScalars sc;
-    GKS_CUDA(cudaMemcpyAsync(&sc, H->scal, sizeof(sc), cudaMemcpyDeviceToHost, H->stream));
-    GKS_CUDA(cudaStreamSynchronize(H->stream));
+    TRY(collect_step(G, &gh));
+    const DevScalars& sc = G->sh->sc;
     info->matvecs += gh.matvecs;
     const int nbad = (int)sc.stat[2];
     if (nbad == 0) {
@@ -684,13 +817,17 @@ static int advance_device(GksHandle* G, GksStepInfo* info) {
       info->dt_min = sc.stat[3];
       info->solver_cycles = gh.ncycles;
       info->retried = retried;
+      G->steps += 1;
       if (g_prof_on) prof_harvest();
       return GKS_OK;
     }
     info->nbad = nbad;
     if (attempt == 0) {
+      // stepping.py:286-293: halve dt on the offending cells and redo the attempt (uncaptured)
       GKS_LAUNCH(KC_UPDATE, k_halve_dt, blocks_for(H->n_owned, 256), 256, 0, H->stream, H->n_owned, H->bad, H->dt);
       TRY(halo_exchange(H, H->hx, H->dt, 1, H->stream));
+      GKS_LAUNCH(KC_SCALAR, k_status_init, 1, 1, 0, H->stream, G->phase_status, PH_N);
+      TRY(enqueue_attempt(G));
       retried = 1;
     }
   }
@@ -924,6 +1061,12 @@ int gks_state_download(GksHandle* G, double* q, double* grad) {
   if (q) GKS_CUDA(cudaMemcpyAsync(q, H->q, H->nc * 5 * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
   if (grad) GKS_CUDA(cudaMemcpyAsync(grad, H->grad, H->nc * 15 * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
   GKS_CUDA(cudaStreamSynchronize(H->stream));
+  return GKS_OK;
+}
+
+int gks_set_graph(GksHandle* G, int enable) {
+  if (!G) return GKS_ERR_BAD_ARG;
+  G->graph = enable ? 1 : 0;
   return GKS_OK;
 }
 

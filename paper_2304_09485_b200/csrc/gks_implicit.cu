@@ -26,6 +26,12 @@
 
 namespace gks {
 
+#define TRY_GM(x)          \
+  do {                     \
+    int _r = (x);          \
+    if (_r) return _r;     \
+  } while (0)
+
 static constexpr int RB_THREADS = 256;
 static constexpr int CELLS_PER_BLOCK = 32;  // (cell,row) kernels: 160 threads
 
@@ -362,6 +368,20 @@ __global__ void k_dinv_apply(int64_t nc, const double* __restrict__ dinv, const 
 // GMRES scalar kernels (single thread): krylov.py:70-131
 // ---------------------------------------------------------------------------
 #define GH(i, jj) g->h[(i) * GM_MMAX + (jj)]
+
+// header of the device GMRES state (only the scalars before `dots` need it)
+__global__ void k_gm_init(GmresDev* g, int m, int restarts, double rtol, double atol) {
+  char* p = (char*)g;
+  for (size_t i = 0; i < offsetof(GmresDev, dots); ++i) p[i] = 0;
+  g->m = m;
+  g->restarts = restarts;
+  g->rtol = rtol;
+  g->atol = atol;
+}
+
+__global__ void k_status_init(int* st, int n) {
+  for (int i = 0; i < n; ++i) st[4 * i] = 0, st[4 * i + 1] = 0x7fffffff, st[4 * i + 2] = 0, st[4 * i + 3] = 0;
+}
 
 __global__ void k_gm_cycle_begin(GmresDev* g) { g->notdone = !g->done; }
 
@@ -704,15 +724,20 @@ void axpy_dot(BlockSys* A, int64_t n, double* w, const double* v, const double* 
 
 // Restarted left-preconditioned GMRES (krylov.py:55-140) on device vectors;
 // x_dev receives the solution.  matvec == nullptr: A v is the block spmv.
-int gmres_device(BlockSys* A, const double* b_dev, double* x_dev, const GmresParams& P, GmresHost* out,
-                 const MatvecFn* matvec) {
+// gmres_enqueue only launches (no host synchronisation, so a whole implicit
+// step can be captured in a CUDA graph); gmres_collect reads the device
+// state back.  check_dinv: refuse a singular Jacobi preconditioner on the
+// host (needs a synchronised Jacobian assembly; the graph path checks the
+// Jacobian's status word after the step instead).
+int gmres_enqueue(BlockSys* A, const double* b_dev, double* x_dev, const GmresParams& P, const MatvecFn* matvec,
+                  bool check_dinv) {
   const int64_t n = A->nc * 5;
   const int m = P.m;
   if (m < 1 || m > GM_MMAX || P.restarts < 1 || P.restarts > GM_RMAX || P.kmax < 0) {
     set_error("gmres: krylov_dim must be in [1, %d], restarts in [1, %d]", GM_MMAX, GM_RMAX);
     return GKS_ERR_BAD_ARG;
   }
-  if (!A->dinv_ok) {
+  if (check_dinv && !A->dinv_ok) {
     set_error("singular diagonal block in Jacobi preconditioner");
     return GKS_ERR_SINGULAR;
   }
@@ -722,16 +747,7 @@ int gmres_device(BlockSys* A, const double* b_dev, double* x_dev, const GmresPar
   if (rc) return rc;
   cudaStream_t s = A->stream;
   GmresDev* g = W->g;
-  {
-    // only the header of the struct needs initialising
-    GmresDev g0;
-    memset(&g0, 0, offsetof(GmresDev, dots));
-    g0.m = m;
-    g0.restarts = P.restarts;
-    g0.rtol = P.rtol;
-    g0.atol = P.atol;
-    GKS_CUDA(cudaMemcpyAsync(g, &g0, offsetof(GmresDev, dots), cudaMemcpyHostToDevice, s));
-  }
+  GKS_LAUNCH(KC_SCALAR, k_gm_init, 1, 1, 0, s, g, m, P.restarts, P.rtol, P.atol);
   GKS_CUDA(cudaMemsetAsync(x_dev, 0, ld * sizeof(double), s));
   const int* act = &g->active;
   const int* notdone = &g->notdone;
@@ -780,8 +796,9 @@ int gmres_device(BlockSys* A, const double* b_dev, double* x_dev, const GmresPar
     }
     GKS_LAUNCH(KC_SCALAR, k_gm_cycle_end, 1, 1, 0, s, g, cyc);
     GKS_LAUNCH(KC_VEC, k_gm_update_x, grid, RB_THREADS, 0, s, n, ld, x_dev, W->V, g);
-    if (P.check_ortho && out) {
+    if (P.check_ortho) {
       // Gram matrix of the cycle's basis (krylov.py:778-782), host-side check
+      // (synchronises: never used inside a captured step)
       GmresDev gh;
       GKS_CUDA(cudaMemcpyAsync(&gh, g, offsetof(GmresDev, dots), cudaMemcpyDeviceToHost, s));
       GKS_CUDA(cudaStreamSynchronize(s));
@@ -793,16 +810,17 @@ int gmres_device(BlockSys* A, const double* b_dev, double* x_dev, const GmresPar
           for (int b = 0; b < ju; ++b) {
             double acc = 0.0;
             for (int64_t i = 0; i < n; ++i) acc += hv[a * ld + i] * hv[b * ld + i];
-            out->ortho_error = std::max(out->ortho_error, fabs(acc - (a == b ? 1.0 : 0.0)));
+            W->ortho_error = std::max(W->ortho_error, fabs(acc - (a == b ? 1.0 : 0.0)));
           }
       }
     }
   }
   GKS_CUDA(cudaGetLastError());
-  GmresDev* gh = new GmresDev;
-  GKS_CUDA(cudaMemcpyAsync(gh, g, sizeof(GmresDev), cudaMemcpyDeviceToHost, s));
-  GKS_CUDA(cudaStreamSynchronize(s));
-  int ret = GKS_OK;
+  return GKS_OK;
+}
+
+// Fill `out` from a host copy of the device GMRES state; returns its error.
+int gmres_result(const GmresDev* gh, GmresHost* out) {
   if (out) {
     out->ncycles = gh->ncycles;
     out->breakdown = gh->breakdown_any;
@@ -816,8 +834,24 @@ int gmres_device(BlockSys* A, const double* b_dev, double* x_dev, const GmresPar
   if (gh->err) {
     set_error(gh->err == GKS_ERR_NONFINITE ? "GMRES diverged: non-finite Arnoldi vector" : "GMRES failed (%d)",
               gh->err);
-    ret = gh->err;
+    return gh->err;
   }
+  return GKS_OK;
+}
+
+int gmres_device(BlockSys* A, const double* b_dev, double* x_dev, const GmresParams& P, GmresHost* out,
+                 const MatvecFn* matvec) {
+  A->ws.ortho_error = 0.0;
+  TRY_GM(gmres_enqueue(A, b_dev, x_dev, P, matvec, true));
+  GmresDev* gh = new GmresDev;
+  cudaError_t e = cudaMemcpyAsync(gh, A->ws.g, sizeof(GmresDev), cudaMemcpyDeviceToHost, A->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(A->stream);
+  if (e != cudaSuccess) {
+    delete gh;
+    return cuda_fail(e, "gmres collect", __FILE__, __LINE__);
+  }
+  if (out) out->ortho_error = A->ws.ortho_error;
+  const int ret = gmres_result(gh, out);
   delete gh;
   return ret;
 }
@@ -825,9 +859,8 @@ int gmres_device(BlockSys* A, const double* b_dev, double* x_dev, const GmresPar
 // ---------------------------------------------------------------------------
 // Jacobian assembly on the handle's mesh
 // ---------------------------------------------------------------------------
-int jacobian_assemble(Handle* H, BlockSys* A, const double* ghosts_dev) {
-  const int st0[4] = {0, 0x7fffffff, 0, 0};
-  GKS_CUDA(cudaMemcpyAsync(A->status, st0, sizeof(st0), cudaMemcpyHostToDevice, H->stream));
+int jacobian_enqueue(Handle* H, BlockSys* A, const double* ghosts_dev) {
+  GKS_LAUNCH(KC_SCALAR, k_status_init, 1, 1, 0, H->stream, A->status, 1);
   if (H->nfi)
     GKS_LAUNCH(KC_JAC_FACE, k_jac_faces, blocks_for(H->nfi, 128), 128, 0, H->stream, H->nfi, H->interior_faces, H->f_own, H->f_nbr,
                                                                  H->f_normal, H->f_area, H->q, H->face_slot,
@@ -839,6 +872,11 @@ int jacobian_assemble(Handle* H, BlockSys* A, const double* ghosts_dev) {
              H->cjd, H->f_own, H->f_nbr, H->f_normal, H->f_area, H->bidx, ghosts_dev, H->q, H->vol, H->dt, H->gamma,
              A->diag, A->dinv, A->status);
   GKS_CUDA(cudaGetLastError());
+  return GKS_OK;
+}
+
+int jacobian_assemble(Handle* H, BlockSys* A, const double* ghosts_dev) {
+  TRY_GM(jacobian_enqueue(H, A, ghosts_dev));
   int st[4];
   GKS_CUDA(cudaMemcpyAsync(st, A->status, sizeof(st), cudaMemcpyDeviceToHost, H->stream));
   GKS_CUDA(cudaStreamSynchronize(H->stream));

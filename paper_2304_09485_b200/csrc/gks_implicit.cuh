@@ -35,6 +35,7 @@ struct KrylovWS {
   double* partial = nullptr;
   unsigned int* counter = nullptr;
   GmresDev* g = nullptr;
+  double ortho_error = 0.0;  // host-side Gram check (GmresParams::check_ortho)
 };
 
 // Block-row matrix: diagonal blocks + CSR off-diagonal blocks (jacobian.py:74-126)
@@ -86,5 +87,11 @@ void bs_jacobi(BlockSys* A, const double* b, double* z, double* tmp, int kmax, c
 int gmres_device(BlockSys* A, const double* b_dev, double* x_dev, const GmresParams& P, GmresHost* out,
                  const MatvecFn* matvec);
 int jacobian_assemble(Handle* H, BlockSys* A, const double* ghosts_dev);
+// launch-only halves (CUDA-graph capturable) and the host readback
+int jacobian_enqueue(Handle* H, BlockSys* A, const double* ghosts_dev);
+int gmres_enqueue(BlockSys* A, const double* b_dev, double* x_dev, const GmresParams& P, const MatvecFn* matvec,
+                  bool check_dinv);
+int gmres_result(const GmresDev* gh, GmresHost* out);
+__global__ void k_status_init(int* st, int n);
 
 }  // namespace gks

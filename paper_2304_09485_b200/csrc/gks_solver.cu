@@ -600,12 +600,7 @@ void reset_status(Handle* H) {
     if (_r) return _r;     \
   } while (0)
 
-int check_status(Handle* H, const char* what) {
-  int st[4];
-  // every rank must agree on failure: the error code is max-reduced first
-  if (H->comm) TRY_STATUS(allreduce(H, H->status, 1, 1, 2, H->stream));
-  GKS_CUDA(cudaMemcpyAsync(st, H->status, sizeof(st), cudaMemcpyDeviceToHost, H->stream));
-  GKS_CUDA(cudaStreamSynchronize(H->stream));
+int status_report(Handle* H, const char* what, const int* st) {
   if (st[0] == 0) return GKS_OK;
   set_error_index(st[1]);
   if (st[0] == GKS_ERR_UNPHYSICAL && st[2] > 0 && st[2] - 1 < (int)H->patch_names.size())
@@ -614,6 +609,15 @@ int check_status(Handle* H, const char* what) {
   else
     set_error("%s: error %d at index %d", what, st[0], st[1]);
   return st[0];
+}
+
+int check_status(Handle* H, const char* what) {
+  int st[4];
+  // every rank must agree on failure: the error code is max-reduced first
+  if (H->comm) TRY_STATUS(allreduce(H, H->status, 1, 1, 2, H->stream));
+  GKS_CUDA(cudaMemcpyAsync(st, H->status, sizeof(st), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaStreamSynchronize(H->stream));
+  return status_report(H, what, st);
 }
 
 int local_dt_device(Handle* H) {

@@ -283,5 +283,7 @@ int jacobian_device(Handle* H, const double* q, bool ghosts_given);
 void count_launch(int n);
 void set_error_index(int64_t i);
 int check_status(Handle* H, const char* what);
+// message + code for a host copy of a device error word (0: no error)
+int status_report(Handle* H, const char* what, const int* st);
 
 }  // namespace gks

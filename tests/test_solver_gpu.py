@@ -138,3 +138,26 @@ def test_advance_history(case):
         assert relmax(f.q, g["q_after"][k]) < 1e-9
     if solver.compact:
         assert relmax(f.grad, g["grad_after"]) < 1e-8
+
+
+def test_graph_replay_matches_uncaptured(case):
+    """Steps after the first replay a captured CUDA graph of the whole step;
+    the result must be bit-for-bit the uncaptured launch sequence's."""
+    from paper_2304_09485_b200 import _native as N
+    from paper_2304_09485_b200.stepping import SolutionField
+
+    name, mesh, _, g = case
+    runs = []
+    for graph in (1, 0):
+        _, s = build(name)
+        N.check(N.load().gks_set_graph(s._handle, graph))
+        s.upload(fld_of(g, s))
+        hist = [s.advance_resident() for _ in range(5)]
+        out = s.download()
+        runs.append((hist, out))
+    (h1, o1), (h0, o0) = runs
+    assert [(i.res_rho_l1, i.res_l2, i.dt_min, i.solver_cycles) for i in h1] == \
+        [(i.res_rho_l1, i.res_l2, i.dt_min, i.solver_cycles) for i in h0]
+    assert np.array_equal(o1.q, o0.q)
+    if o1.grad is not None:
+        assert np.array_equal(o1.grad, o0.grad)
