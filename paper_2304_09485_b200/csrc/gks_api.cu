@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "gks_implicit.cuh"
+#include "gks_stage.cuh"
 
 extern "C" {
 // native setup internals (gks_setup.cpp)
@@ -135,6 +136,24 @@ static std::vector<T> pad_records(const std::vector<T>& src, int64_t nc, int64_t
   return out;
 }
 
+// Re-stride per-cell records of E entries to the staging stride (gks_stage.cuh
+// rec_stride_*), zero-filled.
+template <class T>
+static std::vector<T> restride(const std::vector<T>& src, int64_t nc, int64_t E) {
+  const int64_t Es = sizeof(T) == 8 ? rec_stride_f64((int)E) : (sizeof(T) == 4 ? rec_stride_i32((int)E) : E);
+  if (Es == E) return src;
+  std::vector<T> out((size_t)nc * Es, T(0));
+  for (int64_t c = 0; c < nc; ++c)
+    for (int64_t e = 0; e < E; ++e) out[c * Es + e] = src[c * E + e];
+  return out;
+}
+
+template <class T>
+static int upload_rec(Handle* H, T** dst, const std::vector<T>& src, int64_t nc) {
+  const std::vector<T> v = restride(src, nc, nc ? (int64_t)src.size() / nc : 0);
+  return upload(H, dst, v.data(), v.size());
+}
+
 static bool weno_shape(int K, int M, int S, int* Kt, int* Mt, int* St) {
   if (M <= 4 && S <= 6 && K <= 16) { *Kt = std::max(K, 13); *Mt = 4; *St = 6; return true; }
   if (M <= 8 && S <= 3 && K <= 24) { *Kt = 24; *Mt = 8; *St = 3; return true; }
@@ -232,7 +251,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
       for (int d = 0; d < 9; ++d)
         for (int e = d; e < 9; ++e) packed[c * 45 + idx++] = hf[c * 81 + d * 9 + e];
     }
-    TRY(upload(H, &H->beta, packed.data(), packed.size()));
+    TRY(upload_rec(H, &H->beta, packed, nc));
   }
 
   // faces
@@ -393,14 +412,14 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
           for (int j = 0; j < H->HA; ++j) dst[j] = src[j];
           for (int j = 0; j < 3 * H->HG; ++j) dst[At + j] = src[H->HA + j];
         }
-      TRY(upload(H, &H->big_op, opt.data(), opt.size()));
+      TRY(upload_rec(H, &H->big_op, opt, nc));
     }
-    { auto v = pad_records(ag, nc, 1, H->HA, 1, At, self_i); TRY(upload(H, &H->avg_gather, v.data(), v.size())); }
-    { auto v = pad_records(gg, nc, 1, H->HG, 1, Gt, self_i); TRY(upload(H, &H->grad_gather, v.data(), v.size())); }
-    { auto v = pad_records(gs, nc, 1, H->HG, 1, Gt, zero_d); TRY(upload(H, &H->grad_scale, v.data(), v.size())); }
-    { auto v = pad_records(so, nc, H->HM, 21, Mt, 21, zero_d); TRY(upload(H, &H->sub_op, v.data(), v.size())); }
-    { auto v = pad_records(sg, nc, H->HM, 2, Mt, 2, self_i); TRY(upload(H, &H->sub_gather, v.data(), v.size())); }
-    { auto v = pad_records(act, nc, 1, H->HM, 1, Mt, zero_b); TRY(upload(H, &H->sub_active, v.data(), v.size())); }
+    { auto v = pad_records(ag, nc, 1, H->HA, 1, At, self_i); TRY(upload_rec(H, &H->avg_gather, v, nc)); }
+    { auto v = pad_records(gg, nc, 1, H->HG, 1, Gt, self_i); TRY(upload_rec(H, &H->grad_gather, v, nc)); }
+    { auto v = pad_records(gs, nc, 1, H->HG, 1, Gt, zero_d); TRY(upload_rec(H, &H->grad_scale, v, nc)); }
+    { auto v = pad_records(so, nc, H->HM, 21, Mt, 21, zero_d); TRY(upload_rec(H, &H->sub_op, v, nc)); }
+    { auto v = pad_records(sg, nc, H->HM, 2, Mt, 2, self_i); TRY(upload_rec(H, &H->sub_gather, v, nc)); }
+    { auto v = pad_records(act, nc, 1, H->HM, 1, Mt, zero_b); TRY(upload_rec(H, &H->sub_active, v, nc)); }
   } else {
     std::vector<double> op, so;
     std::vector<int> bg, sg;
@@ -421,13 +440,13 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
       return GKS_ERR_BAD_ARG;
     }
     H->Kt = Kt; H->Mt = Mt; H->St = St;
-    { auto v = pad_records(op, nc, 9, H->K, 9, Kt, zero_d); TRY(upload(H, &H->big_op, v.data(), v.size())); }
-    { auto v = pad_records(bg, nc, 1, H->K, 1, Kt, self_i); TRY(upload(H, &H->big_gather, v.data(), v.size())); }
+    { auto v = pad_records(op, nc, 9, H->K, 9, Kt, zero_d); TRY(upload_rec(H, &H->big_op, v, nc)); }
+    { auto v = pad_records(bg, nc, 1, H->K, 1, Kt, self_i); TRY(upload_rec(H, &H->big_gather, v, nc)); }
     {
       // sub operator (M, 3, S) -> (Mt, 3, St)
       auto v = pad_records(so, nc * H->M, 3, H->S, 3, St, zero_d);  // pad S
       auto w = pad_records(v, nc, H->M, 3 * St, Mt, 3 * St, zero_d);  // pad M
-      TRY(upload(H, &H->sub_op, w.data(), w.size()));
+      TRY(upload_rec(H, &H->sub_op, w, nc));
     }
     {
       std::vector<int> v((size_t)nc * Mt * St);
@@ -435,9 +454,9 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
         for (int mm = 0; mm < Mt; ++mm)
           for (int s2 = 0; s2 < St; ++s2)
             v[(c * Mt + mm) * St + s2] = (mm < H->M && s2 < H->S) ? sg[(c * H->M + mm) * H->S + s2] : (int)c;
-      TRY(upload(H, &H->sub_gather, v.data(), v.size()));
+      TRY(upload_rec(H, &H->sub_gather, v, nc));
     }
-    { auto v = pad_records(act, nc, 1, H->M, 1, Mt, zero_b); TRY(upload(H, &H->sub_active, v.data(), v.size())); }
+    { auto v = pad_records(act, nc, 1, H->M, 1, Mt, zero_b); TRY(upload_rec(H, &H->sub_active, v, nc)); }
   }
 
   // state and work buffers

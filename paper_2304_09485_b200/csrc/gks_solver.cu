@@ -157,15 +157,16 @@ enum : int { HT_OP = 0, HT_AG, HT_GG, HT_GS, HT_SO, HT_SG, HT_ACT, HT_BETA, HT_N
 using WenoTile = Tile<WT_N>;
 using HwenoTile = Tile<HT_N>;
 
+// Record bytes in HBM (strides from rec_stride_*, gks_stage.cuh).
 inline WenoTile weno_tile(int K, int M, int S, const double* big_op, const int* big_gather, const double* sub_op,
                           const int* sub_gather, const int8_t* sub_active, const double* beta, bool linear) {
   TileBuilder<WT_N> b(RT);
-  b.add(WT_OP, big_op, 9u * K * 8u);
-  b.add(WT_GI, big_gather, (uint32_t)K * 4u);
-  b.add(WT_SO, sub_op, 3u * M * S * 8u, !linear);
-  b.add(WT_SG, sub_gather, (uint32_t)(M * S) * 4u, !linear);
+  b.add(WT_OP, big_op, 8u * rec_stride_f64(9 * K));
+  b.add(WT_GI, big_gather, 4u * rec_stride_i32(K));
+  b.add(WT_SO, sub_op, 8u * rec_stride_f64(3 * M * S), !linear);
+  b.add(WT_SG, sub_gather, 4u * rec_stride_i32(M * S), !linear);
   b.add(WT_ACT, sub_active, (uint32_t)M, !linear);
-  b.add(WT_BETA, beta, 45u * 8u, !linear);
+  b.add(WT_BETA, beta, 8u * rec_stride_f64(45), !linear);
   return b.t;
 }
 
@@ -173,14 +174,14 @@ inline HwenoTile hweno_tile(int HA, int HG, int M, const double* big_op, const i
                             const int* grad_gather, const double* grad_scale, const double* sub_op,
                             const int* sub_gather, const int8_t* sub_active, const double* beta, bool linear) {
   TileBuilder<HT_N> b(RT);
-  b.add(HT_OP, big_op, 9u * (HA + 3 * HG) * 8u);
-  b.add(HT_AG, avg_gather, (uint32_t)HA * 4u);
-  b.add(HT_GG, grad_gather, (uint32_t)HG * 4u);
-  b.add(HT_GS, grad_scale, (uint32_t)HG * 8u);
-  b.add(HT_SO, sub_op, (uint32_t)M * 21u * 8u, !linear);
-  b.add(HT_SG, sub_gather, (uint32_t)M * 2u * 4u, !linear);
+  b.add(HT_OP, big_op, 8u * rec_stride_f64(9 * (HA + 3 * HG)));
+  b.add(HT_AG, avg_gather, 4u * rec_stride_i32(HA));
+  b.add(HT_GG, grad_gather, 4u * rec_stride_i32(HG));
+  b.add(HT_GS, grad_scale, 8u * rec_stride_f64(HG));
+  b.add(HT_SO, sub_op, 8u * rec_stride_f64(21 * M), !linear);
+  b.add(HT_SG, sub_gather, 4u * rec_stride_i32(2 * M), !linear);
   b.add(HT_ACT, sub_active, (uint32_t)M, !linear);
-  b.add(HT_BETA, beta, 45u * 8u, !linear);
+  b.add(HT_BETA, beta, 8u * rec_stride_f64(45), !linear);
   return b.t;
 }
 

@@ -70,6 +70,12 @@ __host__ __device__ constexpr uint32_t stage_stride(uint32_t bytes) {
   return (bytes % 8 != 0 || ((bytes / 8) & 3u) != 0) ? bytes : bytes + 16u;
 }
 
+// Record strides in HBM: the handle stores every per-cell record with a
+// stride that is already conflict-free in shared memory (doubles: odd or
+// 2 mod 4; 32-bit words: odd), so each array is one chunk copy per tile.
+__host__ __device__ constexpr int rec_stride_f64(int e) { return e % 4 == 0 ? e + 2 : e; }
+__host__ __device__ constexpr int rec_stride_i32(int e) { return e % 2 == 0 ? e + 1 : e; }
+
 // One staged array of the tile: record bytes, smem stride, smem offset.
 struct StageArr {
   const unsigned char* src;  // global base of record 0
@@ -121,26 +127,25 @@ struct TileBuilder {
   }
 };
 
-// Warp 0 arms the tile's mbarrier and issues its bulk copies; the whole CTA
-// then synchronises once so nobody waits on an uninitialised barrier.
+// Thread 0 arms the tile's mbarrier, the CTA synchronises once (nobody may
+// wait on an uninitialised barrier), then warp 0 issues the bulk copies
+// while the other warps go on to their first global loads.
 template <int N>
 __device__ __forceinline__ void stage_tile(unsigned char* sm, uint64_t* bar, const Tile<N>& T, int64_t c0, int n) {
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    if (lane == 0) {
-      uint32_t tx = 0;
-#pragma unroll
-      for (int a = 0; a < N; ++a)
-        if (T.a[a].bytes) tx += stage_tx(T.a[a], n);
-      mbar_init(bar, 1);
-      mbar_expect_tx(bar, tx);
-    }
-    __syncwarp();
+  if (threadIdx.x == 0) {
+    uint32_t tx = 0;
 #pragma unroll
     for (int a = 0; a < N; ++a)
-      if (T.a[a].bytes) stage_issue(sm, T.a[a], c0, n, lane, bar);
+      if (T.a[a].bytes) tx += stage_tx(T.a[a], n);
+    mbar_init(bar, 1);
+    mbar_expect_tx(bar, tx);
   }
   __syncthreads();
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int a = 0; a < N; ++a)
+      if (T.a[a].bytes) stage_issue(sm, T.a[a], c0, n, threadIdx.x, bar);
+  }
 }
 
 }  // namespace gks

@@ -17,23 +17,9 @@ from pathlib import Path
 import numpy as np
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-from bench import c2_mesh, c2_problem  # noqa: E402
+from bench import c2_mesh, c2_problem, cavity_problem  # noqa: E402
 from paper_2304_09485_b200 import meshgen as MG  # noqa: E402
-from paper_2304_09485_b200.boundary import PatchSpec  # noqa: E402
-from paper_2304_09485_b200.mesh import generate_box_mesh  # noqa: E402
-from paper_2304_09485_b200.stepping import SolutionField, Solver, SolverOptions, initial_field  # noqa: E402
-
-GAMMA = 1.4
-
-
-def cavity_problem(n, compact, re=100.0):
-    mesh = generate_box_mesh((1, 1, 1), (n, n, n), split="tet")
-    lam_wall = GAMMA / 2.0
-    patches = {nm: PatchSpec(nm, "wall_noslip_isothermal", lambda_wall=lam_wall) for nm in mesh.patch_names}
-    patches["ymax"] = PatchSpec("ymax", "wall_noslip_isothermal", lambda_wall=lam_wall,
-                                velocity=np.array([0.15, 0.0, 0.0]))
-    fld = initial_field(mesh, [1.0, 0.0, 0.0, 0.0, 1.0 / GAMMA], GAMMA, compact=compact)
-    return mesh, patches, fld.q, fld.grad, dict(model="viscous", mu=0.15 / re)
+from paper_2304_09485_b200.stepping import SolutionField, Solver, SolverOptions  # noqa: E402
 
 
 def main():
