@@ -56,8 +56,8 @@ __device__ __forceinline__ void maxw_full(Maxw& m, const double w[5], const KinC
   m.V[0] = 1.0; m.V[1] = w[2]; recur<6>(m.V, w[2], h);
   m.W[0] = 1.0; m.W[1] = w[3]; recur<6>(m.W, w[3], h);
   m.X[0] = 1.0;
-  m.X[1] = kc.nd / (2.0 * w[4]);
-  m.X[2] = kc.nd * (kc.nd + 2.0) / (4.0 * w[4] * w[4]);
+  m.X[1] = kc.nd * h;                    // N / (2 lam)
+  m.X[2] = kc.nd * (kc.nd + 2.0) * h * h;  // N (N + 2) / (4 lam^2)
 }
 
 // Replace the u table by its half-range version: sign = +1 (u>0) or -1 (u<0).
@@ -162,20 +162,36 @@ __device__ __forceinline__ void gram_acc(const double G[5][5], const double s[5]
     acc[i] += scale * (G[i][0] * s[0] + G[i][1] * s[1] + G[i][2] * s[2] + G[i][3] * s[3] + G[i][4] * s[4]);
 }
 
+// Per-state constants of the micro-slope solve (shared by the 4 solves of
+// one Maxwellian: 3 spatial slopes + the time slope).
+struct SlopeConst {
+  double U, V, W, lam, ir, k2, c4;  // ir = 1/rho, k2 = |u|^2 + (N+3)/(2 lam), c4 = 4 lam^2 / (N+3)
+};
+
+__device__ __forceinline__ SlopeConst slope_const(const double w[5], const KinConst& kc) {
+  SlopeConst s;
+  s.U = w[1]; s.V = w[2]; s.W = w[3]; s.lam = w[4];
+  s.ir = 1.0 / w[0];
+  s.k2 = s.U * s.U + s.V * s.V + s.W * s.W + 0.5 * kc.n3 / s.lam;
+  s.c4 = 4.0 * s.lam * s.lam / kc.n3;
+  return s;
+}
+
 // kinetic.py:271-302 closed-form solve of <a psi> = dq / rho.
-__device__ __forceinline__ void micro_slope(const double w[5], const double dq[5],
-                                            const KinConst& kc, double a[5]) {
-  const double ir = 1.0 / w[0];
-  const double b0 = dq[0] * ir, b1 = dq[1] * ir, b2 = dq[2] * ir, b3 = dq[3] * ir, b4 = dq[4] * ir;
-  const double U = w[1], V = w[2], W = w[3], lam = w[4];
-  const double k2 = U * U + V * V + W * W + 0.5 * kc.n3 / lam;
+__device__ __forceinline__ void micro_slope(const SlopeConst& s, const double dq[5], double a[5]) {
+  const double b0 = dq[0] * s.ir, b1 = dq[1] * s.ir, b2 = dq[2] * s.ir, b3 = dq[3] * s.ir, b4 = dq[4] * s.ir;
+  const double U = s.U, V = s.V, W = s.W, lam = s.lam;
   const double r1 = b1 - U * b0, r2 = b2 - V * b0, r3 = b3 - W * b0;
-  const double r4 = 2.0 * b4 - k2 * b0;
-  a[4] = 4.0 * lam * lam * (r4 - 2.0 * U * r1 - 2.0 * V * r2 - 2.0 * W * r3) / kc.n3;
+  const double r4 = 2.0 * b4 - s.k2 * b0;
+  a[4] = s.c4 * (r4 - 2.0 * U * r1 - 2.0 * V * r2 - 2.0 * W * r3);
   a[3] = 2.0 * lam * r3 - W * a[4];
   a[2] = 2.0 * lam * r2 - V * a[4];
   a[1] = 2.0 * lam * r1 - U * a[4];
-  a[0] = b0 - U * a[1] - V * a[2] - W * a[3] - 0.5 * a[4] * k2;
+  a[0] = b0 - U * a[1] - V * a[2] - W * a[3] - 0.5 * a[4] * s.k2;
+}
+
+__device__ __forceinline__ void micro_slope(const double w[5], const double dq[5], const KinConst& kc, double a[5]) {
+  micro_slope(slope_const(w, kc), dq, a);
 }
 
 // Conserved -> primitive; returns false on rho <= 0 / e <= 0 / non-finite
@@ -183,7 +199,8 @@ __device__ __forceinline__ void micro_slope(const double w[5], const double dq[5
 __device__ __forceinline__ bool cons_to_prim(const double q[5], const KinConst& kc, double w[5]) {
   const double rho = q[0];
   if (!(rho > 0.0) || !isfinite(rho)) return false;
-  const double u = q[1] / rho, v = q[2] / rho, ww = q[3] / rho;
+  const double ir = 1.0 / rho;
+  const double u = q[1] * ir, v = q[2] * ir, ww = q[3] * ir;
   const double e = q[4] - 0.5 * (q[1] * u + q[2] * v + q[3] * ww);
   if (!(e > 0.0) || !isfinite(e)) return false;
   w[0] = rho; w[1] = u; w[2] = v; w[3] = ww;
@@ -305,8 +322,9 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
     double A[5];
     Maxw m;
     maxw_full(m, w, kc);
+    const SlopeConst sc = slope_const(w, kc);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) micro_slope(w, a[k], kc, a[k]);  // slopes -> micro-slopes in place
+    for (int k = 0; k < 3; ++k) micro_slope(sc, a[k], a[k]);  // slopes -> micro-slopes in place
     {
       // time slope from the compatibility condition (kinetic.py:305-312)
       const double zero5[5] = {0, 0, 0, 0, 0};
@@ -314,7 +332,7 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
       wmom<0, true>(m, zero5, a, D);
 #pragma unroll
       for (int i = 0; i < 5; ++i) D[i] = -rho * D[i];
-      micro_slope(w, D, kc, A);
+      micro_slope(sc, D, A);
     }
     maxw_half_u(m, w, side ? -1.0 : 1.0);
     double t[5];
@@ -374,15 +392,16 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
   double ab[3][5], Ab[5];
   Maxw m0;
   maxw_full(m0, w0, kc);
+  const SlopeConst sc0 = slope_const(w0, kc);
 #pragma unroll
-  for (int k = 0; k < 3; ++k) micro_slope(w0, dqa[k], kc, ab[k]);
+  for (int k = 0; k < 3; ++k) micro_slope(sc0, dqa[k], ab[k]);
   {
     const double zero5[5] = {0, 0, 0, 0, 0};
     double D[5];
     wmom<0, true>(m0, zero5, ab, D);
 #pragma unroll
     for (int i = 0; i < 5; ++i) D[i] = -w0[0] * D[i];
-    micro_slope(w0, D, kc, Ab);
+    micro_slope(sc0, D, Ab);
   }
   if (VISCOUS) {
     if (tau < 0.0) tau = collision_tau(pl, pr, dt, true, mu, w0);

@@ -325,40 +325,38 @@ __global__ void __launch_bounds__(RT_THREADS, GKS_RECON_MINB) k_recon_hweno(int6
 // ---------------------------------------------------------------------------
 // K3: fused face kernel, one thread per face quadrature point
 // ---------------------------------------------------------------------------
+// Face value and Cartesian gradient of one side's reconstruction at a face
+// point (recon.py:297-314): val = Q_c + phi . C_c, grad = dphi . C_c with
+// phi = mono((x - x_c) / h) - avg0 and dphi = d mono / dx (recon.py:48-57).
+// The scaled-chart gradient rows are sparse (4 of 9 entries per axis) and
+// share the factor 1/h, so they are summed first and scaled once: one
+// division per side instead of the table's 27 per-entry ones (ncu r01: 125
+// FP64 divisions per face point before).  Rounding differs from the
+// reference's stored tables by an ulp (parity bar 1e-12, tests/).
 __device__ __forceinline__ void eval_side(const double* __restrict__ q, const double* __restrict__ coef,
                                           const double* __restrict__ cen, const double* __restrict__ h,
                                           const double* __restrict__ avg0, int64_t c, const double x[3],
                                           double val[5], double g[3][5]) {
-  const double hc = h[c];
-  const double xt[3] = {(x[0] - cen[3 * c]) / hc, (x[1] - cen[3 * c + 1]) / hc, (x[2] - cen[3 * c + 2]) / hc};
-  const double mono[9] = {xt[0], xt[1], xt[2], xt[0] * xt[0], xt[0] * xt[1],
-                          xt[0] * xt[2], xt[1] * xt[1], xt[1] * xt[2], xt[2] * xt[2]};
-  double phi[9];
-#pragma unroll
-  for (int d = 0; d < 9; ++d) phi[d] = mono[d] - avg0[c * 9 + d];
-  const double ih = 1.0 / hc;
-  // d mono / d xt (recon.py:48-57) divided by h
-  const double gx[9] = {1, 0, 0, 2 * xt[0], xt[1], xt[2], 0, 0, 0};
-  const double gy[9] = {0, 1, 0, 0, xt[0], 0, 2 * xt[1], xt[2], 0};
-  const double gz[9] = {0, 0, 1, 0, 0, xt[0], 0, xt[1], 2 * xt[2]};
+  const double ih = 1.0 / h[c];
+  const double x0 = (x[0] - cen[3 * c]) * ih, x1 = (x[1] - cen[3 * c + 1]) * ih, x2 = (x[2] - cen[3 * c + 2]) * ih;
+  const double* A = avg0 + c * 9;
+  const double phi[9] = {x0 - A[0],      x1 - A[1],      x2 - A[2],      x0 * x0 - A[3], x0 * x1 - A[4],
+                         x0 * x2 - A[5], x1 * x1 - A[6], x1 * x2 - A[7], x2 * x2 - A[8]};
+  const double tx0 = 2.0 * x0, tx1 = 2.0 * x1, tx2 = 2.0 * x2;
   const double* C = coef + c * 45;
 #pragma unroll
   for (int k = 0; k < 5; ++k) {
-    double v = 0.0, a = 0.0, b = 0.0, e = 0.0;
+    double cd[9];
 #pragma unroll
-    for (int d = 0; d < 9; ++d) {
-      const double cd = C[d * 5 + k];
-      v += phi[d] * cd;
-      a += (gx[d] / hc) * cd;
-      b += (gy[d] / hc) * cd;
-      e += (gz[d] / hc) * cd;
-    }
+    for (int d = 0; d < 9; ++d) cd[d] = C[d * 5 + k];
+    double v = 0.0;
+#pragma unroll
+    for (int d = 0; d < 9; ++d) v += phi[d] * cd[d];
     val[k] = q[c * 5 + k] + v;
-    g[0][k] = a;
-    g[1][k] = b;
-    g[2][k] = e;
+    g[0][k] = (cd[0] + tx0 * cd[3] + x1 * cd[4] + x2 * cd[5]) * ih;
+    g[1][k] = (cd[1] + x0 * cd[4] + tx1 * cd[6] + x2 * cd[7]) * ih;
+    g[2][k] = (cd[2] + x0 * cd[5] + x1 * cd[7] + tx2 * cd[8]) * ih;
   }
-  (void)ih;
 }
 
 // value only (no gradients): the pre-loop pressures of the inviscid collision time
@@ -366,13 +364,11 @@ __device__ __forceinline__ void eval_value(const double* __restrict__ q, const d
                                            const double* __restrict__ cen, const double* __restrict__ h,
                                            const double* __restrict__ avg0, int64_t c, const double x[3],
                                            double val[5]) {
-  const double hc = h[c];
-  const double xt[3] = {(x[0] - cen[3 * c]) / hc, (x[1] - cen[3 * c + 1]) / hc, (x[2] - cen[3 * c + 2]) / hc};
-  const double mono[9] = {xt[0], xt[1], xt[2], xt[0] * xt[0], xt[0] * xt[1],
-                          xt[0] * xt[2], xt[1] * xt[1], xt[1] * xt[2], xt[2] * xt[2]};
-  double phi[9];
-#pragma unroll
-  for (int d = 0; d < 9; ++d) phi[d] = mono[d] - avg0[c * 9 + d];
+  const double ih = 1.0 / h[c];
+  const double x0 = (x[0] - cen[3 * c]) * ih, x1 = (x[1] - cen[3 * c + 1]) * ih, x2 = (x[2] - cen[3 * c + 2]) * ih;
+  const double* A = avg0 + c * 9;
+  const double phi[9] = {x0 - A[0],      x1 - A[1],      x2 - A[2],      x0 * x0 - A[3], x0 * x1 - A[4],
+                         x0 * x2 - A[5], x1 * x1 - A[6], x1 * x2 - A[7], x2 * x2 - A[8]};
   const double* C = coef + c * 45;
 #pragma unroll
   for (int k = 0; k < 5; ++k) {
