@@ -27,12 +27,14 @@ struct Maxw {
   double V[6];  // <v^b>, b = 0..5
   double W[6];  // <w^c>, c = 0..5
   double X[3];  // <xi^2s>, s = 0..2
+  double h;     // 1 / (2 lam)
 };
 
 struct KinConst {
   double gamma;
   double nd;   // internal dof N = (5 - 3 gamma)/(gamma - 1)
   double n3;   // N + 3
+  double c4n;  // 4 / (N + 3)
 };
 
 __host__ __device__ inline KinConst make_kin(double gamma) {
@@ -40,6 +42,7 @@ __host__ __device__ inline KinConst make_kin(double gamma) {
   k.gamma = gamma;
   k.nd = (5.0 - 3.0 * gamma) / (gamma - 1.0);
   k.n3 = k.nd + 3.0;
+  k.c4n = 4.0 / k.n3;
   return k;
 }
 
@@ -52,6 +55,7 @@ __device__ __forceinline__ void recur(double* m, double mean, double h) {
 // Full-range tables of a primitive state (rho, U, V, W, lam).
 __device__ __forceinline__ void maxw_full(Maxw& m, const double w[5], const KinConst& kc) {
   const double h = 0.5 / w[4];
+  m.h = h;
   m.U[0] = 1.0; m.U[1] = w[1]; recur<7>(m.U, w[1], h);
   m.V[0] = 1.0; m.V[1] = w[2]; recur<6>(m.V, w[2], h);
   m.W[0] = 1.0; m.W[1] = w[3]; recur<6>(m.W, w[3], h);
@@ -61,13 +65,16 @@ __device__ __forceinline__ void maxw_full(Maxw& m, const double w[5], const KinC
 }
 
 // Replace the u table by its half-range version: sign = +1 (u>0) or -1 (u<0).
+// Needs m.h = 1/(2 lam) from maxw_full; exp(-lam u^2) / (2 sqrt(pi lam)) is
+// formed as exp(.) sqrt(lam) h / sqrt(pi) (no division).
 __device__ __forceinline__ void maxw_half_u(Maxw& m, const double w[5], double sign) {
   const double lam = w[4], u = w[1];
   const double rl = sqrt(lam);
-  const double g = 0.5 * exp(-lam * u * u) / sqrt(M_PI * lam);
+  constexpr double kInvSqrtPi = 0.56418958354775628695;  // 1 / sqrt(pi)
+  const double g = kInvSqrtPi * exp(-lam * u * u) * rl * m.h;
   m.U[0] = 0.5 * erfc(-sign * rl * u);
   m.U[1] = u * m.U[0] + sign * g;
-  recur<7>(m.U, u, 0.5 / lam);
+  recur<7>(m.U, u, m.h);
 }
 
 // One group of weight monomials sharing the factor v^B w^C xi^2S, with a
@@ -168,13 +175,18 @@ struct SlopeConst {
   double U, V, W, lam, ir, k2, c4;  // ir = 1/rho, k2 = |u|^2 + (N+3)/(2 lam), c4 = 4 lam^2 / (N+3)
 };
 
-__device__ __forceinline__ SlopeConst slope_const(const double w[5], const KinConst& kc) {
+// h = 1 / (2 lam) (Maxw::h)
+__device__ __forceinline__ SlopeConst slope_const(const double w[5], const KinConst& kc, double h) {
   SlopeConst s;
   s.U = w[1]; s.V = w[2]; s.W = w[3]; s.lam = w[4];
   s.ir = 1.0 / w[0];
-  s.k2 = s.U * s.U + s.V * s.V + s.W * s.W + 0.5 * kc.n3 / s.lam;
-  s.c4 = 4.0 * s.lam * s.lam / kc.n3;
+  s.k2 = s.U * s.U + s.V * s.V + s.W * s.W + kc.n3 * h;
+  s.c4 = kc.c4n * s.lam * s.lam;
   return s;
+}
+
+__device__ __forceinline__ SlopeConst slope_const(const double w[5], const KinConst& kc) {
+  return slope_const(w, kc, 0.5 / w[4]);
 }
 
 // kinetic.py:271-302 closed-form solve of <a psi> = dq / rho.
@@ -322,7 +334,7 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
     double A[5];
     Maxw m;
     maxw_full(m, w, kc);
-    const SlopeConst sc = slope_const(w, kc);
+    const SlopeConst sc = slope_const(w, kc, m.h);
 #pragma unroll
     for (int k = 0; k < 3; ++k) micro_slope(sc, a[k], a[k]);  // slopes -> micro-slopes in place
     {
@@ -392,7 +404,7 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
   double ab[3][5], Ab[5];
   Maxw m0;
   maxw_full(m0, w0, kc);
-  const SlopeConst sc0 = slope_const(w0, kc);
+  const SlopeConst sc0 = slope_const(w0, kc, m0.h);
 #pragma unroll
   for (int k = 0; k < 3; ++k) micro_slope(sc0, dqa[k], ab[k]);
   {
