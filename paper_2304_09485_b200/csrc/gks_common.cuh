@@ -8,11 +8,12 @@
 
 #include "../../include/gks.h"
 
-// Minimum resident 128-thread CTAs per SM (register budgets) for the FP64
-// flux kernels, chosen by measurement (profiles/r01): the face kernel runs
-// best at 128 regs/thread (4 CTAs), the batch kernel at 168 (3 CTAs).
+// Minimum resident CTAs per SM (register budgets), chosen by measurement
+// (profiles/r01): the 128-thread FP64 flux kernels run best at 168
+// regs/thread (3 CTAs; 4 CTAs / 128 regs was 5 % slower after the division
+// cuts), the 160-thread reconstruction kernels at 96 (4 CTAs).
 #ifndef GKS_FACE_MINB
-#define GKS_FACE_MINB 4
+#define GKS_FACE_MINB 3
 #endif
 #ifndef GKS_FLUX_MINB
 #define GKS_FLUX_MINB 3
