@@ -535,6 +535,17 @@ def run_ours(args):
         except Exception as exc:
             conv = {"error": str(exc)}
 
+    if roof is not None:
+        # DRAM traffic of the same kernel on the same workload from the
+        # committed ncu --set full capture (profiles/), per launch
+        key = f"{args.workload}_n{args.n}"
+        for tf in sorted(ROOT.glob("profiles/*/ncu_traffic.json"), reverse=True):
+            ent = json.loads(tf.read_text()).get(key, {}).get(roof["kernel"])
+            if ent:
+                roof["traffic"] = ent["dram_bytes_per_launch"]
+                roof["traffic_source"] = f"{tf.relative_to(ROOT)} ({ent['kernel']})"
+                break
+
     cb = None
     if not args.no_cpu_baseline:
         try:
