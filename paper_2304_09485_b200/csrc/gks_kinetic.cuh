@@ -99,10 +99,14 @@ __device__ __forceinline__ void group_acc(const Maxw& m, const double (&k)[NA], 
   o[4] += 0.5 * (s2 * vwx + s0 * (m.X[S] * (m.V[B + 2] * m.W[C] + m.V[B] * m.W[C + 2]) + vw * m.X[S + 1]));
 }
 
-// <u^P W(c) psi> with W(c) = s.psi(c) + DIR * sum_k c_k d_k.psi(c).
-// The 23 weight monomials (8 without DIR) fall into 13 (6) groups.
+// <u^P W(c) psi> with W(c) = s.psi(c) + DIR * ds * sum_k c_k d_k.psi(c).
+// The 23 weight monomials (8 without DIR) fall into 13 (6) groups.  The
+// directional coefficients come scaled by ds on the fly (the flux passes'
+// time-coefficient factor) instead of as a materialised scaled copy: 15
+// fewer live doubles across the side loop.
 template <int P, bool DIR>
-__device__ __forceinline__ void wmom(const Maxw& m, const double s[5], const double (*d)[5], double o[5]) {
+__device__ __forceinline__ void wmom(const Maxw& m, const double s[5], const double (*d)[5], double ds,
+                                     double o[5]) {
   o[0] = o[1] = o[2] = o[3] = o[4] = 0.0;
   const double hs = 0.5 * s[4];
   if (!DIR) {
@@ -114,20 +118,20 @@ __device__ __forceinline__ void wmom(const Maxw& m, const double s[5], const dou
     group_acc<P, 0, 0, 1, 1>(m, {hs}, o);              // xi^2
     return;
   }
-  const double hu = 0.5 * d[0][4], hv = 0.5 * d[1][4], hw = 0.5 * d[2][4];
-  group_acc<P, 0, 0, 0, 4>(m, {s[0], s[1] + d[0][0], hs + d[0][1], hu}, o);  // 1, u, u^2, u^3
-  group_acc<P, 1, 0, 0, 3>(m, {s[2] + d[1][0], d[0][2] + d[1][1], hv}, o);   // v, uv, u^2 v
-  group_acc<P, 0, 1, 0, 3>(m, {s[3] + d[2][0], d[0][3] + d[2][1], hw}, o);   // w, uw, u^2 w
-  group_acc<P, 2, 0, 0, 2>(m, {hs + d[1][2], hu}, o);                       // v^2, u v^2
-  group_acc<P, 0, 2, 0, 2>(m, {hs + d[2][3], hu}, o);                       // w^2, u w^2
-  group_acc<P, 0, 0, 1, 2>(m, {hs, hu}, o);                                 // xi^2, u xi^2
-  group_acc<P, 1, 1, 0, 1>(m, {d[1][3] + d[2][2]}, o);                      // vw
-  group_acc<P, 3, 0, 0, 1>(m, {hv}, o);                                     // v^3
-  group_acc<P, 0, 3, 0, 1>(m, {hw}, o);                                     // w^3
-  group_acc<P, 1, 2, 0, 1>(m, {hv}, o);                                     // v w^2
-  group_acc<P, 2, 1, 0, 1>(m, {hw}, o);                                     // v^2 w
-  group_acc<P, 1, 0, 1, 1>(m, {hv}, o);                                     // v xi^2
-  group_acc<P, 0, 1, 1, 1>(m, {hw}, o);                                     // w xi^2
+  const double hu = 0.5 * ds * d[0][4], hv = 0.5 * ds * d[1][4], hw = 0.5 * ds * d[2][4];
+  group_acc<P, 0, 0, 0, 4>(m, {s[0], s[1] + ds * d[0][0], hs + ds * d[0][1], hu}, o);         // 1, u, u^2, u^3
+  group_acc<P, 1, 0, 0, 3>(m, {s[2] + ds * d[1][0], ds * (d[0][2] + d[1][1]), hv}, o);       // v, uv, u^2 v
+  group_acc<P, 0, 1, 0, 3>(m, {s[3] + ds * d[2][0], ds * (d[0][3] + d[2][1]), hw}, o);       // w, uw, u^2 w
+  group_acc<P, 2, 0, 0, 2>(m, {hs + ds * d[1][2], hu}, o);                                   // v^2, u v^2
+  group_acc<P, 0, 2, 0, 2>(m, {hs + ds * d[2][3], hu}, o);                                   // w^2, u w^2
+  group_acc<P, 0, 0, 1, 2>(m, {hs, hu}, o);                                                  // xi^2, u xi^2
+  group_acc<P, 1, 1, 0, 1>(m, {ds * (d[1][3] + d[2][2])}, o);                                // vw
+  group_acc<P, 3, 0, 0, 1>(m, {hv}, o);                                                      // v^3
+  group_acc<P, 0, 3, 0, 1>(m, {hw}, o);                                                      // w^3
+  group_acc<P, 1, 2, 0, 1>(m, {hv}, o);                                                      // v w^2
+  group_acc<P, 2, 1, 0, 1>(m, {hw}, o);                                                      // v^2 w
+  group_acc<P, 1, 0, 1, 1>(m, {hv}, o);                                                      // v xi^2
+  group_acc<P, 0, 1, 1, 1>(m, {hw}, o);                                                      // w xi^2
 }
 
 // Gram matrix G_ij = <u^P psi_i psi_j> of one Maxwellian.  Every weight
@@ -160,6 +164,47 @@ __device__ __forceinline__ void gram(const Maxw& m, double G[5][5]) {
   for (int i = 1; i < 5; ++i)
 #pragma unroll
     for (int j = 0; j < i; ++j) G[i][j] = G[j][i];
+}
+
+// For the NS vectors s_k: acc_k += scale * G s_k and q0 += scale * G e_0
+// (the first column), with G = <u^P psi psi^T> formed one unique entry at a
+// time and scattered into both of its symmetric positions at once: no
+// 25-entry matrix is ever live (ncu r01: the materialised G was the face
+// kernel's largest spill site).  Same products as gram + gram_acc, summed in
+// a different order.
+template <int P, int NS>
+__device__ __forceinline__ void gram_scatter(const Maxw& m, double scale, const double* const (&sv)[NS],
+                                             double* const (&av)[NS], double q0[5]) {
+  const double* U = m.U + P;
+  const double* V = m.V;
+  const double* W = m.W;
+  const double x1 = m.X[1];
+  const double r = V[2] + W[2] + x1;  // <v^2 + w^2 + xi^2>
+  auto put = [&](int i, int j, double g) {
+    g *= scale;
+    if (j == 0) q0[i] += g;
+    else if (i == 0) q0[j] += g;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      av[k][i] += g * sv[k][j];
+      if (i != j) av[k][j] += g * sv[k][i];
+    }
+  };
+  put(0, 0, U[0]);
+  put(0, 1, U[1]);
+  put(0, 2, U[0] * V[1]);
+  put(0, 3, U[0] * W[1]);
+  put(0, 4, 0.5 * (U[2] + U[0] * r));
+  put(1, 1, U[2]);
+  put(1, 2, U[1] * V[1]);
+  put(1, 3, U[1] * W[1]);
+  put(1, 4, 0.5 * (U[3] + U[1] * r));
+  put(2, 2, U[0] * V[2]);
+  put(2, 3, U[0] * V[1] * W[1]);
+  put(2, 4, 0.5 * (U[2] * V[1] + U[0] * (V[3] + V[1] * (W[2] + x1))));
+  put(3, 3, U[0] * W[2]);
+  put(3, 4, 0.5 * (U[2] * W[1] + U[0] * (W[3] + W[1] * (V[2] + x1))));
+  put(4, 4, 0.25 * (U[4] + 2.0 * U[2] * r + U[0] * (V[4] + W[4] + m.X[2] + 2.0 * (V[2] * W[2] + (V[2] + W[2]) * x1))));
 }
 
 // acc += scale * G s
@@ -341,42 +386,34 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
       // time slope from the compatibility condition (kinetic.py:305-312)
       const double zero5[5] = {0, 0, 0, 0, 0};
       double D[5];
-      wmom<0, true>(m, zero5, a, D);
+      wmom<0, true>(m, zero5, a, 1.0, D);
 #pragma unroll
       for (int i = 0; i < 5; ++i) D[i] = -rho * D[i];
       micro_slope(sc, D, A);
     }
     maxw_half_u(m, w, side ? -1.0 : 1.0);
     double t[5];
-    {
-      double G[5][5];
-      gram<0>(m, G);
-#pragma unroll
-      for (int i = 0; i < 5; ++i) q0[i] += rho * G[i][0];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) gram_acc(G, a[k], rho, dqa[k]);
-      if (VISCOUS && POINT) gram_acc(G, A, rho, P6);
+    if (VISCOUS && POINT) {
+      const double* const sv[4] = {a[0], a[1], a[2], A};
+      double* const av[4] = {dqa[0], dqa[1], dqa[2], P6};
+      gram_scatter<0, 4>(m, rho, sv, av, q0);
+    } else {
+      const double* const sv[3] = {a[0], a[1], a[2]};
+      double* const av[3] = {dqa[0], dqa[1], dqa[2]};
+      gram_scatter<0, 3>(m, rho, sv, av, q0);
     }
     if (tau_known && !VISCOUS) {
-      double sw[5], dw[3][5];
+      double sw[5];
 #pragma unroll
       for (int i = 0; i < 5; ++i) sw[i] = tc.c6 * A[i];
       sw[0] += tc.c4;
-#pragma unroll
-      for (int k = 0; k < 3; ++k)
-#pragma unroll
-        for (int i = 0; i < 5; ++i) dw[k][i] = tc.c5 * a[k][i];
-      wmom<1, true>(m, sw, dw, t);
+      wmom<1, true>(m, sw, a, tc.c5, t);
 #pragma unroll
       for (int i = 0; i < 5; ++i) F[i] += rho * t[i];
       if (POINT) {
 #pragma unroll
         for (int i = 0; i < 5; ++i) sw[i] = tc.f3 * A[i];
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-#pragma unroll
-          for (int i = 0; i < 5; ++i) dw[k][i] = tc.f2 * a[k][i];
-        wmom<0, true>(m, sw, dw, t);
+        wmom<0, true>(m, sw, a, tc.f2, t);
 #pragma unroll
         for (int i = 0; i < 5; ++i) P[i] += rho * t[i];
       }
@@ -389,11 +426,11 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
         for (int i = 0; i < 5; ++i) F[i] += rho * Gu[i][0];
         gram_acc(Gu, A, rho, F6);
       }
-      wmom<1, true>(m, zero5, a, t);
+      wmom<1, true>(m, zero5, a, 1.0, t);
 #pragma unroll
       for (int i = 0; i < 5; ++i) F5[i] += rho * t[i];
       if (POINT) {
-        wmom<0, true>(m, zero5, a, t);
+        wmom<0, true>(m, zero5, a, 1.0, t);
 #pragma unroll
         for (int i = 0; i < 5; ++i) P[i] += rho * t[i];
       }
@@ -410,7 +447,7 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
   {
     const double zero5[5] = {0, 0, 0, 0, 0};
     double D[5];
-    wmom<0, true>(m0, zero5, ab, D);
+    wmom<0, true>(m0, zero5, ab, 1.0, D);
 #pragma unroll
     for (int i = 0; i < 5; ++i) D[i] = -w0[0] * D[i];
     micro_slope(sc0, D, Ab);
@@ -425,15 +462,11 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
     }
   }
   {
-    double s[5], d[3][5], o[5];
+    double s[5], o[5];
 #pragma unroll
     for (int i = 0; i < 5; ++i) s[i] = tc.c3 * Ab[i];
     s[0] += tc.c1;
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-#pragma unroll
-      for (int i = 0; i < 5; ++i) d[k][i] = tc.c2 * ab[k][i];
-    wmom<1, true>(m0, s, d, o);
+    wmom<1, true>(m0, s, ab, tc.c2, o);
 #pragma unroll
     for (int i = 0; i < 5; ++i) flux[i] = w0[0] * o[i] + F[i];
   }
@@ -441,15 +474,11 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
 #pragma unroll
     for (int i = 0; i < 5; ++i) point[i] = tc.f1 * q0[i] + P[i];
     if (tc.g1 != 0.0 || tc.g2 != 0.0 || tc.g3 != 0.0) {
-      double s[5], d[3][5], o[5];
+      double s[5], o[5];
 #pragma unroll
       for (int i = 0; i < 5; ++i) s[i] = tc.g3 * Ab[i];
       s[0] += tc.g1;
-#pragma unroll
-      for (int k = 0; k < 3; ++k)
-#pragma unroll
-        for (int i = 0; i < 5; ++i) d[k][i] = tc.g2 * ab[k][i];
-      wmom<0, true>(m0, s, d, o);
+      wmom<0, true>(m0, s, ab, tc.g2, o);
 #pragma unroll
       for (int i = 0; i < 5; ++i) point[i] += w0[0] * o[i];
     }
