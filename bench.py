@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--scheme", default=None, choices=("weno_gmres", "hweno_gmres"))
     p.add_argument("--jacobian", default=None, choices=("roe", "frechet"))
     p.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of decomposition")
+    p.add_argument("--reorder", default="none", choices=("none", "rcm", "morton"),
+                   help="device-side locality renumbering of the mesh (reorder.py)")
     p.add_argument("--cpu-n", type=int, default=None, help="bounded CPU sample size (c1 box divisions / c2 cube-face cells)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-converge", action="store_true", help="skip the wall-time-to-1e-10 leg")
@@ -403,7 +405,8 @@ def run_ours(args):
     mesh, patches, q0, g0, workload, extra = build_workload(args, compact)
     t_mesh = time.perf_counter() - t0
     t0 = time.perf_counter()
-    opts = SolverOptions(scheme=args.scheme, patches=patches, jacobian=args.jacobian, device=local, **extra)
+    opts = SolverOptions(scheme=args.scheme, patches=patches, jacobian=args.jacobian, device=local,
+                         reorder=args.reorder, **extra)
     decomp = world > 1 and not args.replicas
     if decomp:
         from paper_2304_09485_b200.distributed import DistributedSolver
@@ -559,7 +562,7 @@ def run_ours(args):
         "scaling": "strong" if decomp else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload,
                    "cells": nc, "faces": sizes["nf"], "face_points": sizes["nfq"], "scheme": args.scheme,
-                   "jacobian": args.jacobian, "gmres": "m=10, restarts=3, jacobi_sweeps=2, rtol=0",
+                   "jacobian": args.jacobian, "reorder": args.reorder, "gmres": "m=10, restarts=3, jacobi_sweeps=2, rtol=0",
                    "residual_evals_per_step": evals / args.steps,
                    "parallelism": ("replicas" if not decomp else f"cell-partitioned RCB x{world}, NCCL halo + allreduce")
                    if world > 1 else "single",

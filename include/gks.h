@@ -88,6 +88,12 @@ typedef struct GksMeshDesc {
   const int64_t* fq_face;           /* (nfq) */
   const double* fq_point;           /* (nfq,3) */
   const double* fq_weight;          /* (nfq) */
+  /* optional (NULL = identity): reference index of each face / face point
+     of a renumbered mesh (SolverOptions.reorder, reorder.py); the handle
+     sums every per-cell list in this order so results keep the
+     reference's summation order */
+  const int64_t* face_rank;         /* (nf) */
+  const int64_t* fq_rank;           /* (nfq) */
 } GksMeshDesc;
 
 /* ------------------------------------------------------------------ */

@@ -46,7 +46,8 @@ class GksMeshDesc(C.Structure):
                 ("face_owner", C.c_void_p), ("face_neighbor", C.c_void_p), ("face_patch", C.c_void_p),
                 ("face_area", C.c_void_p), ("face_normal", C.c_void_p), ("face_frame", C.c_void_p),
                 ("face_shift", C.c_void_p), ("face_fq_start", C.c_void_p), ("fq_face", C.c_void_p),
-                ("fq_point", C.c_void_p), ("fq_weight", C.c_void_p)]
+                ("fq_point", C.c_void_p), ("fq_weight", C.c_void_p), ("face_rank", C.c_void_p),
+                ("fq_rank", C.c_void_p)]
 
 
 _DESC_FIELDS = {
@@ -71,6 +72,12 @@ def mesh_desc(mesh):
         arr = np.ascontiguousarray(getattr(mesh, name), dtype=dt)
         keep[name] = arr
         setattr(desc, name, arr.ctypes.data)
+    for name in ("face_rank", "fq_rank"):  # renumbered meshes only (reorder.py)
+        val = getattr(mesh, name, None)
+        if val is not None:
+            arr = np.ascontiguousarray(val, dtype=np.int64)
+            keep[name] = arr
+            setattr(desc, name, arr.ctypes.data)
     return desc, keep
 
 

@@ -274,9 +274,24 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   }
   TRY(upload(H, &H->fq_point, m->fq_point, nfq * 3));
 
+  // visiting orders: the reference's face / face-point order (identity
+  // unless the mesh was renumbered, reorder.py)
+  std::vector<int64_t> forder(nf), qorder(nfq);
+  if (m->face_rank) {
+    for (int64_t f = 0; f < nf; ++f) forder[m->face_rank[f]] = f;
+  } else {
+    std::iota(forder.begin(), forder.end(), 0);
+  }
+  if (m->fq_rank) {
+    for (int64_t i = 0; i < nfq; ++i) qorder[m->fq_rank[i]] = i;
+  } else {
+    std::iota(qorder.begin(), qorder.end(), 0);
+  }
+
   // CSR lists (counting sorts keep ascending order inside each group)
   {
-    // assembly: owner fq entries, then neighbour fq entries (stepping.py:225-228)
+    // assembly: owner fq entries, then neighbour fq entries (stepping.py:225-228),
+    // visited in the reference's face-point order
     std::vector<int> cnt(nc + 1, 0);
     for (int64_t i = 0; i < nfq; ++i) {
       const int64_t f = m->fq_face[i];
@@ -285,8 +300,12 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
     }
     std::partial_sum(cnt.begin(), cnt.end(), cnt.begin());
     std::vector<int> pos(cnt.begin(), cnt.end() - 1), list(cnt[nc]);
-    for (int64_t i = 0; i < nfq; ++i) list[pos[m->face_owner[m->fq_face[i]]]++] = (int)(i << 1);
-    for (int64_t i = 0; i < nfq; ++i) {
+    for (int64_t k = 0; k < nfq; ++k) {
+      const int64_t i = qorder[k];
+      list[pos[m->face_owner[m->fq_face[i]]]++] = (int)(i << 1);
+    }
+    for (int64_t k = 0; k < nfq; ++k) {
+      const int64_t i = qorder[k];
       const int64_t nb = m->face_neighbor[m->fq_face[i]];
       if (nb >= 0) list[pos[nb]++] = (int)((i << 1) | 1);
     }
@@ -302,26 +321,39 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
     }
     std::partial_sum(cnt.begin(), cnt.end(), cnt.begin());
     std::vector<int> pos(cnt.begin(), cnt.end() - 1), list(cnt[nc]);
-    for (int64_t f = 0; f < nf; ++f) list[pos[m->face_owner[f]]++] = (int)(f << 1);
-    for (int64_t f = 0; f < nf; ++f)
+    for (int64_t k = 0; k < nf; ++k) {
+      const int64_t f = forder[k];
+      list[pos[m->face_owner[f]]++] = (int)(f << 1);
+    }
+    for (int64_t k = 0; k < nf; ++k) {
+      const int64_t f = forder[k];
       if (m->face_neighbor[f] >= 0) list[pos[m->face_neighbor[f]]++] = (int)((f << 1) | 1);
+    }
     TRY(upload(H, &H->cdt_start, cnt.data(), nc + 1));
     TRY(upload(H, &H->cdt, list.data(), list.size()));
     // Jacobian diagonal: interior own, interior nbr, boundary own (jacobian.py:582-610)
     std::vector<int> pos2(cnt.begin(), cnt.end() - 1), list2(cnt[nc]);
-    for (int64_t f = 0; f < nf; ++f)
+    for (int64_t k = 0; k < nf; ++k) {
+      const int64_t f = forder[k];
       if (m->face_neighbor[f] >= 0) list2[pos2[m->face_owner[f]]++] = (int)(f << 1);
-    for (int64_t f = 0; f < nf; ++f)
+    }
+    for (int64_t k = 0; k < nf; ++k) {
+      const int64_t f = forder[k];
       if (m->face_neighbor[f] >= 0) list2[pos2[m->face_neighbor[f]]++] = (int)((f << 1) | 1);
-    for (int64_t f = 0; f < nf; ++f)
+    }
+    for (int64_t k = 0; k < nf; ++k) {
+      const int64_t f = forder[k];
       if (m->face_neighbor[f] < 0) list2[pos2[m->face_owner[f]]++] = (int)(f << 1);
+    }
     TRY(upload(H, &H->cjd_start, cnt.data(), nc + 1));
     TRY(upload(H, &H->cjd, list2.data(), list2.size()));
   }
   {
     // interior / boundary face lists, Jacobian CSR (lexsort by (row, col), stable)
+    // boundary faces in the reference's face order (ghost rows, stepping.py:242-249)
     std::vector<int> ifaces, bfaces, bidx(nf, -1);
-    for (int64_t f = 0; f < nf; ++f) {
+    for (int64_t k = 0; k < nf; ++k) {
+      const int64_t f = forder[k];
       if (m->face_neighbor[f] >= 0) ifaces.push_back((int)f);
       else { bidx[f] = (int)bfaces.size(); bfaces.push_back((int)f); }
     }

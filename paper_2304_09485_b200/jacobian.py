@@ -161,7 +161,9 @@ def assemble_jacobian(mesh, q, dt_cells, gamma: float = DEFAULT_GAMMA, boundary_
     """
     from .stepping import _jacobian_handle
 
-    h = solver if solver is not None else _jacobian_handle(mesh, gamma)
+    if solver is not None:
+        return solver.assemble_jacobian(q, dt_cells, boundary_ghosts)
+    h = _jacobian_handle(mesh, gamma)
     nc = mesh.ncells
     q = N.f64(q, (nc, 5))
     dt = N.f64(np.broadcast_to(np.asarray(dt_cells, dtype=float), (nc,)))

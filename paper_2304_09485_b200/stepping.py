@@ -76,6 +76,7 @@ class SolverOptions:
     # B200 build additions (reference-equal defaults)
     jacobian: str = "roe"
     device: int = 0
+    reorder: str = "none"  # device-side locality renumbering: "none" | "rcm" | "morton" (reorder.py)
 
     def __post_init__(self):
         if self.scheme not in SCHEMES:
@@ -88,6 +89,10 @@ class SolverOptions:
             raise ValueError(f"weights must be 'nonlinear' or 'linear', got {self.weights!r}")
         if self.jacobian not in JACOBIANS:
             raise ValueError(f"jacobian must be one of {JACOBIANS}")
+        from .reorder import METHODS
+
+        if self.reorder not in METHODS:
+            raise ValueError(f"reorder must be one of {METHODS}, got {self.reorder!r}")
 
 
 def _options_struct(opt: SolverOptions, mesh: Mesh):
@@ -149,14 +154,26 @@ class Solver:
         self.bfaces = np.flatnonzero(mesh.face_neighbor < 0)
         self.bface_patch = [mesh.patch_names[p] for p in mesh.face_patch[self.bfaces]]
 
-        # native setup (stencils + operators) and the device handle
+        # native setup (stencils + operators, always on the reference's
+        # numbering) and the device handle (optionally renumbered, reorder.py)
         self._setup = N.NativeSetup(mesh, schemes=2 if self.compact else 1)
-        self._desc, self._keep = N.mesh_desc(mesh)
         self._opts, self._patch_arr = _options_struct(options, mesh)
-        h = C.c_void_p()
         lib = N.load()
-        rc = lib.gks_create(C.byref(self._desc), self._setup.handle, C.byref(self._opts), int(self.device),
-                            C.byref(h))
+        self._perm = self._sub = None
+        setup = self._setup.handle
+        dev_mesh = mesh
+        if options.reorder != "none":
+            from .reorder import PermutedMesh, cell_order
+
+            dev_mesh = PermutedMesh(mesh, cell_order(mesh, options.reorder))
+            self._perm = dev_mesh.perm
+            sub = C.c_void_p()
+            N.check(lib.gks_setup_subset(setup, N.iptr(dev_mesh.perm), mesh.ncells, N.iptr(dev_mesh.inv),
+                                         mesh.ncells, C.byref(sub)))
+            self._sub = setup = sub
+        self._desc, self._keep = N.mesh_desc(dev_mesh)
+        h = C.c_void_p()
+        rc = lib.gks_create(C.byref(self._desc), setup, C.byref(self._opts), int(self.device), C.byref(h))
         if rc:
             msg = lib.gks_last_error().decode(errors="replace")
             if "patch" in msg:
@@ -170,6 +187,23 @@ class Solver:
         if h is not None and h.value and N._lib is not None:
             N._lib.gks_destroy(h)
             self._handle = None
+        sub = getattr(self, "_sub", None)
+        if sub is not None and sub.value and N._lib is not None:
+            N._lib.gks_setup_free(sub)
+            self._sub = None
+
+    # reference numbering <-> device numbering (identity unless reordered)
+    def _dev(self, a):
+        if a is None or self._perm is None:
+            return a
+        return np.ascontiguousarray(a[self._perm])
+
+    def _host(self, a):
+        if a is None or self._perm is None:
+            return a
+        out = np.empty_like(a)
+        out[self._perm] = a
+        return out
 
     @property
     def stencils(self):
@@ -181,12 +215,12 @@ class Solver:
     # -- helpers ----------------------------------------------------------------
 
     def _q(self, fld):
-        return N.f64(fld.q, (self.mesh.ncells, 5))
+        return self._dev(N.f64(fld.q, (self.mesh.ncells, 5)))
 
     def _grad(self, fld):
         if fld.grad is None:
             return None
-        return N.f64(fld.grad, (self.mesh.ncells, 3, 5))
+        return self._dev(N.f64(fld.grad, (self.mesh.ncells, 3, 5)))
 
     def _raise(self, rc, where):
         lib = N.load()
@@ -211,7 +245,7 @@ class Solver:
         rc = N.load().gks_local_dt(self._handle, N.dptr(q), N.dptr(dt))
         if rc:
             self._raise(rc, "dt")
-        return dt
+        return self._host(dt)
 
     # -- residual -------------------------------------------------------------------
 
@@ -224,14 +258,14 @@ class Solver:
         nc = self.mesh.ncells
         q = self._q(fld)
         grad = self._grad(fld)
-        dt = N.f64(np.broadcast_to(np.asarray(dt_cells, dtype=float), (nc,)))
+        dt = self._dev(N.f64(np.broadcast_to(np.asarray(dt_cells, dtype=float), (nc,))))
         res = np.empty((nc, 5))
         gout = np.empty((nc, 3, 5)) if with_gradients else None
         rc = N.load().gks_residual(self._handle, N.dptr(q), N.dptr(grad), N.dptr(dt), int(bool(with_gradients)),
                                    N.dptr(res), N.dptr(gout))
         if rc:
             self._raise(rc, "residual")
-        return res, gout
+        return self._host(res), self._host(gout)
 
     # -- implicit step ----------------------------------------------------------------
 
@@ -254,13 +288,25 @@ class Solver:
     def assemble_jacobian(self, q, dt, ghosts=None) -> BlockJacobian:
         """Roe Jacobian on this solver's device handle (a view; next assembly overwrites it)."""
         lib = N.load()
-        q = N.f64(q, (self.mesh.ncells, 5))
-        dt = N.f64(np.broadcast_to(np.asarray(dt, dtype=float), (self.mesh.ncells,)))
-        g = None if ghosts is None else N.f64(ghosts, (-1, 5))
+        q = self._dev(N.f64(q, (self.mesh.ncells, 5)))
+        dt = self._dev(N.f64(np.broadcast_to(np.asarray(dt, dtype=float), (self.mesh.ncells,))))
+        g = None if ghosts is None else N.f64(ghosts, (-1, 5))  # boundary faces: reference order on the device too
         rc = lib.gks_assemble_jacobian(self._handle, N.dptr(q), N.dptr(dt), N.dptr(g))
         if rc:
             self._raise(rc, "jac")
-        return BlockJacobian(_handle=lib.gks_jacobian(self._handle), _owner=self)
+        view = BlockJacobian(_handle=lib.gks_jacobian(self._handle), _owner=self)
+        if self._perm is None:
+            return view
+        # renumbered handle: hand back the matrix in the reference's numbering
+        # and CSR order (rows, then columns ascending; jacobian.py:181-196)
+        ex = view._export()
+        rows = self._perm[ex["off_row"]]
+        cols = self._perm[ex["off_col"]]
+        order = np.lexsort((cols, rows))
+        nc = self.mesh.ncells
+        rowptr = np.concatenate([[0], np.cumsum(np.bincount(rows, minlength=nc))]).astype(np.int64)
+        return BlockJacobian(self._host(ex["diag"]), ex["off"][order], cols[order], rows[order], rowptr,
+                             device=self.device)
 
     @staticmethod
     def _invalid_cells(q, gamma):
@@ -284,7 +330,7 @@ class Solver:
             rc = N.load().gks_advance(self._handle, N.dptr(q), N.dptr(grad), C.byref(info))
             if rc:
                 self._raise(rc, "advance")
-            return SolutionField(q, grad if self.compact else None), _info(info)
+            return SolutionField(self._host(q), self._host(grad) if self.compact else None), _info(info)
         # composed path (reference structure, stepping.py:270-296) with device calls
         dt = self.local_time_step(fld)
         retried = False
@@ -317,6 +363,16 @@ class Solver:
         if self.compact and (fld.grad is None or not fld.grad.flags.c_contiguous):
             raise SteppingError("compact scheme needs a C-contiguous gradient field")
         info = N.GksStepInfo()
+        if self._perm is not None:
+            # renumbered handle: permuted copies in and out
+            q, g = self._q(fld), self._grad(fld) if self.compact else None
+            rc = N.load().gks_advance(self._handle, N.dptr(q), N.dptr(g), C.byref(info))
+            if rc:
+                self._raise(rc, "advance")
+            fld.q[...] = self._host(q)
+            if self.compact:
+                fld.grad[...] = self._host(g)
+            return _info(info)
         rc = N.load().gks_advance(self._handle, N.dptr(fld.q), N.dptr(fld.grad) if self.compact else None,
                                   C.byref(info))
         if rc:
@@ -341,14 +397,14 @@ class Solver:
             return np.zeros_like(v)
         q = self._q(fld)
         grad = self._grad(fld)
-        dt = N.f64(np.broadcast_to(np.asarray(dt_cells, dtype=float), (nc,)))
-        vv = N.f64(v, (nc, 5))
+        dt = self._dev(N.f64(np.broadcast_to(np.asarray(dt_cells, dtype=float), (nc,))))
+        vv = self._dev(N.f64(v, (nc, 5)))
         out = np.empty((nc, 5))
         rc = N.load().gks_frechet_matvec(self._handle, N.dptr(q), N.dptr(grad), N.dptr(dt), N.dptr(vv),
                                          -1.0 if sigma is None else float(sigma), N.dptr(out))
         if rc:
             self._raise(rc, "residual")
-        return out
+        return self._host(out)
 
     # -- device-resident loop (benchmark / driver) ------------------------------------
 
@@ -360,7 +416,7 @@ class Solver:
         q = np.empty((nc, 5))
         g = np.empty((nc, 3, 5)) if self.compact else None
         N.check(N.load().gks_state_download(self._handle, N.dptr(q), N.dptr(g)))
-        return SolutionField(q, g)
+        return SolutionField(self._host(q), self._host(g))
 
     def advance_resident(self) -> StepInfo:
         info = N.GksStepInfo()
