@@ -63,12 +63,12 @@ def parse():
     a = p.parse_args()
     # configs[1]: inviscid subsonic sphere, non-compact HGKS + matrix-free GMRES
     defaults = {"c1": (64, "weno_gmres", "roe"), "c2": (16, "weno_gmres", "frechet"),
-                "c3": (16, "hweno_gmres", "roe"), "c4": (96, "hweno_gmres", "roe"),
+                "c3": (16, "hweno_gmres", "roe"), "c4": (48, "hweno_gmres", "roe"),
                 "c5": (30, "hweno_gmres", "roe")}[a.workload]
     a.n = a.n or defaults[0]
     a.scheme = a.scheme or defaults[1]
     a.jacobian = a.jacobian or defaults[2]
-    a.cpu_n = a.cpu_n or {"c1": 10, "c2": 2, "c3": 2, "c4": 24, "c5": 2}[a.workload]
+    a.cpu_n = a.cpu_n or {"c1": 10, "c2": 2, "c3": 2, "c4": 12, "c5": 2}[a.workload]
     return a
 
 
@@ -110,8 +110,11 @@ def other_problem(workload, mesh, compact):
         extra = dict(model="viscous", mu=0.0021483050847457627, weights="linear")
     elif workload == "c4":  # cases/m6wing_transonic.ini (Ma 0.8395, AoA 3.06 deg)
         ref = np.array([1.0, 0.8383030214661579, 0.04482495105787847, 0.0, 1.0 / GAMMA])
+        # swept wing between two symmetry planes (slip walls at root and tip)
         patches = {"wing": PatchSpec("wing", "wall_slip_adiabatic"),
-                   "farfield": PatchSpec("farfield", "farfield_riemann", reference=ref)}
+                   "farfield": PatchSpec("farfield", "farfield_riemann", reference=ref),
+                   "root": PatchSpec("root", "wall_slip_adiabatic"),
+                   "tip": PatchSpec("tip", "wall_slip_adiabatic")}
         extra = {}
     else:
         # c5 scale case.  cases/sphere_ma3_inviscid.ini asks for Ma 3, but the
@@ -141,8 +144,9 @@ def build_workload(args, compact):
                                      f"20D), inviscid Ma {MA_C2}, slip wall + Riemann farfield, impulsive start "
                                      f"(configs[1])"), {}
     if args.workload == "c4":
-        mesh = MG.generate_wing_mesh(args.n)
-        label = f"C4 synthetic swept-wing stand-in (lattice {args.n}^3), Ma 0.8395 AoA 3.06, slip wall (configs[3])"
+        mesh = MG.generate_swept_wing_mesh(args.n)
+        label = (f"C4 synthetic body-fitted swept tapered wing between symmetry planes (O-grid n={args.n}), "
+                 f"Ma 0.8395 AoA 3.06, slip walls (configs[3]; ONERA M6 geometry unavailable offline)")
     else:
         mesh = MG.generate_sphere_mesh(args.n)
         label = ("C3 synthetic tet sphere, viscous Re=118 Ma 0.2535, no-slip wall (configs[2])" if args.workload == "c3"

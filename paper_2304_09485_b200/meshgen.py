@@ -10,8 +10,11 @@ generators build the labelled synthetic stand-ins used by configs 2-5:
   cube-face blocks whatever their orientation).
 * generate_carved_sphere_mesh -- older stair-step stand-in: Kuhn tets on a
   stretched lattice with the sphere carved out (kept for tests).
-* generate_wing_mesh -- a swept, tapered, symmetric-section wing carved the
-  same way (the ONERA M6 geometry is not available offline).
+* generate_swept_wing_mesh -- body-fitted swept, tapered wing between two
+  span-end planes: O-grid around a NACA 0012 section, hexes split like the
+  sphere's (config 4; the ONERA M6 geometry is not available offline).
+* generate_wing_mesh -- older carved stair-step wing (kept for tests; its
+  sharp corners make the transonic impulsive start fail).
 
 Cells come out in lattice order (good locality for the device gathers).
 Patch names follow the reference case files: "sphere"/"wing" for the body,
@@ -144,6 +147,51 @@ def _dedup_points(p, scale):
 _HEX_QUADS = np.array(((0, 3, 2, 1), (4, 5, 6, 7), (0, 1, 5, 4), (1, 2, 6, 5), (2, 3, 7, 6), (3, 0, 4, 7)))
 
 
+def _split_hex24(corner, scale, on_wall=None, wall_centre=None):
+    """Split hexes (nh, 8, 3; VTK corner order) into 24 tets each, through the
+    face centres and the cell centre: conforming whatever the orientation of
+    neighbouring hexes.  Face-0 centres of the hexes flagged `on_wall` are
+    moved by `wall_centre` (onto the curved body).  Returns (nodes, tets,
+    tri) with tri (nh, 6, 4, 3) the boundary triangles of every hex face."""
+    nh = len(corner)
+    # corners first; face centres then come from the deduplicated corner
+    # nodes, once per unique face (both hexes of an interior face must see
+    # bit-identical centres or the split is non-conforming)
+    cnodes, cinv = _dedup_points(corner.reshape(-1, 3), scale)
+    cid = cinv.reshape(nh, 8)
+    qn_all = cid[:, _HEX_QUADS]                      # (nh, 6, 4)
+    key = np.sort(qn_all.reshape(-1, 4), axis=1)
+    kv = np.ascontiguousarray(key).view(np.dtype((np.void, 32))).ravel()
+    _, first, finv = np.unique(kv, return_index=True, return_inverse=True)
+    order = np.argsort(first)
+    rank = np.empty_like(order)
+    rank[order] = np.arange(len(order))
+    fid_u = rank[finv].reshape(nh, 6)                # unique face id per hex face, first-occurrence order
+    ukey = key[first[order]]
+    fcen = cnodes[ukey].mean(axis=1)                 # (nfu, 3)
+    if on_wall is not None:
+        wf = np.unique(fid_u[on_wall, 0])
+        fcen[wf] = wall_centre(fcen[wf])
+    ccen = cnodes[cid].mean(axis=1)                  # (nh, 3)
+    nodes = np.concatenate([cnodes, fcen, ccen])
+    nc0, nf0 = len(cnodes), len(fcen)
+    fid = nc0 + fid_u
+    zid = nc0 + nf0 + np.arange(nh)
+    # 24 tets: (edge a, edge b, face centre, cell centre) for each quad edge
+    qn = cid[:, _HEX_QUADS]                          # (nh, 6, 4)
+    a = qn
+    b = np.roll(qn, -1, axis=2)
+    fc = np.broadcast_to(fid[:, :, None], a.shape)
+    cc = np.broadcast_to(zid[:, None, None], a.shape)
+    tets = np.stack([a, b, fc, cc], axis=-1).reshape(-1, 4)
+    vol = _tet_volumes(nodes, tets)
+    flip = vol < 0
+    tets[flip] = tets[flip][:, [0, 2, 1, 3]]
+    if np.any(np.abs(vol) <= 0):
+        raise MeshError("degenerate tet in a hex split")
+    return nodes, tets, np.stack([a, b, fc], axis=-1)
+
+
 def generate_sphere_mesh(n, radius=0.5, far=10.0, nr=None, boundary="farfield"):
     """Body-fitted synthetic tet sphere (configs 2, 3, 5): a cubed-sphere shell.
 
@@ -166,33 +214,12 @@ def generate_sphere_mesh(n, radius=0.5, far=10.0, nr=None, boundary="farfield"):
                                                   indexing="ij"))
     corner = np.stack([P[f, i, j, k], P[f, i + 1, j, k], P[f, i + 1, j + 1, k], P[f, i, j + 1, k],
                        P[f, i, j, k + 1], P[f, i + 1, j, k + 1], P[f, i + 1, j + 1, k + 1], P[f, i, j + 1, k + 1]], 1)
-    nh = len(corner)
-    quads = corner[:, _HEX_QUADS]                    # (nh, 6, 4, 3)
-    fcen = quads.mean(axis=2)                        # (nh, 6, 3)
-    # face 0 (nodes 0-3) lies on r_k: on the wall when k == 0; project its centre onto the sphere
-    wall_c = fcen[:, 0] / np.linalg.norm(fcen[:, 0], axis=1)[:, None] * radius
-    fcen[k == 0, 0] = wall_c[k == 0]
-    ccen = corner.mean(axis=1)                       # (nh, 3)
-    scale = far
-    allpts = np.concatenate([corner.reshape(-1, 3), fcen.reshape(-1, 3), ccen])
-    nodes, inv = _dedup_points(allpts, scale)
-    cid = inv[: nh * 8].reshape(nh, 8)
-    fid = inv[nh * 8: nh * 8 + nh * 6].reshape(nh, 6)
-    zid = inv[nh * 8 + nh * 6:]
-    # 24 tets: (edge a, edge b, face centre, cell centre) for each quad edge
-    qn = cid[:, _HEX_QUADS]                          # (nh, 6, 4)
-    a = qn
-    b = np.roll(qn, -1, axis=2)
-    fc = np.broadcast_to(fid[:, :, None], a.shape)
-    cc = np.broadcast_to(zid[:, None, None], a.shape)
-    tets = np.stack([a, b, fc, cc], axis=-1).reshape(-1, 4)
-    vol = _tet_volumes(nodes, tets)
-    flip = vol < 0
-    tets[flip] = tets[flip][:, [0, 2, 1, 3]]
-    if np.any(np.abs(vol) <= 0):
-        raise MeshError("degenerate tet in the sphere shell")
+    # face 0 (nodes 0-3) lies on r_k: on the wall when k == 0; its centre goes onto the sphere
+    def wall_centre(fc0):
+        return fc0 / np.linalg.norm(fc0, axis=1)[:, None] * radius
+
+    nodes, tets, tri = _split_hex24(corner, far, k == 0, wall_centre)
     # boundary triangles: wall = face 0 of k == 0 hexes, far = face 1 of k == nr-1 hexes
-    tri = np.stack([a, b, fc], axis=-1)               # (nh, 6, 4, 3)
     wall = tri[k == 0, 0].reshape(-1, 3)
     outer_tri = tri[k == nr - 1, 1].reshape(-1, 3)
     if boundary == "farfield":
@@ -202,6 +229,59 @@ def generate_sphere_mesh(n, radius=0.5, far=10.0, nr=None, boundary="farfield"):
         patches = {"sphere": wall, "inlet": outer_tri[xc < 0], "outlet": outer_tri[xc >= 0]}
     else:
         raise MeshError(f"unknown boundary layout {boundary!r}")
+    return Mesh.build(nodes, tets, (), patches)
+
+
+def _naca4_half(x, t):
+    """Closed-trailing-edge NACA 4-digit half thickness at chord fraction x."""
+    return 5.0 * t * (0.2969 * np.sqrt(x) - 0.1260 * x - 0.3516 * x ** 2 + 0.2843 * x ** 3 - 0.1036 * x ** 4)
+
+
+def generate_swept_wing_mesh(n, span=1.5, chord=0.8, taper=0.56, sweep_deg=30.0, thickness=0.12, far=10.0,
+                             nj=None, nk=None):
+    """Body-fitted swept, tapered wing stand-in for config 4 (ONERA M6 geometry
+    is unavailable offline): an O-grid around a NACA 00xx section (closed
+    trailing edge), layered along rays from mid-chord with geometric spacing
+    out to a circle of radius `far` chords, extruded over `span` with the
+    section swept by `sweep_deg` and its chord tapered linearly to
+    `taper` x chord at the far end; each hex split into 24 tets (conforming,
+    as for the sphere).  Every grid line lies on its own ray from mid-chord,
+    so the layers cannot cross.
+
+    n: cells around the section (rounded up to a multiple of 4); nj radial
+    layers (default n/2), nk spanwise layers (default n/4).  About 3 n^3 tets
+    (n = 48: 331k, the size of the reference's M6 mesh).  Patches: "wing",
+    "farfield", "root" and "tip" (span-end planes; slip walls in the C4 case,
+    i.e. a swept wing between symmetry planes).
+    """
+    ni = 4 * max(2, (n + 3) // 4)
+    nj = nj or max(4, ni // 2)
+    nk = nk or max(2, ni // 4)
+    th = np.linspace(0.0, 2.0 * np.pi, ni + 1)[:-1]
+    xa = 0.5 * (1.0 + np.cos(th))                     # unit chord: TE at theta = 0, LE at pi
+    ya = np.sign(np.sin(th)) * _naca4_half(xa, thickness)
+    du = np.stack([xa - 0.5, ya], -1)
+    ra = np.linalg.norm(du, axis=1)
+    u = du / ra[:, None]                              # ray directions from mid-chord
+    g = (far / 0.5) ** (1.0 / nj)
+    sa = np.concatenate([[0.0], np.cumsum(g ** np.arange(nj))])
+    sa /= sa[-1]                                      # 0 -> 1, geometric spacing off the wall
+    r = ra[:, None] + sa[None, :] * (far - ra[:, None])   # (ni, nj+1) unit-chord radii
+    zk = np.linspace(0.0, span, nk + 1)
+    cz = chord * (1.0 - (1.0 - taper) * zk / span)    # local chord
+    xs = zk * np.tan(np.radians(sweep_deg))           # leading-edge sweep offset
+    X = (0.5 + r[:, :, None] * u[:, 0, None, None]) * cz[None, None, :] + xs[None, None, :]
+    Y = (r[:, :, None] * u[:, 1, None, None]) * cz[None, None, :]
+    Z = np.broadcast_to(zk[None, None, :], X.shape)
+    P = np.stack([X, Y, Z], axis=-1)
+    i, j, k = (x.ravel() for x in np.meshgrid(np.arange(ni), np.arange(nj), np.arange(nk), indexing="ij"))
+    ip = (i + 1) % ni
+    # VTK hex order: nodes 0-3 on layer j (face 0 = inner), 4-7 on j+1; face 2 at k, face 4 at k+1
+    corner = np.stack([P[i, j, k], P[ip, j, k], P[ip, j, k + 1], P[i, j, k + 1],
+                       P[i, j + 1, k], P[ip, j + 1, k], P[ip, j + 1, k + 1], P[i, j + 1, k + 1]], 1)
+    nodes, tets, tri = _split_hex24(corner, far * chord + span)
+    patches = {"wing": tri[j == 0, 0].reshape(-1, 3), "farfield": tri[j == nj - 1, 1].reshape(-1, 3),
+               "root": tri[k == 0, 2].reshape(-1, 3), "tip": tri[k == nk - 1, 4].reshape(-1, 3)}
     return Mesh.build(nodes, tets, (), patches)
 
 

@@ -200,3 +200,34 @@ def test_sphere_mesh_parity_with_oracle(scheme):
     q1, g1, oinfo = o.advance(q, grad)
     assert np.max(np.abs(f1.q - q1)) <= 1e-9 * np.max(np.abs(q1))
     assert info.res_rho_l1 == pytest.approx(oinfo["res_rho_l1"], rel=1e-9)
+
+
+@pytest.mark.parametrize("scheme", ["weno_gmres", "hweno_gmres"])
+def test_swept_wing_parity_with_oracle(scheme):
+    """Config 4 physics (m6wing_transonic.ini: Ma 0.8395, AoA 3.06 deg) on the
+    body-fitted swept-wing stand-in: residual and three implicit steps of the
+    device path against the oracle from the impulsive start."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+    from oracle.solver import OracleSolver
+    from paper_2304_09485_b200.stepping import SolutionField, Solver, SolverOptions
+
+    class A:
+        workload, n = "c4", 8
+
+    mesh, patches, q, grad, _, extra = bench.build_workload(A, scheme.startswith("hweno"))
+    s = Solver(mesh, SolverOptions(scheme=scheme, patches=patches, **extra))
+    o = OracleSolver(mesh, scheme=scheme, patches=patches, **extra)
+    fld = SolutionField(q, grad)
+    dt = s.local_time_step(fld)
+    res, _ = s.residual(fld, dt)
+    ores, _ = o.residual(q, grad, dt)
+    assert np.max(np.abs(res - ores)) <= 1e-12 * np.max(np.abs(ores))
+    for _ in range(3):
+        fld, info = s.advance(fld)
+        q, grad, oinfo = o.advance(q, grad)
+        assert np.max(np.abs(fld.q - q)) <= 1e-9 * np.max(np.abs(q))
+        assert info.res_rho_l1 == pytest.approx(oinfo["res_rho_l1"], rel=1e-8)
