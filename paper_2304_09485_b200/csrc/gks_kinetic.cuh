@@ -343,7 +343,13 @@ __device__ __forceinline__ double collision_tau(double pl, double pr, double dt,
 //   F   = sum_s rho_s <u (c4 + c5 a_s.c + c6 A_s) psi>_s  (transport part of the flux)
 // (+ the point-value analogue).  Viscous tau needs W0, so that path keeps
 // the three transport families separate until tau is known.
-template <bool VISCOUS, bool POINT, class SideFn, class PressFn>
+//
+// DEFER (inviscid, tau_in < 0): skip the pressure pre-pass and keep the
+// three transport families separate like the viscous path, taking the side
+// pressures from the loop's own states; tau and the time coefficients follow
+// after the loop.  Saves re-evaluating both reconstructions before the loop
+// (the face kernel's setting).
+template <bool VISCOUS, bool POINT, bool DEFER = false, class SideFn, class PressFn>
 __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const PressFn& get_pressures, double tau_in,
                                                 double dt, double mu, const KinConst& kc, double flux[5], double tp,
                                                 double point[5]) {
@@ -357,13 +363,13 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
   double pl = 0.0, pr = 0.0;
   TimeCoef tc;
   double tau = tau_in;
-  const bool tau_known = !VISCOUS || tau_in >= 0.0;
+  const bool tau_known = (!VISCOUS && !DEFER) || tau_in >= 0.0;
   if (!VISCOUS) {
-    if (tau < 0.0) {
+    if (!DEFER && tau < 0.0) {
       if (!get_pressures(pl, pr)) return 1;
       tau = collision_tau(pl, pr, dt, false, mu, nullptr);
     }
-    tc = time_coefficients(tau, dt, tp);
+    if (tau_known) tc = time_coefficients(tau, dt, tp);
   }
 #pragma unroll 1
   for (int side = 0; side < 2; ++side) {
@@ -371,7 +377,7 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
     if (!get_side(side, w, a)) return 1;
     if (!prim_ok(w)) return 1;
     const double rho = w[0];
-    if (VISCOUS) {
+    if (VISCOUS || DEFER) {
       const double ps = rho / (2.0 * w[4]);
       pl = side ? pl : ps;
       pr = side ? ps : pr;
@@ -393,7 +399,7 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
     }
     maxw_half_u(m, w, side ? -1.0 : 1.0);
     double t[5];
-    if (VISCOUS && POINT) {
+    if ((VISCOUS || DEFER) && POINT) {
       const double* const sv[4] = {a[0], a[1], a[2], A};
       double* const av[4] = {dqa[0], dqa[1], dqa[2], P6};
       gram_scatter<0, 4>(m, rho, sv, av, q0);
@@ -452,8 +458,8 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
     for (int i = 0; i < 5; ++i) D[i] = -w0[0] * D[i];
     micro_slope(sc0, D, Ab);
   }
-  if (VISCOUS) {
-    if (tau < 0.0) tau = collision_tau(pl, pr, dt, true, mu, w0);
+  if (VISCOUS || !tau_known) {
+    if (tau < 0.0) tau = collision_tau(pl, pr, dt, VISCOUS, mu, w0);
     tc = time_coefficients(tau, dt, tp);
 #pragma unroll
     for (int i = 0; i < 5; ++i) {

@@ -29,6 +29,10 @@ namespace gks {
 
 static constexpr int TPB = 128;
 
+#ifndef GKS_FACE_DEFER
+#define GKS_FACE_DEFER true
+#endif
+
 // ---------------------------------------------------------------------------
 // K1: local time step
 // ---------------------------------------------------------------------------
@@ -490,7 +494,7 @@ __global__ void __launch_bounds__(128, GKS_FACE_MINB) k_face(FaceArgs A) {
     return true;
   };
   double fl[5], pv[5];
-  const int rc = interface_flux_t<VISC, POINT>(get, press, -1.0, dtf, A.mu, A.kc, fl, 0.0, pv);
+  const int rc = interface_flux_t<VISC, POINT, GKS_FACE_DEFER>(get, press, -1.0, dtf, A.mu, A.kc, fl, 0.0, pv);
   if (rc) {
     if (ghost_fail) {
       atomicCAS(A.status, 0, GKS_ERR_UNPHYSICAL);
