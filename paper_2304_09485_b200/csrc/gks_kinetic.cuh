@@ -20,6 +20,10 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#ifndef GKS_ERFC_SCALED
+#define GKS_ERFC_SCALED 1
+#endif
+
 namespace gks {
 
 struct Maxw {
@@ -71,8 +75,18 @@ __device__ __forceinline__ void maxw_half_u(Maxw& m, const double w[5], double s
   const double lam = w[4], u = w[1];
   const double rl = sqrt(lam);
   constexpr double kInvSqrtPi = 0.56418958354775628695;  // 1 / sqrt(pi)
-  const double g = kInvSqrtPi * exp(-lam * u * u) * rl * m.h;
+  const double e = exp(-lam * u * u);
+  const double g = kInvSqrtPi * e * rl * m.h;
+#if GKS_ERFC_SCALED
+  // erfc(x) = exp(-x^2) erfcx(x) for x >= 0 and 2 - exp(-x^2) erfcx(-x)
+  // below, reusing exp(-lam u^2) of the Gaussian term: erfcx is branch-light
+  // where erfc switches algorithms across |x| (warp divergence)
+  const double x = -sign * rl * u;
+  const double ex = e * erfcx(fabs(x));
+  m.U[0] = 0.5 * (x >= 0.0 ? ex : 2.0 - ex);
+#else
   m.U[0] = 0.5 * erfc(-sign * rl * u);
+#endif
   m.U[1] = u * m.U[0] + sign * g;
   recur<7>(m.U, u, m.h);
 }
