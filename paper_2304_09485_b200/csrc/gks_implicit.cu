@@ -416,7 +416,7 @@ __global__ void k_gm_cycle_start(GmresDev* g, int cyc) {
 }
 
 // after the first MGS pass of column j: Hessenberg column, re-orthogonalisation test
-__global__ void k_gm_reorth_check(GmresDev* g, int j) {
+__device__ __forceinline__ void gm_reorth_check(GmresDev* g, int j) {
   if (!g->active) { g->reorth_gate = 0; return; }
   g->matvecs += 1;
   for (int i = 0; i <= j; ++i) GH(i, j) = g->dots[i];
@@ -426,7 +426,9 @@ __global__ void k_gm_reorth_check(GmresDev* g, int j) {
   g->reorth_gate = g->reorth;
 }
 
-__global__ void k_gm_givens(GmresDev* g, int j, int cyc) {
+__global__ void k_gm_reorth_check(GmresDev* g, int j) { gm_reorth_check(g, j); }
+
+__device__ __forceinline__ void gm_givens(GmresDev* g, int j, int cyc) {
   if (!g->active) return;
   if (g->reorth) {
     for (int i = 0; i <= j; ++i) GH(i, j) += g->corr[i];
@@ -463,6 +465,99 @@ __global__ void k_gm_givens(GmresDev* g, int j, int cyc) {
   } else {
     g->hdiv = GH(j + 1, j);
   }
+}
+
+__global__ void k_gm_givens(GmresDev* g, int j, int cyc) { gm_givens(g, j, cyc); }
+
+// Deterministic block sum (fixed shuffle tree per warp, then warp 0 over the
+// warp partials); every thread gets the result.
+__device__ __forceinline__ double block_sum_w(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red[32] = v;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+// Whole Arnoldi column j for small systems in ONE single-CTA kernel: the
+// MGS pass (krylov.py:93-96), the conditional re-orthogonalisation
+// (:97-104), the Givens update (:107-124) and v_{j+1} = w / h (:127), with
+// w resident in shared memory.  Replaces 2 (j + 1) + 6 launches per column
+// (dot2, the axpy_dot chain, check, the gated second pass, givens, div):
+// below ~25k unknowns the step is bound by that chain of dependent launches.
+// Same arithmetic per element as the multi-block kernels; the block-level
+// summation order differs (deterministic either way).
+__global__ void __launch_bounds__(1024) k_gm_arnoldi_small(int n, int64_t ld, double* __restrict__ V,
+                                                           const double* __restrict__ wg, GmresDev* g, int j,
+                                                           int cyc) {
+  extern __shared__ double w[];
+  __shared__ double red[33];
+  if (!g->active) return;
+  const int t = threadIdx.x, nt = blockDim.x;
+  double s0 = 0.0, s1 = 0.0;
+  for (int i = t; i < n; i += nt) {
+    const double x = wg[i];
+    w[i] = x;
+    s0 += x * x;
+    s1 += x * V[i];
+  }
+  const double ww = block_sum_w(s0, red);
+  const double d0 = block_sum_w(s1, red);
+  if (t == 0) {
+    g->wscale2 = ww;
+    g->dots[0] = d0;
+  }
+  // pass 0: w -= h_i v_i, fused with the next dot (w . v_{i+1}, or w . w);
+  // pass 1 (only on heavy cancellation): the same with the corrections.
+  // Every thread carries h in a register (the reduction result), thread 0
+  // records it in the device GMRES state.
+  for (int pass = 0; pass < 2; ++pass) {
+    double* hv = pass == 0 ? g->dots : g->corr;
+    double h = d0;
+    if (pass == 1) {
+      double s = 0.0;
+      for (int i = t; i < n; i += nt) s += w[i] * V[i];
+      h = block_sum_w(s, red);
+      if (t == 0) hv[0] = h;
+    }
+    for (int k = 0; k <= j; ++k) {
+      const double* v = V + (int64_t)k * ld;
+      const double* nx = k < j ? V + (int64_t)(k + 1) * ld : nullptr;
+      double s = 0.0;
+      for (int i = t; i < n; i += nt) {
+        const double x = w[i] - h * v[i];
+        w[i] = x;
+        s += x * (nx ? nx[i] : x);
+      }
+      const double r = block_sum_w(s, red);
+      if (t == 0) {
+        if (k < j) hv[k + 1] = r;
+        else g->hnext2 = r;
+      }
+      h = r;
+    }
+    __syncthreads();
+    if (pass == 0) {
+      if (t == 0) gm_reorth_check(g, j);
+      __syncthreads();
+      if (!g->reorth) break;
+    }
+  }
+  if (t == 0) gm_givens(g, j, cyc);
+  __syncthreads();
+  if (!g->active) return;
+  const double d = g->hdiv;
+  double* vn = V + (int64_t)(j + 1) * ld;
+  for (int i = t; i < n; i += nt) vn[i] = w[i] / d;
 }
 
 // back substitution (krylov.py:128-131) and cycle bookkeeping
@@ -754,6 +849,12 @@ int gmres_enqueue(BlockSys* A, const double* b_dev, double* x_dev, const GmresPa
   const int* rgate = &g->reorth_gate;
   const int kmax = P.kmax;
   const int grid = red_grid(n);
+  // small single-rank systems: one kernel per Arnoldi column (w in shared memory)
+  const size_t small_smem = (size_t)n * sizeof(double);
+  const char* small_env = getenv("GKS_GMRES_SMALL");
+  const bool small = !A->red2 && small_smem <= 200 * 1024 && !(small_env && small_env[0] == '0');
+  if (small)
+    GKS_CUDA(cudaFuncSetAttribute(k_gm_arnoldi_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small_smem));
   auto Av = [&](const double* v, double* dst, const int* gate) {
     if (matvec) (*matvec)(v, dst, gate);
     else bs_spmv(A, v, dst, gate);
@@ -775,6 +876,11 @@ int gmres_enqueue(BlockSys* A, const double* b_dev, double* x_dev, const GmresPa
         bs_jacobi(A, W->t, W->w, W->r, kmax, act);
       } else {
         bs_prec_matvec(A, vj, W->w, W->t, W->r, kmax, act);
+      }
+      if (small) {
+        // the whole column in one single-CTA kernel (k_gm_arnoldi_small)
+        GKS_LAUNCH(KC_REDUCE, k_gm_arnoldi_small, 1, 1024, small_smem, s, (int)n, ld, W->V, W->w, g, j, cyc);
+        continue;
       }
       // ||w||^2 and w.v_0 in one pass, then fused axpy + next dot (MGS)
       dot2(A, n, W->w, W->w, W->w, W->V, &g->wscale2, &g->dots[0], act);

@@ -201,3 +201,20 @@ def test_reordered_handle_matches(case, method):
         assert info.res_l2 == pytest.approx(r2_, rel=1e-8, abs=1e-13)
         assert info.solver_cycles == int(cyc)
         assert relmax(f.q, g["q_after"][k]) < 1e-9
+
+
+def test_gmres_multiblock_path_on_reference_system(case, monkeypatch):
+    """The test meshes are small enough for the single-CTA Arnoldi kernel;
+    force the multi-block MGS chain (used above ~25k unknowns) and hold it
+    to the same golden bars."""
+    from paper_2304_09485_b200.jacobian import BlockJacobian
+    from paper_2304_09485_b200.krylov import gmres_solve
+
+    monkeypatch.setenv("GKS_GMRES_SMALL", "0")
+    _, _, _, g = case
+    a = BlockJacobian(g["jac_diag"], g["jac_off"], g["jac_off_col"], g["jac_off_row"], g["jac_rowptr"])
+    x, info = gmres_solve(a, g["res"], m=10, restarts=3, k_max=2)
+    assert info.matvecs == int(g["gmres_matvecs"])
+    norms = np.concatenate([np.asarray(c) for c in info.cycle_residuals])
+    assert np.allclose(norms, g["gmres_cycle_norms"], rtol=1e-9, atol=1e-9 * norms[0])
+    assert relmax(x, g["gmres_x"]) < 1e-9
