@@ -102,6 +102,12 @@ __global__ void k_fill(int64_t n, double* __restrict__ dt, const double* val) {
 // 45 % of all instructions in the runtime-bound version as ISETP/IMAD/BRA.
 static constexpr int RT = 32;
 static constexpr int RT_THREADS = RT * 5;
+// Big-stencil gathers issued straight from the HBM index records, before the
+// tile's bulk copies have landed (measured 0.84 -> 0.72 ms, C2 WENO); the
+// index records are then not staged.
+#ifndef GKS_RECON_EARLY
+#define GKS_RECON_EARLY 1
+#endif
 
 // recon.py:167-195 on one (cell, component); beta packed as the upper
 // triangle (45 entries, row-major).
@@ -166,7 +172,7 @@ inline WenoTile weno_tile(int K, int M, int S, const double* big_op, const int* 
                           const int* sub_gather, const int8_t* sub_active, const double* beta, bool linear) {
   TileBuilder<WT_N> b(RT);
   b.add(WT_OP, big_op, 8u * rec_stride_f64(9 * K));
-  b.add(WT_GI, big_gather, 4u * rec_stride_i32(K));
+  b.add(WT_GI, big_gather, 4u * rec_stride_i32(K), !GKS_RECON_EARLY);
   b.add(WT_SO, sub_op, 8u * rec_stride_f64(3 * M * S), !linear);
   b.add(WT_SG, sub_gather, 4u * rec_stride_i32(M * S), !linear);
   b.add(WT_ACT, sub_active, (uint32_t)M, !linear);
@@ -179,9 +185,9 @@ inline HwenoTile hweno_tile(int HA, int HG, int M, const double* big_op, const i
                             const int* sub_gather, const int8_t* sub_active, const double* beta, bool linear) {
   TileBuilder<HT_N> b(RT);
   b.add(HT_OP, big_op, 8u * rec_stride_f64(9 * (HA + 3 * HG)));
-  b.add(HT_AG, avg_gather, 4u * rec_stride_i32(HA));
-  b.add(HT_GG, grad_gather, 4u * rec_stride_i32(HG));
-  b.add(HT_GS, grad_scale, 8u * rec_stride_f64(HG));
+  b.add(HT_AG, avg_gather, 4u * rec_stride_i32(HA), !GKS_RECON_EARLY);
+  b.add(HT_GG, grad_gather, 4u * rec_stride_i32(HG), !GKS_RECON_EARLY);
+  b.add(HT_GS, grad_scale, 8u * rec_stride_f64(HG), !GKS_RECON_EARLY);
   b.add(HT_SO, sub_op, 8u * rec_stride_f64(21 * M), !linear);
   b.add(HT_SG, sub_gather, 4u * rec_stride_i32(2 * M), !linear);
   b.add(HT_ACT, sub_active, (uint32_t)M, !linear);
@@ -209,13 +215,24 @@ __global__ void __launch_bounds__(RT_THREADS, GKS_RECON_MINB) k_recon_weno(int64
   const int k = threadIdx.x - cl * 5;
   const int64_t c = c0 + cl;
   const double qc = cl < n ? __ldg(q + c * 5 + k) : 0.0;
+  double r[K];
+#if GKS_RECON_EARLY
+  // big-stencil gathers straight from the HBM index records, in flight
+  // while the bulk copies land
+  if (cl < n) {
+    const int* gi = (const int*)(T.a[WT_GI].src + (size_t)c * T.a[WT_GI].rec);
+#pragma unroll
+    for (int j = 0; j < K; ++j) r[j] = __ldg(q + (int64_t)__ldg(gi + j) * 5 + k) - qc;
+  }
+#endif
   mbar_wait(&bar, 0);
   if (cl >= n) return;
   const double* op = staged<double>(sm, T, WT_OP, cl);
+#if !GKS_RECON_EARLY
   const int* gi = staged<int>(sm, T, WT_GI, cl);
-  double r[K];
 #pragma unroll
   for (int j = 0; j < K; ++j) r[j] = __ldg(q + (int64_t)gi[j] * 5 + k) - qc;
+#endif
   double cb[9];
 #pragma unroll
   for (int d = 0; d < 9; ++d) {
@@ -265,24 +282,33 @@ __global__ void __launch_bounds__(RT_THREADS, GKS_RECON_MINB) k_recon_hweno(int6
   const int k = threadIdx.x - cl * 5;
   const int64_t c = c0 + cl;
   const double qc = cl < n ? __ldg(q + c * 5 + k) : 0.0;
-  mbar_wait(&bar, 0);
-  if (cl >= n) return;
   constexpr int W = HA + 3 * HG;
-  const double* op = staged<double>(sm, T, HT_OP, cl);
-  const int* ag = staged<int>(sm, T, HT_AG, cl);
-  const int* gg = staged<int>(sm, T, HT_GG, cl);
-  const double* gs = staged<double>(sm, T, HT_GS, cl);
   // right-hand side: neighbour averages, then h-scaled gradients (hweno.py:147-151)
   double ra[HA], rg[HG][3];
+  // (index records from HBM or shared memory: generic loads)
+  auto gather = [&](const int* ag, const int* gg, const double* gs) {
 #pragma unroll
-  for (int j = 0; j < HA; ++j) ra[j] = __ldg(q + (int64_t)ag[j] * 5 + k) - qc;
+    for (int j = 0; j < HA; ++j) ra[j] = __ldg(q + (int64_t)ag[j] * 5 + k) - qc;
 #pragma unroll
-  for (int g = 0; g < HG; ++g) {
-    const int64_t m = gg[g];
-    const double sc = gs[g];
+    for (int g = 0; g < HG; ++g) {
+      const int64_t m = gg[g];
+      const double sc = gs[g];
 #pragma unroll
-    for (int x = 0; x < 3; ++x) rg[g][x] = sc * __ldg(grad + (m * 3 + x) * 5 + k);
-  }
+      for (int x = 0; x < 3; ++x) rg[g][x] = sc * __ldg(grad + (m * 3 + x) * 5 + k);
+    }
+  };
+#if GKS_RECON_EARLY
+  if (cl < n)
+    gather((const int*)(T.a[HT_AG].src + (size_t)c * T.a[HT_AG].rec),
+           (const int*)(T.a[HT_GG].src + (size_t)c * T.a[HT_GG].rec),
+           (const double*)(T.a[HT_GS].src + (size_t)c * T.a[HT_GS].rec));
+#endif
+  mbar_wait(&bar, 0);
+  if (cl >= n) return;
+  const double* op = staged<double>(sm, T, HT_OP, cl);
+#if !GKS_RECON_EARLY
+  gather(staged<int>(sm, T, HT_AG, cl), staged<int>(sm, T, HT_GG, cl), staged<double>(sm, T, HT_GS, cl));
+#endif
   double cb[9];
 #pragma unroll
   for (int d = 0; d < 9; ++d) {

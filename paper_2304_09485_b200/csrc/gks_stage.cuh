@@ -79,7 +79,8 @@ __host__ __device__ constexpr int rec_stride_i32(int e) { return e % 2 == 0 ? e 
 // One staged array of the tile: record bytes, smem stride, smem offset.
 struct StageArr {
   const unsigned char* src;  // global base of record 0
-  uint32_t bytes;            // record bytes (0: not staged)
+  uint32_t rec;              // record bytes in HBM
+  uint32_t bytes;            // record bytes staged (0: not staged)
   uint32_t stride;           // smem record stride
   uint32_t off;              // smem offset of the tile's record 0
 };
@@ -119,6 +120,7 @@ struct TileBuilder {
   void add(int i, const void* src, uint32_t bytes, bool on = true) {
     StageArr& a = t.a[i];
     a.src = (const unsigned char*)src;
+    a.rec = bytes;
     a.bytes = on ? bytes : 0;
     a.stride = on ? stage_stride(bytes) : 0;
     a.off = off;
