@@ -32,6 +32,10 @@ static constexpr int TPB = 128;
 #ifndef GKS_FACE_DEFER
 #define GKS_FACE_DEFER true
 #endif
+// L2 prefetch of the neighbour side's records at kernel start (1 %, measured)
+#ifndef GKS_FACE_PREFETCH
+#define GKS_FACE_PREFETCH 1
+#endif
 
 // ---------------------------------------------------------------------------
 // K1: local time step
@@ -458,6 +462,17 @@ __global__ void __launch_bounds__(128, GKS_FACE_MINB) k_face(FaceArgs A) {
   const int64_t nb = A.f_nbr[f];
   const int p = nb >= 0 ? -1 : A.f_patch[f];
   const bool wall = p >= 0 && A.patches[p].wall;
+#if GKS_FACE_PREFETCH
+  // the neighbour side's coefficient record is read only after the whole
+  // owner side: start moving its lines into L2 now (no registers held)
+  if (nb >= 0) {
+    const char* pc = (const char*)(A.coef + nb * 45);
+#pragma unroll
+    for (int l = 0; l < 360; l += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(pc + l));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(pc + 359));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)(A.avg0 + nb * 9)));
+  }
+#endif
   const double dtf = nb >= 0 ? fmin(A.dt[o], A.dt[nb]) : A.dt[o];
   int ghost_fail = 0;
   // side 0: owner reconstruction; side 1: neighbour (shifted chart) or ghost
