@@ -22,6 +22,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "gks_implicit.cuh"
 
 namespace gks {
@@ -488,76 +490,109 @@ __device__ __forceinline__ double block_sum_w(double v, double* red) {
   return red[32];
 }
 
-// Whole Arnoldi column j for small systems in ONE single-CTA kernel: the
-// MGS pass (krylov.py:93-96), the conditional re-orthogonalisation
-// (:97-104), the Givens update (:107-124) and v_{j+1} = w / h (:127), with
-// w resident in shared memory.  Replaces 2 (j + 1) + 6 launches per column
-// (dot2, the axpy_dot chain, check, the gated second pass, givens, div):
-// below ~25k unknowns the step is bound by that chain of dependent launches.
-// Same arithmetic per element as the multi-block kernels; the block-level
-// summation order differs (deterministic either way).
-__global__ void __launch_bounds__(1024) k_gm_arnoldi_small(int n, int64_t ld, double* __restrict__ V,
-                                                           const double* __restrict__ wg, GmresDev* g, int j,
-                                                           int cyc) {
+// Whole Arnoldi column j for small and medium systems in ONE kernel: the MGS
+// pass (krylov.py:93-96), the conditional re-orthogonalisation (:97-104),
+// the Givens update (:107-124) and v_{j+1} = w / h (:127).  Replaces
+// 2 (j + 1) + 6 dependent launches per column (dot2, the axpy_dot chain,
+// check, the gated second pass, givens, div): below ~400k unknowns the step
+// is bound by that chain.  CL CTAs form one thread-block cluster; each keeps
+// its slice of w in shared memory, block partials meet through distributed
+// shared memory and are summed by every CTA in rank order (identical,
+// deterministic totals everywhere); the scalar recurrences run on CTA 0 and
+// reach the others through global memory across cluster barriers.  Same
+// arithmetic per element as the multi-block kernels; the summation tree
+// differs (deterministic for a given n).
+template <int CL>
+__device__ __forceinline__ double cluster_sum(double v, double* red, double* part) {
+  const double b = block_sum_w(v, red);
+  if (CL == 1) return b;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  if (threadIdx.x == 0) part[0] = b;
+  cl.sync();
+  double s = 0.0;
+#pragma unroll
+  for (int r = 0; r < CL; ++r) s += *cl.map_shared_rank(part, r);
+  cl.sync();  // nobody overwrites part before everyone has read it
+  return s;
+}
+
+template <int CL>
+__device__ __forceinline__ void cluster_barrier() {
+  if (CL == 1) {
+    __syncthreads();
+  } else {
+    cooperative_groups::this_cluster().sync();
+  }
+}
+
+template <int CL>
+__global__ void __launch_bounds__(1024) k_gm_arnoldi(int n, int64_t ld, double* __restrict__ V,
+                                                     const double* __restrict__ wg, GmresDev* g, int j, int cyc) {
   extern __shared__ double w[];
   __shared__ double red[33];
-  if (!g->active) return;
+  __shared__ double part[1];
+  if (!__ldcg(&g->active)) return;
+  const int rank = CL == 1 ? 0 : (int)cooperative_groups::this_cluster().block_rank();
+  const int chunk = (n + CL - 1) / CL;
+  const int lo = rank * chunk, hi = min(n, lo + chunk), m = max(0, hi - lo);
+  const bool lead = rank == 0 && threadIdx.x == 0;
   const int t = threadIdx.x, nt = blockDim.x;
+  const double* V0 = V + lo;
   double s0 = 0.0, s1 = 0.0;
-  for (int i = t; i < n; i += nt) {
-    const double x = wg[i];
+  for (int i = t; i < m; i += nt) {
+    const double x = wg[lo + i];
     w[i] = x;
     s0 += x * x;
-    s1 += x * V[i];
+    s1 += x * V0[i];
   }
-  const double ww = block_sum_w(s0, red);
-  const double d0 = block_sum_w(s1, red);
-  if (t == 0) {
+  const double ww = cluster_sum<CL>(s0, red, part);
+  const double d0 = cluster_sum<CL>(s1, red, part);
+  if (lead) {
     g->wscale2 = ww;
     g->dots[0] = d0;
   }
   // pass 0: w -= h_i v_i, fused with the next dot (w . v_{i+1}, or w . w);
   // pass 1 (only on heavy cancellation): the same with the corrections.
-  // Every thread carries h in a register (the reduction result), thread 0
-  // records it in the device GMRES state.
+  // Every thread carries h in a register (the reduction result), the lead
+  // thread records it in the device GMRES state.
   for (int pass = 0; pass < 2; ++pass) {
     double* hv = pass == 0 ? g->dots : g->corr;
     double h = d0;
     if (pass == 1) {
       double s = 0.0;
-      for (int i = t; i < n; i += nt) s += w[i] * V[i];
-      h = block_sum_w(s, red);
-      if (t == 0) hv[0] = h;
+      for (int i = t; i < m; i += nt) s += w[i] * V0[i];
+      h = cluster_sum<CL>(s, red, part);
+      if (lead) hv[0] = h;
     }
     for (int k = 0; k <= j; ++k) {
-      const double* v = V + (int64_t)k * ld;
-      const double* nx = k < j ? V + (int64_t)(k + 1) * ld : nullptr;
+      const double* v = V + (int64_t)k * ld + lo;
+      const double* nx = k < j ? V + (int64_t)(k + 1) * ld + lo : nullptr;
       double s = 0.0;
-      for (int i = t; i < n; i += nt) {
+      for (int i = t; i < m; i += nt) {
         const double x = w[i] - h * v[i];
         w[i] = x;
         s += x * (nx ? nx[i] : x);
       }
-      const double r = block_sum_w(s, red);
-      if (t == 0) {
+      const double r = cluster_sum<CL>(s, red, part);
+      if (lead) {
         if (k < j) hv[k + 1] = r;
         else g->hnext2 = r;
       }
       h = r;
     }
-    __syncthreads();
     if (pass == 0) {
-      if (t == 0) gm_reorth_check(g, j);
-      __syncthreads();
-      if (!g->reorth) break;
+      if (lead) gm_reorth_check(g, j);
+      cluster_barrier<CL>();
+      if (!__ldcg(&g->reorth)) break;
     }
   }
-  if (t == 0) gm_givens(g, j, cyc);
-  __syncthreads();
-  if (!g->active) return;
-  const double d = g->hdiv;
-  double* vn = V + (int64_t)(j + 1) * ld;
-  for (int i = t; i < n; i += nt) vn[i] = w[i] / d;
+  if (lead) gm_givens(g, j, cyc);
+  cluster_barrier<CL>();
+  if (!__ldcg(&g->active)) return;
+  const double d = __ldcg(&g->hdiv);
+  double* vn = V + (int64_t)(j + 1) * ld + lo;
+  for (int i = t; i < m; i += nt) vn[i] = w[i] / d;
 }
 
 // back substitution (krylov.py:128-131) and cycle bookkeeping
@@ -817,6 +852,89 @@ void axpy_dot(BlockSys* A, int64_t n, double* w, const double* v, const double* 
   if (A->red2) A->red2(out, nullptr);
 }
 
+// Cluster size of the fused Arnoldi-column kernel for n unknowns: slices of
+// <= 16k doubles (128 KB of shared memory) per CTA, clusters of up to 16
+// CTAs (non-portable size, checked against the device once); 0 = use the
+// multi-block chain.
+static constexpr int kArnoldiSlice = 16384;
+
+template <int CL>
+static int arnoldi_attr(size_t smem) {
+  static bool ok = [smem] {
+    if (cudaFuncSetAttribute(k_gm_arnoldi<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kArnoldiSlice * sizeof(double))) != cudaSuccess)
+      return false;
+    if (CL > 8 && cudaFuncSetAttribute(k_gm_arnoldi<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                      cudaSuccess)
+      return false;
+    if (CL == 1) return true;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(CL);
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = kArnoldiSlice * sizeof(double);
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    return cudaOccupancyMaxActiveClusters(&nclusters, k_gm_arnoldi<CL>, &cfg) == cudaSuccess && nclusters > 0;
+  }();
+  (void)smem;
+  cudaGetLastError();
+  return ok ? CL : 0;
+}
+
+static int arnoldi_cluster(int64_t n) {
+  const int64_t need = (n + kArnoldiSlice - 1) / kArnoldiSlice;
+  if (need <= 1) return arnoldi_attr<1>(0);
+  if (need <= 2) return arnoldi_attr<2>(0);
+  if (need <= 4) return arnoldi_attr<4>(0);
+  if (need <= 8) return arnoldi_attr<8>(0);
+  if (need <= 16) return arnoldi_attr<16>(0);
+  return 0;
+}
+
+template <int CL>
+static int launch_arnoldi_cl(cudaStream_t s, int n, int64_t ld, double* V, const double* w, GmresDev* g, int j,
+                             int cyc) {
+  const size_t smem = (size_t)((n + CL - 1) / CL) * sizeof(double);
+  if (CL == 1) {
+    GKS_LAUNCH(KC_REDUCE, k_gm_arnoldi<1>, 1, 1024, smem, s, n, ld, V, w, g, j, cyc);
+    return GKS_OK;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(CL);
+  cfg.blockDim = dim3(1024);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaEvent_t pa = g_prof_on ? prof_begin(s) : nullptr;
+  GKS_CUDA(cudaLaunchKernelEx(&cfg, k_gm_arnoldi<CL>, n, ld, V, w, g, j, cyc));
+  count_launch(1);
+  if (pa) prof_end(KC_REDUCE, s, pa);
+  return GKS_OK;
+}
+
+static int launch_arnoldi(int cl, cudaStream_t s, int n, int64_t ld, double* V, const double* w, GmresDev* g, int j,
+                          int cyc) {
+  switch (cl) {
+    case 1: return launch_arnoldi_cl<1>(s, n, ld, V, w, g, j, cyc);
+    case 2: return launch_arnoldi_cl<2>(s, n, ld, V, w, g, j, cyc);
+    case 4: return launch_arnoldi_cl<4>(s, n, ld, V, w, g, j, cyc);
+    case 8: return launch_arnoldi_cl<8>(s, n, ld, V, w, g, j, cyc);
+    default: return launch_arnoldi_cl<16>(s, n, ld, V, w, g, j, cyc);
+  }
+}
+
 // Restarted left-preconditioned GMRES (krylov.py:55-140) on device vectors;
 // x_dev receives the solution.  matvec == nullptr: A v is the block spmv.
 // gmres_enqueue only launches (no host synchronisation, so a whole implicit
@@ -849,12 +967,11 @@ int gmres_enqueue(BlockSys* A, const double* b_dev, double* x_dev, const GmresPa
   const int* rgate = &g->reorth_gate;
   const int kmax = P.kmax;
   const int grid = red_grid(n);
-  // small single-rank systems: one kernel per Arnoldi column (w in shared memory)
-  const size_t small_smem = (size_t)n * sizeof(double);
+  // single-rank systems below ~400k unknowns: one (cluster) kernel per
+  // Arnoldi column, w in shared memory (k_gm_arnoldi)
   const char* small_env = getenv("GKS_GMRES_SMALL");
-  const bool small = !A->red2 && small_smem <= 200 * 1024 && !(small_env && small_env[0] == '0');
-  if (small)
-    GKS_CUDA(cudaFuncSetAttribute(k_gm_arnoldi_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small_smem));
+  int cl = 0;  // cluster size of the fused column kernel, 0 = multi-block chain
+  if (!A->red2 && !(small_env && small_env[0] == '0')) cl = arnoldi_cluster(n);
   auto Av = [&](const double* v, double* dst, const int* gate) {
     if (matvec) (*matvec)(v, dst, gate);
     else bs_spmv(A, v, dst, gate);
@@ -877,9 +994,9 @@ int gmres_enqueue(BlockSys* A, const double* b_dev, double* x_dev, const GmresPa
       } else {
         bs_prec_matvec(A, vj, W->w, W->t, W->r, kmax, act);
       }
-      if (small) {
-        // the whole column in one single-CTA kernel (k_gm_arnoldi_small)
-        GKS_LAUNCH(KC_REDUCE, k_gm_arnoldi_small, 1, 1024, small_smem, s, (int)n, ld, W->V, W->w, g, j, cyc);
+      if (cl) {
+        // the whole column in one kernel (k_gm_arnoldi)
+        TRY_GM(launch_arnoldi(cl, s, (int)n, ld, W->V, W->w, g, j, cyc));
         continue;
       }
       // ||w||^2 and w.v_0 in one pass, then fused axpy + next dot (MGS)
