@@ -502,18 +502,22 @@ __device__ __forceinline__ double block_sum_w(double v, double* red) {
 // reach the others through global memory across cluster barriers.  Same
 // arithmetic per element as the multi-block kernels; the summation tree
 // differs (deterministic for a given n).
+// Partials alternate between two slots, so one cluster barrier per sum is
+// enough: a CTA can only overwrite a slot after the next barrier, which every
+// CTA reaches only once it has read that slot.
 template <int CL>
-__device__ __forceinline__ double cluster_sum(double v, double* red, double* part) {
+__device__ __forceinline__ double cluster_sum(double v, double* red, double* part, int& slot) {
   const double b = block_sum_w(v, red);
   if (CL == 1) return b;
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
-  if (threadIdx.x == 0) part[0] = b;
+  double* p = part + slot;
+  slot ^= 1;
+  if (threadIdx.x == 0) *p = b;
   cl.sync();
   double s = 0.0;
 #pragma unroll
-  for (int r = 0; r < CL; ++r) s += *cl.map_shared_rank(part, r);
-  cl.sync();  // nobody overwrites part before everyone has read it
+  for (int r = 0; r < CL; ++r) s += *cl.map_shared_rank(p, r);
   return s;
 }
 
@@ -526,28 +530,37 @@ __device__ __forceinline__ void cluster_barrier() {
   }
 }
 
+// w stays in registers: each of the 1024 threads owns up to AW elements of
+// its CTA's slice (element t + u * 1024), so every pass issues all of a
+// thread's loads at once (a strided loop left one L2 round trip in flight
+// per iteration: 15 us per pass, measured).
+static constexpr int AW = 16;
+
 template <int CL>
-__global__ void __launch_bounds__(1024) k_gm_arnoldi(int n, int64_t ld, double* __restrict__ V,
+__global__ void __launch_bounds__(1024, 1) k_gm_arnoldi(int n, int64_t ld, double* __restrict__ V,
                                                      const double* __restrict__ wg, GmresDev* g, int j, int cyc) {
-  extern __shared__ double w[];
   __shared__ double red[33];
-  __shared__ double part[1];
+  __shared__ double part[2];
+  int slot = 0;
   if (!__ldcg(&g->active)) return;
   const int rank = CL == 1 ? 0 : (int)cooperative_groups::this_cluster().block_rank();
   const int chunk = (n + CL - 1) / CL;
   const int lo = rank * chunk, hi = min(n, lo + chunk), m = max(0, hi - lo);
   const bool lead = rank == 0 && threadIdx.x == 0;
-  const int t = threadIdx.x, nt = blockDim.x;
+  const int t = threadIdx.x;
   const double* V0 = V + lo;
+  double w[AW];
   double s0 = 0.0, s1 = 0.0;
-  for (int i = t; i < m; i += nt) {
-    const double x = wg[lo + i];
-    w[i] = x;
-    s0 += x * x;
-    s1 += x * V0[i];
+#pragma unroll
+  for (int u = 0; u < AW; ++u) {
+    const int i = t + u * 1024;
+    w[u] = i < m ? wg[lo + i] : 0.0;
+    const double v = i < m ? V0[i] : 0.0;
+    s0 += w[u] * w[u];
+    s1 += w[u] * v;
   }
-  const double ww = cluster_sum<CL>(s0, red, part);
-  const double d0 = cluster_sum<CL>(s1, red, part);
+  const double ww = cluster_sum<CL>(s0, red, part, slot);
+  const double d0 = cluster_sum<CL>(s1, red, part, slot);
   if (lead) {
     g->wscale2 = ww;
     g->dots[0] = d0;
@@ -561,20 +574,37 @@ __global__ void __launch_bounds__(1024) k_gm_arnoldi(int n, int64_t ld, double* 
     double h = d0;
     if (pass == 1) {
       double s = 0.0;
-      for (int i = t; i < m; i += nt) s += w[i] * V0[i];
-      h = cluster_sum<CL>(s, red, part);
+#pragma unroll
+      for (int u = 0; u < AW; ++u) {
+        const int i = t + u * 1024;
+        s += w[u] * (i < m ? V0[i] : 0.0);
+      }
+      h = cluster_sum<CL>(s, red, part, slot);
       if (lead) hv[0] = h;
     }
     for (int k = 0; k <= j; ++k) {
       const double* v = V + (int64_t)k * ld + lo;
       const double* nx = k < j ? V + (int64_t)(k + 1) * ld + lo : nullptr;
       double s = 0.0;
-      for (int i = t; i < m; i += nt) {
-        const double x = w[i] - h * v[i];
-        w[i] = x;
-        s += x * (nx ? nx[i] : x);
+      if (nx) {
+#pragma unroll
+        for (int u = 0; u < AW; ++u) {
+          const int i = t + u * 1024;
+          const double vi = i < m ? __ldcg(v + i) : 0.0;
+          const double xi = i < m ? __ldcg(nx + i) : 0.0;
+          w[u] = w[u] - h * vi;
+          s += w[u] * xi;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < AW; ++u) {
+          const int i = t + u * 1024;
+          const double vi = i < m ? __ldcg(v + i) : 0.0;
+          w[u] = w[u] - h * vi;
+          s += w[u] * w[u];
+        }
       }
-      const double r = cluster_sum<CL>(s, red, part);
+      const double r = cluster_sum<CL>(s, red, part, slot);
       if (lead) {
         if (k < j) hv[k + 1] = r;
         else g->hnext2 = r;
@@ -592,7 +622,11 @@ __global__ void __launch_bounds__(1024) k_gm_arnoldi(int n, int64_t ld, double* 
   if (!__ldcg(&g->active)) return;
   const double d = __ldcg(&g->hdiv);
   double* vn = V + (int64_t)(j + 1) * ld + lo;
-  for (int i = t; i < m; i += nt) vn[i] = w[i] / d;
+#pragma unroll
+  for (int u = 0; u < AW; ++u) {
+    const int i = t + u * 1024;
+    if (i < m) vn[i] = w[u] / d;
+  }
 }
 
 // back substitution (krylov.py:128-131) and cycle bookkeeping
@@ -853,17 +887,14 @@ void axpy_dot(BlockSys* A, int64_t n, double* w, const double* v, const double* 
 }
 
 // Cluster size of the fused Arnoldi-column kernel for n unknowns: slices of
-// <= 16k doubles (128 KB of shared memory) per CTA, clusters of up to 16
+// <= 16k doubles (16 registers x 1024 threads) per CTA, clusters of up to 16
 // CTAs (non-portable size, checked against the device once); 0 = use the
 // multi-block chain.
-static constexpr int kArnoldiSlice = 16384;
+static constexpr int kArnoldiSlice = AW * 1024;
 
 template <int CL>
 static int arnoldi_attr(size_t smem) {
   static bool ok = [smem] {
-    if (cudaFuncSetAttribute(k_gm_arnoldi<CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(kArnoldiSlice * sizeof(double))) != cudaSuccess)
-      return false;
     if (CL > 8 && cudaFuncSetAttribute(k_gm_arnoldi<CL>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
                       cudaSuccess)
       return false;
@@ -876,7 +907,7 @@ static int arnoldi_attr(size_t smem) {
     at[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(CL);
     cfg.blockDim = dim3(1024);
-    cfg.dynamicSmemBytes = kArnoldiSlice * sizeof(double);
+    cfg.dynamicSmemBytes = 0;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int nclusters = 0;
@@ -900,7 +931,7 @@ static int arnoldi_cluster(int64_t n) {
 template <int CL>
 static int launch_arnoldi_cl(cudaStream_t s, int n, int64_t ld, double* V, const double* w, GmresDev* g, int j,
                              int cyc) {
-  const size_t smem = (size_t)((n + CL - 1) / CL) * sizeof(double);
+  const size_t smem = 0;
   if (CL == 1) {
     GKS_LAUNCH(KC_REDUCE, k_gm_arnoldi<1>, 1, 1024, smem, s, n, ld, V, w, g, j, cyc);
     return GKS_OK;
