@@ -412,13 +412,28 @@ def run_ours(args):
     opts = SolverOptions(scheme=args.scheme, patches=patches, jacobian=args.jacobian, device=local,
                          reorder=args.reorder, **extra)
     decomp = world > 1 and not args.replicas
+    decomp_note = None
+    solver = None
     if decomp:
         from paper_2304_09485_b200.distributed import DistributedSolver
 
-        uid = [DistributedSolver.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        solver = DistributedSolver(mesh, opts, rank=rank, nranks=world, comm_id=uid[0])
-    else:
+        try:
+            uid = [DistributedSolver.unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            solver = DistributedSolver(mesh, opts, rank=rank, nranks=world, comm_id=uid[0])
+            ok = 1
+        except Exception as exc:  # every rank decides together below
+            decomp_note = f"decomposition unavailable ({exc}); ran independent replicas"
+            print(decomp_note, file=sys.stderr, flush=True)
+            ok = 0
+        import torch
+
+        flag = torch.tensor([ok], dtype=torch.int32, device=f"cuda:{local}")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            decomp = False
+            solver = None
+    if solver is None:
         solver = Solver(mesh, opts)
     t_setup = time.perf_counter() - t0
     nc = mesh.ncells
@@ -570,6 +585,7 @@ def run_ours(args):
                    "residual_evals_per_step": evals / args.steps,
                    "parallelism": ("replicas" if not decomp else f"cell-partitioned RCB x{world}, NCCL halo + allreduce")
                    if world > 1 else "single",
+                   "decomposition_note": decomp_note,
                    "l2": "inputs > L2 (operators %.1f GB)" % (sum(model_bytes[k] for k in ("recon",)) / 1e9),
                    "setup_s": round(t_setup, 2), "mesh_s": round(t_mesh, 2)},
         "e2e": e2e,
