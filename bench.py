@@ -384,6 +384,33 @@ def converge_leg(args, threshold=1e-10, max_steps=12000):
             "cells": mesh.ncells}
 
 
+def paper_table_leg(steps=100, warmup=5):
+    """The paper's only published performance table:
+    computational time per 100 implicit steps of the Re 1000 lid-driven cavity
+    on 48,000 tets, non-compact (weno_gmres) and compact (hweno_gmres) GMRES;
+    Quadro RTX 8000: 30 s and 32 s.  Same physics here
+    (cases/cavity_re1000_full.ini) on the uniform 6*20^3 box (the paper graded
+    its wall layer), state resident in HBM, host wall clock around the loop."""
+    from paper_2304_09485_b200.stepping import SolutionField, Solver, SolverOptions
+
+    out = {"case": "lid-driven cavity Re 1000, 6*20^3 = 48,000 tets (cases/cavity_re1000_full.ini), CFL 2",
+           "published": {"weno_gmres": 30.0, "hweno_gmres": 32.0, "unit": "s per 100 steps",
+                         "hardware": "Quadro RTX 8000 (PAPER.md:1195-1196)"}}
+    for scheme in ("weno_gmres", "hweno_gmres"):
+        mesh, patches, q, g, extra = cavity_problem(20, scheme.startswith("hweno"), re=1000.0)
+        s = Solver(mesh, SolverOptions(scheme=scheme, patches=patches, jacobian="roe", **extra))
+        s.upload(SolutionField(q, g))
+        for _ in range(warmup):
+            s.advance_resident()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            s.advance_resident()
+        el = time.perf_counter() - t0
+        out[scheme] = {"seconds_per_100_steps": 100.0 * el / steps, "ms_per_step": 1000.0 * el / steps,
+                       "speedup_vs_paper_gpu": out["published"][scheme] / (100.0 * el / steps)}
+    return out
+
+
 def cpu_step_seconds_cavity(args, steps=3):
     """Oracle seconds per step on the convergence-leg case (1 core)."""
     from oracle.solver import OracleSolver
@@ -568,6 +595,13 @@ def run_ours(args):
                 roof["traffic_source"] = f"{tf.relative_to(ROOT)} ({ent['kernel']})"
                 break
 
+    paper = None
+    if not args.no_converge and world == 1:
+        try:
+            paper = paper_table_leg()
+        except Exception as exc:
+            paper = {"error": str(exc)}
+
     cb = None
     if not args.no_cpu_baseline:
         try:
@@ -601,6 +635,7 @@ def run_ours(args):
         "step_info": {"res_rho_l1": infos[-1].res_rho_l1, "res_l2": infos[-1].res_l2,
                       "solver_cycles": infos[-1].solver_cycles},
         "time_to_threshold": conv,
+        "paper_table": paper,
         "paper_gpu_derived": {"value": 1.60e5, "unit": UNIT, "note": "Quadro RTX 8000, cavity 48k tets (BASELINE.md)"},
     }
     print(json.dumps(line), flush=True)
