@@ -577,6 +577,9 @@ __global__ void k_assemble(int64_t nc, const int* __restrict__ cfq_start, const 
   double r[5] = {0, 0, 0, 0, 0};
   double g[3][5] = {};
   const bool wantg = grad_new != nullptr;
+  // unrolled so several entries' index and record loads are in flight at
+  // once (the list walk is a dependent index -> record chain per entry)
+#pragma unroll 4
   for (int e = cfq_start[c]; e < cfq_start[c + 1]; ++e) {
     const int64_t i = cfq[e] >> 1;
     const bool is_nbr = cfq[e] & 1;
