@@ -97,6 +97,19 @@ typedef struct GksMeshDesc {
 } GksMeshDesc;
 
 /* ------------------------------------------------------------------ */
+/* Native ugks-mesh reader (host, no GPU needed).  Replaces the per-line */
+/* parse of load_mesh (mesh/fileio.py:42-103); returns GKS_ERR_BAD_ARG  */
+/* on any grammar violation (the Python caller then re-parses to raise  */
+/* the reference's exact MeshError).  Patch faces come back (nf, 4),    */
+/* padded with -1, with their widths (3 or 4).                          */
+typedef struct GksUgks GksUgks;
+int gks_ugks_read(const char* path, GksUgks** out);
+int gks_ugks_sizes(const GksUgks* m, int64_t* nnodes, int64_t* ntets, int64_t* nhexes, int64_t* npatches);
+int gks_ugks_patch(const GksUgks* m, int64_t k, char* name, int64_t cap, int64_t* nfaces);
+int gks_ugks_copy(const GksUgks* m, double* nodes, int64_t* tets, int64_t* hexes, int64_t* faces, int8_t* widths);
+void gks_ugks_free(GksUgks* m);
+
+/* ------------------------------------------------------------------ */
 /* Native setup (host, no GPU needed): stencil selection and the        */
 /* reconstruction operators.  Replaces mesh.build_stencils              */
 /* (stencils.py:119-192), ReconGeometry (recon.py:104-164),             */

@@ -201,6 +201,11 @@ SIGNATURES = [
     ("gks_state_download", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
     ("gks_advance_resident", C.c_int, [C.c_void_p, C.c_void_p]),
     ("gks_set_graph", C.c_int, [C.c_void_p, C.c_int]),
+    ("gks_ugks_read", C.c_int, [C.c_char_p, C.c_void_p]),
+    ("gks_ugks_sizes", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("gks_ugks_patch", C.c_int, [C.c_void_p, C.c_int64, C.c_char_p, C.c_int64, C.c_void_p]),
+    ("gks_ugks_copy", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("gks_ugks_free", None, [C.c_void_p]),
     ("gks_event_record", C.c_int, [C.c_void_p, C.c_int]),
     ("gks_event_elapsed", C.c_int, [C.c_void_p, C.c_int, C.c_int, c_double_p]),
     ("gks_handle_info", C.c_int64, [C.c_void_p, C.c_int]),

@@ -562,8 +562,62 @@ MAGIC = "ugks-mesh"
 VERSION = 1
 
 
+def _load_native(path):
+    """Fast path: the C++ reader in libgks.so (gks_meshio.cpp).  Returns the
+    construction data, or None when the native reader rejects the file (the
+    reference-shaped parser below then runs and raises its exact error)."""
+    import ctypes as C
+
+    from . import _native as N
+
+    lib = N.load()
+    h = C.c_void_p()
+    if lib.gks_ugks_read(str(path).encode(), C.byref(h)) != 0:
+        return None
+    try:
+        sz = [C.c_int64() for _ in range(4)]
+        N.check(lib.gks_ugks_sizes(h, *[C.byref(x) for x in sz]))
+        nn, nt, nh, npatch = (int(x.value) for x in sz)
+        names, counts = [], []
+        buf = C.create_string_buffer(4096)
+        for k in range(npatch):
+            nf = C.c_int64()
+            N.check(lib.gks_ugks_patch(h, k, buf, len(buf), C.byref(nf)))
+            names.append(buf.value.decode("ascii"))
+            counts.append(int(nf.value))
+        total = sum(counts)
+        nodes = np.empty((nn, 3))
+        tets = np.empty((nt, 4), dtype=np.int64)
+        hexes = np.empty((nh, 8), dtype=np.int64)
+        faces = np.empty((max(total, 1), 4), dtype=np.int64)
+        widths = np.empty(max(total, 1), dtype=np.int8)
+        N.check(lib.gks_ugks_copy(h, N.dptr(nodes), N.iptr(tets), N.iptr(hexes), N.iptr(faces),
+                                  widths.ctypes.data_as(C.c_void_p)))
+    finally:
+        lib.gks_ugks_free(h)
+    patch_faces = {}
+    pos = 0
+    for name, nf in zip(names, counts):
+        f, w = faces[pos: pos + nf], widths[pos: pos + nf]
+        pos += nf
+        if nf and np.all(w == w[0]):
+            patch_faces[name] = np.ascontiguousarray(f[:, : int(w[0])])
+        else:
+            patch_faces[name] = [tuple(int(x) for x in r[: int(k)]) for r, k in zip(f, w)]
+    return nodes, tets, hexes, patch_faces
+
+
 def load_mesh(path, periodic_pairs=()):
-    """Parse, build and validate a ugks-mesh ASCII file (fileio.py:42-103)."""
+    """Parse, build and validate a ugks-mesh ASCII file (fileio.py:42-103).
+
+    The file is read by the native parser (gks_ugks_read); anything it
+    rejects is re-parsed here, line by line, to raise the reference's error."""
+    fast = _load_native(path)
+    if fast is not None:
+        nodes, tets, hexes, patch_faces = fast
+        mesh = Mesh.build(nodes, tets, hexes, patch_faces, periodic_pairs=periodic_pairs)
+        mesh.validate()
+        return mesh
     with open(path, "r", encoding="ascii") as fh:
         raw = [ln.split("#", 1)[0].strip() for ln in fh.read().splitlines()]
     lines = [ln for ln in raw if ln]
