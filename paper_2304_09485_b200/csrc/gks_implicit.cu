@@ -387,34 +387,46 @@ __global__ void k_status_init(int* st, int n) {
 
 __global__ void k_gm_cycle_begin(GmresDev* g) { g->notdone = !g->done; }
 
+// cycle start: thread 0 decides (krylov.py:71-80), then the block clears the
+// Hessenberg matrix and the rotated right-hand side (one thread doing 4k
+// dependent stores was 11 us per cycle)
 __global__ void k_gm_cycle_start(GmresDev* g, int cyc) {
-  if (!g->notdone) { g->active = 0; return; }
-  g->matvecs += 1;
-  const double beta = sqrt(g->beta2);
-  g->beta = beta;
-  if (!g->target_set) {
-    g->target = g->rtol * beta + g->atol;
-    g->target_set = 1;
+  __shared__ int go;
+  if (threadIdx.x == 0) {
+    go = 0;
+    if (!g->notdone) {
+      g->active = 0;
+    } else {
+      g->matvecs += 1;
+      const double beta = sqrt(g->beta2);
+      g->beta = beta;
+      if (!g->target_set) {
+        g->target = g->rtol * beta + g->atol;
+        g->target_set = 1;
+      }
+      g->j_used = 0;
+      g->breakdown = 0;
+      g->norms[cyc * (GM_MMAX + 1)] = beta;
+      g->nnorms[cyc] = 1;
+      if (beta == 0.0 || beta <= g->target) {
+        g->done = 1;
+        g->active = 0;
+      } else if (!isfinite(beta)) {
+        g->err = GKS_ERR_NONFINITE;
+        g->done = 1;
+        g->active = 0;
+      } else {
+        g->active = 1;
+        go = 1;
+      }
+    }
   }
-  g->j_used = 0;
-  g->breakdown = 0;
-  g->norms[cyc * (GM_MMAX + 1)] = beta;
-  g->nnorms[cyc] = 1;
-  if (beta == 0.0 || beta <= g->target) {
-    g->done = 1;
-    g->active = 0;
-    return;
-  }
-  if (!isfinite(beta)) {
-    g->err = GKS_ERR_NONFINITE;
-    g->done = 1;
-    g->active = 0;
-    return;
-  }
-  g->active = 1;
-  for (int i = 0; i < (GM_MMAX + 1) * GM_MMAX; ++i) g->h[i] = 0.0;
-  for (int i = 0; i <= GM_MMAX; ++i) g->gv[i] = 0.0;
-  g->gv[0] = beta;
+  __syncthreads();
+  if (!go) return;
+  for (int i = threadIdx.x; i < (GM_MMAX + 1) * GM_MMAX; i += blockDim.x) g->h[i] = 0.0;
+  for (int i = threadIdx.x; i <= GM_MMAX; i += blockDim.x) g->gv[i] = 0.0;
+  __syncthreads();
+  if (threadIdx.x == 0) g->gv[0] = g->beta;
 }
 
 // after the first MGS pass of column j: Hessenberg column, re-orthogonalisation test
@@ -430,13 +442,28 @@ __device__ __forceinline__ void gm_reorth_check(GmresDev* g, int j) {
 
 __global__ void k_gm_reorth_check(GmresDev* g, int j) { gm_reorth_check(g, j); }
 
-__device__ __forceinline__ void gm_givens(GmresDev* g, int j, int cyc) {
+// Givens update of column j (krylov.py:107-124).  The column, the stored
+// rotations and the right-hand side entries are read into registers before
+// anything is written back: through one GmresDev* every load would otherwise
+// wait for the previous store (a dependent L2 round trip per entry).
+// scratch: 3 (GM_MMAX + 1) doubles of shared memory (one thread uses it)
+__device__ __forceinline__ void gm_givens(GmresDev* g, int j, int cyc, double* scratch) {
   if (!g->active) return;
-  if (g->reorth) {
-    for (int i = 0; i <= j; ++i) GH(i, j) += g->corr[i];
-    GH(j + 1, j) = sqrt(g->hnext2);
+  double* hc = scratch;
+  double* cs = scratch + GM_MMAX + 1;
+  double* sn = scratch + 2 * (GM_MMAX + 1);
+  for (int i = 0; i <= j + 1; ++i) hc[i] = GH(i, j);
+  for (int i = 0; i < j; ++i) {
+    cs[i] = g->cs[i];
+    sn[i] = g->sn[i];
   }
-  if (!isfinite(GH(j + 1, j))) {
+  const double gj = g->gv[j];
+  if (g->reorth) {
+    for (int i = 0; i <= j; ++i) hc[i] += g->corr[i];
+    hc[j + 1] = sqrt(g->hnext2);
+  }
+  if (!isfinite(hc[j + 1])) {
+    if (g->reorth) GH(j + 1, j) = hc[j + 1];
     g->err = GKS_ERR_NONFINITE;
     g->done = 1;
     g->active = 0;
@@ -444,32 +471,40 @@ __device__ __forceinline__ void gm_givens(GmresDev* g, int j, int cyc) {
     return;
   }
   for (int i = 0; i < j; ++i) {
-    const double t = g->cs[i] * GH(i, j) + g->sn[i] * GH(i + 1, j);
-    GH(i + 1, j) = -g->sn[i] * GH(i, j) + g->cs[i] * GH(i + 1, j);
-    GH(i, j) = t;
+    const double t = cs[i] * hc[i] + sn[i] * hc[i + 1];
+    hc[i + 1] = -sn[i] * hc[i] + cs[i] * hc[i + 1];
+    hc[i] = t;
   }
-  const double denom = hypot(GH(j, j), GH(j + 1, j));
-  g->cs[j] = GH(j, j) / denom;
-  g->sn[j] = GH(j + 1, j) / denom;
-  GH(j, j) = denom;
-  g->gv[j + 1] = -g->sn[j] * g->gv[j];
-  g->gv[j] = g->cs[j] * g->gv[j];
+  const double denom = hypot(hc[j], hc[j + 1]);
+  const double c = hc[j] / denom;
+  const double sj = hc[j + 1] / denom;
+  hc[j] = denom;
+  for (int i = 0; i <= j + 1; ++i) GH(i, j) = hc[i];
+  g->cs[j] = c;
+  g->sn[j] = sj;
+  g->gv[j + 1] = -sj * gj;
+  g->gv[j] = c * gj;
   double* norms = g->norms + cyc * (GM_MMAX + 1);
-  const double last = fabs(g->gv[j + 1]);
-  norms[g->nnorms[cyc]++] = last;
+  const double last = fabs(-sj * gj);
+  const int nn = g->nnorms[cyc];
+  norms[nn] = last;
+  g->nnorms[cyc] = nn + 1;
   g->j_used = j + 1;
-  if (GH(j + 1, j) <= 1e-13 * g->wscale) {
+  if (hc[j + 1] <= 1e-13 * g->wscale) {
     g->breakdown = 1;
     g->breakdown_any = 1;
     g->active = 0;
   } else if (last <= fmax(1e-15 * norms[0], g->target)) {
     g->active = 0;
   } else {
-    g->hdiv = GH(j + 1, j);
+    g->hdiv = hc[j + 1];
   }
 }
 
-__global__ void k_gm_givens(GmresDev* g, int j, int cyc) { gm_givens(g, j, cyc); }
+__global__ void k_gm_givens(GmresDev* g, int j, int cyc) {
+  __shared__ double scratch[3 * (GM_MMAX + 1)];
+  gm_givens(g, j, cyc, scratch);
+}
 
 // Deterministic block sum (fixed shuffle tree per warp, then warp 0 over the
 // warp partials); every thread gets the result.
@@ -541,6 +576,7 @@ __global__ void __launch_bounds__(1024, 1) k_gm_arnoldi(int n, int64_t ld, doubl
                                                      const double* __restrict__ wg, GmresDev* g, int j, int cyc) {
   __shared__ double red[33];
   __shared__ double part[2];
+  __shared__ double scratch[3 * (GM_MMAX + 1)];
   int slot = 0;
   if (!__ldcg(&g->active)) return;
   const int rank = CL == 1 ? 0 : (int)cooperative_groups::this_cluster().block_rank();
@@ -617,7 +653,7 @@ __global__ void __launch_bounds__(1024, 1) k_gm_arnoldi(int n, int64_t ld, doubl
       if (!__ldcg(&g->reorth)) break;
     }
   }
-  if (lead) gm_givens(g, j, cyc);
+  if (lead) gm_givens(g, j, cyc, scratch);
   cluster_barrier<CL>();
   if (!__ldcg(&g->active)) return;
   const double d = __ldcg(&g->hdiv);
@@ -630,15 +666,20 @@ __global__ void __launch_bounds__(1024, 1) k_gm_arnoldi(int n, int64_t ld, doubl
 }
 
 // back substitution (krylov.py:128-131) and cycle bookkeeping
+// back substitution (krylov.py:128-131) on a register copy of the
+// triangle (independent loads first, no store-to-load round trips)
 __global__ void k_gm_cycle_end(GmresDev* g, int cyc) {
   g->ny = 0;
   if (!g->notdone) return;
   const int ju = g->err ? 0 : g->j_used;
+  __shared__ double y[GM_MMAX], gv[GM_MMAX];
+  for (int i = 0; i < ju; ++i) gv[i] = g->gv[i];
   for (int i = ju - 1; i >= 0; --i) {
     double dot = 0.0;
-    for (int k = i + 1; k < ju; ++k) dot += GH(i, k) * g->y[k];
-    g->y[i] = (g->gv[i] - dot) / GH(i, i);
+    for (int k = i + 1; k < ju; ++k) dot += GH(i, k) * y[k];
+    y[i] = (gv[i] - dot) / GH(i, i);
   }
+  for (int i = 0; i < ju; ++i) g->y[i] = y[i];
   g->ny = ju;
   g->ncycles = cyc + 1;
   const double last = g->norms[cyc * (GM_MMAX + 1) + g->nnorms[cyc] - 1];
@@ -918,8 +959,23 @@ static int arnoldi_attr(size_t smem) {
   return ok ? CL : 0;
 }
 
+// Preferred slice per CTA (GKS_ARNOLDI_SLICE).  More CTAs spread the vector
+// passes over more SMs, at one cluster barrier per sum; measured, the
+// fewest CTAs win (3k-cell cavity: 1 CTA 1.62 ms/step, 4 CTAs 1.89).
+static int64_t arnoldi_target_slice() {
+  static const int64_t v = [] {
+    const char* e = getenv("GKS_ARNOLDI_SLICE");
+    const int64_t x = e ? atoll(e) : kArnoldiSlice;
+    return std::min<int64_t>(std::max<int64_t>(x, 1024), kArnoldiSlice);
+  }();
+  return v;
+}
+
 static int arnoldi_cluster(int64_t n) {
-  const int64_t need = (n + kArnoldiSlice - 1) / kArnoldiSlice;
+  if (n > 16 * (int64_t)kArnoldiSlice) return 0;
+  const int64_t slice = arnoldi_target_slice();
+  const int64_t need = std::max<int64_t>(std::min<int64_t>((n + slice - 1) / slice, 16),
+                                         (n + kArnoldiSlice - 1) / kArnoldiSlice);
   if (need <= 1) return arnoldi_attr<1>(0);
   if (need <= 2) return arnoldi_attr<2>(0);
   if (need <= 4) return arnoldi_attr<4>(0);
@@ -1014,7 +1070,7 @@ int gmres_enqueue(BlockSys* A, const double* b_dev, double* x_dev, const GmresPa
     GKS_LAUNCH(KC_VEC, k_sub, grid, RB_THREADS, 0, s, n, W->r, b_dev, W->t, notdone);
     bs_jacobi(A, W->r, W->z, W->w, kmax, notdone);
     dot2(A, n, W->z, W->z, nullptr, nullptr, &g->beta2, nullptr, notdone);
-    GKS_LAUNCH(KC_SCALAR, k_gm_cycle_start, 1, 1, 0, s, g, cyc);
+    GKS_LAUNCH(KC_SCALAR, k_gm_cycle_start, 1, 256, 0, s, g, cyc);
     GKS_LAUNCH(KC_VEC, k_div, grid, RB_THREADS, 0, s, n, W->V, W->z, &g->beta, act);
     for (int j = 0; j < m; ++j) {
       const double* vj = W->V + (int64_t)j * ld;
