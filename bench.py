@@ -288,7 +288,7 @@ def kernel_model(solver, compact):
 
 # -- CPU baseline (oracle) -------------------------------------------------------------
 
-def cpu_baseline(args, steps, label):
+def cpu_baseline(args, steps, label, warm=True):
     from oracle.solver import OracleSolver
     from paper_2304_09485_b200 import mesh as M
 
@@ -303,7 +303,8 @@ def cpu_baseline(args, steps, label):
     t0 = time.perf_counter()
     s = OracleSolver(mesh, scheme=args.scheme, patches=patches, jacobian=args.jacobian, **extra)
     setup = time.perf_counter() - t0
-    q, grad, info = s.advance(q, grad)  # warm-up
+    if warm:
+        q, grad, info = s.advance(q, grad)  # warm-up
     evals = 0
     t0 = time.perf_counter()
     for _ in range(steps):
@@ -322,7 +323,7 @@ def _reference_worker(payload):
     os.environ["OMP_NUM_THREADS"] = "1"
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     ns, steps = payload
-    return cpu_baseline(argparse.Namespace(**ns), steps, "reference arm")
+    return cpu_baseline(argparse.Namespace(**ns), steps, "reference arm", warm=False)
 
 
 def run_reference(args):
@@ -332,7 +333,9 @@ def run_reference(args):
     world, rank, local, dist = dist_init(args)
     if rank != 0:
         return 0
-    steps = max(1, min(args.steps, 5))
+    # numpy has nothing to warm up; one step per core keeps the arm to a few
+    # minutes when every core runs a sample (16-core GPU hosts: ~2 min)
+    steps = 1
     ncores = os.cpu_count() or 1
     nproc = max(1, min(ncores, 32))
     ns = dict(vars(args))
@@ -350,7 +353,7 @@ def run_reference(args):
               sample=f"{nproc} concurrent single-threaded samples (host has {ncores} cores), each: {cb['sample']}")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-        "steps": steps, "warmup": 1, "ms_per_step": secs * 1000.0 / steps, "higher_is_better": True,
+        "steps": steps, "warmup": 0, "ms_per_step": secs * 1000.0 / steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.workload.upper()} (bounded CPU sample, lattice n={args.cpu_n})",
                    "scheme": args.scheme, "jacobian": args.jacobian},
