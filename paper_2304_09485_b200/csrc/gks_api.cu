@@ -702,12 +702,15 @@ void dot2(BlockSys* A, int64_t n, const double* a, const double* b, const double
 
 // J v (mode 0: Frechet derivative; mode 1: V/dt v - derivative) with the step
 // residual H->res as the base point; q_base = H->q, dt = H->dt.
+// qq_cached: ||Q||^2 is already in red[1] (constant over one GMRES solve;
+// the same reduction, so sigma is bit-identical to recomputing it)
 static void frechet_apply(Handle* H, BlockSys* A, const double* v, double* out, int mode, const int* gate,
-                          const double* fixed_sigma) {
+                          const double* fixed_sigma, bool qq_cached = false) {
   const int64_t n = H->n_owned * 5;
   double* sig = &H->scal->sigma;
   if (!fixed_sigma) {
-    dot2(A, n, v, v, H->q, H->q, &H->scal->red[0], &H->scal->red[1], gate);
+    if (qq_cached) dot2(A, n, v, v, nullptr, nullptr, &H->scal->red[0], nullptr, gate);
+    else dot2(A, n, v, v, H->q, H->q, &H->scal->red[0], &H->scal->red[1], gate);
     GKS_LAUNCH(KC_SCALAR, k_sigma, 1, 1, 0, H->stream, H->scal->red, sig, nullptr);
   } else {
     sig = const_cast<double*>(fixed_sigma);
@@ -745,8 +748,12 @@ static int enqueue_attempt(GksHandle* G) {
   P.kmax = H->jacobi_sweeps;
   P.rtol = H->gmres_rtol;
   MatvecFn mf = [H, A](const double* v, double* out, const int* gate) {
-    frechet_apply(H, A, v, out, 1, gate, nullptr);
+    frechet_apply(H, A, v, out, 1, gate, nullptr, true);
   };
+  if (H->jac_mode == GKS_JAC_FRECHET) {
+    const int64_t n = H->n_owned * 5;
+    dot2(A, n, H->q, H->q, nullptr, nullptr, &H->scal->red[1], nullptr, nullptr);
+  }
   TRY(gmres_enqueue(A, H->res, H->dq, P, H->jac_mode == GKS_JAC_FRECHET ? &mf : nullptr, false));
   GKS_LAUNCH(KC_UPDATE, k_update, blocks_for(H->n_owned, 256), 256, 0, H->stream, H->n_owned, H->q, H->dq, H->q_new,
              H->bad);
