@@ -24,7 +24,7 @@ from paper_2304_09485_b200.stepping import SolutionField, Solver, SolverOptions 
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("--case", default="sphere", choices=("sphere", "cavity"))
+    p.add_argument("--case", default="sphere", choices=("sphere", "cavity", "c3", "c4"))
     p.add_argument("--n", type=int, default=4)
     p.add_argument("--re", type=float, default=100.0)
     p.add_argument("--max-steps", type=int, default=4000)
@@ -40,6 +40,14 @@ def main():
     if a.case == "sphere":
         mesh = c2_mesh(a.n, MG)
         patches, q, g = c2_problem(mesh, compact)
+    elif a.case in ("c3", "c4"):
+        # the bench's C3 (viscous sphere Re 118, linear weights) / C4 (swept wing) physics
+        from bench import other_problem
+
+        mesh = MG.generate_sphere_mesh(a.n) if a.case == "c3" else MG.generate_swept_wing_mesh(a.n)
+        patches, q, g, extra = other_problem(a.case, mesh, compact)
+        if "weights" in extra:
+            a.weights = extra.pop("weights")
     else:
         mesh, patches, q, g, extra = cavity_problem(a.n, compact, a.re)
     t0 = time.perf_counter()
@@ -51,8 +59,13 @@ def main():
     t0 = time.perf_counter()
     t_abs = t_rel = None
     s_abs = s_rel = None
+    error = None
     for k in range(1, a.max_steps + 1):
-        info = s.advance_resident()
+        try:
+            info = s.advance_resident()
+        except Exception as exc:  # report how far the run got
+            error = f"step {k}: {exc}"
+            break
         hist.append(info.res_rho_l1)
         t = time.perf_counter() - t0
         if t_abs is None and info.res_rho_l1 < a.threshold and info.res_l2 < 1e4 * a.threshold:
@@ -62,7 +75,10 @@ def main():
         if t_abs is not None and t_rel is not None:
             break
     el = time.perf_counter() - t0
+    if not hist:
+        hist = [float("nan")]
     print(json.dumps({"case": a.case, "n": a.n, "cells": mesh.ncells, "scheme": a.scheme, "jacobian": a.jacobian,
+                      "error": error,
                       "cfl": a.cfl, "weights": a.weights, "setup_s": round(t_setup, 2),
                       "steps_abs": s_abs, "seconds_abs": t_abs, "steps_rel10": s_rel, "seconds_rel10": t_rel,
                       "steps_run": len(hist), "seconds_run": el, "ms_per_step": 1000 * el / len(hist),
