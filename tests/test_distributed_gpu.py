@@ -63,20 +63,26 @@ def test_rank_local_residual_bitwise(scheme):
             assert np.array_equal(g, gnew[own])
 
 
-def test_one_rank_nccl_communicator_matches(monkeypatch):
+@pytest.mark.parametrize("scheme,jac", [("weno_gmres", "roe"), ("weno_gmres", "frechet"), ("hweno_gmres", "roe")])
+def test_one_rank_nccl_communicator_matches(monkeypatch, scheme, jac):
+    import dataclasses
+
     from paper_2304_09485_b200.distributed import DistributedSolver
     from paper_2304_09485_b200.stepping import SolutionField, Solver
 
     # communicator handles reduce through NCCL between the MGS kernels; hold
     # the communicator-free reference to the same multi-block chain (not the
-    # fused single-rank Arnoldi kernel) so the comparison stays bitwise
+    # fused single-rank Arnoldi kernel) so the comparison stays bitwise.
+    # Three steps: the second and third replay the captured step graph (with
+    # the NCCL calls inside it).
     monkeypatch.setenv("GKS_GMRES_SMALL", "0")
-    mesh, opts, q, grad = setup_case("weno_gmres")
+    mesh, opts, q, grad = setup_case(scheme)
+    opts = dataclasses.replace(opts, jacobian=jac)
     ref = Solver(mesh, opts)
-    ref.upload(SolutionField(q))
+    ref.upload(SolutionField(q, grad))
     ds = DistributedSolver(mesh, opts, rank=0, nranks=1, comm_id=DistributedSolver.unique_id())
-    ds.upload(SolutionField(q))
-    for _ in range(2):
+    ds.upload(SolutionField(q, grad))
+    for _ in range(3):
         a = ref.advance_resident()
         b = ds.advance_resident()
         assert a.res_rho_l1 == b.res_rho_l1 and a.res_l2 == b.res_l2 and a.solver_cycles == b.solver_cycles
