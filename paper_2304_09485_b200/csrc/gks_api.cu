@@ -858,8 +858,22 @@ static int advance_device(GksHandle* G, GksStepInfo* info) {
     set_error("scheme 'weno_lusgs' (sequential LUSGS sweep) is not part of the device path");
     return GKS_ERR_BAD_ARG;
   }
-  if (graph_enabled(G)) TRY(run_step_graph(G));
-  else TRY(enqueue_step(G));
+  bool launched = false;
+  if (graph_enabled(G)) {
+    if (run_step_graph(G) == GKS_OK) {
+      launched = true;
+    } else {
+      // capture/instantiation refused (nothing of the step has run): step
+      // uncaptured from now on rather than fail
+      cudaGetLastError();
+      G->graph = 0;
+      for (StepGraph& g : G->graphs) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        g = StepGraph();
+      }
+    }
+  }
+  if (!launched) TRY(enqueue_step(G));
   int retried = 0;
   for (int attempt = 0; attempt < 2; ++attempt) {
     GmresHost gh;
