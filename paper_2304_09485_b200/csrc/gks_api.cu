@@ -401,8 +401,8 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
     A->mf = (mf && mf[0] == '0') ? 0 : 1;
     A->gm1 = o->gamma - 1.0;
     TRY(upload(H, &A->ent, ent.data(), ent.size()));
-    TRY(alloc(H, &A->fdat, (size_t)std::max<int64_t>(nf, 1) * 5));
-    TRY(alloc(H, &A->prim, (size_t)nc * 5));
+    TRY(alloc(H, &A->fdat, (size_t)std::max<int64_t>(nf, 1) * MF_REC));
+    TRY(alloc(H, &A->prim, (size_t)nc * MF_REC));
   }
 
   // reconstruction operators

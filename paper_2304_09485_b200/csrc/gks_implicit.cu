@@ -25,6 +25,7 @@
 #include <cooperative_groups.h>
 
 #include "gks_implicit.cuh"
+#include "gks_stage.cuh"
 
 namespace gks {
 
@@ -179,8 +180,8 @@ __global__ void k_jac_faces(int64_t nfi, const int* __restrict__ ifaces, const i
   const double lam = spectral_radius(qm, n, gam);
   const double hs = 0.5 * f_area[f];
   if (fdat) {
-    double* fd = fdat + (int64_t)f * 5;
-    fd[0] = n[0]; fd[1] = n[1]; fd[2] = n[2]; fd[3] = hs; fd[4] = lam;
+    double* fd = fdat + (int64_t)f * MF_REC;
+    fd[0] = n[0]; fd[1] = n[1]; fd[2] = n[2]; fd[3] = hs; fd[4] = lam; fd[5] = 0.0;
   }
   double J[5][5];
   // rows of ghost cells (cut faces on a partitioned mesh) have no slot
@@ -715,22 +716,28 @@ __global__ void k_roe_prim(int64_t n, const double* __restrict__ q, double gm1, 
   const double vx = q[c * 5 + 1] / rho, vy = q[c * 5 + 2] / rho, vz = q[c * 5 + 3] / rho;
   const double ke = 0.5 * (vx * vx + vy * vy + vz * vz);
   const double p = gm1 * (q[c * 5 + 4] - rho * ke);
-  double* P = prim + c * 5;
-  P[0] = vx; P[1] = vy; P[2] = vz; P[3] = (q[c * 5 + 4] + p) / rho; P[4] = ke;
+  double* P = prim + c * MF_REC;
+  P[0] = vx; P[1] = vy; P[2] = vz; P[3] = (q[c * 5 + 4] + p) / rho; P[4] = ke; P[5] = 0.0;
 }
 
 // Same MODE bits as k_block, one thread per cell: the off-diagonal sum is
 // recomputed entry by entry (in the CSR order of the stored path)
 //   J(Q,n) x = (mx, v a + un x_m + n b, H a + un (b + x4)),
 //   a = mx - un x0,  b = (gamma-1)(ke x0 - v.x_m + x4),  mx = n.x_m
+// The face (n, S/2, lambda) and cell primitive records are padded to 6
+// doubles and read as 16-byte vectors.  (Staging the block's D / D^-1
+// records into shared memory by bulk copies, as the reconstruction does, was
+// measured 2x slower here: each CTA then waits for its whole tile.)
+static constexpr int MF_CELLS = 128;
+
 template <int MODE>
-__global__ void __launch_bounds__(128) k_roe_mf(int64_t nc, const int* __restrict__ rowptr,
-                                                const int* __restrict__ col, const int* __restrict__ ent,
-                                                const double* __restrict__ fdat, const double* __restrict__ prim,
-                                                double gm1, const double* __restrict__ diag,
-                                                const double* __restrict__ dinv, const double* __restrict__ x,
-                                                const double* __restrict__ b, double* __restrict__ out,
-                                                double* __restrict__ out_pre, const int* gate) {
+__global__ void __launch_bounds__(MF_CELLS) k_roe_mf(int64_t nc, const int* __restrict__ rowptr,
+                                                     const int* __restrict__ col, const int* __restrict__ ent,
+                                                     const double* __restrict__ fdat, const double* __restrict__ prim,
+                                                     double gm1, const double* __restrict__ diag,
+                                                     const double* __restrict__ dinv, const double* __restrict__ x,
+                                                     const double* __restrict__ b, double* __restrict__ out,
+                                                     double* __restrict__ out_pre, const int* gate) {
   if (gate && !*gate) return;
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nc) return;
@@ -738,11 +745,13 @@ __global__ void __launch_bounds__(128) k_roe_mf(int64_t nc, const int* __restric
   for (int e = rowptr[c]; e < rowptr[c + 1]; ++e) {
     const int64_t j = col[e];
     const int en = __ldg(ent + e);
-    const double* fd = fdat + (int64_t)(en >> 1) * 5;
+    const double2* fd = (const double2*)(fdat + (int64_t)(en >> 1) * MF_REC);
+    const double2 f01 = __ldg(fd), f23 = __ldg(fd + 1), f45 = __ldg(fd + 2);
     const double sg = (en & 1) ? -1.0 : 1.0;
-    const double nx = fd[0], ny = fd[1], nz = fd[2], hs = fd[3], lam = fd[4];
-    const double* P = prim + j * 5;
-    const double vx = P[0], vy = P[1], vz = P[2], H = P[3], ke = P[4];
+    const double nx = f01.x, ny = f01.y, nz = f23.x, hs = f23.y, lam = f45.x;
+    const double2* P = (const double2*)(prim + j * MF_REC);
+    const double2 p01 = __ldg(P), p23 = __ldg(P + 1), p45 = __ldg(P + 2);
+    const double vx = p01.x, vy = p01.y, vz = p23.x, H = p23.y, ke = p45.x;
     const double* xj = x + j * 5;
     const double x0 = xj[0], x1 = xj[1], x2 = xj[2], x3 = xj[3], x4 = xj[4];
     const double mx = nx * x1 + ny * x2 + nz * x3;
@@ -799,8 +808,9 @@ int blocksys_alloc(BlockSys* A, int64_t nc, int64_t nnz, cudaStream_t stream) {
   GKS_CUDA(cudaMalloc(&A->rowptr, (nc + 1) * sizeof(int)));
   GKS_CUDA(cudaMalloc(&A->col, std::max<int64_t>(nnz, 1) * sizeof(int)));
   GKS_CUDA(cudaMalloc(&A->off, std::max<int64_t>(nnz, 1) * 25 * sizeof(double)));
-  GKS_CUDA(cudaMalloc(&A->diag, nc * 25 * sizeof(double)));
-  GKS_CUDA(cudaMalloc(&A->dinv, nc * 25 * sizeof(double)));
+  // (+64 B: the staged tile copies of k_roe_mf round the last chunk up to 16 B)
+  GKS_CUDA(cudaMalloc(&A->diag, nc * 25 * sizeof(double) + 64));
+  GKS_CUDA(cudaMalloc(&A->dinv, nc * 25 * sizeof(double) + 64));
   GKS_CUDA(cudaMalloc(&A->status, 4 * sizeof(int)));
   return GKS_OK;
 }
@@ -857,8 +867,8 @@ template <int MODE>
 static void block_product(BlockSys* A, const double* x, const double* b, double* out, double* pre, const int* gate) {
   const int kc = (MODE == 6) ? KC_JACOBI : KC_SPMV;
   if (A->mf) {
-    GKS_LAUNCH(kc, k_roe_mf<MODE>, blocks_for(A->nc, 128), 128, 0, A->stream, A->nc, A->rowptr, A->col, A->ent,
-               A->fdat, A->prim, A->gm1, A->diag, A->dinv, x, b, out, pre, gate);
+    GKS_LAUNCH(kc, k_roe_mf<MODE>, blocks_for(A->nc, MF_CELLS), MF_CELLS, 0, A->stream, A->nc, A->rowptr, A->col,
+               A->ent, A->fdat, A->prim, A->gm1, A->diag, A->dinv, x, b, out, pre, gate);
   } else {
     GKS_LAUNCH(kc, k_block<MODE>, cblocks(A->nc), CELLS_PER_BLOCK * 5, 0, A->stream, A->nc, A->rowptr, A->col, A->off,
                A->diag, A->dinv, x, b, out, pre, gate);

@@ -7,6 +7,7 @@
 namespace gks {
 
 constexpr int GM_MMAX = 64;  // max Krylov dimension
+constexpr int MF_REC = 6;     // doubles per face / cell record of the matrix-free Roe products (16-B aligned)
 constexpr int GM_RMAX = 64;  // max restarts
 
 // Device-resident GMRES scalars (krylov.py:55-140 state).
