@@ -919,6 +919,21 @@ static int advance_device(GksHandle* G, GksStepInfo* info) {
 
 }  // namespace gks
 
+// Diagonal blocks live on the device in block-SoA order (entry k of every
+// cell contiguous: [k * nc + c]) so the one-thread-per-cell products read
+// them coalesced; the C ABI exchanges the reference's (nc, 5, 5) layout.
+static std::vector<double> blocks_to_soa(const double* aos, int64_t nc) {
+  std::vector<double> v((size_t)nc * 25);
+  for (int64_t c = 0; c < nc; ++c)
+    for (int k = 0; k < 25; ++k) v[(size_t)k * nc + c] = aos[c * 25 + k];
+  return v;
+}
+
+static void blocks_from_soa(const std::vector<double>& soa, int64_t nc, double* aos) {
+  for (int64_t c = 0; c < nc; ++c)
+    for (int k = 0; k < 25; ++k) aos[c * 25 + k] = soa[(size_t)k * nc + c];
+}
+
 static int bs_check_size(GksBlockSystem* a) {
   if (!a) {
     set_error("null block system");
@@ -963,7 +978,10 @@ int gks_blocksys_create(int64_t nc, int64_t nnz, const double* diag, const doubl
     GKS_CUDA(cudaMemcpy(a->sys.col, cl.data(), nnz * sizeof(int), cudaMemcpyHostToDevice));
     GKS_CUDA(cudaMemcpy(a->sys.off, off, nnz * 25 * sizeof(double), cudaMemcpyHostToDevice));
   }
-  GKS_CUDA(cudaMemcpy(a->sys.diag, diag, nc * 25 * sizeof(double), cudaMemcpyHostToDevice));
+  {
+    const std::vector<double> d = blocks_to_soa(diag, nc);
+    GKS_CUDA(cudaMemcpy(a->sys.diag, d.data(), nc * 25 * sizeof(double), cudaMemcpyHostToDevice));
+  }
   TRY(blocksys_invert_diag(&a->sys));
   a->owned = true;
   *out = a;
@@ -986,7 +1004,11 @@ int gks_blocksys_export(GksBlockSystem* a, double* diag, double* off, int64_t* o
   TRY(bs_check_size(a));
   BlockSys* A = &a->sys;
   GKS_CUDA(cudaStreamSynchronize(A->stream));
-  if (diag) GKS_CUDA(cudaMemcpy(diag, A->diag, A->nc * 25 * sizeof(double), cudaMemcpyDeviceToHost));
+  if (diag) {
+    std::vector<double> d((size_t)A->nc * 25);
+    GKS_CUDA(cudaMemcpy(d.data(), A->diag, d.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    blocks_from_soa(d, A->nc, diag);
+  }
   if (off && A->nnz) GKS_CUDA(cudaMemcpy(off, A->off, A->nnz * 25 * sizeof(double), cudaMemcpyDeviceToHost));
   std::vector<int> rp(A->nc + 1), cl(std::max<int64_t>(A->nnz, 1));
   GKS_CUDA(cudaMemcpy(rp.data(), A->rowptr, (A->nc + 1) * sizeof(int), cudaMemcpyDeviceToHost));
@@ -1022,7 +1044,11 @@ int gks_blocksys_diag_inverses(GksBlockSystem* a, double* out) {
   TRY(bs_check_size(a));
   BlockSys* A = &a->sys;
   GKS_CUDA(cudaStreamSynchronize(A->stream));
-  GKS_CUDA(cudaMemcpy(out, A->dinv, A->nc * 25 * sizeof(double), cudaMemcpyDeviceToHost));
+  {
+    std::vector<double> d((size_t)A->nc * 25);
+    GKS_CUDA(cudaMemcpy(d.data(), A->dinv, d.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    blocks_from_soa(d, A->nc, out);
+  }
   return GKS_OK;
 }
 

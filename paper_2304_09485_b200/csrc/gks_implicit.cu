@@ -281,25 +281,25 @@ __global__ void k_jac_diag(int64_t nc, const int* __restrict__ cjd_start, const 
       for (int j = 0; j < 5; ++j) D[i * 5 + j] += hs * ((side ? -J[i][j] : J[i][j]) + (i == j ? lam : 0.0));
     (void)sg;
   }
-  for (int i = 0; i < 25; ++i) diag[c * 25 + i] = D[i];
+  for (int i = 0; i < 25; ++i) diag[(size_t)i * nc + c] = D[i];
   double X[25];
   if (!inv5(D, X)) {
     raise_dev(status, GKS_ERR_SINGULAR, (int)c);
     for (int i = 0; i < 25; ++i) X[i] = NAN;
   }
-  for (int i = 0; i < 25; ++i) dinv[c * 25 + i] = X[i];
+  for (int i = 0; i < 25; ++i) dinv[(size_t)i * nc + c] = X[i];
 }
 
 __global__ void k_dinv_only(int64_t nc, const double* __restrict__ diag, double* __restrict__ dinv, int* status) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nc) return;
   double D[25], X[25];
-  for (int i = 0; i < 25; ++i) D[i] = diag[c * 25 + i];
+  for (int i = 0; i < 25; ++i) D[i] = diag[(size_t)i * nc + c];
   if (!inv5(D, X)) {
     raise_dev(status, GKS_ERR_SINGULAR, (int)c);
     for (int i = 0; i < 25; ++i) X[i] = NAN;
   }
-  for (int i = 0; i < 25; ++i) dinv[c * 25 + i] = X[i];
+  for (int i = 0; i < 25; ++i) dinv[(size_t)i * nc + c] = X[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -331,9 +331,9 @@ __global__ void __launch_bounds__(CELLS_PER_BLOCK * 5) k_block(int64_t nc, const
       o += B[0] * xc[0] + B[1] * xc[1] + B[2] * xc[2] + B[3] * xc[3] + B[4] * xc[4];
     }
     if (MODE & 1) {
-      const double* Dr = diag + c * 25 + row * 5;
+      const double* Dr = diag + (size_t)row * 5 * nc + c;  // block-SoA: entry k at k * nc
       const double* xc = x + c * 5;
-      const double d = Dr[0] * xc[0] + Dr[1] * xc[1] + Dr[2] * xc[2] + Dr[3] * xc[3] + Dr[4] * xc[4];
+      const double d = Dr[0] * xc[0] + Dr[nc] * xc[1] + Dr[2 * nc] * xc[2] + Dr[3 * nc] * xc[3] + Dr[4 * nc] * xc[4];
       acc = d + o;
     } else {
       acc = o;
@@ -345,9 +345,9 @@ __global__ void __launch_bounds__(CELLS_PER_BLOCK * 5) k_block(int64_t nc, const
     sm[threadIdx.x] = acc;
     __syncthreads();
     if (c < nc) {
-      const double* Xr = dinv + c * 25 + row * 5;
+      const double* Xr = dinv + (size_t)row * 5 * nc + c;
       const double* t = sm + lc * 5;
-      out[c * 5 + row] = Xr[0] * t[0] + Xr[1] * t[1] + Xr[2] * t[2] + Xr[3] * t[3] + Xr[4] * t[4];
+      out[c * 5 + row] = Xr[0] * t[0] + Xr[nc] * t[1] + Xr[2 * nc] * t[2] + Xr[3 * nc] * t[3] + Xr[4 * nc] * t[4];
     }
   } else if (c < nc) {
     out[c * 5 + row] = acc;
@@ -362,9 +362,9 @@ __global__ void k_dinv_apply(int64_t nc, const double* __restrict__ dinv, const 
   if (t >= nc * 5) return;
   const int64_t c = t / 5;
   const int row = (int)(t - c * 5);
-  const double* Xr = dinv + c * 25 + row * 5;
+  const double* Xr = dinv + (size_t)row * 5 * nc + c;
   const double* bc = b + c * 5;
-  z[t] = Xr[0] * bc[0] + Xr[1] * bc[1] + Xr[2] * bc[2] + Xr[3] * bc[3] + Xr[4] * bc[4];
+  z[t] = Xr[0] * bc[0] + Xr[nc] * bc[1] + Xr[2 * nc] * bc[2] + Xr[3 * nc] * bc[3] + Xr[4 * nc] * bc[4];
 }
 
 // ---------------------------------------------------------------------------
@@ -770,9 +770,9 @@ __global__ void __launch_bounds__(MF_CELLS) k_roe_mf(int64_t nc, const int* __re
   for (int i = 0; i < 5; ++i) {
     double acc = o[i];
     if (MODE & 1) {
-      const double* Dr = diag + c * 25 + i * 5;
+      const double* Dr = diag + (size_t)i * 5 * nc + c;  // block-SoA: entry k at k * nc
       const double* xc = x + c * 5;
-      acc = (Dr[0] * xc[0] + Dr[1] * xc[1] + Dr[2] * xc[2] + Dr[3] * xc[3] + Dr[4] * xc[4]) + acc;
+      acc = (Dr[0] * xc[0] + Dr[nc] * xc[1] + Dr[2 * nc] * xc[2] + Dr[3 * nc] * xc[3] + Dr[4 * nc] * xc[4]) + acc;
     }
     if (MODE & 2) acc = b[c * 5 + i] - acc;
     r[i] = acc;
@@ -781,8 +781,8 @@ __global__ void __launch_bounds__(MF_CELLS) k_roe_mf(int64_t nc, const int* __re
   if (MODE & 4) {
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-      const double* Xr = dinv + c * 25 + i * 5;
-      out[c * 5 + i] = Xr[0] * r[0] + Xr[1] * r[1] + Xr[2] * r[2] + Xr[3] * r[3] + Xr[4] * r[4];
+      const double* Xr = dinv + (size_t)i * 5 * nc + c;
+      out[c * 5 + i] = Xr[0] * r[0] + Xr[nc] * r[1] + Xr[2 * nc] * r[2] + Xr[3 * nc] * r[3] + Xr[4 * nc] * r[4];
     }
   } else {
 #pragma unroll
