@@ -667,18 +667,32 @@ __global__ void __launch_bounds__(1024, 1) k_gm_arnoldi(int n, int64_t ld, doubl
 }
 
 // back substitution (krylov.py:128-131) and cycle bookkeeping
-// back substitution (krylov.py:128-131) on a register copy of the
-// triangle (independent loads first, no store-to-load round trips)
+// back substitution (krylov.py:128-131): the block copies the triangle and
+// the rotated right-hand side into shared memory in parallel, one thread
+// solves (a single thread walking the triangle in global memory waited on one
+// L2 round trip per row: 10 us per cycle)
 __global__ void k_gm_cycle_end(GmresDev* g, int cyc) {
-  g->ny = 0;
+  extern __shared__ double sh[];  // (m^2 + 2 m) doubles, m = g->m
+  __shared__ int ju_s;
+  const int mm = g->m;
+  double* tri = sh;
+  double* gv = sh + mm * mm;
+  double* y = gv + mm;
+  if (threadIdx.x == 0) {
+    g->ny = 0;
+    ju_s = (!g->notdone || g->err) ? 0 : g->j_used;
+  }
+  __syncthreads();
   if (!g->notdone) return;
-  const int ju = g->err ? 0 : g->j_used;
-  __shared__ double y[GM_MMAX], gv[GM_MMAX];
-  for (int i = 0; i < ju; ++i) gv[i] = g->gv[i];
+  const int ju = ju_s;
+  for (int t = threadIdx.x; t < ju * ju; t += blockDim.x) tri[t] = GH(t / ju, t % ju);
+  for (int t = threadIdx.x; t < ju; t += blockDim.x) gv[t] = g->gv[t];
+  __syncthreads();
+  if (threadIdx.x != 0) return;
   for (int i = ju - 1; i >= 0; --i) {
     double dot = 0.0;
-    for (int k = i + 1; k < ju; ++k) dot += GH(i, k) * y[k];
-    y[i] = (gv[i] - dot) / GH(i, i);
+    for (int k = i + 1; k < ju; ++k) dot += tri[i * ju + k] * y[k];
+    y[i] = (gv[i] - dot) / tri[i * ju + i];
   }
   for (int i = 0; i < ju; ++i) g->y[i] = y[i];
   g->ny = ju;
@@ -1142,7 +1156,7 @@ int gmres_enqueue(BlockSys* A, const double* b_dev, double* x_dev, const GmresPa
       GKS_LAUNCH(KC_SCALAR, k_gm_givens, 1, 1, 0, s, g, j, cyc);
       GKS_LAUNCH(KC_VEC, k_div, grid, RB_THREADS, 0, s, n, W->V + (int64_t)(j + 1) * ld, W->w, &g->hdiv, act);
     }
-    GKS_LAUNCH(KC_SCALAR, k_gm_cycle_end, 1, 1, 0, s, g, cyc);
+    GKS_LAUNCH(KC_SCALAR, k_gm_cycle_end, 1, 128, (size_t)(m * m + 2 * m) * sizeof(double), s, g, cyc);
     GKS_LAUNCH(KC_VEC, k_gm_update_x, grid, RB_THREADS, 0, s, n, ld, x_dev, W->V, g);
     if (P.check_ortho) {
       // Gram matrix of the cycle's basis (krylov.py:778-782), host-side check
