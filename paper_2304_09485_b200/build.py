@@ -75,7 +75,7 @@ def build(verbose=False, force=False, ptxas_verbose=False, defines=(), out=None)
     for src in cu:
         obj = BUILD / (src.stem + ".o")
         extra = ["-Xptxas", "-v"] if ptxas_verbose else []
-        dflags = [f"-D{d}" for d in defines]
+        dflags = [f"-D{d}" for d in defines] + os.environ.get("GKS_NVCC_EXTRA", "").split()
         _run([nvcc, *ARCH, *NVCC_FLAGS, *dflags, *extra, "-c", str(src), "-o", str(obj)], verbose or ptxas_verbose)
         objs.append(obj)
     for src in cpp:
