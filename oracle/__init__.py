@@ -11,15 +11,20 @@ Rules:
   * the product path never imports, links or executes this package;
   * the oracle is pinned against golden vectors produced by the reference
     itself (tests/golden/make_golden.py, run in the build container where the
-    reference is importable) -- see tests/test_oracle_golden.py.
+    reference is importable) -- tests/test_oracle_flux.py,
+    tests/test_oracle_solver.py, tests/test_setup.py.
+  * the reference is pure Python, so there is no compiled oracle/_ref: the
+    bench's reference arm times this restatement on the host cores.
 
 Modules
-  kinetic   Maxwellian moments, micro-slopes   (gks3d/kinetic.py)
-  flux      interface distribution, flux       (gks3d/flux.py)
-  mesh      mesh geometry, box generator       (gks3d/mesh/geometry.py, boxgen.py)
-  stencils  stencil selection                  (gks3d/mesh/stencils.py)
-  recon     WENO / HWENO operators + combine   (gks3d/recon.py, hweno.py)
-  boundary  ghost states                       (gks3d/boundary.py)
-  implicit  Roe Jacobian, GMRES, Jacobi        (gks3d/jacobian.py, krylov.py)
-  solver    residual / advance orchestration   (gks3d/stepping.py)
+  kinetic   Maxwellian moments, micro-slopes, time slope   (gks3d/kinetic.py)
+  flux      interface distribution, time-integrated flux, point value, KFVS,
+            collision time, frame rotations               (gks3d/flux.py)
+  recon     stencil selection, WENO / HWENO operators and combination,
+            compact gradient update                        (gks3d/mesh/stencils.py,
+                                                            recon.py, hweno.py)
+  solver    ghost states, local dt, residual, Roe Jacobian, Jacobi, GMRES,
+            advance, Frechet JVP                           (gks3d/boundary.py,
+                                                            stepping.py, jacobian.py,
+                                                            krylov.py)
 """
