@@ -268,6 +268,15 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   {
     auto fqf = to_i32(m->fq_face, nfq);
     TRY(upload(H, &H->fq_face, fqf.data(), nfq));
+    // uniform points per face in face order: the face kernel derives the
+    // face from the point index instead of loading it (one dependent load less)
+    H->fq_nq = 0;
+    if (nf > 0 && nfq % nf == 0 && nfq / nf <= 64) {
+      const int nq = (int)(nfq / nf);
+      bool uni = true;
+      for (int64_t i = 0; i < nfq && uni; ++i) uni = fqf[i] == (int)(i / nq);
+      if (uni) H->fq_nq = nq;
+    }
     std::vector<double> ws(nfq);
     for (int64_t i = 0; i < nfq; ++i) ws[i] = m->fq_weight[i] * m->face_area[m->fq_face[i]];
     TRY(upload(H, &H->fq_ws, ws.data(), nfq));

@@ -446,6 +446,7 @@ struct FaceArgs {
   double mu;
   KinConst kc;
   int want_point;
+  int fq_nq;
   double* contrib;
   double* qpt;
   int* status;
@@ -457,7 +458,7 @@ __global__ void __launch_bounds__(128, GKS_FACE_MINB) k_face(FaceArgs A) {
   if (A.gate && !*A.gate) return;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.nfq) return;
-  const int f = A.fq_face[i];
+  const int f = A.fq_nq ? (int)((uint32_t)i / (uint32_t)A.fq_nq) : A.fq_face[i];
   const int64_t o = A.f_own[f];
   const int64_t nb = A.f_nbr[f];
   const int p = nb >= 0 ? -1 : A.f_patch[f];
@@ -744,6 +745,7 @@ int residual_device(Handle* H, const double* q, double* res, bool with_gradients
   A.fq_point = H->fq_point; A.fq_ws = H->fq_ws; A.f_frame = H->f_frame; A.f_normal = H->f_normal;
   A.f_shift = H->f_shift; A.patches = H->patches; A.model = H->model; A.mu = H->mu; A.kc = H->kc;
   A.want_point = with_gradients ? 1 : 0;
+  A.fq_nq = H->fq_nq;
   A.contrib = H->contrib; A.qpt = H->qpt; A.status = H->status; A.gate = gate;
   const int fb = blocks_for(H->nfq, 128);
   if (H->model == 1) {

@@ -81,6 +81,7 @@ struct Handle {
   double *f_area = nullptr, *f_normal = nullptr, *f_frame = nullptr, *f_shift = nullptr;
   // fq points
   int* fq_face = nullptr;
+  int fq_nq = 0;  // > 0: fq_face[i] == i / fq_nq (uniform points per face)
   double *fq_point = nullptr, *fq_ws = nullptr;
   // cell -> fq CSR (assembly order), entries fq<<1 | is_neighbor
   int *cfq_start = nullptr, *cfq = nullptr;
