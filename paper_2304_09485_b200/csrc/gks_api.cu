@@ -703,9 +703,6 @@ __global__ void k_halve_dt(int64_t nc, const int8_t* bad, double* dt);
 __global__ void k_sigma(const double* vv_qq, double* sigma, double* out_zero_flag);
 __global__ void k_perturb(int64_t n, const double* q, const double* v, const double* sigma, double* out,
                           const int* gate);
-__global__ void k_frechet_combine(int64_t nc, const double* r1, const double* r0, const double* sigma,
-                                  const double* v, const double* vol, const double* dt, int mode, double* out,
-                                  const int* gate);
 void dot2(BlockSys* A, int64_t n, const double* a, const double* b, const double* c, const double* d, double* o0,
           double* o1, const int* gate);
 
@@ -726,9 +723,15 @@ static void frechet_apply(Handle* H, BlockSys* A, const double* v, double* out, 
   }
   GKS_LAUNCH(KC_VEC, k_perturb, blocks_for(n, 256), 256, 0, H->stream, n, H->q, v, sig, H->qtmp, gate);
   halo_exchange(H, H->hq, H->qtmp, 5, H->stream);
-  residual_device(H, H->qtmp, H->res2, false, gate);
-  GKS_LAUNCH(KC_VEC, k_frechet_combine, blocks_for(n, 256), 256, 0, H->stream, H->n_owned, H->res2, H->res, sig, v,
-             H->vol, H->dt, mode, out, gate);
+  // the combine runs as the assembly's epilogue (no r1 round trip through HBM)
+  FrechetEpi fe;
+  fe.r0 = H->res;
+  fe.sigma = sig;
+  fe.v = v;
+  fe.dt = H->dt;
+  fe.mode = mode;
+  fe.out = out;
+  residual_device(H, H->qtmp, H->res2, false, gate, &fe);
 }
 
 // One attempt of the step on the current dt: residual -> Roe Jacobian ->

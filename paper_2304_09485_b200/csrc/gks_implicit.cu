@@ -1365,17 +1365,5 @@ __global__ void k_perturb(int64_t n, const double* __restrict__ q, const double*
     out[i] = q[i] + s * v[i];
 }
 
-// mode 0: out = (r1 - r0) / s ; mode 1: out = V/dt v - (r1 - r0) / s  (s == 0 -> derivative 0)
-__global__ void k_frechet_combine(int64_t nc, const double* __restrict__ r1, const double* __restrict__ r0,
-                                  const double* sigma, const double* __restrict__ v, const double* __restrict__ vol,
-                                  const double* __restrict__ dt, int mode, double* __restrict__ out, const int* gate) {
-  if (gate && !*gate) return;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nc * 5) return;
-  const double s = *sigma;
-  const double d = s == 0.0 ? 0.0 : (r1[i] - r0[i]) / s;
-  out[i] = mode ? (vol[i / 5] / dt[i / 5]) * v[i] - d : d;
-}
-
 }  // namespace gks
 

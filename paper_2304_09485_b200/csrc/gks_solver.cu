@@ -571,7 +571,8 @@ __global__ void k_assemble(int64_t nc, const int* __restrict__ cfq_start, const 
                            const double* __restrict__ contrib, const double* __restrict__ qpt,
                            const int* __restrict__ fq_face, const double* __restrict__ fq_ws,
                            const double* __restrict__ f_normal, const double* __restrict__ vol,
-                           double* __restrict__ res, double* __restrict__ grad_new, const int* gate) {
+                           double* __restrict__ res, double* __restrict__ grad_new, const int* gate,
+                           FrechetEpi fe) {
   if (gate && !*gate) return;
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nc) return;
@@ -602,8 +603,22 @@ __global__ void k_assemble(int64_t nc, const int* __restrict__ cfq_start, const 
       }
     }
   }
+  if (fe.out) {
+    // the Frechet combine (formerly its own pass) on the unwritten residual.
+    // Staging the block's residual through shared memory for coalesced
+    // stores was slower (0.22 -> 0.27 ms on C2: the carve-out takes L1 from
+    // the contribution gathers)
+    const double s = *fe.sigma;
 #pragma unroll
-  for (int k = 0; k < 5; ++k) res[c * 5 + k] = r[k];
+    for (int k = 0; k < 5; ++k) {
+      const int64_t e = c * 5 + k;
+      const double d = s == 0.0 ? 0.0 : (r[k] - fe.r0[e]) / s;
+      fe.out[e] = fe.mode ? (vol[c] / fe.dt[c]) * fe.v[e] - d : d;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) res[c * 5 + k] = r[k];
+  }
   if (wantg) {
     const double V = vol[c];
 #pragma unroll
@@ -735,7 +750,8 @@ static int recon_device(Handle* H, const double* q, const int* gate) {
   return GKS_ERR_BAD_ARG;
 }
 
-int residual_device(Handle* H, const double* q, double* res, bool with_gradients, const int* gate) {
+int residual_device(Handle* H, const double* q, double* res, bool with_gradients, const int* gate,
+                    const FrechetEpi* fe) {
   // owned + layer-1 ghosts (redundant reconstruction), RT cells per CTA
   if (int rc = recon_device(H, q, gate)) return rc;
   FaceArgs A;
@@ -757,7 +773,8 @@ int residual_device(Handle* H, const double* q, double* res, bool with_gradients
   }
   GKS_LAUNCH(KC_ASSEMBLE, k_assemble, blocks_for(H->n_owned, TPB), TPB, 0, H->stream, H->n_owned, H->cfq_start, H->cfq, H->contrib, H->qpt,
                                                              H->fq_face, H->fq_ws, H->f_normal, H->vol, res,
-                                                             with_gradients ? H->grad_new : nullptr, gate);
+                                                             with_gradients ? H->grad_new : nullptr, gate,
+                                                             fe ? *fe : FrechetEpi{});
   GKS_CUDA(cudaGetLastError());
   return GKS_OK;
 }

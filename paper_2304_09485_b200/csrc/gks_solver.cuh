@@ -272,7 +272,18 @@ __device__ __forceinline__ double spectral_radius(const double q[5], const doubl
 }
 
 // host-side entry points shared across translation units
-int residual_device(Handle* H, const double* q, double* res, bool with_gradients, const int* gate);
+// Frechet epilogue of the assembly (stepping.py:298-313): instead of the
+// residual r1 write out = (r1 - r0)/s (mode 0) or V/dt v - (r1 - r0)/s (mode 1)
+struct FrechetEpi {
+  const double* r0 = nullptr;
+  const double* sigma = nullptr;
+  const double* v = nullptr;
+  const double* dt = nullptr;
+  int mode = 0;
+  double* out = nullptr;
+};
+int residual_device(Handle* H, const double* q, double* res, bool with_gradients, const int* gate,
+                    const FrechetEpi* fe = nullptr);
 void reset_status(Handle* H);
 int halo_exchange(Handle* H, HaloMap& X, double* arr, int width, cudaStream_t s);
 int allreduce(Handle* H, void* dev, int64_t count, int dtype, int op, cudaStream_t s);  // dtype 0 f64 1 i32; op 0 sum 1 min 2 max
