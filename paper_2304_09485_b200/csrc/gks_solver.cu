@@ -104,7 +104,13 @@ __global__ void k_fill(int64_t n, double* __restrict__ dt, const double* val) {
 // columns, the cell itself as padded gather index, inactive padded
 // sub-stencils), so the kernels carry no runtime bounds: ncu r01 measured
 // 45 % of all instructions in the runtime-bound version as ISETP/IMAD/BRA.
-static constexpr int RT = 32;
+// 24 cells: a tile's staged records (60-93 KB) then fit 3 CTAs per SM, so
+// one CTA's bulk copies overlap the others' compute (measured against
+// 8 / 16 / 32: C2 HWENO recon 1.20 -> 0.97 ms, WENO 0.74 -> 0.71 ms)
+#ifndef GKS_RT
+#define GKS_RT 24
+#endif
+static constexpr int RT = GKS_RT;
 static constexpr int RT_THREADS = RT * 5;
 // Big-stencil gathers issued straight from the HBM index records, before the
 // tile's bulk copies have landed (measured 0.84 -> 0.72 ms, C2 WENO); the
