@@ -8,7 +8,7 @@ from paper_2304_09485_b200.config import ConfigError, load_config, parse_patch
 from paper_2304_09485_b200.driver import ResidualHistory
 from paper_2304_09485_b200.mesh import MeshError, generate_box_mesh, load_mesh, save_mesh
 from paper_2304_09485_b200.meshgen import generate_carved_sphere_mesh, generate_sphere_mesh, generate_wing_mesh
-from paper_2304_09485_b200.output import read_residual_csv, write_residual_csv, write_vtk
+from paper_2304_09485_b200.output import read_residual_csv, read_vtk, write_residual_csv, write_vtk
 
 
 def test_config_defaults_and_patches(tmp_path):
@@ -73,6 +73,34 @@ def test_vtk_writer(tmp_path):
     q[0, 0] = np.nan
     with pytest.raises(ValueError):
         write_vtk(mesh, q, tmp_path / "bad.vtk")
+
+
+@pytest.mark.parametrize("split", ["tet", "hex"])
+def test_vtk_binary_matches_ascii(tmp_path, split):
+    mesh = generate_box_mesh((1, 1, 1), (3, 2, 2), split=split, perturb=0.1 if split == "tet" else 0.0, seed=5)
+    rng = np.random.default_rng(11)
+    q = np.column_stack([1 + 0.1 * rng.random(mesh.ncells), 0.1 * rng.standard_normal((mesh.ncells, 3)),
+                         2.5 + 0.1 * rng.random(mesh.ncells)])
+    g = rng.standard_normal((mesh.ncells, 3, 5))
+    write_vtk(mesh, q, tmp_path / "a.vtk", gradients=g)
+    write_vtk(mesh, q, tmp_path / "b.vtk", gradients=g, binary=True)
+    a, b = read_vtk(tmp_path / "a.vtk"), read_vtk(tmp_path / "b.vtk")
+    assert a.pop("encoding") == "ASCII" and b.pop("encoding") == "BINARY"
+    assert a.keys() == b.keys() and "grad_rhoE" in a
+    for k in a:  # %.17g round-trips float64 exactly
+        assert np.array_equal(a[k], b[k]), k
+    np.testing.assert_array_equal(a["points"], mesh.nodes)
+    assert (tmp_path / "b.vtk").stat().st_size < (tmp_path / "a.vtk").stat().st_size
+
+
+def test_vtk_mixed_cells_binary(tmp_path):
+    from paper_2304_09485_b200.output import _cell_records
+    sizes = np.array([4, 8, 4])
+    class M:
+        ncells = 3
+        cell_nodes = np.arange(24).reshape(3, 8)
+    rec = _cell_records(M, sizes)
+    assert rec.tolist() == [4, 0, 1, 2, 3, 8, *range(8, 16), 4, 16, 17, 18, 19]
 
 
 def test_mesh_file_round_trip(tmp_path):
