@@ -44,6 +44,16 @@ ymax = farfield_riemann
     assert opts.jacobian == "frechet" and opts.mu == 0.01
     mesh = cfg.build_mesh()
     assert mesh.ncells == 6 * 64
+    assert cfg.vtk_format == "ascii"
+
+
+def test_config_output_format(tmp_path):
+    ini = tmp_path / "o.ini"
+    ini.write_text("[output]\ndirectory = run\nformat = Binary\n")
+    assert load_config(ini).vtk_format == "binary"
+    ini.write_text("[output]\nformat = hdf5\n")
+    with pytest.raises(ConfigError):
+        load_config(ini)
 
 
 def test_config_errors(tmp_path):
