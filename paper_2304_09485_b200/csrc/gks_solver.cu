@@ -634,6 +634,59 @@ __global__ void k_assemble(int64_t nc, const int* __restrict__ cfq_start, const 
   }
 }
 
+// Same assembly with one thread per (cell, component): five independent
+// list walks per cell instead of one, so five times the contribution loads
+// are in flight per cell, and the res / Frechet epilogue stores coalesce.
+// Each component is summed over the same list in the same order as
+// k_assemble (bitwise-identical results).
+__global__ void k_assemble5(int64_t nc, const int* __restrict__ cfq_start, const int* __restrict__ cfq,
+                            const double* __restrict__ contrib, const double* __restrict__ qpt,
+                            const int* __restrict__ fq_face, const double* __restrict__ fq_ws,
+                            const double* __restrict__ f_normal, const double* __restrict__ vol,
+                            double* __restrict__ res, double* __restrict__ grad_new, const int* gate,
+                            FrechetEpi fe) {
+  if (gate && !*gate) return;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nc * 5) return;
+  const int64_t c = t / 5;
+  const int k = (int)(t - c * 5);
+  double r = 0.0;
+  double g[3] = {0.0, 0.0, 0.0};
+  const bool wantg = grad_new != nullptr;
+  const int e1 = cfq_start[c + 1];
+#pragma unroll 4
+  for (int e = cfq_start[c]; e < e1; ++e) {
+    const int ce = cfq[e];
+    const int64_t i = ce >> 1;
+    const bool is_nbr = ce & 1;
+    const double cc = contrib[i * 5 + k];
+    r = is_nbr ? r + cc : r - cc;
+    if (wantg) {
+      const int f = fq_face[i];
+      const double ws = fq_ws[i];
+      const double pv = qpt[i * 5 + k];
+#pragma unroll
+      for (int x = 0; x < 3; ++x) {
+        const double wn = ws * f_normal[3 * f + x];
+        const double tt = wn * pv;
+        g[x] = is_nbr ? g[x] - tt : g[x] + tt;
+      }
+    }
+  }
+  if (fe.out) {
+    const double sg = *fe.sigma;
+    const double d = sg == 0.0 ? 0.0 : (r - fe.r0[t]) / sg;
+    fe.out[t] = fe.mode ? (vol[c] / fe.dt[c]) * fe.v[t] - d : d;
+  } else {
+    res[t] = r;
+  }
+  if (wantg) {
+    const double V = vol[c];
+#pragma unroll
+    for (int x = 0; x < 3; ++x) grad_new[(c * 3 + x) * 5 + k] = g[x] / V;
+  }
+}
+
 // ghost of the cell-average owner state per boundary face (stepping.py:242-249)
 __global__ void k_boundary_ghosts(int64_t nbf, const int* __restrict__ bfaces, const int* __restrict__ f_own,
                                   const int* __restrict__ f_patch, const double* __restrict__ f_normal,
@@ -777,10 +830,18 @@ int residual_device(Handle* H, const double* q, double* res, bool with_gradients
     if (with_gradients) GKS_LAUNCH(KC_FACE, (k_face<false, true>), fb, 128, 0, H->stream, A);
     else GKS_LAUNCH(KC_FACE, (k_face<false, false>), fb, 128, 0, H->stream, A);
   }
-  GKS_LAUNCH(KC_ASSEMBLE, k_assemble, blocks_for(H->n_owned, TPB), TPB, 0, H->stream, H->n_owned, H->cfq_start, H->cfq, H->contrib, H->qpt,
-                                                             H->fq_face, H->fq_ws, H->f_normal, H->vol, res,
-                                                             with_gradients ? H->grad_new : nullptr, gate,
-                                                             fe ? *fe : FrechetEpi{});
+  static const int asm5 = [] {
+    const char* e = getenv("GKS_ASSEMBLE5");
+    return e ? atoi(e) : 1;
+  }();
+  if (asm5)
+    GKS_LAUNCH(KC_ASSEMBLE, k_assemble5, blocks_for(H->n_owned * 5, 160), 160, 0, H->stream, H->n_owned, H->cfq_start,
+               H->cfq, H->contrib, H->qpt, H->fq_face, H->fq_ws, H->f_normal, H->vol, res,
+               with_gradients ? H->grad_new : nullptr, gate, fe ? *fe : FrechetEpi{});
+  else
+    GKS_LAUNCH(KC_ASSEMBLE, k_assemble, blocks_for(H->n_owned, TPB), TPB, 0, H->stream, H->n_owned, H->cfq_start,
+               H->cfq, H->contrib, H->qpt, H->fq_face, H->fq_ws, H->f_normal, H->vol, res,
+               with_gradients ? H->grad_new : nullptr, gate, fe ? *fe : FrechetEpi{});
   GKS_CUDA(cudaGetLastError());
   return GKS_OK;
 }
