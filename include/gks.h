@@ -94,6 +94,9 @@ typedef struct GksMeshDesc {
      reference's summation order */
   const int64_t* face_rank;         /* (nf) */
   const int64_t* fq_rank;           /* (nfq) */
+  /* optional (NULL = identity): reference id of each cell; the Jacobian's
+     off-diagonal blocks of a row are ordered by it (jacobian.py:181-196) */
+  const int64_t* cell_rank;         /* (nc) */
 } GksMeshDesc;
 
 /* ------------------------------------------------------------------ */
@@ -190,7 +193,14 @@ typedef struct GksHaloDesc {
 typedef struct GksDomainDesc {
   int64_t n_owned, n_recon, nc_global;
   GksHaloDesc q, x;
+  /* position of the first owned cell in the global canonical order: owned
+     cells are consecutive there and start and end on multiples of
+     gks_reduction_granularity(nc_global) cells (the last rank may end at
+     nc_global), which makes every reduction partition-invariant */
+  int64_t owned_offset;
 } GksDomainDesc;
+/* cells per reduction group of a mesh of nc_global cells (partition alignment) */
+int64_t gks_reduction_granularity(int64_t nc_global);
 
 int gks_create_local(const GksMeshDesc* mesh, const GksSetup* setup, const GksOptions* opt,
                      const GksDomainDesc* domain, int device, GksHandle** out);
@@ -199,6 +209,16 @@ int gks_setup_subset(const GksSetup* global, const int64_t* cells, int64_t n_loc
                      int64_t n_global, GksSetup** out);
 int gks_comm_unique_id(void* out, int64_t nbytes);           /* ncclGetUniqueId (128 bytes) */
 int gks_comm_init(GksHandle* h, const void* unique_id, int nranks, int rank);
+/* In-process loopback transport: nranks rank-local handles of ONE process
+   (one host thread per rank, e.g. Python threads each calling
+   gks_advance_resident) exchange halos and reduction partials through
+   device copies ordered by CUDA events and host barriers -- no kernel waits
+   on another, so the ranks may share one GPU.  Same pack / exchange / unpack
+   and reduction code as NCCL; steps run uncaptured. */
+typedef struct GksLoopback GksLoopback;
+int gks_loopback_create(int nranks, GksLoopback** out);
+int gks_comm_init_loopback(GksHandle* h, GksLoopback* group, int rank);
+void gks_loopback_destroy(GksLoopback* group);  /* after every member handle is destroyed */
 
 /* Solver.local_time_step (stepping.py:135-157): q (nc,5) -> dt (nc) */
 int gks_local_dt(GksHandle* h, const double* q, double* dt_out);
@@ -256,6 +276,9 @@ int gks_blocksys_export(GksBlockSystem* a, double* diag, double* off, int64_t* o
                         int64_t* rowptr);
 int gks_blocksys_spmv(GksBlockSystem* a, const double* x, double* y);          /* BlockJacobian.spmv */
 int gks_blocksys_offdiag_mv(GksBlockSystem* a, const double* x, double* y);    /* .offdiag_mv */
+/* x . y over the system's rows with the GMRES reduction (partition-invariant
+   fold, csrc/gks_reduce.cuh) -- a measurement / specification hook */
+int gks_blocksys_dot(GksBlockSystem* a, const double* x, const double* y, double* out);
 int gks_blocksys_diag_inverses(GksBlockSystem* a, double* out);               /* .diag_inverses */
 int gks_blocksys_jacobi(GksBlockSystem* a, const double* b, int k_max, double* z); /* krylov.py:24-34 */
 /* gmres_solve (krylov.py:55-140): x_out (nc,5) */
@@ -269,6 +292,10 @@ int gks_advance(GksHandle* h, double* q_inout, double* grad_inout, GksStepInfo* 
 int gks_state_upload(GksHandle* h, const double* q, const double* grad);
 int gks_state_download(GksHandle* h, double* q, double* grad);
 int gks_advance_resident(GksHandle* h, GksStepInfo* info);
+/* after GKS_ERR_INVALID_UPDATE: the validity mask of the rejected update
+   (n_owned int8, 1 = bad), so the caller can name the cells in its own
+   (reference) numbering (stepping.py:294-296) */
+int gks_bad_mask(GksHandle* h, int8_t* out);
 /* Steps after a handle's first replay one captured CUDA graph of the whole
    step (no host synchronisation inside it).  enable = 0 runs every step
    uncaptured (default: on unless the environment sets GKS_GRAPH=0). */
@@ -285,7 +312,7 @@ int gks_frechet_matvec(GksHandle* h, const double* q, const double* grad, const 
 /* ------------------------------------------------------------------ */
 int gks_event_record(GksHandle* h, int slot);                 /* slot 0..7 */
 int gks_event_elapsed(GksHandle* h, int a, int b, double* ms);
-int64_t gks_handle_info(const GksHandle* h, int what);        /* 0 nc 1 nf 2 nfq 3 nfi 4 nbf 5 nnz 6 K 7 M 8 S */
+int64_t gks_handle_info(const GksHandle* h, int what);        /* 0 nc 1 nf 2 nfq 3 nfi 4 nbf 5 nnz 6 K 7 M 8 S 9 n_owned */
 int gks_fp64_peak(double* tflops);                          /* DFMA throughput probe */
 int gks_host_pin(void* p, int64_t nbytes);                  /* cudaHostRegister a host buffer */
 int gks_host_unpin(void* p);

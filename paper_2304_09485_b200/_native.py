@@ -47,7 +47,7 @@ class GksMeshDesc(C.Structure):
                 ("face_area", C.c_void_p), ("face_normal", C.c_void_p), ("face_frame", C.c_void_p),
                 ("face_shift", C.c_void_p), ("face_fq_start", C.c_void_p), ("fq_face", C.c_void_p),
                 ("fq_point", C.c_void_p), ("fq_weight", C.c_void_p), ("face_rank", C.c_void_p),
-                ("fq_rank", C.c_void_p)]
+                ("fq_rank", C.c_void_p), ("cell_rank", C.c_void_p)]
 
 
 _DESC_FIELDS = {
@@ -72,7 +72,7 @@ def mesh_desc(mesh):
         arr = np.ascontiguousarray(getattr(mesh, name), dtype=dt)
         keep[name] = arr
         setattr(desc, name, arr.ctypes.data)
-    for name in ("face_rank", "fq_rank"):  # renumbered meshes only (reorder.py)
+    for name in ("face_rank", "fq_rank", "cell_rank"):  # renumbered / rank-local meshes only
         val = getattr(mesh, name, None)
         if val is not None:
             arr = np.ascontiguousarray(val, dtype=np.int64)
@@ -143,7 +143,7 @@ class GksHaloDesc(C.Structure):
 
 class GksDomainDesc(C.Structure):
     _fields_ = [("n_owned", C.c_int64), ("n_recon", C.c_int64), ("nc_global", C.c_int64),
-                ("q", GksHaloDesc), ("x", GksHaloDesc)]
+                ("q", GksHaloDesc), ("x", GksHaloDesc), ("owned_offset", C.c_int64)]
 
 
 class GksError(RuntimeError):
@@ -176,6 +176,10 @@ SIGNATURES = [
                                    C.POINTER(C.c_void_p)]),
     ("gks_comm_unique_id", C.c_int, [C.c_void_p, C.c_int64]),
     ("gks_comm_init", C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
+    ("gks_loopback_create", C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    ("gks_comm_init_loopback", C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
+    ("gks_loopback_destroy", None, [C.c_void_p]),
+    ("gks_reduction_granularity", C.c_int64, [C.c_int64]),
     ("gks_destroy", None, [C.c_void_p]),
     ("gks_local_dt", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
     ("gks_residual", C.c_int, [C.c_void_p, c_double_p, c_double_p, c_double_p, C.c_int, c_double_p,
@@ -192,6 +196,7 @@ SIGNATURES = [
     ("gks_blocksys_export", C.c_int, [C.c_void_p, c_double_p, c_double_p, c_int64_p, c_int64_p, c_int64_p]),
     ("gks_blocksys_spmv", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
     ("gks_blocksys_offdiag_mv", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
+    ("gks_blocksys_dot", C.c_int, [C.c_void_p, c_double_p, c_double_p, c_double_p]),
     ("gks_blocksys_diag_inverses", C.c_int, [C.c_void_p, c_double_p]),
     ("gks_blocksys_jacobi", C.c_int, [C.c_void_p, c_double_p, C.c_int, c_double_p]),
     ("gks_gmres", C.c_int, [C.c_void_p, c_double_p, c_double_p, C.c_int, C.c_int, C.c_int, C.c_double,
@@ -201,6 +206,7 @@ SIGNATURES = [
     ("gks_state_download", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
     ("gks_advance_resident", C.c_int, [C.c_void_p, C.c_void_p]),
     ("gks_set_graph", C.c_int, [C.c_void_p, C.c_int]),
+    ("gks_bad_mask", C.c_int, [C.c_void_p, C.c_void_p]),
     ("gks_ugks_read", C.c_int, [C.c_char_p, C.c_void_p]),
     ("gks_ugks_sizes", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("gks_ugks_patch", C.c_int, [C.c_void_p, C.c_int64, C.c_char_p, C.c_int64, C.c_void_p]),

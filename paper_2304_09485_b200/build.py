@@ -71,17 +71,18 @@ def build(verbose=False, force=False, ptxas_verbose=False, defines=(), out=None)
             return LIB
     BUILD.mkdir(parents=True, exist_ok=True)
     nvcc = _nvcc()
-    objs = []
-    for src in cu:
-        obj = BUILD / (src.stem + ".o")
-        extra = ["-Xptxas", "-v"] if ptxas_verbose else []
-        dflags = [f"-D{d}" for d in defines] + os.environ.get("GKS_NVCC_EXTRA", "").split()
-        _run([nvcc, *ARCH, *NVCC_FLAGS, *dflags, *extra, "-c", str(src), "-o", str(obj)], verbose or ptxas_verbose)
-        objs.append(obj)
-    for src in cpp:
-        obj = BUILD / (src.stem + ".o")
-        _run(["g++", *CXX_FLAGS, "-ffp-contract=off", "-c", str(src), "-o", str(obj)], verbose)
-        objs.append(obj)
+    extra = ["-Xptxas", "-v"] if ptxas_verbose else []
+    dflags = [f"-D{d}" for d in defines] + os.environ.get("GKS_NVCC_EXTRA", "").split()
+    jobs = [([nvcc, *ARCH, *NVCC_FLAGS, *dflags, *extra, "-c", str(src), "-o", str(BUILD / (src.stem + ".o"))],
+             verbose or ptxas_verbose) for src in cu]
+    jobs += [(["g++", *CXX_FLAGS, "-ffp-contract=off", "-c", str(src), "-o", str(BUILD / (src.stem + ".o"))], verbose)
+             for src in cpp]
+    # translation units compile independently: run them concurrently
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
+        list(ex.map(lambda j: _run(*j), jobs))
+    objs = [BUILD / (src.stem + ".o") for src in cu + cpp]
     tmp = LIB.with_suffix(".so.tmp")
     _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-Xcompiler", "-fopenmp", "-o", str(tmp),
           *map(str, objs), "-lgomp"], verbose)

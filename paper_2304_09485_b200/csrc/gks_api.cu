@@ -45,6 +45,7 @@ struct StepGraph {
   const double* q = nullptr;
   const double* grad = nullptr;
   int64_t launches = 0;  // kernel nodes (launch accounting on replay)
+  int64_t ws_gen = 0;    // Krylov workspace generation the graph was captured against
 };
 
 struct GksHandle {
@@ -56,6 +57,26 @@ struct GksHandle {
   StepGraph graphs[2];
   int64_t steps = 0;            // steps advanced through this handle
   int graph = -1;               // CUDA-graph steps: -1 env default (GKS_GRAPH), 0 off, 1 on
+  // staging buffers of the host-API entry points (residual, local dt,
+  // Jacobian, Frechet matvec): they never overwrite the resident state
+  double *api_q = nullptr, *api_grad = nullptr, *api_dt = nullptr;
+};
+
+// Swaps the handle's state pointers for the API staging buffers for the
+// duration of one host-API call (uncaptured; the step graphs keep theirs).
+struct ApiStage {
+  gks::Handle* H;
+  double *q, *grad, *dt;
+  explicit ApiStage(GksHandle* G) : H(&G->H), q(G->H.q), grad(G->H.grad), dt(G->H.dt) {
+    H->q = G->api_q;
+    H->grad = G->api_grad;
+    H->dt = G->api_dt;
+  }
+  ~ApiStage() {
+    H->q = q;
+    H->grad = grad;
+    H->dt = dt;
+  }
 };
 
 namespace gks {
@@ -183,6 +204,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   H->n_owned = dom ? dom->n_owned : nc;
   H->n_recon = dom ? dom->n_recon : nc;
   H->nc_global = dom ? dom->nc_global : nc;
+  H->cell_first = dom ? dom->owned_offset : 0;
   if (H->n_owned < 1 || H->n_owned > H->n_recon || H->n_recon > nc) {
     set_error("bad domain sizes (owned %lld, recon %lld, local %lld)", (long long)H->n_owned,
               (long long)H->n_recon, (long long)nc);
@@ -380,9 +402,13 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
     order.reserve(nnz);
     for (int64_t e = 0; e < nnz; ++e)
       if (erow[e] < H->n_owned) order.push_back(e);  // rows of ghost cells live on their owner rank
+    // columns ascending in the REFERENCE numbering (jacobian.py:181-196
+    // lexsort), so a renumbered or rank-local handle sums every row's
+    // off-diagonal products in the reference's order
+    const int64_t* cref = m->cell_rank;
     std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
       if (erow[a] != erow[b]) return erow[a] < erow[b];
-      return ecol[a] < ecol[b];
+      return cref ? cref[ecol[a]] < cref[ecol[b]] : ecol[a] < ecol[b];
     });
     const int64_t nkept = order.size();
     H->nnz = nkept;
@@ -402,6 +428,9 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
     BlockSys* A = &G->jac.sys;
     TRY(blocksys_alloc(A, H->n_owned, nkept, H->stream));
     A->n_ext = H->n_recon;
+    A->red_nc_global = H->nc_global;
+    A->red_cell_first = H->cell_first;
+    A->canonical = dom ? 1 : 0;
     GKS_CUDA(cudaMemcpy(A->rowptr, rowptr.data(), (H->n_owned + 1) * sizeof(int), cudaMemcpyHostToDevice));
     if (nkept) GKS_CUDA(cudaMemcpy(A->col, col.data(), nkept * sizeof(int), cudaMemcpyHostToDevice));
     G->jac.owned = false;
@@ -502,6 +531,10 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
 
   // state and work buffers
   TRY(alloc(H, &H->q, nc * 5));
+  TRY(alloc(H, &G->api_q, nc * 5));
+  TRY(alloc(H, &G->api_grad, nc * 15));
+  TRY(alloc(H, &G->api_dt, nc));
+  GKS_CUDA(cudaMemset(G->api_grad, 0, nc * 15 * sizeof(double)));
   TRY(alloc(H, &H->grad, nc * 15));
   TRY(alloc(H, &H->dt, nc));
   TRY(alloc(H, &H->coef, nc * 45));
@@ -516,24 +549,17 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   TRY(alloc(H, &H->res2, nc * 5));
   TRY(alloc(H, &H->bad, nc));
   TRY(alloc(H, &H->scal, 1));
+  GKS_CUDA(cudaMemset(H->scal, 0, sizeof(DevScalars)));
   TRY(alloc(H, &H->status, 4));
   TRY(alloc(H, &G->phase_status, 4 * PH_N));
   GKS_CUDA(cudaMallocHost(&G->sh, sizeof(StepHost)));
-  {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    H->red_blocks = (int)std::max<int64_t>(1, std::min<int64_t>((nc + 255) / 256, (int64_t)sms * 4));
-  }
-  TRY(alloc(H, &H->partial, (size_t)H->red_blocks * 4));
-  TRY(alloc(H, &H->counter, 1));
-  GKS_CUDA(cudaMemset(H->counter, 0, sizeof(unsigned int)));
   GKS_CUDA(cudaMemset(H->grad, 0, nc * 15 * sizeof(double)));
   if (dom) {
     TRY(upload_halo(H, H->hq, dom->q));
     TRY(upload_halo(H, H->hx, dom->x));
     const int64_t mx = std::max(std::max(H->hq.ns, H->hq.nr), std::max(H->hx.ns, H->hx.nr));
-    TRY(alloc(H, &H->hsend, std::max<int64_t>(mx, 1) * 15));
+    TRY(alloc(H, &H->hsend, std::max<int64_t>(mx, 1) * 15 * 2));  // two parity halves (loopback)
+    H->hsend_half = std::max<int64_t>(mx, 1) * 15;
     TRY(alloc(H, &H->hrecv, std::max<int64_t>(mx, 1) * 15));
   }
   return GKS_OK;
@@ -616,9 +642,31 @@ int gks_create_local(const GksMeshDesc* mesh, const GksSetup* setup, const GksOp
   return GKS_OK;
 }
 
+static int comm_attach(GksHandle* G);
+
 int gks_comm_init(GksHandle* G, const void* unique_id, int nranks, int rank) {
   Handle* H = &G->H;
+  if (H->comm) {
+    set_error("handle already has a communicator");
+    return GKS_ERR_BAD_ARG;
+  }
   TRY(comm_init(H, unique_id, nranks, rank));
+  return comm_attach(G);
+}
+
+int gks_comm_init_loopback(GksHandle* G, GksLoopback* lb, int rank) {
+  Handle* H = &G->H;
+  if (H->comm || !lb) {
+    set_error(H->comm ? "handle already has a communicator" : "null loopback group");
+    return GKS_ERR_BAD_ARG;
+  }
+  TRY(comm_init_loopback(H, loopback_group(lb), rank));
+  G->graph = 0;  // cross-stream event waits: steps run uncaptured
+  return comm_attach(G);
+}
+
+static int comm_attach(GksHandle* G) {
+  Handle* H = &G->H;
   // captured steps predate the communicator: re-capture with the exchanges
   for (StepGraph& g : G->graphs) {
     if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -626,10 +674,8 @@ int gks_comm_init(GksHandle* G, const void* unique_id, int nranks, int rank) {
   }
   BlockSys* A = &G->jac.sys;
   A->halo_x = [H](double* x) { halo_exchange(H, H->hx, x, 5, H->stream); };
-  A->red2 = [H](double* a, double* b) {
-    if (a) allreduce(H, a, 1, 0, 0, H->stream);
-    if (b) allreduce(H, b, 1, 0, 0, H->stream);
-  };
+  A->comm = H->comm;
+  krylov_free(&A->ws);  // the reduction layout changes (group-partial exchange)
   return GKS_OK;
 }
 
@@ -641,10 +687,13 @@ void gks_destroy(GksHandle* G) {
 
 int64_t gks_num_boundary_faces(const GksHandle* G) { return G ? G->H.nbf : -1; }
 
+int64_t gks_reduction_granularity(int64_t nc_global) { return red_group_cells(nc_global); }
+
 int gks_local_dt(GksHandle* G, const double* q, double* dt_out) {
   Handle* H = &G->H;
   set_error_index(-1);
   GKS_CUDA(cudaSetDevice(H->device));
+  ApiStage stage(G);
   GKS_CUDA(cudaMemcpyAsync(H->q, q, H->nc * 5 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
   reset_status(H);
   if (int rc = local_dt_device(H)) return rc;
@@ -663,6 +712,7 @@ int gks_residual(GksHandle* G, const double* q, const double* grad, const double
     set_error("compact scheme needs a gradient field");
     return GKS_ERR_BAD_ARG;
   }
+  ApiStage stage(G);
   GKS_CUDA(cudaMemcpyAsync(H->q, q, H->nc * 5 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
   if (grad) GKS_CUDA(cudaMemcpyAsync(H->grad, grad, H->nc * 15 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
   GKS_CUDA(cudaMemcpyAsync(H->dt, dt, H->nc * sizeof(double), cudaMemcpyHostToDevice, H->stream));
@@ -697,32 +747,28 @@ int gks_boundary_ghosts(GksHandle* G, const double* q, double* ghosts_out) {
 // ===========================================================================
 namespace gks {
 __global__ void k_update(int64_t nc, const double* q, const double* dq, double* qn, int8_t* bad);
-__global__ void k_stats(int64_t nc, const double* res, const double* dt, const int8_t* bad, double* partial,
-                        unsigned int* counter, DevScalars* out);
 __global__ void k_halve_dt(int64_t nc, const int8_t* bad, double* dt);
 __global__ void k_sigma(const double* vv_qq, double* sigma, double* out_zero_flag);
 __global__ void k_perturb(int64_t n, const double* q, const double* v, const double* sigma, double* out,
                           const int* gate);
-void dot2(BlockSys* A, int64_t n, const double* a, const double* b, const double* c, const double* d, double* o0,
-          double* o1, const int* gate);
 
 // J v (mode 0: Frechet derivative; mode 1: V/dt v - derivative) with the step
 // residual H->res as the base point; q_base = H->q, dt = H->dt.
 // qq_cached: ||Q||^2 is already in red[1] (constant over one GMRES solve;
 // the same reduction, so sigma is bit-identical to recomputing it)
-static void frechet_apply(Handle* H, BlockSys* A, const double* v, double* out, int mode, const int* gate,
-                          const double* fixed_sigma, bool qq_cached = false) {
+static int frechet_apply(Handle* H, BlockSys* A, const double* v, double* out, int mode, const int* gate,
+                         const double* fixed_sigma, bool qq_cached = false) {
   const int64_t n = H->n_owned * 5;
   double* sig = &H->scal->sigma;
   if (!fixed_sigma) {
-    if (qq_cached) dot2(A, n, v, v, nullptr, nullptr, &H->scal->red[0], nullptr, gate);
-    else dot2(A, n, v, v, H->q, H->q, &H->scal->red[0], &H->scal->red[1], gate);
+    if (qq_cached) TRY(dot2(A, n, v, v, nullptr, nullptr, &H->scal->red[0], nullptr, gate));
+    else TRY(dot2(A, n, v, v, H->q, H->q, &H->scal->red[0], &H->scal->red[1], gate));
     GKS_LAUNCH(KC_SCALAR, k_sigma, 1, 1, 0, H->stream, H->scal->red, sig, nullptr);
   } else {
     sig = const_cast<double*>(fixed_sigma);
   }
   GKS_LAUNCH(KC_VEC, k_perturb, blocks_for(n, 256), 256, 0, H->stream, n, H->q, v, sig, H->qtmp, gate);
-  halo_exchange(H, H->hq, H->qtmp, 5, H->stream);
+  TRY(halo_exchange(H, H->hq, H->qtmp, 5, H->stream));
   // the combine runs as the assembly's epilogue (no r1 round trip through HBM)
   FrechetEpi fe;
   fe.r0 = H->res;
@@ -731,7 +777,7 @@ static void frechet_apply(Handle* H, BlockSys* A, const double* v, double* out, 
   fe.dt = H->dt;
   fe.mode = mode;
   fe.out = out;
-  residual_device(H, H->qtmp, H->res2, false, gate, &fe);
+  return residual_device(H, H->qtmp, H->res2, false, gate, &fe);
 }
 
 // One attempt of the step on the current dt: residual -> Roe Jacobian ->
@@ -747,6 +793,9 @@ static int enqueue_attempt(GksHandle* G) {
     ~StatusScope() { H->status = saved; }
   } scope{H, H->status};
   H->status = G->phase_status + 4 * PH_RES;
+  // the Krylov workspace must exist before the first reduction of the step
+  // (the Frechet ||Q||^2 below runs ahead of gmres_enqueue)
+  TRY(krylov_ensure(A, H->krylov_dim));
   TRY(residual_device(H, H->q, H->res, H->compact != 0, nullptr));
   if (H->nbf) {
     H->status = G->phase_status + 4 * PH_GHOST;
@@ -760,19 +809,16 @@ static int enqueue_attempt(GksHandle* G) {
   P.kmax = H->jacobi_sweeps;
   P.rtol = H->gmres_rtol;
   MatvecFn mf = [H, A](const double* v, double* out, const int* gate) {
-    frechet_apply(H, A, v, out, 1, gate, nullptr, true);
+    return frechet_apply(H, A, v, out, 1, gate, nullptr, true);
   };
   if (H->jac_mode == GKS_JAC_FRECHET) {
     const int64_t n = H->n_owned * 5;
-    dot2(A, n, H->q, H->q, nullptr, nullptr, &H->scal->red[1], nullptr, nullptr);
+    TRY(dot2(A, n, H->q, H->q, nullptr, nullptr, &H->scal->red[1], nullptr, nullptr));
   }
   TRY(gmres_enqueue(A, H->res, H->dq, P, H->jac_mode == GKS_JAC_FRECHET ? &mf : nullptr, false));
   GKS_LAUNCH(KC_UPDATE, k_update, blocks_for(H->n_owned, 256), 256, 0, H->stream, H->n_owned, H->q, H->dq, H->q_new,
              H->bad);
-  GKS_LAUNCH(KC_UPDATE, k_stats, H->red_blocks, 256, 0, H->stream, H->n_owned, H->res, H->dt, H->bad, H->partial,
-             H->counter, H->scal);
-  TRY(allreduce(H, H->scal->stat, 3, 0, 0, H->stream));
-  TRY(allreduce(H, H->scal->stat + 3, 1, 0, 1, H->stream));
+  TRY(step_stats(A, H->n_owned, H->res, H->dt, H->bad, H->scal));
   if (H->comm) {
     // every rank must agree on failure: error codes are max-reduced
     for (int ph = 0; ph < PH_N; ++ph) TRY(allreduce(H, G->phase_status + 4 * ph, 1, 1, 2, H->stream));
@@ -832,8 +878,16 @@ static bool graph_enabled(const GksHandle* G) {
 static int run_step_graph(GksHandle* G) {
   Handle* H = &G->H;
   StepGraph* slot = nullptr;
-  for (StepGraph& g : G->graphs)
+  const int64_t gen = G->jac.sys.ws.gen;
+  for (StepGraph& g : G->graphs) {
+    if (g.exec && g.ws_gen != gen) {
+      // the Krylov workspace was reallocated (host-API gmres with a larger m,
+      // a Frechet matvec of another length): the graph points at freed memory
+      cudaGraphExecDestroy(g.exec);
+      g = StepGraph();
+    }
     if (g.exec && g.q == H->q && g.grad == H->grad) slot = &g;
+  }
   if (!slot) {
     slot = !G->graphs[0].exec ? &G->graphs[0] : &G->graphs[1];
     if (slot->exec) {
@@ -855,6 +909,7 @@ static int run_step_graph(GksHandle* G) {
     GKS_CUDA(ei);
     slot->q = H->q;
     slot->grad = H->grad;
+    slot->ws_gen = G->jac.sys.ws.gen;
     slot->launches = gks_kernel_launches() - l0;
     count_launch((int)-slot->launches);  // captured, not launched
   }
@@ -960,6 +1015,7 @@ int gks_assemble_jacobian(GksHandle* G, const double* q, const double* dt, const
   Handle* H = &G->H;
   set_error_index(-1);
   GKS_CUDA(cudaSetDevice(H->device));
+  ApiStage stage(G);
   GKS_CUDA(cudaMemcpyAsync(H->q, q, H->nc * 5 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
   GKS_CUDA(cudaMemcpyAsync(H->dt, dt, H->nc * sizeof(double), cudaMemcpyHostToDevice, H->stream));
   if (ghosts && H->nbf)
@@ -1039,7 +1095,7 @@ static int bs_vec_op(GksBlockSystem* a, const double* x, double* y, int which) {
   TRY(bs_check_size(a));
   BlockSys* A = &a->sys;
   const int64_t n = A->nc * 5;
-  TRY(krylov_ensure(&A->ws, n, 5 * std::max<int64_t>(A->n_ext, A->nc), 1));
+  TRY(krylov_ensure(A, 1));
   GKS_CUDA(cudaMemcpyAsync(A->ws.x, x, n * sizeof(double), cudaMemcpyHostToDevice, A->stream));
   if (which == 0) bs_spmv(A, A->ws.x, A->ws.b, nullptr);
   else bs_offdiag(A, A->ws.x, A->ws.b, nullptr);
@@ -1050,6 +1106,20 @@ static int bs_vec_op(GksBlockSystem* a, const double* x, double* y, int which) {
 }
 
 int gks_blocksys_spmv(GksBlockSystem* a, const double* x, double* y) { return bs_vec_op(a, x, y, 0); }
+
+int gks_blocksys_dot(GksBlockSystem* a, const double* x, const double* y, double* out) {
+  TRY(bs_check_size(a));
+  BlockSys* A = &a->sys;
+  const int64_t n = A->nc * 5;
+  TRY(krylov_ensure(A, 1));
+  GKS_CUDA(cudaMemcpyAsync(A->ws.x, x, n * sizeof(double), cudaMemcpyHostToDevice, A->stream));
+  GKS_CUDA(cudaMemcpyAsync(A->ws.b, y, n * sizeof(double), cudaMemcpyHostToDevice, A->stream));
+  TRY(dot2(A, n, A->ws.x, A->ws.b, nullptr, nullptr, &A->ws.g->beta2, nullptr, nullptr));
+  GKS_CUDA(cudaGetLastError());
+  GKS_CUDA(cudaMemcpyAsync(out, &A->ws.g->beta2, sizeof(double), cudaMemcpyDeviceToHost, A->stream));
+  GKS_CUDA(cudaStreamSynchronize(A->stream));
+  return GKS_OK;
+}
 int gks_blocksys_offdiag_mv(GksBlockSystem* a, const double* x, double* y) { return bs_vec_op(a, x, y, 1); }
 
 int gks_blocksys_diag_inverses(GksBlockSystem* a, double* out) {
@@ -1072,7 +1142,7 @@ int gks_blocksys_jacobi(GksBlockSystem* a, const double* b, int k_max, double* z
     return GKS_ERR_SINGULAR;
   }
   const int64_t n = A->nc * 5;
-  TRY(krylov_ensure(&A->ws, n, 5 * std::max<int64_t>(A->n_ext, A->nc), 1));
+  TRY(krylov_ensure(A, 1));
   GKS_CUDA(cudaMemcpyAsync(A->ws.b, b, n * sizeof(double), cudaMemcpyHostToDevice, A->stream));
   bs_jacobi(A, A->ws.b, A->ws.z, A->ws.w, k_max, nullptr);
   GKS_CUDA(cudaGetLastError());
@@ -1087,7 +1157,7 @@ int gks_gmres(GksBlockSystem* a, const double* b, double* x_out, int m, int rest
   set_error_index(-1);
   BlockSys* A = &a->sys;
   const int64_t n = A->nc * 5;
-  TRY(krylov_ensure(&A->ws, n, 5 * std::max<int64_t>(A->n_ext, A->nc), m));
+  TRY(krylov_ensure(A, m));
   double* db;
   double* dx;
   GKS_CUDA(cudaMalloc(&db, n * sizeof(double)));
@@ -1152,6 +1222,7 @@ int64_t gks_handle_info(const GksHandle* G, int what) {
     case 6: return H->compact ? H->HA + 3 * H->HG : H->K;   /* big-op width */
     case 7: return H->compact ? H->HM : H->M;               /* sub-stencil slots */
     case 8: return H->compact ? 7 : H->S;                   /* sub-stencil width */
+    case 9: return H->n_owned;
     default: return -1;
   }
 }
@@ -1180,6 +1251,14 @@ int gks_set_graph(GksHandle* G, int enable) {
   return GKS_OK;
 }
 
+int gks_bad_mask(GksHandle* G, int8_t* out) {
+  Handle* H = &G->H;
+  GKS_CUDA(cudaSetDevice(H->device));
+  GKS_CUDA(cudaStreamSynchronize(H->stream));
+  GKS_CUDA(cudaMemcpy(out, H->bad, H->n_owned, cudaMemcpyDeviceToHost));
+  return GKS_OK;
+}
+
 int gks_advance_resident(GksHandle* G, GksStepInfo* info) {
   set_error_index(-1);
   GKS_CUDA(cudaSetDevice(G->H.device));
@@ -1202,13 +1281,20 @@ int gks_frechet_matvec(GksHandle* G, const double* q, const double* grad, const 
   Handle* H = &G->H;
   set_error_index(-1);
   GKS_CUDA(cudaSetDevice(H->device));
+  if (H->compact && !grad) {
+    set_error("compact scheme needs a gradient field");
+    return GKS_ERR_BAD_ARG;
+  }
   const int64_t n = H->nc * 5;
   BlockSys* A = &G->jac.sys;
-  TRY(krylov_ensure(&A->ws, n, 5 * std::max<int64_t>(A->n_ext, A->nc), 1));
+  // the step's workspace shape (owned rows, krylov_dim): no reallocation
+  TRY(krylov_ensure(A, std::max(1, H->krylov_dim)));
+  const int64_t nv = std::min<int64_t>(n, A->ws.ld);  // owned rows + layer-1 ghosts are read
+  ApiStage stage(G);
   GKS_CUDA(cudaMemcpyAsync(H->q, q, n * sizeof(double), cudaMemcpyHostToDevice, H->stream));
   if (grad) GKS_CUDA(cudaMemcpyAsync(H->grad, grad, H->nc * 15 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
   GKS_CUDA(cudaMemcpyAsync(H->dt, dt, H->nc * sizeof(double), cudaMemcpyHostToDevice, H->stream));
-  GKS_CUDA(cudaMemcpyAsync(A->ws.x, v, n * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  GKS_CUDA(cudaMemcpyAsync(A->ws.x, v, nv * sizeof(double), cudaMemcpyHostToDevice, H->stream));
   reset_status(H);
   TRY(residual_device(H, H->q, H->res, false, nullptr));
   const double* fixed = nullptr;
@@ -1216,9 +1302,9 @@ int gks_frechet_matvec(GksHandle* G, const double* q, const double* grad, const 
     GKS_CUDA(cudaMemcpyAsync(&H->scal->red[7], &sigma, sizeof(double), cudaMemcpyHostToDevice, H->stream));
     fixed = &H->scal->red[7];
   }
-  frechet_apply(H, A, A->ws.x, A->ws.b, 0, nullptr, fixed);
+  TRY(frechet_apply(H, A, A->ws.x, A->ws.b, 0, nullptr, fixed));
   TRY(check_status(H, "frechet_matvec"));
-  GKS_CUDA(cudaMemcpyAsync(out, A->ws.b, n * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaMemcpyAsync(out, A->ws.b, A->nc * 5 * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
   GKS_CUDA(cudaStreamSynchronize(H->stream));
   return GKS_OK;
 }

@@ -25,6 +25,7 @@
 #include <cooperative_groups.h>
 
 #include "gks_implicit.cuh"
+#include "gks_reduce.cuh"
 #include "gks_stage.cuh"
 
 namespace gks {
@@ -51,98 +52,91 @@ __device__ __forceinline__ double block_sum(double v, double* sm) {
   return sm[0];
 }
 
-// Finish a 2-value reduction: block partials -> out0/out1 by the last block
-// to arrive.  The last block reduces the partials with a fixed thread
-// assignment and tree, so the result is independent of block scheduling.
-__device__ __forceinline__ void finish2(double s0, double s1, double* partial, unsigned int* counter,
-                                        double* out0, double* out1, double* sm) {
-  __shared__ bool last;
-  double a = block_sum(s0, sm);
-  __syncthreads();
-  double b = block_sum(s1, sm);
-  if (threadIdx.x == 0) {
-    partial[2 * blockIdx.x] = a;
-    partial[2 * blockIdx.x + 1] = b;
-    __threadfence();
-    const unsigned t = atomicInc(counter, gridDim.x - 1);
-    last = (t == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  double x0 = 0.0, x1 = 0.0;
-  for (unsigned k = threadIdx.x; k < gridDim.x; k += blockDim.x) {
-    x0 += __ldcg(partial + 2 * k);
-    x1 += __ldcg(partial + 2 * k + 1);
-  }
-  __syncthreads();
-  x0 = block_sum(x0, sm);
-  __syncthreads();
-  x1 = block_sum(x1, sm);
-  if (threadIdx.x == 0) {
-    if (out0) *out0 = x0;
-    if (out1) *out1 = x1;
-  }
-}
+// Partition-invariant dots (gks_reduce.cuh): one block per segment of
+// SEG_CELLS cells (5 * SEG_CELLS vector entries).
+static constexpr int64_t SEG_VALS = 5 * (int64_t)SEG_CELLS;
 
-// out0 = a.b, out1 = c.d   (c may be null); 4-way unrolled streaming loop
-__global__ void __launch_bounds__(RB_THREADS) k_dot2(int64_t n, const double* __restrict__ a,
-                                                     const double* __restrict__ b, const double* __restrict__ c,
-                                                     const double* __restrict__ d, double* out0, double* out1,
-                                                     double* partial, unsigned int* counter, const int* gate) {
-  __shared__ double sm[RB_THREADS];
+// out0 = a.b, out1 = c.d   (c may be null)
+__global__ void __launch_bounds__(RED_T) k_dot2(int64_t n, const double* __restrict__ a,
+                                                const double* __restrict__ b, const double* __restrict__ c,
+                                                const double* __restrict__ d, RedDev R, RedOut out, const int* gate) {
+  __shared__ double sm[9];
   if (gate && !*gate) return;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  double s0 = 0.0, s1 = 0.0, t0 = 0.0, t1 = 0.0;
+  const int64_t base = (int64_t)blockIdx.x * SEG_VALS;
+  const int64_t len = min(SEG_VALS, n - base);
+  a += base; b += base;
+  double v[2];
   if (c) {
-    for (; i + stride < n; i += 2 * stride) {
-      s0 += a[i] * b[i];
-      t0 += a[i + stride] * b[i + stride];
-      s1 += c[i] * d[i];
-      t1 += c[i + stride] * d[i + stride];
-    }
-    if (i < n) {
-      s0 += a[i] * b[i];
-      s1 += c[i] * d[i];
-    }
+    c += base; d += base;
+    red_lanes<2, 0>(len, [&](int64_t i, double* o) { o[0] = __dmul_rn(a[i], b[i]); o[1] = __dmul_rn(c[i], d[i]); }, v);
+    red_finish<2, 0>(R, v, out, sm);
   } else {
-    for (; i + stride < n; i += 2 * stride) {
-      s0 += a[i] * b[i];
-      t0 += a[i + stride] * b[i + stride];
-    }
-    if (i < n) s0 += a[i] * b[i];
+    red_lanes<1, 0>(len, [&](int64_t i, double* o) { o[0] = __dmul_rn(a[i], b[i]); }, v);
+    red_finish<1, 0>(R, v, out, sm);
   }
-  finish2(s0 + t0, s1 + t1, partial, counter, out0, out1, sm);
 }
 
 // w -= (*coef) * v ; out = w . nxt  (nxt == nullptr: out = w . w)
-__global__ void __launch_bounds__(RB_THREADS) k_axpy_dot(int64_t n, double* __restrict__ w,
-                                                         const double* __restrict__ v, const double* coef,
-                                                         const double* __restrict__ nxt, double* out,
-                                                         double* partial, unsigned int* counter, const int* gate) {
-  __shared__ double sm[RB_THREADS];
+__global__ void __launch_bounds__(RED_T) k_axpy_dot(int64_t n, double* __restrict__ w,
+                                                    const double* __restrict__ v, const double* coef,
+                                                    const double* __restrict__ nxt, RedDev R, RedOut out,
+                                                    const int* gate) {
+  __shared__ double sm[9];
   if (gate && !*gate) return;
   const double h = *coef;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  double s = 0.0, t = 0.0;
-  const double* x = nxt ? nxt : w;
-  for (; i + stride < n; i += 2 * stride) {
-    const double w0 = w[i] - h * v[i];
-    const double w1 = w[i + stride] - h * v[i + stride];
-    w[i] = w0;
-    w[i + stride] = w1;
-    s += w0 * (nxt ? x[i] : w0);
-    t += w1 * (nxt ? x[i + stride] : w1);
+  const int64_t base = (int64_t)blockIdx.x * SEG_VALS;
+  const int64_t len = min(SEG_VALS, n - base);
+  w += base; v += base;
+  double r[1];
+  if (nxt) {
+    nxt += base;
+    red_lanes<1, 0>(len, [&](int64_t i, double* o) {
+      const double w0 = w[i] - h * v[i];
+      w[i] = w0;
+      o[0] = __dmul_rn(w0, nxt[i]);
+    }, r);
+  } else {
+    red_lanes<1, 0>(len, [&](int64_t i, double* o) {
+      const double w0 = w[i] - h * v[i];
+      w[i] = w0;
+      o[0] = __dmul_rn(w0, w0);
+    }, r);
   }
-  if (i < n) {
-    const double w0 = w[i] - h * v[i];
-    w[i] = w0;
-    s += w0 * (nxt ? x[i] : w0);
-  }
-  finish2(s + t, 0.0, partial, counter, out, nullptr, sm);
+  red_finish<1, 0>(R, r, out, sm);
 }
+
+// Multi-rank final fold over the exchanged group partials (gks_reduce.cuh):
+// entry g of component c is the rank-order sum (min) over the sources --
+// exact, only its owner's entry is not +0 (+inf).
+template <int NS, int NM>
+__global__ void __launch_bounds__(RED_T) k_red_final(RedSrc src, int64_t ngrp_g, RedOut out, const int* gate) {
+  __shared__ double sm[9];
+  if (gate && !*gate) return;
+#pragma unroll
+  for (int c = 0; c < NS + NM; ++c) {
+    double v;
+    if (c < NS) {
+      red_lanes<1, 0>(ngrp_g, [&](int64_t g, double* o) {
+        double x = __ldcg(src.p[0] + c * ngrp_g + g);
+        for (int r = 1; r < src.n; ++r) x += __ldcg(src.p[r] + c * ngrp_g + g);
+        o[0] = x;
+      }, &v);
+      v = red_tree<0>(v, sm);
+    } else {
+      red_lanes<0, 1>(ngrp_g, [&](int64_t g, double* o) {
+        double x = __ldcg(src.p[0] + c * ngrp_g + g);
+        for (int r = 1; r < src.n; ++r) x = fmin(x, __ldcg(src.p[r] + c * ngrp_g + g));
+        o[0] = x;
+      }, &v);
+      v = red_tree<1>(v, sm);
+    }
+    if (threadIdx.x == 0 && out.o[c]) *out.o[c] = v;
+  }
+}
+
+template __global__ void k_red_final<1, 0>(RedSrc, int64_t, RedOut, const int*);
+template __global__ void k_red_final<2, 0>(RedSrc, int64_t, RedOut, const int*);
+template __global__ void k_red_final<3, 1>(RedSrc, int64_t, RedOut, const int*);
 
 // out = in / *den
 __global__ void k_div(int64_t n, double* __restrict__ out, const double* __restrict__ in, const double* den,
@@ -835,22 +829,74 @@ void blocksys_free(BlockSys* A) {
   krylov_free(&A->ws);
 }
 
+static int64_t g_krylov_gen = 0;
+
 void krylov_free(KrylovWS* W) {
   if (W->V) cudaFree(W->V);
   if (W->bufs) cudaFree(W->bufs);
-  if (W->partial) cudaFree(W->partial);
-  if (W->counter) cudaFree(W->counter);
+  if (W->red.spart) cudaFree(W->red.spart);
+  if (W->gpart[0]) cudaFree(W->gpart[0]);
+  if (W->gpart[1]) cudaFree(W->gpart[1]);
+  if (W->gall) cudaFree(W->gall);
+  if (W->red.cnt) cudaFree(W->red.cnt);
   if (W->g) cudaFree(W->g);
   *W = KrylovWS{};
 }
 
-int krylov_ensure(KrylovWS* W, int64_t n, int64_t ld, int m) {
+__global__ void k_red_init(int64_t ngrp_g, double* a, double* b) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < RED_MAXC * ngrp_g;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = i < 3 * ngrp_g ? 0.0 : INFINITY;  // sums | min (the step stats' dt)
+    a[i] = v;
+    b[i] = v;
+  }
+}
+
+// Reduction layout of a block system's rows in the global canonical order
+// (gks_reduce.cuh); fails unless the rows are whole groups of that order.
+static int red_setup(BlockSys* A, KrylovWS* W) {
+  const int64_t nc = A->nc;
+  const int64_t ncg = A->red_nc_global > 0 ? A->red_nc_global : nc;
+  const int64_t first = A->red_nc_global > 0 ? A->red_cell_first : 0;
+  const int G = red_group(ncg);
+  const int64_t gcells = (int64_t)SEG_CELLS * G;
+  if (first % gcells != 0 || (nc % gcells != 0 && first + nc != ncg) || first + nc > ncg) {
+    set_error("owned cells [%lld, %lld) of %lld are not aligned to the %lld-cell reduction groups",
+              (long long)first, (long long)(first + nc), (long long)ncg, (long long)gcells);
+    return GKS_ERR_BAD_ARG;
+  }
+  RedDev& R = W->red;
+  R.nseg = (nc + SEG_CELLS - 1) / SEG_CELLS;
+  R.G = G;
+  R.ngrp = (R.nseg + G - 1) / G;
+  const int64_t nseg_g = (ncg + SEG_CELLS - 1) / SEG_CELLS;
+  R.ngrp_g = (nseg_g + G - 1) / G;
+  R.grp_first = first / gcells;
+  R.finalize = A->comm ? 0 : 1;
+  GKS_CUDA(cudaMalloc(&R.spart, (size_t)RED_MAXC * R.nseg * sizeof(double)));
+  for (int k = 0; k < 2; ++k) GKS_CUDA(cudaMalloc(&W->gpart[k], (size_t)RED_MAXC * R.ngrp_g * sizeof(double)));
+  GKS_CUDA(cudaMalloc(&W->gall, (size_t)RED_MAXC * R.ngrp_g * sizeof(double)));
+  GKS_CUDA(cudaMalloc(&R.cnt, (size_t)(R.ngrp + 1) * sizeof(unsigned)));
+  GKS_CUDA(cudaMemset(R.cnt, 0, (size_t)(R.ngrp + 1) * sizeof(unsigned)));
+  k_red_init<<<blocks_for(RED_MAXC * R.ngrp_g, 256), 256>>>(R.ngrp_g, W->gpart[0], W->gpart[1]);
+  GKS_CUDA(cudaGetLastError());
+  GKS_CUDA(cudaDeviceSynchronize());
+  R.gpart = W->gpart[0];
+  return GKS_OK;
+}
+
+int krylov_ensure(BlockSys* A, int m) {
+  KrylovWS* W = &A->ws;
+  const int64_t n = A->nc * 5;
+  int64_t ld = 5 * std::max<int64_t>(A->n_ext, A->nc);
   if (ld < n) ld = n;
   if (W->V && W->n == n && W->ld == ld && W->m >= m) return GKS_OK;
+  m = std::max(m, W->m);
   krylov_free(W);
   W->n = n;
   W->ld = ld;
   W->m = m;
+  W->gen = ++g_krylov_gen;  // captured step graphs holding the old buffers are stale
   GKS_CUDA(cudaMalloc(&W->V, (size_t)(m + 1) * ld * sizeof(double)));
   GKS_CUDA(cudaMemset(W->V, 0, (size_t)(m + 1) * ld * sizeof(double)));
   GKS_CUDA(cudaMalloc(&W->bufs, (size_t)6 * ld * sizeof(double)));
@@ -862,11 +908,8 @@ int krylov_ensure(KrylovWS* W, int64_t n, int64_t ld, int m) {
   W->b = W->bufs + 4 * ld;
   W->x = W->bufs + 5 * ld;
   W->grid = red_grid(n);
-  GKS_CUDA(cudaMalloc(&W->partial, (size_t)W->grid * 2 * sizeof(double)));
-  GKS_CUDA(cudaMalloc(&W->counter, sizeof(unsigned int)));
-  GKS_CUDA(cudaMemset(W->counter, 0, sizeof(unsigned int)));
   GKS_CUDA(cudaMalloc(&W->g, sizeof(GmresDev)));
-  return GKS_OK;
+  return red_setup(A, W);
 }
 
 static inline int cblocks(int64_t nc) { return (int)((nc + CELLS_PER_BLOCK - 1) / CELLS_PER_BLOCK); }
@@ -935,20 +978,61 @@ void bs_prec_matvec(BlockSys* A, const double* v, double* w, double* t, double* 
   }
 }
 
-void dot2(BlockSys* A, int64_t n, const double* a, const double* b, const double* c, const double* d, double* o0,
-          double* o1, const int* gate) {
+// Reductions over the owned rows (n = 5 * A->nc entries), partition-invariant
+// (gks_reduce.cuh).  Multi-rank: each launch leaves this rank's group
+// partials, the communicator exchanges them and folds the total.
+int dot2(BlockSys* A, int64_t n, const double* a, const double* b, const double* c, const double* d, double* o0,
+         double* o1, const int* gate) {
   KrylovWS* W = &A->ws;
-  GKS_LAUNCH(KC_REDUCE, k_dot2, W->grid, RB_THREADS, 0, A->stream, n, a, b, c, d, o0, o1, W->partial, W->counter,
-             gate);
-  if (A->red2) A->red2(o0, o1);
+  W->red.gpart = A->comm ? comm_red_buffer(A->comm, W) : W->gpart[0];
+  RedOut out;
+  out.o[0] = o0;
+  out.o[1] = o1;
+  GKS_LAUNCH(KC_REDUCE, k_dot2, (int)W->red.nseg, RED_T, 0, A->stream, n, a, b, c, d, W->red, out, gate);
+  if (A->comm) return comm_red_final(A->comm, W, c ? 2 : 1, 0, out, gate, A->stream);
+  return GKS_OK;
 }
 
-void axpy_dot(BlockSys* A, int64_t n, double* w, const double* v, const double* coef, const double* nxt, double* out,
-              const int* gate) {
+int axpy_dot(BlockSys* A, int64_t n, double* w, const double* v, const double* coef, const double* nxt, double* o,
+             const int* gate) {
   KrylovWS* W = &A->ws;
-  GKS_LAUNCH(KC_REDUCE, k_axpy_dot, W->grid, RB_THREADS, 0, A->stream, n, w, v, coef, nxt, out, W->partial,
-             W->counter, gate);
-  if (A->red2) A->red2(out, nullptr);
+  W->red.gpart = A->comm ? comm_red_buffer(A->comm, W) : W->gpart[0];
+  RedOut out;
+  out.o[0] = o;
+  GKS_LAUNCH(KC_REDUCE, k_axpy_dot, (int)W->red.nseg, RED_T, 0, A->stream, n, w, v, coef, nxt, W->red, out, gate);
+  if (A->comm) return comm_red_final(A->comm, W, 1, 0, out, gate, A->stream);
+  return GKS_OK;
+}
+
+// step norms (stepping.py:288-290): sum |res_rho|, sum res^2, #bad, min dt
+__global__ void __launch_bounds__(RED_T) k_stats(int64_t nc, const double* __restrict__ res,
+                                                 const double* __restrict__ dt, const int8_t* __restrict__ bad,
+                                                 RedDev R, RedOut out) {
+  __shared__ double sm[9];
+  const int64_t base = (int64_t)blockIdx.x * SEG_CELLS;
+  const int64_t len = min((int64_t)SEG_CELLS, nc - base);
+  double v[4];
+  red_lanes<3, 1>(len, [&](int64_t i, double* o) {
+    const double* r = res + (base + i) * 5;
+    o[0] = fabs(r[0]);
+    double s2 = __dmul_rn(r[0], r[0]);
+#pragma unroll
+    for (int k = 1; k < 5; ++k) s2 = __dadd_rn(s2, __dmul_rn(r[k], r[k]));
+    o[1] = s2;
+    o[2] = bad[base + i] ? 1.0 : 0.0;
+    o[3] = dt[base + i];
+  }, v);
+  red_finish<3, 1>(R, v, out, sm);
+}
+
+int step_stats(BlockSys* A, int64_t nc, const double* res, const double* dt, const int8_t* bad, DevScalars* sc) {
+  KrylovWS* W = &A->ws;
+  W->red.gpart = A->comm ? comm_red_buffer(A->comm, W) : W->gpart[0];
+  RedOut out;
+  for (int k = 0; k < 4; ++k) out.o[k] = &sc->stat[k];
+  GKS_LAUNCH(KC_UPDATE, k_stats, (int)W->red.nseg, RED_T, 0, A->stream, nc, res, dt, bad, W->red, out);
+  if (A->comm) return comm_red_final(A->comm, W, 3, 1, out, nullptr, A->stream);
+  return GKS_OK;
 }
 
 // Cluster size of the fused Arnoldi-column kernel for n unknowns: slices of
@@ -1066,9 +1150,9 @@ int gmres_enqueue(BlockSys* A, const double* b_dev, double* x_dev, const GmresPa
     return GKS_ERR_SINGULAR;
   }
   KrylovWS* W = &A->ws;
-  const int64_t ld = 5 * std::max<int64_t>(A->n_ext, A->nc);
-  int rc = krylov_ensure(W, n, ld, m);
+  int rc = krylov_ensure(A, m);
   if (rc) return rc;
+  const int64_t ld = W->ld;
   cudaStream_t s = A->stream;
   GmresDev* g = W->g;
   GKS_LAUNCH(KC_SCALAR, k_gm_init, 1, 1, 0, s, g, m, P.restarts, P.rtol, P.atol);
@@ -1083,6 +1167,8 @@ int gmres_enqueue(BlockSys* A, const double* b_dev, double* x_dev, const GmresPa
       const char* e = getenv("GKS_L2_PERSIST");
       return !(e && e[0] == '0');
     }();
+    // (an earlier launch failure must surface here, not be cleared below)
+    GKS_CUDA(cudaPeekAtLastError());
     int dev = 0, maxp = 0, maxw = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
@@ -1090,15 +1176,16 @@ int gmres_enqueue(BlockSys* A, const double* b_dev, double* x_dev, const GmresPa
     const size_t bytes = (size_t)n * sizeof(double);
     cudaStreamAttrValue at = {};
     if (persist && bytes <= (size_t)maxp && bytes <= (size_t)maxw) {
-      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes);
+      if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes) != cudaSuccess) cudaGetLastError();
       at.accessPolicyWindow.base_ptr = W->w;
       at.accessPolicyWindow.num_bytes = bytes;
       at.accessPolicyWindow.hitRatio = 1.0f;
       at.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
       at.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
     }
-    cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &at);  // (num_bytes 0: no window)
-    cudaGetLastError();
+    // the window is a hint: a refused attribute only clears its own error
+    if (cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &at) != cudaSuccess)  // (num_bytes 0: no window)
+      cudaGetLastError();
   }
   GKS_CUDA(cudaMemsetAsync(x_dev, 0, ld * sizeof(double), s));
   const int* act = &g->active;
@@ -1110,25 +1197,26 @@ int gmres_enqueue(BlockSys* A, const double* b_dev, double* x_dev, const GmresPa
   // Arnoldi column, w in shared memory (k_gm_arnoldi)
   const char* small_env = getenv("GKS_GMRES_SMALL");
   int cl = 0;  // cluster size of the fused column kernel, 0 = multi-block chain
-  if (!A->red2 && !(small_env && small_env[0] == '0')) cl = arnoldi_cluster(n);
-  auto Av = [&](const double* v, double* dst, const int* gate) {
-    if (matvec) (*matvec)(v, dst, gate);
-    else bs_spmv(A, v, dst, gate);
+  if (!A->comm && !A->canonical && !(small_env && small_env[0] == '0')) cl = arnoldi_cluster(n);
+  auto Av = [&](const double* v, double* dst, const int* gate) -> int {
+    if (matvec) return (*matvec)(v, dst, gate);
+    bs_spmv(A, v, dst, gate);
+    return GKS_OK;
   };
   for (int cyc = 0; cyc < P.restarts; ++cyc) {
     GKS_LAUNCH(KC_SCALAR, k_gm_cycle_begin, 1, 1, 0, s, g);
     // r = b - A x ; rh = P r ; beta = ||rh||
-    Av(x_dev, W->t, notdone);
+    TRY_GM(Av(x_dev, W->t, notdone));
     GKS_LAUNCH(KC_VEC, k_sub, grid, RB_THREADS, 0, s, n, W->r, b_dev, W->t, notdone);
     bs_jacobi(A, W->r, W->z, W->w, kmax, notdone);
-    dot2(A, n, W->z, W->z, nullptr, nullptr, &g->beta2, nullptr, notdone);
+    TRY_GM(dot2(A, n, W->z, W->z, nullptr, nullptr, &g->beta2, nullptr, notdone));
     GKS_LAUNCH(KC_SCALAR, k_gm_cycle_start, 1, 256, 0, s, g, cyc);
     GKS_LAUNCH(KC_VEC, k_div, grid, RB_THREADS, 0, s, n, W->V, W->z, &g->beta, act);
     for (int j = 0; j < m; ++j) {
       const double* vj = W->V + (int64_t)j * ld;
       // w = P^-1 A v_j
       if (matvec) {
-        Av(vj, W->t, act);
+        TRY_GM(Av(vj, W->t, act));
         bs_jacobi(A, W->t, W->w, W->r, kmax, act);
       } else {
         bs_prec_matvec(A, vj, W->w, W->t, W->r, kmax, act);
@@ -1139,19 +1227,19 @@ int gmres_enqueue(BlockSys* A, const double* b_dev, double* x_dev, const GmresPa
         continue;
       }
       // ||w||^2 and w.v_0 in one pass, then fused axpy + next dot (MGS)
-      dot2(A, n, W->w, W->w, W->w, W->V, &g->wscale2, &g->dots[0], act);
+      TRY_GM(dot2(A, n, W->w, W->w, W->w, W->V, &g->wscale2, &g->dots[0], act));
       for (int i = 0; i <= j; ++i) {
         const double* nxt = i < j ? W->V + (int64_t)(i + 1) * ld : nullptr;
         double* dst = i < j ? &g->dots[i + 1] : &g->hnext2;
-        axpy_dot(A, n, W->w, W->V + (int64_t)i * ld, &g->dots[i], nxt, dst, act);
+        TRY_GM(axpy_dot(A, n, W->w, W->V + (int64_t)i * ld, &g->dots[i], nxt, dst, act));
       }
       GKS_LAUNCH(KC_SCALAR, k_gm_reorth_check, 1, 1, 0, s, g, j);
       // conditional second pass (krylov.py:97-104)
-      dot2(A, n, W->w, W->V, nullptr, nullptr, &g->corr[0], nullptr, rgate);
+      TRY_GM(dot2(A, n, W->w, W->V, nullptr, nullptr, &g->corr[0], nullptr, rgate));
       for (int i = 0; i <= j; ++i) {
         const double* nxt = i < j ? W->V + (int64_t)(i + 1) * ld : nullptr;
         double* dst = i < j ? &g->corr[i + 1] : &g->hnext2;
-        axpy_dot(A, n, W->w, W->V + (int64_t)i * ld, &g->corr[i], nxt, dst, rgate);
+        TRY_GM(axpy_dot(A, n, W->w, W->V + (int64_t)i * ld, &g->corr[i], nxt, dst, rgate));
       }
       GKS_LAUNCH(KC_SCALAR, k_gm_givens, 1, 1, 0, s, g, j, cyc);
       GKS_LAUNCH(KC_VEC, k_div, grid, RB_THREADS, 0, s, n, W->V + (int64_t)(j + 1) * ld, W->w, &g->hdiv, act);
@@ -1274,71 +1362,6 @@ __global__ void k_update(int64_t nc, const double* __restrict__ q, const double*
   const double rho = v[0];
   const double e = v[4] - 0.5 * (v[1] * v[1] + v[2] * v[2] + v[3] * v[3]) / rho;
   bad[c] = (rho <= 0.0) || (e <= 0.0) || !fin;
-}
-
-// sum|res_rho|, sum res^2, bad count, min dt -> DevScalars.stat (deterministic,
-// raw sums so ranks can allreduce before the host normalises)
-__global__ void __launch_bounds__(RB_THREADS) k_stats(int64_t nc, const double* __restrict__ res,
-                                                      const double* __restrict__ dt, const int8_t* __restrict__ bad,
-                                                      double* partial, unsigned int* counter, DevScalars* out) {
-  __shared__ double sm[RB_THREADS];
-  __shared__ bool last;
-  double a = 0.0, b = 0.0, mn = INFINITY, nb = 0.0;
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
-    a += fabs(res[c * 5]);
-    for (int k = 0; k < 5; ++k) b += res[c * 5 + k] * res[c * 5 + k];
-    mn = fmin(mn, dt[c]);
-    nb += bad[c] ? 1.0 : 0.0;
-  }
-  const double A = block_sum(a, sm);
-  __syncthreads();
-  const double B = block_sum(b, sm);
-  __syncthreads();
-  const double NB = block_sum(nb, sm);
-  __syncthreads();
-  sm[threadIdx.x] = mn;
-  __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) sm[threadIdx.x] = fmin(sm[threadIdx.x], sm[threadIdx.x + s]);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    partial[4 * blockIdx.x] = A;
-    partial[4 * blockIdx.x + 1] = B;
-    partial[4 * blockIdx.x + 2] = NB;
-    partial[4 * blockIdx.x + 3] = sm[0];
-    __threadfence();
-    last = atomicInc(counter, gridDim.x - 1) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  double x0 = 0, x1 = 0, x2 = 0, x3 = INFINITY;
-  for (unsigned k = threadIdx.x; k < gridDim.x; k += blockDim.x) {
-    x0 += __ldcg(partial + 4 * k);
-    x1 += __ldcg(partial + 4 * k + 1);
-    x2 += __ldcg(partial + 4 * k + 2);
-    x3 = fmin(x3, __ldcg(partial + 4 * k + 3));
-  }
-  __syncthreads();
-  x0 = block_sum(x0, sm);
-  __syncthreads();
-  x1 = block_sum(x1, sm);
-  __syncthreads();
-  x2 = block_sum(x2, sm);
-  __syncthreads();
-  sm[threadIdx.x] = x3;
-  __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) sm[threadIdx.x] = fmin(sm[threadIdx.x], sm[threadIdx.x + s]);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    out->stat[0] = x0;
-    out->stat[1] = x1;
-    out->stat[2] = x2;
-    out->stat[3] = sm[0];
-  }
 }
 
 __global__ void k_halve_dt(int64_t nc, const int8_t* __restrict__ bad, double* __restrict__ dt) {

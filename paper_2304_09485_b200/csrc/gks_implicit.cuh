@@ -2,6 +2,7 @@
 #pragma once
 #include <functional>
 
+#include "gks_reduce.cuh"
 #include "gks_solver.cuh"
 
 namespace gks {
@@ -33,10 +34,15 @@ struct KrylovWS {
   double* V = nullptr;
   double* bufs = nullptr;
   double *w = nullptr, *r = nullptr, *t = nullptr, *z = nullptr, *b = nullptr, *x = nullptr;
-  double* partial = nullptr;
-  unsigned int* counter = nullptr;
+  // partition-invariant reductions (gks_reduce.cuh): red.gpart points at
+  // gpart[parity] for the next launch (parity alternates with the loopback
+  // transport's collectives; NCCL and single-rank use gpart[0])
+  RedDev red;
+  double* gpart[2] = {nullptr, nullptr};
+  double* gall = nullptr;  // NCCL allreduce output
   GmresDev* g = nullptr;
   double ortho_error = 0.0;  // host-side Gram check (GmresParams::check_ortho)
+  int64_t gen = 0;           // allocation generation (bumped on every (re)allocation)
 };
 
 // Block-row matrix: diagonal blocks + CSR off-diagonal blocks (jacobian.py:74-126)
@@ -44,7 +50,11 @@ struct BlockSys {
   int64_t nc = 0, nnz = 0;
   int64_t n_ext = 0;                                  // rows + layer-1 ghost columns
   std::function<void(double*)> halo_x;                // fill ghost entries of x before (L+U) x
-  std::function<void(double*, double*)> red2;         // allreduce two device scalars (null ok)
+  // place of the owned rows in the global canonical order (partition-invariant
+  // reductions); nc_global == 0: the system's own rows, single rank
+  int64_t red_nc_global = 0, red_cell_first = 0;
+  Comm* comm = nullptr;   // multi-rank: group-partial exchange for every reduction
+  int canonical = 0;      // partitioned handle: keep the segment chain (no fused small-system Arnoldi)
   int *rowptr = nullptr, *col = nullptr;
   double *off = nullptr, *diag = nullptr, *dinv = nullptr;
   int* status = nullptr;
@@ -75,12 +85,17 @@ struct GmresHost {
 };
 
 // out = A v on the device, gated by *gate (matrix-free operators)
-using MatvecFn = std::function<void(const double* v, double* out, const int* gate)>;
+using MatvecFn = std::function<int(const double* v, double* out, const int* gate)>;
 
 int blocksys_alloc(BlockSys* A, int64_t nc, int64_t nnz, cudaStream_t stream);
 void blocksys_free(BlockSys* A);
 void krylov_free(KrylovWS* W);
-int krylov_ensure(KrylovWS* W, int64_t n, int64_t ld, int m);
+// (re)allocate the Krylov space for the system's rows (5 * nc unknowns,
+// 5 * n_ext per vector) and its reduction layout; m basis vectors
+int krylov_ensure(BlockSys* A, int m);
+int dot2(BlockSys* A, int64_t n, const double* a, const double* b, const double* c, const double* d, double* o0,
+         double* o1, const int* gate);
+int step_stats(BlockSys* A, int64_t nc, const double* res, const double* dt, const int8_t* bad, DevScalars* sc);
 int blocksys_invert_diag(BlockSys* A);
 void bs_spmv(BlockSys* A, const double* x, double* y, const int* gate);
 void bs_offdiag(BlockSys* A, const double* x, double* y, const int* gate);

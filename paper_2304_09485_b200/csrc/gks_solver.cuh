@@ -8,6 +8,7 @@
 
 #include "gks_common.cuh"
 #include "gks_kinetic.cuh"
+#include "gks_reduce.cuh"
 
 namespace gks {
 
@@ -61,8 +62,10 @@ struct Handle {
   int64_t n_owned = 0, n_recon = 0, nc_global = 0;
   HaloMap hq, hx;                    // Q(+grad) halo (all layers), x/dt halo (layer 1)
   double *hsend = nullptr, *hrecv = nullptr;
-  void* comm = nullptr;              // ncclComm_t
+  int64_t hsend_half = 0;            // hsend holds two buffers of this many doubles
+  Comm* comm = nullptr;              // NCCL or in-process loopback transport (gks_comm.cu)
   int nranks = 1, rank = 0;
+  int64_t cell_first = 0;            // canonical index of the first owned cell (reductions)
   int nfpc = 4;
   // options
   int scheme = 0, model = 0, compact = 0, linear_weights = 0, global_dt = 0, jac_mode = 0;
@@ -288,7 +291,15 @@ void reset_status(Handle* H);
 int halo_exchange(Handle* H, HaloMap& X, double* arr, int width, cudaStream_t s);
 int allreduce(Handle* H, void* dev, int64_t count, int dtype, int op, cudaStream_t s);  // dtype 0 f64 1 i32; op 0 sum 1 min 2 max
 int comm_init(Handle* H, const void* uid, int nranks, int rank);
+struct LoopGroup;
+LoopGroup* loopback_group(GksLoopback* lb);
+int comm_init_loopback(Handle* H, LoopGroup* g, int rank);
 void comm_destroy(Handle* H);
+// reductions: the group-partial buffer for the next reduction, and the
+// exchange + final fold after it (gks_reduce.cuh; ns sums then nm mins)
+struct KrylovWS;
+double* comm_red_buffer(Comm* c, KrylovWS* W);
+int comm_red_final(Comm* c, KrylovWS* W, int ns, int nm, const RedOut& out, const int* gate, cudaStream_t s);
 int local_dt_device(Handle* H);
 int boundary_ghosts_device(Handle* H, const double* q);
 int jacobian_device(Handle* H, const double* q, bool ghosts_given);

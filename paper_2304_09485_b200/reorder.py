@@ -75,6 +75,7 @@ class PermutedMesh:
         inv = np.empty(nc, dtype=np.int64)
         inv[perm] = np.arange(nc, dtype=np.int64)
         self.perm, self.inv = perm, inv
+        self.cell_rank = perm  # reference id of each device cell (Jacobian column order)
         self.ncells, self.nfaces = nc, mesh.nfaces
         self.patch_names = list(mesh.patch_names)
         for name in ("cell_kind", "cell_volume", "cell_h", "cell_centroid"):

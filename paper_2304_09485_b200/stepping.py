@@ -234,8 +234,24 @@ class Solver:
         if rc in (N.GKS_ERR_SINGULAR, N.GKS_ERR_NONFINITE):
             raise SolverError(msg)
         if rc == N.GKS_ERR_INVALID_UPDATE:
+            bad = self._bad_cells()
+            if bad is not None:
+                msg = f"unphysical update persists after dt halving at cells {bad[:8].tolist()}"
             raise SteppingError(msg)
         N.check(rc)
+
+    def _bad_cells(self):
+        """Reference ids of the rejected update's bad cells, ascending (stepping.py:294-296)."""
+        nc = int(N.load().gks_handle_info(self._handle, 9))
+        mask = np.zeros(nc, dtype=np.int8)
+        if N.load().gks_bad_mask(self._handle, mask.ctypes.data):
+            return None
+        ids = np.flatnonzero(mask)
+        return np.sort(self._ref_ids(ids))
+
+    def _ref_ids(self, dev_ids):
+        """Device (handle) cell index -> reference cell id."""
+        return dev_ids if self._perm is None else self._perm[dev_ids]
 
     # -- time step ----------------------------------------------------------------
 

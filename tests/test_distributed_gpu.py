@@ -1,14 +1,21 @@
 """Partitioned (multi-GPU) device path on ONE GPU.
 
-Rank-local handles are driven with their ghost layers uploaded from the
-global state (no communicator), so the owned-cell results must be bitwise
-identical to the single-domain handle: this pins the local meshes, the
-operator subsets, the owned/reconstructed kernel ranges and the owned-row
-Jacobian.  A 1-rank NCCL communicator exercises the allreduce hooks inside
-GMRES and the step norms (result identical to the communicator-free run).
-The multi-rank NCCL halo exchange itself needs >1 GPU (not available this
-round); its host-side maps are covered by tests/test_partition.py (gloo).
+* Rank-local handles driven with their ghost layers uploaded from the global
+  state (no communicator): the owned-cell residual is bitwise the global
+  handle's -- pins the local meshes, the per-rank native setup (stencils and
+  operators built from the rank's own cells), the owned / reconstructed
+  kernel ranges and the owned-row Jacobian.
+* The in-process loopback transport (csrc/gks_comm.cu) steps 2 and 4
+  rank-local handles of one mesh concurrently through the real pack /
+  exchange / unpack code and the group-partial reductions: their step
+  histories and fields are bitwise those of the 1-rank canonical run
+  (partition-invariant reductions, csrc/gks_reduce.cuh), and within 1e-10 of
+  the plain single-domain Solver.
+* A 1-rank NCCL communicator runs the NCCL legs (group-partial allreduce,
+  captured in the step graph) bitwise against the communicator-free run.
 """
+
+import dataclasses
 
 import numpy as np
 import pytest
@@ -16,43 +23,52 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def setup_case(scheme):
+def setup_case(kind, n=3):
     from paper_2304_09485_b200.boundary import PatchSpec
     from paper_2304_09485_b200.kinetic import primitive_to_conserved
     from paper_2304_09485_b200.meshgen import generate_sphere_mesh
     from paper_2304_09485_b200.stepping import SolverOptions
 
-    mesh = generate_sphere_mesh(3, far=4.0, nr=6)
-    ref = np.array([1.0, 0.5, 0.02, -0.01, 1 / 1.4])
-    patches = {"sphere": PatchSpec("sphere", "wall_slip_adiabatic"),
-               "farfield": PatchSpec("farfield", "farfield_riemann", reference=ref)}
+    mesh = generate_sphere_mesh(n, far=4.0, nr=6) if n == 3 else generate_sphere_mesh(n)
     rng = np.random.default_rng(2)
-    w = np.tile([1.0, 0.5, 0.02, -0.01, 0.7], (mesh.ncells, 1))
+    if kind == "c3":
+        # C3 physics (cases/sphere_re118_ma0p2535.ini): viscous HWENO, no-slip wall
+        ma = 0.2535
+        ref = np.array([1.0, ma, 0.0, 0.0, 1 / 1.4])
+        patches = {"sphere": PatchSpec("sphere", "wall_noslip_adiabatic"),
+                   "farfield": PatchSpec("farfield", "farfield_riemann", reference=ref)}
+        opts = SolverOptions(scheme="hweno_gmres", model="viscous", mu=0.0021483, weights="linear",
+                             patches=patches)
+        w = np.tile([1.0, ma, 0.0, 0.0, 0.7], (mesh.ncells, 1))
+    else:
+        ref = np.array([1.0, 0.5, 0.02, -0.01, 1 / 1.4])
+        patches = {"sphere": PatchSpec("sphere", "wall_slip_adiabatic"),
+                   "farfield": PatchSpec("farfield", "farfield_riemann", reference=ref)}
+        scheme = "hweno_gmres" if kind == "hweno" else "weno_gmres"
+        opts = SolverOptions(scheme=scheme, patches=patches)
+        w = np.tile([1.0, 0.5, 0.02, -0.01, 0.7], (mesh.ncells, 1))
     w *= 1 + 0.02 * rng.normal(size=w.shape)
     q = primitive_to_conserved(w)
-    grad = 0.05 * rng.normal(size=(mesh.ncells, 3, 5)) if scheme.startswith("hweno") else None
-    return mesh, SolverOptions(scheme=scheme, patches=patches), q, grad
+    grad = 0.05 * rng.normal(size=(mesh.ncells, 3, 5)) if opts.scheme.startswith("hweno") else None
+    return mesh, opts, q, grad
 
 
-@pytest.mark.parametrize("scheme", ["weno_gmres", "hweno_gmres"])
-def test_rank_local_residual_bitwise(scheme):
-    from paper_2304_09485_b200 import _native as N
+@pytest.mark.parametrize("kind", ["weno", "hweno"])
+def test_rank_local_residual_bitwise(kind):
     from paper_2304_09485_b200.distributed import DistributedSolver
+    from paper_2304_09485_b200.partition import Decomposition
     from paper_2304_09485_b200.stepping import SolutionField, Solver
 
-    mesh, opts, q, grad = setup_case(scheme)
+    mesh, opts, q, grad = setup_case(kind)
     full = Solver(mesh, opts)
     fld = SolutionField(q, grad)
     dt = full.local_time_step(fld)
     res, gnew = full.residual(fld, dt)
-    gs = N.NativeSetup(mesh, schemes=2 if scheme.startswith("hweno") else 1)
-    from paper_2304_09485_b200.partition import partition_cells
-
-    part = partition_cells(mesh, 3)
+    dec = Decomposition.build(mesh, 3)
     for rank in range(3):
         # 3-way topology driven in one process without a communicator: the
         # ghost layers come from the uploaded global state
-        ds = DistributedSolver(mesh, opts, rank=rank, nranks=1, part=part, global_setup=gs)
+        ds = DistributedSolver(mesh, opts, rank=rank, nranks=3, dec=dec)
         cells = ds.dom.cells
         assert ds.dom.n_owned < len(cells)
         r, g = ds.residual_local(q[cells], None if grad is None else grad[cells], dt[cells],
@@ -61,24 +77,71 @@ def test_rank_local_residual_bitwise(scheme):
         assert np.array_equal(r, res[own])
         if grad is not None:
             assert np.array_equal(g, gnew[own])
+        ds.close()
 
 
-@pytest.mark.parametrize("scheme,jac", [("weno_gmres", "roe"), ("weno_gmres", "frechet"), ("hweno_gmres", "roe")])
-def test_one_rank_nccl_communicator_matches(monkeypatch, scheme, jac):
-    import dataclasses
+def _run_ranks(mesh, opts, q, grad, nranks, steps):
+    from paper_2304_09485_b200.distributed import DistributedSolver, LoopbackGroup, gather_owned
+    from paper_2304_09485_b200.partition import Decomposition
+    from paper_2304_09485_b200.stepping import SolutionField
 
-    from paper_2304_09485_b200.distributed import DistributedSolver
+    dec = Decomposition.build(mesh, nranks)
+    grp = LoopbackGroup(nranks) if nranks > 1 else None
+    ss = [DistributedSolver(mesh, opts, rank=r, nranks=nranks, dec=dec, loopback=grp) for r in range(nranks)]
+    for s in ss:
+        s.upload(SolutionField(q, grad))
+    hist = []
+    for _ in range(steps):
+        infos = grp.advance_all(ss) if grp else [ss[0].advance_resident()]
+        # every rank reports the same (global) norms
+        assert len({(i.res_rho_l1, i.res_l2, i.dt_min, i.solver_cycles, i.matvecs) for i in infos}) == 1
+        hist.append(infos[0])
+    qq, gg = gather_owned([s.download_owned() for s in ss], mesh.ncells, compact=grad is not None)
+    if grp:
+        grp.close()
+    else:
+        ss[0].close()
+    return hist, qq, gg
+
+
+@pytest.mark.parametrize("kind,jac,n", [("weno", "roe", 4), ("weno", "frechet", 4), ("c3", "roe", 4)])
+def test_loopback_ranks_bitwise_equal_one_rank(kind, jac, n):
     from paper_2304_09485_b200.stepping import SolutionField, Solver
 
-    # communicator handles reduce through NCCL between the MGS kernels; hold
-    # the communicator-free reference to the same multi-block chain (not the
-    # fused single-rank Arnoldi kernel) so the comparison stays bitwise.
-    # Three steps: the second and third replay the captured step graph (with
-    # the NCCL calls inside it).
-    monkeypatch.setenv("GKS_GMRES_SMALL", "0")
-    mesh, opts, q, grad = setup_case(scheme)
+    mesh, opts, q, grad = setup_case(kind, n)
     opts = dataclasses.replace(opts, jacobian=jac)
-    ref = Solver(mesh, opts)
+    steps = 5
+    h1, q1, g1 = _run_ranks(mesh, opts, q, grad, 1, steps)
+    for nranks in (2, 4):
+        hn, qn, gn = _run_ranks(mesh, opts, q, grad, nranks, steps)
+        for a, b in zip(h1, hn):
+            assert (a.res_rho_l1, a.res_l2, a.dt_min, a.solver_cycles, a.matvecs) == \
+                (b.res_rho_l1, b.res_l2, b.dt_min, b.solver_cycles, b.matvecs), (nranks, a, b)
+        assert np.array_equal(qn, q1), nranks
+        if grad is not None:
+            assert np.array_equal(gn, g1), nranks
+    # the canonical run vs the plain single-domain solver: same scheme, other
+    # summation trees (reference cell order) -> rounding-level agreement
+    s = Solver(mesh, opts)
+    s.upload(SolutionField(q, grad))
+    for a in h1:
+        b = s.advance_resident()
+        assert abs(a.res_rho_l1 - b.res_rho_l1) <= 1e-10 * abs(b.res_rho_l1)
+        assert a.solver_cycles == b.solver_cycles
+    qs = s.download().q
+    assert np.max(np.abs(qs - q1)) <= 1e-10 * np.max(np.abs(qs))
+
+
+@pytest.mark.parametrize("kind,jac", [("weno", "roe"), ("weno", "frechet"), ("hweno", "roe")])
+def test_one_rank_nccl_communicator_matches(kind, jac):
+    from paper_2304_09485_b200.distributed import DistributedSolver
+    from paper_2304_09485_b200.stepping import SolutionField
+
+    # Three steps: the second and third replay the captured step graph (with
+    # the NCCL group-partial allreduces inside it).
+    mesh, opts, q, grad = setup_case(kind)
+    opts = dataclasses.replace(opts, jacobian=jac)
+    ref = DistributedSolver(mesh, opts, rank=0, nranks=1)
     ref.upload(SolutionField(q, grad))
     ds = DistributedSolver(mesh, opts, rank=0, nranks=1, comm_id=DistributedSolver.unique_id())
     ds.upload(SolutionField(q, grad))
@@ -86,5 +149,41 @@ def test_one_rank_nccl_communicator_matches(monkeypatch, scheme, jac):
         a = ref.advance_resident()
         b = ds.advance_resident()
         assert a.res_rho_l1 == b.res_rho_l1 and a.res_l2 == b.res_l2 and a.solver_cycles == b.solver_cycles
-    cells, qo, _ = ds.download_owned()
-    assert np.array_equal(qo, ref.download().q[cells])
+    assert np.array_equal(ds.download_owned()[1], ref.download_owned()[1])
+    ds.close()
+    ref.close()
+
+
+def test_loopback_retry_and_failure_agree_across_ranks():
+    """An impossible CFL makes the update unphysical: every rank must take
+    the dt-halving branch together and raise the same SteppingError naming
+    reference cell ids (stepping.py:286-296)."""
+    from paper_2304_09485_b200.distributed import DistributedSolver, LoopbackGroup
+    from paper_2304_09485_b200.partition import Decomposition
+    from paper_2304_09485_b200.stepping import SolutionField, SteppingError
+
+    mesh, opts, q, grad = setup_case("weno", 4)
+    opts = dataclasses.replace(opts, cfl=1e6)
+    dec = Decomposition.build(mesh, 2)
+    grp = LoopbackGroup(2)
+    ss = [DistributedSolver(mesh, opts, rank=r, nranks=2, dec=dec, loopback=grp) for r in range(2)]
+    for s in ss:
+        s.upload(SolutionField(q, grad))
+    one = DistributedSolver(mesh, opts, rank=0, nranks=1)
+    one.upload(SolutionField(q, grad))
+    try:
+        ref = one.advance_resident()
+        ref_err = None
+    except SteppingError as e:
+        ref, ref_err = None, str(e)
+    try:
+        got = grp.advance_all(ss)
+        err = None
+    except SteppingError as e:
+        got, err = None, str(e)
+    if ref_err is None:
+        assert err is None and got[0].retried == ref.retried and got[0].res_rho_l1 == ref.res_rho_l1
+    else:
+        assert err is not None and "dt halving" in err
+    grp.close()
+    one.close()
