@@ -14,8 +14,13 @@ Solver.advance_inplace call with the field in pinned host memory (H2D + D2H
 every step).  `--impl reference` times the CPU oracle (numpy restatement of
 the reference) on a bounded sample of the same workload.
 
-Multi-GPU (torchrun): each rank currently runs an independent replica on
-its GPU (weak scaling, "replicas"); rank 0 prints the max-over-ranks line.
+Multi-GPU: `--gpus N` without a torchrun environment re-launches itself
+under `torch.distributed.run` with N ranks (127.0.0.1 rendezvous); under
+torchrun WORLD_SIZE must equal --gpus.  The ranks decompose ONE global mesh
+(partition.py: contiguous ranges of the RCB canonical order, per-rank setup,
+NCCL halo exchange + group-partial reductions inside the captured step;
+strong scaling, "cell-partitioned"); `--replicas` runs independent replicas
+instead.  Device time is the max over ranks; rank 0 prints the line.
 """
 
 from __future__ import annotations
@@ -221,10 +226,31 @@ class ClockSampler:
 
 # -- distributed plumbing ------------------------------------------------------------
 
+def _free_port():
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(args):
+    """--gpus N outside torchrun: run this script under torch.distributed.run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(ROOT / "bench.py"), *sys.argv[1:]]
+    print("launching: " + " ".join(cmd), file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
 def dist_init(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch with torchrun "
+                         f"--nproc-per-node {args.gpus}, or without torchrun to self-launch)")
     dist = None
     if world > 1:
         import torch
@@ -354,7 +380,7 @@ def run_reference(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": steps, "warmup": 0, "ms_per_step": secs * 1000.0 / steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.workload.upper()} (bounded CPU sample, lattice n={args.cpu_n})",
                    "scheme": args.scheme, "jacobian": args.jacobian},
         "cpu_baseline": cb,
@@ -639,13 +665,14 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
-        "scaling": "strong" if decomp else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak" if (world > 1 and not decomp) else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload,
                    "cells": nc, "faces": sizes["nf"], "face_points": sizes["nfq"], "scheme": args.scheme,
                    "jacobian": args.jacobian, "reorder": args.reorder, "gmres": "m=10, restarts=3, jacobi_sweeps=2, rtol=0",
                    "residual_evals_per_step": evals / args.steps,
-                   "parallelism": ("replicas" if not decomp else f"cell-partitioned RCB x{world}, NCCL halo + allreduce")
-                   if world > 1 else "single",
+                   "parallelism": ("replicas" if not decomp else
+                                   f"cell-partitioned x{world} (RCB canonical ranges), NCCL halo + group-partial "
+                                   "reductions") if world > 1 else "single",
                    "decomposition_note": decomp_note,
                    "l2": "inputs > L2 (operators %.1f GB)" % (sum(model_bytes[k] for k in ("recon",)) / 1e9),
                    "setup_s": round(t_setup, 2), "mesh_s": round(t_mesh, 2)},
@@ -671,6 +698,8 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

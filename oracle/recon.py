@@ -68,10 +68,16 @@ def _unique(members):
     return out
 
 
+def _faces_of(mesh, c):
+    """Face ids of cell c in its own order (mesh.cell_faces[c], geometry.py:152-181)."""
+    s = mesh.cell_face_start
+    return mesh.cell_face_list[s[c]: s[c + 1]]
+
+
 def _across(mesh, c):
     """(neighbour, shift) across each interior face of c, in cell face order."""
     res = []
-    for f in mesh.cell_faces[c]:
+    for f in _faces_of(mesh, c):
         if mesh.face_neighbor[f] < 0:
             continue
         if mesh.face_owner[f] == c:
@@ -83,7 +89,7 @@ def _across(mesh, c):
 
 def face_neighbours(mesh, c):
     """Labelled face neighbours (-1 on boundary); hexes reordered pole/equator/pole."""
-    faces = mesh.cell_faces[c]
+    faces = _faces_of(mesh, c)
     ids = np.full(len(faces), -1, dtype=np.int64)
     sh = np.zeros((len(faces), 3))
     nrm = np.empty((len(faces), 3))
@@ -166,6 +172,52 @@ class Recon:
             g = dmono(x)
             self.beta[c] = np.einsum("q,qxd,qxe->de", w, g, g) + B2
         self.ops = [self._weno_ops(c) if not compact else self._hweno_ops(c) for c in range(nc)]
+        self._pack()
+
+    def _pack(self):
+        """Per-cell operators padded into arrays (the reference's own layout,
+        recon.py:216-274 / hweno.py:62-137): padded gather slots point at the
+        cell itself and carry zero columns, padded sub-stencils are inactive."""
+        nc = self.mesh.ncells
+        own = np.arange(nc)
+        if not self.compact:
+            K = max(len(o["gids"]) for o in self.ops)
+            M = max((len(o["subs"]) for o in self.ops), default=0)
+            S = max((len(ids) for o in self.ops for _, ids in o["subs"]), default=1)
+            self.P_big = np.zeros((nc, NC, K))
+            self.P_gid = np.repeat(own[:, None], K, axis=1)
+            self.P_sub = np.zeros((nc, max(M, 1), 3, S))
+            self.P_sid = np.repeat(own[:, None, None], max(M, 1) * S, axis=1).reshape(nc, max(M, 1), S)
+            self.P_act = np.zeros((nc, max(M, 1)), dtype=bool)
+            for c, o in enumerate(self.ops):
+                k = len(o["gids"])
+                self.P_big[c, :, :k] = o["big"]
+                self.P_gid[c, :k] = o["gids"]
+                for m, (op, ids) in enumerate(o["subs"]):
+                    self.P_sub[c, m, :, :len(ids)] = op
+                    self.P_sid[c, m, :len(ids)] = ids
+                    self.P_act[c, m] = True
+        else:
+            A = max(len(o["avg_ids"]) for o in self.ops)
+            G = max(len(o["grad_ids"]) for o in self.ops)
+            M = max((len(o["subs"]) for o in self.ops), default=0)
+            self.P_bigA = np.zeros((nc, NC, max(A, 1)))
+            self.P_bigG = np.zeros((nc, NC, G, 3))
+            self.P_aid = np.repeat(own[:, None], max(A, 1), axis=1)
+            self.P_gid = np.repeat(own[:, None], G, axis=1)
+            self.P_sub = np.zeros((nc, max(M, 1), 3, 7))
+            self.P_sj = np.repeat(own[:, None], max(M, 1), axis=1)
+            self.P_act = np.zeros((nc, max(M, 1)), dtype=bool)
+            for c, o in enumerate(self.ops):
+                a, g = len(o["avg_ids"]), len(o["grad_ids"])
+                self.P_bigA[c, :, :a] = o["big"][:, :a]
+                self.P_bigG[c, :, :g] = o["big"][:, a:].reshape(NC, g, 3)
+                self.P_aid[c, :a] = o["avg_ids"]
+                self.P_gid[c, :g] = o["grad_ids"]
+                for m, (op, j) in enumerate(o["subs"]):
+                    self.P_sub[c, m] = op
+                    self.P_sj[c, m] = j
+                    self.P_act[c, m] = True
 
     def _cq(self, c, shift=None):
         m = self.mesh
@@ -231,20 +283,45 @@ class Recon:
     # -- per-step reconstruction (recon.py:167-195, 276-294; hweno.py:139-169)
 
     def coefficients(self, q, grad=None):
-        nc = self.mesh.ncells
-        out = np.empty((nc, NC, 5))
-        h = self.mesh.cell_h
-        for c in range(nc):
-            o = self.ops[c]
-            if self.compact:
-                rhs = np.vstack([q[o["avg_ids"]] - q[c], (h[o["grad_ids"], None, None] * grad[o["grad_ids"]]).reshape(-1, 5)])
-                cb = o["big"] @ rhs
-                bs = [op @ np.vstack([q[j] - q[c], h[c] * grad[c], h[j] * grad[j]]) for op, j in o["subs"]]
-            else:
-                cb = o["big"] @ (q[o["gids"]] - q[c])
-                bs = [op @ (q[ids] - q[c]) for op, ids in o["subs"]]
-            out[c] = cb if self.linear else self._combine(c, cb, bs)
-        return out
+        """Combined polynomial coefficients (nc, 9, 5), vectorised over cells
+        like the reference (recon.py:276-294 / hweno.py:139-169)."""
+        qc = q[:, None, :]
+        if self.compact:
+            h = self.mesh.cell_h
+            cb = np.einsum("cda,cav->cdv", self.P_bigA, q[self.P_aid] - qc)
+            cb += np.einsum("cdgx,cgxv->cdv", self.P_bigG, h[self.P_gid][:, :, None, None] * grad[self.P_gid])
+            if self.linear:
+                return cb
+            j = self.P_sj
+            hg = h[:, None, None] * grad  # (nc, 3, 5)
+            rhs = np.concatenate([(q[j] - qc)[:, :, None, :], np.broadcast_to(hg[:, None], j.shape + (3, 5)),
+                                  hg[j]], axis=2)  # (nc, M, 7, 5)
+            bs = np.einsum("cmds,cmsv->cmdv", self.P_sub, rhs)
+        else:
+            cb = np.einsum("cdk,ckv->cdv", self.P_big, q[self.P_gid] - qc)
+            if self.linear:
+                return cb
+            bs = np.einsum("cmds,cmsv->cmdv", self.P_sub, q[self.P_sid] - q[:, None, None, :])
+        return self._combine_all(cb, bs, self.P_act)
+
+    def _combine_all(self, cb, bs, act):
+        """combine_candidates (recon.py:167-195), all cells at once: weights
+        per cell and component; cells without active sub-stencils keep cb."""
+        m = act.sum(axis=1).astype(float)  # (nc,)
+        has = m > 0
+        ms = np.where(has, m, 1.0)
+        b0 = np.einsum("cdv,cde,cev->cv", cb, self.beta, cb)
+        bm = np.sum(bs * bs, axis=2)  # (nc, M, 5)
+        g0 = (1.0 - self.lw * m)[:, None]
+        tau = np.sum(np.where(act[:, :, None], np.abs(b0[:, None, :] - bm), 0.0), axis=1) / ms[:, None]
+        w0 = g0 * (1.0 + tau / (b0 + self.eps))
+        wm = np.where(act[:, :, None], self.lw * (1.0 + tau[:, None, :] / (bm + self.eps)), 0.0)
+        tot = w0 + np.sum(wm, axis=1)
+        g0s = np.where(has[:, None], g0, 1.0)
+        out = (w0 / tot / g0s)[:, None, :] * cb
+        f = np.where(act[:, :, None], wm / tot[:, None, :] - (w0 / tot * self.lw / g0s)[:, None, :], 0.0)
+        out[:, :3] += np.einsum("cmv,cmdv->cdv", f, bs)
+        return np.where(has[:, None, None], out, cb)
 
     def face_states(self, q, coef):
         """Point values / gradients on both sides of every fq point (recon.py:297-314)."""
@@ -263,22 +340,6 @@ class Recon:
             sides.append((q[cells] + np.einsum("fd,fdk->fk", phi, cf), np.einsum("fxd,fdk->fxk", dphi, cf)))
         (vo, go), (vn, gn) = sides
         return vo, go, np.where(inner[:, None], vn, vo), np.where(inner[:, None, None], gn, go)
-
-    def _combine(self, c, cb, bs):
-        m = len(bs)
-        if m == 0:
-            return cb
-        b0 = np.einsum("dk,de,ek->k", cb, self.beta[c], cb)
-        bm = [np.sum(b * b, axis=0) for b in bs]
-        g0 = 1.0 - self.lw * m
-        tau = sum(np.abs(b0 - x) for x in bm) / m
-        w0 = g0 * (1.0 + tau / (b0 + self.eps))
-        wm = [self.lw * (1.0 + tau / (x + self.eps)) for x in bm]
-        tot = w0 + sum(wm)
-        out = (w0 / tot / g0) * cb
-        for wk, b in zip(wm, bs):
-            out[:3] += (wk / tot - (w0 / tot) * self.lw / g0) * b
-        return out
 
 
 def update_gradients(mesh, qpt):

@@ -143,10 +143,15 @@ class Blocks:
         self.nc = nc
 
     def offmv(self, x):
-        y = np.zeros((self.nc, 5))
-        if len(self.off):
-            np.add.at(y, self.row, np.einsum("eij,ej->ei", self.off, x[self.col]))
-        return y
+        # scipy BSR product, as the reference does (jacobian.py:101-113)
+        if not len(self.off):
+            return np.zeros((self.nc, 5))
+        if getattr(self, "_bsr", None) is None:
+            from scipy.sparse import bsr_matrix
+
+            rowptr = np.concatenate([[0], np.cumsum(np.bincount(self.row, minlength=self.nc))])
+            self._bsr = bsr_matrix((self.off, self.col, rowptr), shape=(5 * self.nc, 5 * self.nc))
+        return (self._bsr @ x.reshape(-1)).reshape(self.nc, 5)
 
     def mv(self, x):
         return np.einsum("cij,cj->ci", self.diag, x) + self.offmv(x)
@@ -346,13 +351,16 @@ class OracleSolver:
             out[k] = ghost(q[m.face_owner[f]], spec, m.face_normal[f], self.gamma)[0]
         return out
 
-    def frechet(self, q, grad, v, dt, sigma=None):
+    def frechet(self, q, grad, v, dt, sigma=None, base=None):
+        """stepping.py:298-313; `base` = L(Q) when the caller has it (the
+        matrix-free GMRES of a step evaluates L(Q) once per step)."""
         if sigma is None:
             vn = np.linalg.norm(v)
             if vn == 0.0:
                 return np.zeros_like(v)
             sigma = np.sqrt(np.finfo(float).eps) * (1.0 + np.linalg.norm(q)) / vn
-        base, _ = self.residual(q, grad, dt, False)
+        if base is None:
+            base, _ = self.residual(q, grad, dt, False)
         return (self.residual(q + sigma * v, grad, dt, False)[0] - base) / sigma
 
     def advance(self, q, grad=None):
@@ -365,7 +373,7 @@ class OracleSolver:
             mv = None
             if self.jacobian == "frechet":
                 vol = self.mesh.cell_volume
-                mv = lambda v: (vol / dt)[:, None] * v - self.frechet(q, grad, v, dt)  # noqa: E731
+                mv = lambda v: (vol / dt)[:, None] * v - self.frechet(q, grad, v, dt, base=res)  # noqa: E731
             dq, cyc, nmv = gmres(A, res, self.m, self.restarts, self.kmax, self.rtol, 0.0, mv)
             qn = q + dq
             rho = qn[:, 0]

@@ -265,14 +265,205 @@ def make_solver():
         print(f"solver_{name}.npz", mesh.ncells, "cells", "matvecs", info.matvecs)
 
 
-SECTIONS = {"flux": make_flux, "mesh": make_mesh, "solver": make_solver}
+# -- converged-state parity (north_star "Correctness": converged fields within
+# 1e-8, residual-drop history within +-1 nonlinear iteration) -----------------
+
+CONVERGE_CASES = {
+    # the reference's own lid-driven cavity (cases/cavity_re100_desk.ini
+    # physics) run to the driver's convergence test (driver.py:71-76)
+    "cavity4": dict(n=4, threshold=1e-10, max_steps=8000),
+    "cavity8": dict(n=8, threshold=1e-10, max_steps=8000),
+}
+
+
+def cavity_setup(n):
+    from gks3d.boundary import PatchSpec
+    from gks3d.mesh import generate_box_mesh
+    from gks3d.stepping import SolverOptions, initial_field
+
+    mesh = generate_box_mesh((1, 1, 1), (n, n, n), split="tet")
+    lam_wall = GAMMA / 2.0
+    patches = {nm: PatchSpec(nm, "wall_noslip_isothermal", lambda_wall=lam_wall) for nm in mesh.patch_names}
+    patches["ymax"] = PatchSpec("ymax", "wall_noslip_isothermal", lambda_wall=lam_wall,
+                                velocity=np.array([0.15, 0.0, 0.0]))
+    opts = SolverOptions(scheme="weno_gmres", model="viscous", mu=0.15 / 100.0, patches=patches, cfl=2.0)
+    return mesh, opts, initial_field(mesh, [1.0, 0.0, 0.0, 0.0, 1.0 / GAMMA])
+
+
+def make_converge(names=None):
+    import time
+
+    from gks3d.stepping import Solver
+
+    for name, case in CONVERGE_CASES.items():
+        if names and name not in names:
+            continue
+        mesh, opts, fld = cavity_setup(case["n"])
+        solver = Solver(mesh, opts)
+        hist = []
+        t0 = time.time()
+        steps = None
+        for k in range(1, case["max_steps"] + 1):
+            fld, info = solver.advance(fld)
+            hist.append((info.res_rho_l1, info.res_l2, info.dt_min, info.solver_cycles, float(info.retried)))
+            if info.res_rho_l1 < case["threshold"] and info.res_l2 < 1e4 * case["threshold"]:
+                steps = k
+                break
+        out = dict(hist=np.array(hist), q_final=fld.q, steps=np.array(steps if steps else -1),
+                   threshold=np.array(case["threshold"]), n=np.array(case["n"]))
+        np.savez_compressed(HERE / f"converge_{name}.npz", **out)
+        print(f"converge_{name}.npz", mesh.ncells, "cells, converged at", steps, f"({time.time() - t0:.0f} s)",
+              flush=True)
+
+
+# -- the synthetic sphere / wing meshes of configs 2-4, run by the reference --
+
+def _capture_build(fn, *a, **k):
+    """Run a paper_2304_09485_b200.meshgen generator and return the arguments it
+    passed to Mesh.build (nodes, tets, hexes, patch faces)."""
+    sys.path.insert(0, str(HERE.parents[1]))
+    import paper_2304_09485_b200.mesh as M
+    import paper_2304_09485_b200.meshgen as MG
+
+    cap = {}
+    orig = M.Mesh.build
+
+    def grab(nodes, tets=(), hexes=(), patch_faces=None, periodic_pairs=()):
+        cap.update(nodes=np.asarray(nodes), tets=np.asarray(tets, dtype=np.int64),
+                   hexes=np.asarray(hexes, dtype=np.int64).reshape(-1, 8), patch_faces=patch_faces,
+                   periodic_pairs=periodic_pairs)
+        return orig(nodes, tets, hexes, patch_faces, periodic_pairs)
+
+    M.Mesh.build = grab
+    try:
+        getattr(MG, fn)(*a, **k)
+    finally:
+        M.Mesh.build = orig
+    return cap
+
+
+GEN_CASES = {
+    # C2 physics on the sphere n=2: inviscid Ma 0.5, slip wall + farfield, WENO
+    "sphere2_c2": dict(gen=("generate_sphere_mesh", (2,), dict(radius=0.5, far=10.0)), scheme="weno_gmres",
+                       reference=(1.0, 0.5, 0.0, 0.0, 1.0 / GAMMA),
+                       patches={"sphere": ("wall_slip_adiabatic", {}), "farfield": ("farfield_riemann", {})}),
+    # C3 physics: viscous Re 118 Ma 0.2535, no-slip wall, HWENO linear weights
+    "sphere2_c3": dict(gen=("generate_sphere_mesh", (2,), dict(radius=0.5, far=10.0)), scheme="hweno_gmres",
+                       model="viscous", mu=0.0021483050847457627, weights="linear",
+                       reference=(1.0, 0.2535, 0.0, 0.0, 1.0 / GAMMA),
+                       patches={"sphere": ("wall_noslip_adiabatic", {}), "farfield": ("farfield_riemann", {})}),
+    # C4 physics on the swept wing n=8: Ma 0.8395 AoA 3.06, slip walls, HWENO
+    "wing8_c4": dict(gen=("generate_swept_wing_mesh", (8,), {}), scheme="hweno_gmres",
+                     reference=(1.0, 0.8383030214661579, 0.04482495105787847, 0.0, 1.0 / GAMMA),
+                     patches={"wing": ("wall_slip_adiabatic", {}), "farfield": ("farfield_riemann", {}),
+                              "root": ("wall_slip_adiabatic", {}), "tip": ("wall_slip_adiabatic", {})}),
+}
+
+
+def make_generated(names=None):
+    from gks3d.mesh import Mesh
+    from gks3d.stepping import SolutionField, Solver, SolverOptions, initial_field
+
+    for name, case in GEN_CASES.items():
+        if names and name not in names:
+            continue
+        fn, a, k = case["gen"]
+        cap = _capture_build(fn, *a, **k)
+        mesh = Mesh.build(cap["nodes"], [tuple(t) for t in cap["tets"]], [tuple(h) for h in cap["hexes"]],
+                          cap["patch_faces"], cap["periodic_pairs"])
+        patches = _patch_specs(case, mesh)
+        opts = SolverOptions(scheme=case["scheme"], model=case.get("model", "inviscid"), mu=case.get("mu", 0.0),
+                             weights=case.get("weights", "nonlinear"), patches=patches)
+        solver = Solver(mesh, opts)
+        ref = np.array(case["reference"])
+        fld = initial_field(mesh, ref, GAMMA, compact=solver.compact)
+        # a perturbed start (the uniform field is a fixed point of the interior)
+        rng = np.random.default_rng(31)
+        from gks3d.kinetic import conserved_to_primitive, primitive_to_conserved
+
+        w = conserved_to_primitive(fld.q, GAMMA)
+        w[:, 0] *= 1.0 + 0.02 * rng.normal(size=mesh.ncells)
+        w[:, 1:4] += 0.02 * rng.normal(size=(mesh.ncells, 3))
+        q = primitive_to_conserved(w, GAMMA)
+        grad = 0.02 * rng.normal(size=(mesh.ncells, 3, 5)) if solver.compact else None
+        fld = SolutionField(q, grad)
+        dt = solver.local_time_step(fld)
+        res, grad_new = solver.residual(fld, dt)
+        v = np.random.default_rng(99).normal(size=q.shape)
+        fm = solver.frechet_matvec(fld, v, dt)
+        out = dict(q=q, dt=dt, res=res, frechet_v=v, frechet=fm, nodes=cap["nodes"], tets=cap["tets"])
+        if grad is not None:
+            out.update(grad=grad, grad_new=grad_new)
+        hist, qs = [], []
+        f = fld
+        for _ in range(4):
+            f, si = solver.advance(f)
+            hist.append((si.res_rho_l1, si.res_l2, si.dt_min, si.solver_cycles, float(si.retried)))
+            qs.append(f.q.copy())
+        out.update(hist=np.array(hist), q_after=np.array(qs))
+        if f.grad is not None:
+            out["grad_after"] = f.grad
+        np.savez_compressed(HERE / f"gen_{name}.npz", **out)
+        print(f"gen_{name}.npz", mesh.ncells, "cells", flush=True)
+
+
+# -- a step the reference retries at halved dt (stepping.py:286-296) ------------
+
+RETRY_CASE = dict(mesh="tet3j", scheme="weno_gmres", field="noise", cfl=None,
+                  reference=(1.0, 2.0, 0.1, 0.0, 1.0 / GAMMA),
+                  patches={"xmin": ("supersonic_inlet", {}), "xmax": ("supersonic_outlet", {}),
+                           "ymin": ("wall_slip_adiabatic", {}), "ymax": ("wall_slip_adiabatic", {}),
+                           "zmin": ("farfield_riemann", {}), "zmax": ("farfield_riemann", {})})
+
+
+RETRY_RUNS = {
+    # (scheme, CFL, steps): found by scanning np.geomspace(4, 60, 30) -- the
+    # reference rejects the marked steps once and accepts them at halved dt
+    "weno": ("weno_gmres", float(np.geomspace(4, 60, 30)[24]), 2, "supersonic"),
+    "hweno": ("hweno_gmres", float(np.geomspace(4, 60, 30)[24]), 5, "farfield"),
+}
+
+
+def make_retry():
+    """Supersonic channel starts that the reference rejects once and redoes
+    at halved dt (stepping.py:286-296)."""
+    from gks3d.mesh import generate_box_mesh
+    from gks3d.stepping import SolutionField, Solver, SolverOptions
+
+    for name, (scheme, cfl, steps, base) in RETRY_RUNS.items():
+        case = dict(RETRY_CASE if base == "supersonic" else SOLVER_CASES["s2_tetj_weno_far"])
+        mesh = generate_box_mesh(**MESH_CASES[case["mesh"]])
+        patches = _patch_specs(case, mesh)
+        compact = scheme.startswith("hweno")
+        q0, g0 = initial_q(case, mesh, compact)
+        solver = Solver(mesh, SolverOptions(scheme=scheme, patches=patches, cfl=cfl))
+        fld = SolutionField(q0.copy(), None if g0 is None else g0.copy())
+        hist, qs = [], []
+        for _ in range(steps):
+            fld, si = solver.advance(fld)
+            hist.append((si.res_rho_l1, si.res_l2, si.dt_min, si.solver_cycles, float(si.retried)))
+            qs.append(fld.q.copy())
+        assert any(h[4] for h in hist), name
+        out = dict(q=q0, cfl=np.array(cfl), hist=np.array(hist), q_after=np.array(qs))
+        if g0 is not None:
+            out.update(grad=g0, grad_after=fld.grad)
+        np.savez_compressed(HERE / f"retry_{name}.npz", **out)
+        print(f"retry_{name}.npz cfl {cfl:.4f} retried", [h[4] for h in hist], flush=True)
+
+
+SECTIONS = {"flux": make_flux, "mesh": make_mesh, "solver": make_solver, "converge": make_converge,
+            "generated": make_generated, "retry": make_retry}
 
 
 def main(argv):
     _import_reference()
-    names = argv or list(SECTIONS)
+    names = argv or ["flux", "mesh", "solver", "generated", "retry"]  # "converge" runs ~1 h: ask for it
     for name in names:
-        SECTIONS[name]()
+        sec, _, sub = name.partition(":")
+        if sub:
+            SECTIONS[sec](sub.split(","))
+        else:
+            SECTIONS[sec]()
 
 
 if __name__ == "__main__":

@@ -122,14 +122,16 @@ def test_loopback_ranks_bitwise_equal_one_rank(kind, jac, n):
             assert np.array_equal(gn, g1), nranks
     # the canonical run vs the plain single-domain solver: same scheme, other
     # summation trees (reference cell order) -> rounding-level agreement
+    # (Frechet: rounding amplified by the finite-difference step, ~1/sigma)
+    tol = 1e-10 if jac == "roe" else 1e-7
     s = Solver(mesh, opts)
     s.upload(SolutionField(q, grad))
     for a in h1:
         b = s.advance_resident()
-        assert abs(a.res_rho_l1 - b.res_rho_l1) <= 1e-10 * abs(b.res_rho_l1)
+        assert abs(a.res_rho_l1 - b.res_rho_l1) <= tol * abs(b.res_rho_l1)
         assert a.solver_cycles == b.solver_cycles
     qs = s.download().q
-    assert np.max(np.abs(qs - q1)) <= 1e-10 * np.max(np.abs(qs))
+    assert np.max(np.abs(qs - q1)) <= tol * np.max(np.abs(qs))
 
 
 @pytest.mark.parametrize("kind,jac", [("weno", "roe"), ("weno", "frechet"), ("hweno", "roe")])
@@ -187,3 +189,26 @@ def test_loopback_retry_and_failure_agree_across_ranks():
         assert err is not None and "dt halving" in err
     grp.close()
     one.close()
+
+
+@pytest.mark.parametrize("nc", [1000, 23040, 400_000])
+def test_device_dot_is_the_specified_fold(nc):
+    """gks_blocksys_dot (the GMRES reduction) equals the numpy statement of
+    the partition-invariant fold bit for bit (tests/_fold.py)."""
+    import ctypes as C
+
+    import _fold
+    from paper_2304_09485_b200 import _native as N
+
+    lib = N.load()
+    rng = np.random.default_rng(nc)
+    diag = np.tile(np.eye(5), (nc, 1, 1))
+    rowptr = np.zeros(nc + 1, dtype=np.int64)
+    h = C.c_void_p()
+    N.check(lib.gks_blocksys_create(nc, 0, N.dptr(diag.reshape(-1)), None, None, N.iptr(rowptr), 0, C.byref(h)))
+    x = rng.normal(size=(nc, 5)) * np.exp(3 * rng.normal(size=(nc, 1)))
+    y = rng.normal(size=(nc, 5))
+    out = C.c_double()
+    N.check(lib.gks_blocksys_dot(h, N.dptr(x), N.dptr(y), C.byref(out)))
+    lib.gks_blocksys_destroy(h)
+    assert out.value == _fold.dot(x, y)
