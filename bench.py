@@ -73,7 +73,8 @@ def parse():
     a.n = a.n or defaults[0]
     a.scheme = a.scheme or defaults[1]
     a.jacobian = a.jacobian or defaults[2]
-    a.cpu_n = a.cpu_n or {"c1": 10, "c2": 2, "c3": 2, "c4": 12, "c5": 2}[a.workload]
+    # bounded CPU samples of >= 2e4 cells (C2/C3/C5 sphere n=4: 23,040; C1 box 16: 24,576; C4 wing 20: 24,000)
+    a.cpu_n = a.cpu_n or {"c1": 16, "c2": 4, "c3": 4, "c4": 20, "c5": 4}[a.workload]
     return a
 
 
@@ -314,74 +315,112 @@ def kernel_model(solver, compact):
 
 # -- CPU baseline (oracle) -------------------------------------------------------------
 
-def cpu_baseline(args, steps, label, warm=True):
-    from oracle.solver import OracleSolver
-    from paper_2304_09485_b200 import mesh as M
+CPU_NOTE = ("oracle/ numpy restatement of the reference, single-threaded (OMP/OPENBLAS threads = 1); measured "
+            "in the build container on C2 n=2 at 0.7-0.9x the reference package's own s/step (profiles/r02/"
+            "cpu_calibration.json), i.e. a slightly faster-than-reference baseline")
 
-    n = args.cpu_n
+
+def cpu_sample(payload):
+    """One warmed single-threaded oracle sample of the workload (own process):
+    setup (not timed), one warm residual, then `steps` timed full steps."""
+    ns, jac, steps = payload
+    from threadpoolctl import threadpool_limits
+
+    threadpool_limits(1)  # the reference is single-threaded numpy
+    from oracle.solver import OracleSolver
+
+    args = argparse.Namespace(**ns)
+    args.jacobian = jac
+    args.n = args.cpu_n
     compact = args.scheme.startswith("hweno")
-    saved = args.n
-    args.n = n
-    try:
-        mesh, patches, q, grad, _, extra = build_workload(args, compact)
-    finally:
-        args.n = saved
+    mesh, patches, q, grad, _, extra = build_workload(args, compact)
     t0 = time.perf_counter()
-    s = OracleSolver(mesh, scheme=args.scheme, patches=patches, jacobian=args.jacobian, **extra)
+    s = OracleSolver(mesh, scheme=args.scheme, patches=patches, jacobian=jac, **extra)
     setup = time.perf_counter() - t0
-    if warm:
-        q, grad, info = s.advance(q, grad)  # warm-up
+    # warm-up (first-call caches, lazy imports): one full step of the same
+    # solver in Roe mode (a Frechet step costs ~34 residuals) + one JVP
+    s.jacobian = "roe"
+    s.advance(q, grad)
+    s.jacobian = jac
+    if jac == "frechet":
+        s.frechet(q, grad, np.ones_like(q), s.local_dt(q))
     evals = 0
     t0 = time.perf_counter()
     for _ in range(steps):
         q, grad, info = s.advance(q, grad)
-        evals += 1 + (info["matvecs"] - 1 if args.jacobian == "frechet" else 0)
+        evals += 1 + (info["matvecs"] if jac == "frechet" else 0)
     el = time.perf_counter() - t0
-    return {"value": mesh.ncells * evals / el, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{label}: oracle OracleSolver.advance x{steps} on {args.workload.upper()} n={n} "
-                      f"({mesh.ncells} cells), "
-                      f"{args.scheme}/{args.jacobian}, numpy single-thread; setup {setup:.1f}s not timed",
-            "seconds": el}
+    nc = mesh.ncells
+    return {"value": nc * evals / el, "unit": UNIT, "cell_steps_per_s": nc * steps / el, "cores": 1,
+            "kind": "port", "jacobian": jac, "cells": nc, "steps": steps, "seconds": el,
+            "residual_evals_per_step": evals / steps,
+            "sample": f"OracleSolver.advance x{steps} (warmed) on {args.workload.upper()} n={args.cpu_n} ({nc} cells), "
+                      f"{args.scheme}/{jac}, 1 thread; setup {setup:.0f} s not timed"}
+
+
+def cpu_steps(jac):
+    return 1 if jac == "frechet" else 3
+
+
+def start_cpu_baseline(args):
+    """Roe and Frechet samples in two background processes (they overlap the
+    GPU legs); returns a callable that collects them."""
+    import multiprocessing as mp
+
+    ns = dict(vars(args))
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[k] = "1"  # inherited by the spawned samples (read at their numpy import)
+    pool = mp.get_context("spawn").Pool(2)
+    res = {jac: pool.apply_async(cpu_sample, ((ns, jac, cpu_steps(jac)),)) for jac in ("roe", "frechet")}
+
+    def collect():
+        try:
+            out = {jac: r.get(timeout=1800) for jac, r in res.items()}
+        finally:
+            pool.terminate()
+        cb = dict(out[args.jacobian])
+        cb["note"] = CPU_NOTE
+        cb["modes"] = {jac: {k: out[jac][k] for k in ("value", "cell_steps_per_s", "seconds", "residual_evals_per_step",
+                                                      "sample")} for jac in out}
+        return cb
+
+    return collect
 
 
 def _reference_worker(payload):
-    """One single-threaded oracle sample (run in its own process)."""
-    os.environ["OMP_NUM_THREADS"] = "1"
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    ns, steps = payload
-    return cpu_baseline(argparse.Namespace(**ns), steps, "reference arm", warm=False)
+    return cpu_sample(payload)
 
 
 def run_reference(args):
     """The reference's CPU path (its numpy restatement, oracle/) on every host
-    core: one independent single-threaded sample per core (the reference is
-    single-threaded numpy), throughputs summed."""
+    core: one independent single-threaded warmed sample per core (the
+    reference is single-threaded numpy) of the same workload and mode,
+    throughputs summed."""
     world, rank, local, dist = dist_init(args)
     if rank != 0:
         return 0
-    # numpy has nothing to warm up; one step per core keeps the arm to a few
-    # minutes when every core runs a sample (16-core GPU hosts: ~2 min)
-    steps = 1
     ncores = os.cpu_count() or 1
     nproc = max(1, min(ncores, 32))
     ns = dict(vars(args))
-    if nproc == 1:
-        samples = [_reference_worker((ns, steps))]
-    else:
-        import multiprocessing as mp
+    steps = cpu_steps(args.jacobian)
+    import multiprocessing as mp
 
-        with mp.get_context("spawn").Pool(nproc) as pool:
-            samples = pool.map(_reference_worker, [(ns, steps)] * nproc)
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[k] = "1"
+    with mp.get_context("spawn").Pool(nproc) as pool:
+        samples = pool.map(_reference_worker, [(ns, args.jacobian, steps)] * nproc)
     value = sum(c["value"] for c in samples)
+    csteps = sum(c["cell_steps_per_s"] for c in samples)
     secs = statistics.mean(c["seconds"] for c in samples)
     cb = dict(samples[0])
-    cb.update(value=value, cores=nproc, seconds=secs,
+    cb.update(value=value, cell_steps_per_s=csteps, cores=nproc, seconds=secs, note=CPU_NOTE,
               sample=f"{nproc} concurrent single-threaded samples (host has {ncores} cores), each: {cb['sample']}")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-        "steps": steps, "warmup": 0, "ms_per_step": secs * 1000.0 / steps, "higher_is_better": True,
+        "steps": steps, "warmup": 1, "ms_per_step": secs * 1000.0 / steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.workload.upper()} (bounded CPU sample, lattice n={args.cpu_n})",
+        "cell_steps_per_s": csteps,
+        "config": {"workload": f"{args.workload.upper()} (bounded CPU sample, n={args.cpu_n}, {cb['cells']} cells)",
                    "scheme": args.scheme, "jacobian": args.jacobian},
         "cpu_baseline": cb,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -479,6 +518,8 @@ def cpu_step_seconds_cavity(args, steps=3):
 
 def run_ours(args):
     world, rank, local, dist = dist_init(args)
+    # the CPU baseline samples run in background processes, overlapping the GPU legs
+    cpu_collect = start_cpu_baseline(args) if (rank == 0 and world == 1 and not args.no_cpu_baseline) else None
     from paper_2304_09485_b200 import _native as N
     from paper_2304_09485_b200 import mesh as M
     from paper_2304_09485_b200.stepping import SolutionField, Solver, SolverOptions
@@ -656,14 +697,15 @@ def run_ours(args):
             paper = {"error": str(exc)}
 
     cb = None
-    if not args.no_cpu_baseline:
+    if cpu_collect is not None:
         try:
-            cb = cpu_baseline(args, 2, "cpu_baseline")
+            cb = cpu_collect()
         except Exception as exc:  # keep the GPU line even if the CPU leg fails
             cb = {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "cell_steps_per_s": (1 if decomp else world) * nc * args.steps / (ms_total / 1000.0),
         "warmup": args.warmup, "ms_per_step": ms_total / args.steps, "higher_is_better": True,
         "scaling": "weak" if (world > 1 and not decomp) else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload,
