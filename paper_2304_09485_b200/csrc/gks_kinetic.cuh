@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <type_traits>
+
 #ifndef GKS_ERFC_SCALED
 #define GKS_ERFC_SCALED 1
 #endif
@@ -123,6 +125,9 @@ __device__ __forceinline__ void wmom(const Maxw& m, const double s[5], const dou
                                      double o[5]) {
   o[0] = o[1] = o[2] = o[3] = o[4] = 0.0;
   const double hs = 0.5 * s[4];
+  // (two accumulators per output, alternating groups, to halve the add
+  // chain of the 13 groups: measured slower, 2.73 vs 2.67 ms on C2 -- the
+  // kernel is limited by register pressure, not by this chain)
   if (!DIR) {
     group_acc<P, 0, 0, 0, 3>(m, {s[0], s[1], hs}, o);  // 1, u, u^2
     group_acc<P, 1, 0, 0, 1>(m, {s[2]}, o);            // v
@@ -358,15 +363,29 @@ __device__ __forceinline__ double collision_tau(double pl, double pr, double dt,
 // (+ the point-value analogue).  Viscous tau needs W0, so that path keeps
 // the three transport families separate until tau is known.
 //
-// DEFER (inviscid, tau_in < 0): skip the pressure pre-pass and keep the
-// three transport families separate like the viscous path, taking the side
-// pressures from the loop's own states; tau and the time coefficients follow
-// after the loop.  Saves re-evaluating both reconstructions before the loop
-// (the face kernel's setting).
-template <bool VISCOUS, bool POINT, bool DEFER = false, class SideFn, class PressFn>
+// TAU (inviscid, tau_in < 0) chooses where the collision time comes from:
+//   0: get_pressures(pl, pr) before the loop (both sides re-evaluated);
+//   1 (DEFER): keep the three transport families separate like the viscous
+//      path and take both pressures from the loop's own states; tau after
+//      the loop;
+//   2 (PRE_R): get_pressures(pl, pr) provides the RIGHT pressure only
+//      (one side re-evaluated before the loop); the left one comes from
+//      side 0's loop state, so tau is known before any transport moment and
+//      both sides take the folded single-weight path (10 fewer doubles live
+//      across the loop, one Gram pass per side less than DEFER).
+// dt: the time window, or a callable returning it (evaluated where it is
+// first needed, so its loads need not complete before the side loop).
+template <class DT>
+__device__ __forceinline__ double dt_value(const DT& d) {
+  if constexpr (std::is_arithmetic<DT>::value) return d;
+  else return d();
+}
+
+template <bool VISCOUS, bool POINT, int TAU = 0, class SideFn, class PressFn, class DT = double>
 __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const PressFn& get_pressures, double tau_in,
-                                                double dt, double mu, const KinConst& kc, double flux[5], double tp,
+                                                const DT& dt_in, double mu, const KinConst& kc, double flux[5], double tp,
                                                 double point[5]) {
+  double dt = -1.0;  // dt_value(dt_in) once needed
   double q0[5] = {0, 0, 0, 0, 0};
   double dqa[3][5] = {};
   double F[5] = {0, 0, 0, 0, 0};   // folded transport flux (known tau) / base family (viscous)
@@ -375,15 +394,23 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
   double P[5] = {0, 0, 0, 0, 0};   // point value transport part (known tau) / slope family (viscous)
   double P6[5] = {0, 0, 0, 0, 0};  // viscous only
   double pl = 0.0, pr = 0.0;
+  constexpr bool DEFER = TAU == 1;
+  constexpr bool PRE_R = TAU == 2 && !VISCOUS;
   TimeCoef tc;
   double tau = tau_in;
   const bool tau_known = (!VISCOUS && !DEFER) || tau_in >= 0.0;
   if (!VISCOUS) {
-    if (!DEFER && tau < 0.0) {
+    if (PRE_R && tau < 0.0) {
       if (!get_pressures(pl, pr)) return 1;
+    } else if (!DEFER && tau < 0.0) {
+      if (!get_pressures(pl, pr)) return 1;
+      dt = dt_value(dt_in);
       tau = collision_tau(pl, pr, dt, false, mu, nullptr);
     }
-    if (tau_known) tc = time_coefficients(tau, dt, tp);
+    if (tau_known && !(PRE_R && tau < 0.0)) {
+      dt = dt_value(dt_in);
+      tc = time_coefficients(tau, dt, tp);
+    }
   }
 #pragma unroll 1
   for (int side = 0; side < 2; ++side) {
@@ -395,6 +422,15 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
       const double ps = rho / (2.0 * w[4]);
       pl = side ? pl : ps;
       pr = side ? ps : pr;
+    }
+    if (PRE_R && tau < 0.0) {
+      // (first pass only: side 0)  the right pressure came from the
+      // pre-pass: tau from side 0's state.  A data condition, not side == 0,
+      // so the compiler keeps one copy of the loop body
+      pl = rho / (2.0 * w[4]);
+      dt = dt_value(dt_in);
+      tau = collision_tau(pl, pr, dt, false, mu, nullptr);
+      tc = time_coefficients(tau, dt, tp);
     }
     double A[5];
     Maxw m;
@@ -440,11 +476,11 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
     } else {
       const double zero5[5] = {0, 0, 0, 0, 0};
       {
-        double Gu[5][5];
-        gram<1>(m, Gu);
-#pragma unroll
-        for (int i = 0; i < 5; ++i) F[i] += rho * Gu[i][0];
-        gram_acc(Gu, A, rho, F6);
+        // F += rho G_u e_0, F6 += rho G_u A with G_u = <u psi psi^T>, one
+        // unique entry at a time (no 25-entry matrix live across the loop body)
+        const double* const sv[1] = {A};
+        double* const av[1] = {F6};
+        gram_scatter<1, 1>(m, rho, sv, av, F);
       }
       wmom<1, true>(m, zero5, a, 1.0, t);
 #pragma unroll
@@ -473,6 +509,7 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
     micro_slope(sc0, D, Ab);
   }
   if (VISCOUS || !tau_known) {
+    dt = dt_value(dt_in);
     if (tau < 0.0) tau = collision_tau(pl, pr, dt, VISCOUS, mu, w0);
     tc = time_coefficients(tau, dt, tp);
 #pragma unroll

@@ -29,8 +29,8 @@ namespace gks {
 
 static constexpr int TPB = 128;
 
-#ifndef GKS_FACE_DEFER
-#define GKS_FACE_DEFER true
+#ifndef GKS_FACE_TAU
+#define GKS_FACE_TAU 1  // interface_flux_t TAU mode of the inviscid face kernel (gks_kinetic.cuh)
 #endif
 // L2 prefetch of the neighbour side's records at kernel start (1 %, measured)
 #ifndef GKS_FACE_PREFETCH
@@ -459,6 +459,10 @@ struct FaceArgs {
   const int* gate;
 };
 
+// (Staging the CTA's owner / neighbour cell records in shared memory with
+// cp.async before the compute was measured 32 % slower: 3.52 vs 2.66 ms on
+// C2 -- the CTA-wide barrier serialises load and compute phases and the
+// 45 KB of records per CTA take L1 from the spills.)
 template <bool VISC, bool POINT>
 __global__ void __launch_bounds__(128, GKS_FACE_MINB) k_face(FaceArgs A) {
   if (A.gate && !*A.gate) return;
@@ -469,28 +473,47 @@ __global__ void __launch_bounds__(128, GKS_FACE_MINB) k_face(FaceArgs A) {
   const int64_t nb = A.f_nbr[f];
   const int p = nb >= 0 ? -1 : A.f_patch[f];
   const bool wall = p >= 0 && A.patches[p].wall;
+  auto eval_cell = [&](bool own, const double x[3], double v[5], double g[3][5]) {
+    eval_side(A.q, A.coef, A.cen, A.h, A.avg0, own ? o : nb, x, v, g);
+  };
+  auto eval_cell_value = [&](bool own, const double x[3], double v[5]) {
+    eval_value(A.q, A.coef, A.cen, A.h, A.avg0, own ? o : nb, x, v);
+  };
 #if GKS_FACE_PREFETCH
+  {
   // the neighbour side's coefficient record is read only after the whole
   // owner side: start moving its lines into L2 now (no registers held)
   if (nb >= 0) {
     const char* pc = (const char*)(A.coef + nb * 45);
+#if GKS_FACE_PREFETCH == 2
+    // into L1 (the kernel uses no shared memory: 12 warps x 32 x 440 B fit)
+#pragma unroll
+    for (int l = 0; l < 360; l += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(pc + l));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(pc + 359));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"((const char*)(A.avg0 + nb * 9)));
+#else
 #pragma unroll
     for (int l = 0; l < 360; l += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(pc + l));
     asm volatile("prefetch.global.L2 [%0];" ::"l"(pc + 359));
     asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)(A.avg0 + nb * 9)));
+#endif
+  }
   }
 #endif
-  const double dtf = nb >= 0 ? fmin(A.dt[o], A.dt[nb]) : A.dt[o];
+  // face window min(dt_owner, dt_nbr), read where the flux first needs it
+  // (after the side loop for the inviscid face): its loads need not land
+  // before the reconstruction gathers start
+  auto dtf = [&]() { return nb >= 0 ? fmin(A.dt[o], A.dt[nb]) : A.dt[o]; };
   int ghost_fail = 0;
   // side 0: owner reconstruction; side 1: neighbour (shifted chart) or ghost
   auto get = [&](int side, double w[5], double sl[3][5]) {
     const double x[3] = {A.fq_point[3 * i], A.fq_point[3 * i + 1], A.fq_point[3 * i + 2]};
     double v[5], g[3][5];
     if (side == 0 || nb < 0) {
-      eval_side(A.q, A.coef, A.cen, A.h, A.avg0, o, x, v, g);
+      eval_cell(true, x, v, g);
     } else {
       const double xs[3] = {x[0] - A.f_shift[3 * f], x[1] - A.f_shift[3 * f + 1], x[2] - A.f_shift[3 * f + 2]};
-      eval_side(A.q, A.coef, A.cen, A.h, A.avg0, nb, xs, v, g);
+      eval_cell(false, xs, v, g);
     }
     if (side == 1 && nb < 0) {
       const DevPatch P = A.patches[p];
@@ -520,12 +543,12 @@ __global__ void __launch_bounds__(128, GKS_FACE_MINB) k_face(FaceArgs A) {
   auto press = [&](double& pl, double& pr) {
     const double x[3] = {A.fq_point[3 * i], A.fq_point[3 * i + 1], A.fq_point[3 * i + 2]};
     double v[5], w[5];
-    eval_value(A.q, A.coef, A.cen, A.h, A.avg0, o, x, v);
+    eval_cell_value(true, x, v);
     if (!cons_to_prim(v, A.kc, w)) return false;
     pl = w[0] / (2.0 * w[4]);
     if (nb >= 0) {
       const double xs[3] = {x[0] - A.f_shift[3 * f], x[1] - A.f_shift[3 * f + 1], x[2] - A.f_shift[3 * f + 2]};
-      eval_value(A.q, A.coef, A.cen, A.h, A.avg0, nb, xs, v);
+      eval_cell_value(false, xs, v);
     } else {
       const DevPatch P = A.patches[p];
       const double nrm[3] = {A.f_normal[3 * f], A.f_normal[3 * f + 1], A.f_normal[3 * f + 2]};
@@ -541,8 +564,36 @@ __global__ void __launch_bounds__(128, GKS_FACE_MINB) k_face(FaceArgs A) {
     pr = w[0] / (2.0 * w[4]);
     return true;
   };
+  // TAU mode 2: the right state's pressure only (the left one comes from
+  // the side loop), in the local frame like the loop's own states
+  auto press_r = [&](double& pl, double& pr) {
+    (void)pl;
+    const double x[3] = {A.fq_point[3 * i], A.fq_point[3 * i + 1], A.fq_point[3 * i + 2]};
+    double v[5], w[5], ql[5];
+    if (nb >= 0) {
+      const double xs[3] = {x[0] - A.f_shift[3 * f], x[1] - A.f_shift[3 * f + 1], x[2] - A.f_shift[3 * f + 2]};
+      eval_cell_value(false, xs, v);
+    } else {
+      eval_cell_value(true, x, v);
+      const DevPatch P = A.patches[p];
+      const double nrm[3] = {A.f_normal[3 * f], A.f_normal[3 * f + 1], A.f_normal[3 * f + 2]};
+      double vg[5];
+      if (!ghost_state(v, P, nrm, A.kc, vg)) {
+        ghost_fail = 1;
+        return false;
+      }
+#pragma unroll
+      for (int k = 0; k < 5; ++k) v[k] = vg[k];
+    }
+    to_local_state(v, A.f_frame + 9 * f, ql);
+    if (!cons_to_prim(ql, A.kc, w)) return false;
+    pr = w[0] / (2.0 * w[4]);
+    return true;
+  };
   double fl[5], pv[5];
-  const int rc = interface_flux_t<VISC, POINT, GKS_FACE_DEFER>(get, press, -1.0, dtf, A.mu, A.kc, fl, 0.0, pv);
+  int rc;
+  if (GKS_FACE_TAU == 2) rc = interface_flux_t<VISC, POINT, 2>(get, press_r, -1.0, dtf, A.mu, A.kc, fl, 0.0, pv);
+  else rc = interface_flux_t<VISC, POINT, GKS_FACE_TAU>(get, press, -1.0, dtf, A.mu, A.kc, fl, 0.0, pv);
   if (rc) {
     if (ghost_fail) {
       atomicCAS(A.status, 0, GKS_ERR_UNPHYSICAL);
