@@ -284,8 +284,9 @@ def kernel_model(solver, compact):
     from paper_2304_09485_b200 import _native as N
 
     lib = N.load()
-    info = [int(lib.gks_handle_info(solver._handle, k)) for k in range(9)]
-    nc, nf, nfq, nfi, nbf, nnz, K, M, S = info
+    info = [int(lib.gks_handle_info(solver._handle, k)) for k in range(11)]
+    nc, nf, nfq, nfi, nbf, nnz, K, M, S, _, nent = info
+    slots = os.environ.get("GKS_ASSEMBLE_SLOTS", "1") != "0"
     per_row = nnz / nc
     mf = os.environ.get("GKS_ROE_MF", "1") != "0"
     if mf:
@@ -301,7 +302,10 @@ def kernel_model(solver, compact):
         # bytes per launch (HBM-bound kernels), unique compulsory traffic
         "spmv_dinv": spmv,
         "jacobi_sweep": sweep,
-        "assemble": nfq * 40 + nc * (4 + 40) + (nfq * 2) * 4,
+        # slot assembly (residuals without the gradient update): a contiguous
+        # segmented sum of the signed contributions the face kernel wrote
+        "assemble": (nent * 40 + nc * (4 + 40)) if (slots and not compact) else
+                    (nfq * 40 + nc * (4 + 40) + (nfq * 2) * 4),
         "recon": nc * ((9 * K * 8 + K * 4 + M * 3 * S * 8 + M * S * 4 + M + 360 + 40 + 360) if not compact else
                        (9 * K * 8 + M * 21 * 8 + M * 8 + 360 + 40 + 120 + 360)),
         "jac_faces": nfi * (8 + 2 * 40 + 32 + 2 * 200 + 40),

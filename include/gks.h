@@ -312,7 +312,7 @@ int gks_frechet_matvec(GksHandle* h, const double* q, const double* grad, const 
 /* ------------------------------------------------------------------ */
 int gks_event_record(GksHandle* h, int slot);                 /* slot 0..7 */
 int gks_event_elapsed(GksHandle* h, int a, int b, double* ms);
-int64_t gks_handle_info(const GksHandle* h, int what);        /* 0 nc 1 nf 2 nfq 3 nfi 4 nbf 5 nnz 6 K 7 M 8 S 9 n_owned */
+int64_t gks_handle_info(const GksHandle* h, int what);        /* 0 nc 1 nf 2 nfq 3 nfi 4 nbf 5 nnz 6 K 7 M 8 S 9 n_owned 10 assembly entries */
 int gks_fp64_peak(double* tflops);                          /* DFMA throughput probe */
 int gks_host_pin(void* p, int64_t nbytes);                  /* cudaHostRegister a host buffer */
 int gks_host_unpin(void* p);

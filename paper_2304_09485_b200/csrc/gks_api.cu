@@ -342,6 +342,18 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
     }
     TRY(upload(H, &H->cfq_start, cnt.data(), nc + 1));
     TRY(upload(H, &H->cfq, list.data(), list.size()));
+    {
+      std::vector<int2> slot(nfq, make_int2(-1, -1));
+      const int64_t nent = cnt[H->n_owned];  // entries of owned cells (they come first)
+      H->nent = nent;
+      for (int64_t e = 0; e < nent; ++e) {
+        const int v = list[e];
+        if (v & 1) slot[v >> 1].y = (int)e;
+        else slot[v >> 1].x = (int)e;
+      }
+      TRY(upload(H, &H->fq_slot, slot.data(), slot.size()));
+      TRY(alloc(H, &H->slots, std::max<int64_t>(nent, 1) * 5));
+    }
   }
   {
     // local dt: owner faces then neighbour faces (stepping.py:144-154)
@@ -1223,6 +1235,7 @@ int64_t gks_handle_info(const GksHandle* G, int what) {
     case 7: return H->compact ? H->HM : H->M;               /* sub-stencil slots */
     case 8: return H->compact ? 7 : H->S;                   /* sub-stencil width */
     case 9: return H->n_owned;
+    case 10: return H->nent;  /* assembly entries (slots) of the owned cells */
     default: return -1;
   }
 }

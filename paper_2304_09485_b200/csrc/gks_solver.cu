@@ -454,6 +454,8 @@ struct FaceArgs {
   int want_point;
   int fq_nq;
   double* contrib;
+  const int2* fq_slot;  // slot mode (non-null): contributions go to the assembly slots
+  double* slots;
   double* qpt;
   int* status;
   const int* gate;
@@ -607,11 +609,29 @@ __global__ void __launch_bounds__(128, GKS_FACE_MINB) k_face(FaceArgs A) {
   if (wall) fl[0] = 0.0;
   const double* F = A.f_frame + 9 * f;
   const double ws = A.fq_ws[i];
-  double* out = A.contrib + i * 5;
-  out[0] = ws * fl[0];
-  out[4] = ws * fl[4];
+  double c[5];
+  c[0] = ws * fl[0];
+  c[4] = ws * fl[4];
 #pragma unroll
-  for (int d = 0; d < 3; ++d) out[1 + d] = ws * (F[d] * fl[1] + F[3 + d] * fl[2] + F[6 + d] * fl[3]);
+  for (int d = 0; d < 3; ++d) c[1 + d] = ws * (F[d] * fl[1] + F[3 + d] * fl[2] + F[6 + d] * fl[3]);
+  if (A.fq_slot) {
+    // owner entry -c, neighbour entry +c (stepping.py:225-228)
+    const int2 sl = A.fq_slot[i];
+    if (sl.x >= 0) {
+      double* so = A.slots + (int64_t)sl.x * 5;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) so[k] = -c[k];
+    }
+    if (sl.y >= 0) {
+      double* sn = A.slots + (int64_t)sl.y * 5;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) sn[k] = c[k];
+    }
+  } else {
+    double* out = A.contrib + i * 5;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) out[k] = c[k];
+  }
   if (POINT) {
     double* qp = A.qpt + i * 5;
     qp[0] = pv[0];
@@ -704,9 +724,24 @@ __global__ void k_assemble5(int64_t nc, const int* __restrict__ cfq_start, const
   double r = 0.0;
   double g[3] = {0.0, 0.0, 0.0};
   const bool wantg = grad_new != nullptr;
-  const int e1 = cfq_start[c + 1];
+  const int e0 = cfq_start[c], e1 = cfq_start[c + 1];
+  int e = e0;
+  if (!wantg) {
+    // batches of 8: all index loads, then all contribution loads in flight,
+    // then the sums in list order
+    for (; e + 8 <= e1; e += 8) {
+      int ce[8];
+      double cc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) ce[u] = __ldg(cfq + e + u);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) cc[u] = contrib[(int64_t)(ce[u] >> 1) * 5 + k];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) r = (ce[u] & 1) ? r + cc[u] : r - cc[u];
+    }
+  }
 #pragma unroll 4
-  for (int e = cfq_start[c]; e < e1; ++e) {
+  for (; e < e1; ++e) {
     const int ce = cfq[e];
     const int64_t i = ce >> 1;
     const bool is_nbr = ce & 1;
@@ -735,6 +770,32 @@ __global__ void k_assemble5(int64_t nc, const int* __restrict__ cfq_start, const
     const double V = vol[c];
 #pragma unroll
     for (int x = 0; x < 3; ++x) grad_new[(c * 3 + x) * 5 + k] = g[x] / V;
+  }
+}
+
+// Slot assembly: the face kernel has written every signed contribution into
+// its cell's CSR slot, so a cell's residual is a contiguous segmented sum
+// (one thread per (cell, component), coalesced 40-byte slot records, no
+// index walk).  Same entries in the same order with the same signs as
+// k_assemble5 (r - c == r + (-c)): bitwise-identical results.
+__global__ void k_assemble_slots(int64_t nc, const int* __restrict__ cfq_start, const double* __restrict__ slots,
+                                 const double* __restrict__ vol, double* __restrict__ res, const int* gate,
+                                 FrechetEpi fe) {
+  if (gate && !*gate) return;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nc * 5) return;
+  const int64_t c = t / 5;
+  const int k = (int)(t - c * 5);
+  const int e0 = cfq_start[c], e1 = cfq_start[c + 1];
+  double r = 0.0;
+#pragma unroll 4
+  for (int e = e0; e < e1; ++e) r += __ldcs(slots + (int64_t)e * 5 + k);
+  if (fe.out) {
+    const double sg = *fe.sigma;
+    const double d = sg == 0.0 ? 0.0 : (r - fe.r0[t]) / sg;
+    fe.out[t] = fe.mode ? (vol[c] / fe.dt[c]) * fe.v[t] - d : d;
+  } else {
+    res[t] = r;
   }
 }
 
@@ -873,6 +934,14 @@ int residual_device(Handle* H, const double* q, double* res, bool with_gradients
   A.want_point = with_gradients ? 1 : 0;
   A.fq_nq = H->fq_nq;
   A.contrib = H->contrib; A.qpt = H->qpt; A.status = H->status; A.gate = gate;
+  static const int slot_env = [] {
+    const char* e = getenv("GKS_ASSEMBLE_SLOTS");
+    return e ? atoi(e) : 0;
+  }();
+  // slot assembly for residuals without the gradient update
+  const bool slot_mode = slot_env && !with_gradients;
+  A.fq_slot = slot_mode ? H->fq_slot : nullptr;
+  A.slots = H->slots;
   const int fb = blocks_for(H->nfq, 128);
   if (H->model == 1) {
     if (with_gradients) GKS_LAUNCH(KC_FACE, (k_face<true, true>), fb, 128, 0, H->stream, A);
@@ -885,7 +954,10 @@ int residual_device(Handle* H, const double* q, double* res, bool with_gradients
     const char* e = getenv("GKS_ASSEMBLE5");
     return e ? atoi(e) : 1;
   }();
-  if (asm5)
+  if (slot_mode)
+    GKS_LAUNCH(KC_ASSEMBLE, k_assemble_slots, blocks_for(H->n_owned * 5, 160), 160, 0, H->stream, H->n_owned,
+               H->cfq_start, H->slots, H->vol, res, gate, fe ? *fe : FrechetEpi{});
+  else if (asm5)
     GKS_LAUNCH(KC_ASSEMBLE, k_assemble5, blocks_for(H->n_owned * 5, 160), 160, 0, H->stream, H->n_owned, H->cfq_start,
                H->cfq, H->contrib, H->qpt, H->fq_face, H->fq_ws, H->f_normal, H->vol, res,
                with_gradients ? H->grad_new : nullptr, gate, fe ? *fe : FrechetEpi{});

@@ -88,6 +88,13 @@ struct Handle {
   double *fq_point = nullptr, *fq_ws = nullptr;
   // cell -> fq CSR (assembly order), entries fq<<1 | is_neighbor
   int *cfq_start = nullptr, *cfq = nullptr;
+  // slot assembly: per fq point the CSR positions of its owner / neighbour
+  // entries (int2, -1 = none or not an owned cell); the face kernel writes
+  // its signed contribution into both, the assembly is a contiguous
+  // segmented sum (same order and signs as the CSR walk: bitwise equal)
+  int2* fq_slot = nullptr;
+  double* slots = nullptr;  // (nent, 5)
+  int64_t nent = 0;
   // cell -> face CSR for local dt (owner faces then neighbour faces), face<<1 | is_neighbor
   int *cdt_start = nullptr, *cdt = nullptr;
   // cell -> face CSR for the Jacobian diagonal, face<<1 | is_neighbor (interior own, interior nbr, boundary own)
