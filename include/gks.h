@@ -61,6 +61,22 @@ int gks_flux_batch(int64_t n, const double* wl, const double* wr, const double* 
                    const double* sr, const double* tau, const double* dt, const double* tp,
                    double gamma, double* flux_out, double* point_out);
 
+/* build_interface intermediates (flux.py:69-107, InterfaceBatch fields):
+   al, ar (n,3,5) micro-slopes, atl, atr (n,5) time slopes, w0 (n,5)
+   compatibility state, abar (n,3,5), atbar (n,5) its slopes; sl/sr NULL =
+   zero slopes */
+int gks_interface_data(int64_t n, const double* wl, const double* wr, const double* sl,
+                       const double* sr, double gamma, double* al, double* ar, double* atl,
+                       double* atr, double* w0, double* abar, double* atbar);
+/* solve_micro_slope (kinetic.py:271-302, time_slope = 0: in = dq (n,5)) or
+   solve_time_slope (:305-312, time_slope = 1: in = micro-slopes (n,3,5)) of
+   primitive states w (n,5) -> out (n,5) */
+int gks_slopes(int64_t n, const double* w, const double* in, int time_slope, double gamma, double* out);
+/* build_moments (kinetic.py:140-162): order-first (order+1, n) tables of
+   <u^p> full / u>0 / u<0, <v^p>, <w^p> and (3, n) <xi^2s> */
+int gks_moment_table(int64_t n, const double* w, double gamma, int order, double* u_full,
+                     double* u_pos, double* u_neg, double* v_full, double* w_full, double* xi);
+
 /* ------------------------------------------------------------------ */
 /* Mesh view passed to the native setup and to gks_create.  All arrays   */
 /* are the host Mesh arrays of paper_2304_09485_b200.mesh (same layout   */
@@ -231,6 +247,15 @@ int gks_residual(GksHandle* h, const double* q, const double* grad, const double
 /* Solver._boundary_ghosts (stepping.py:242-249): ghost of the cell-average
    owner state per boundary face, (nbf,5) in ascending boundary-face order */
 int gks_boundary_ghosts(GksHandle* h, const double* q, double* ghosts_out);
+/* boundary.ghost_state / ghost_gradients (boundary.py:66-171) for n points
+   of one patch: conserved q (n,5), outward normals (n,3), optional
+   gradients (n,3,5) -> q_out (n,5), grad_out (n,3,5) */
+struct GksPatchDesc;
+int gks_ghost_batch(int64_t n, const struct GksPatchDesc* patch, const double* q, const double* normal,
+                    const double* grad, double gamma, double* q_out, double* grad_out);
+/* hweno.update_gradients (hweno.py:172-194): cell-averaged gradients
+   (nc,3,5) from face-point values (nfq,5) by the Gauss theorem */
+int gks_update_gradients(GksHandle* h, const double* qpt, double* grad_out);
 int64_t gks_num_boundary_faces(const GksHandle* h);
 
 /* ------------------------------------------------------------------ */

@@ -164,6 +164,11 @@ SIGNATURES = [
                                  c_double_p, c_double_p, c_double_p, C.c_double, c_double_p,
                                  c_double_p]),
     ("gks_flux_bench", C.c_int, [C.c_int64, C.c_int, C.c_double, c_double_p]),
+    ("gks_interface_data", C.c_int, [C.c_int64, c_double_p, c_double_p, c_double_p, c_double_p, C.c_double,
+                                     c_double_p, c_double_p, c_double_p, c_double_p, c_double_p, c_double_p,
+                                     c_double_p]),
+    ("gks_moment_table", C.c_int, [C.c_int64, c_double_p, C.c_double, C.c_int, c_double_p, c_double_p,
+                                   c_double_p, c_double_p, c_double_p, c_double_p]),
     ("gks_setup_build", C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     ("gks_setup_free", None, [C.c_void_p]),
     ("gks_setup_query", C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
@@ -185,6 +190,10 @@ SIGNATURES = [
     ("gks_residual", C.c_int, [C.c_void_p, c_double_p, c_double_p, c_double_p, C.c_int, c_double_p,
                                c_double_p]),
     ("gks_boundary_ghosts", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
+    ("gks_update_gradients", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
+    ("gks_ghost_batch", C.c_int, [C.c_int64, C.c_void_p, c_double_p, c_double_p, c_double_p, C.c_double,
+                                  c_double_p, c_double_p]),
+    ("gks_slopes", C.c_int, [C.c_int64, c_double_p, c_double_p, C.c_int, C.c_double, c_double_p]),
     ("gks_num_boundary_faces", C.c_int64, [C.c_void_p]),
     ("gks_assemble_jacobian", C.c_int, [C.c_void_p, c_double_p, c_double_p, c_double_p]),
     ("gks_jacobian", C.c_void_p, [C.c_void_p]),

@@ -59,7 +59,7 @@ struct GksHandle {
   int graph = -1;               // CUDA-graph steps: -1 env default (GKS_GRAPH), 0 off, 1 on
   // staging buffers of the host-API entry points (residual, local dt,
   // Jacobian, Frechet matvec): they never overwrite the resident state
-  double *api_q = nullptr, *api_grad = nullptr, *api_dt = nullptr;
+  double *api_q = nullptr, *api_grad = nullptr, *api_dt = nullptr, *api_qpt = nullptr;
 };
 
 // Swaps the handle's state pointers for the API staging buffers for the
@@ -189,6 +189,22 @@ static bool hweno_shape(int HA, int HG, int M, int* At, int* Gt, int* Mt) {
   return false;
 }
 
+// PatchSpec (boundary.py:26-48) -> device record: reference state as a
+// primitive (rho, U, V, W, lam) (boundary.py:50-53), wall flags
+static DevPatch dev_patch(const GksPatchDesc& d) {
+  DevPatch P;
+  P.kind = d.kind;
+  P.wall = d.kind == PK_WALL_NOSLIP_ISOTHERMAL || d.kind == PK_WALL_NOSLIP_ADIABATIC ||
+           d.kind == PK_WALL_SLIP_ADIABATIC;
+  P.wall_moving = d.velocity[0] != 0.0 || d.velocity[1] != 0.0 || d.velocity[2] != 0.0;
+  P.ref[0] = d.reference[0]; P.ref[1] = d.reference[1]; P.ref[2] = d.reference[2];
+  P.ref[3] = d.reference[3];
+  P.ref[4] = d.reference[0] / (2.0 * d.reference[4]);
+  P.lambda_wall = d.lambda_wall;
+  for (int k = 0; k < 3; ++k) P.vel[k] = d.velocity[k];
+  return P;
+}
+
 int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const GksOptions* o, int device,
                   const GksDomainDesc* dom) {
   Handle* H = &G->H;
@@ -231,19 +247,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   }
   H->npatch = o->npatch;
   H->patches_h.resize(std::max(o->npatch, 1));
-  for (int p = 0; p < o->npatch; ++p) {
-    const GksPatchDesc& d = o->patches[p];
-    DevPatch& P = H->patches_h[p];
-    P.kind = d.kind;
-    P.wall = d.kind == PK_WALL_NOSLIP_ISOTHERMAL || d.kind == PK_WALL_NOSLIP_ADIABATIC ||
-             d.kind == PK_WALL_SLIP_ADIABATIC;
-    P.wall_moving = d.velocity[0] != 0.0 || d.velocity[1] != 0.0 || d.velocity[2] != 0.0;
-    P.ref[0] = d.reference[0]; P.ref[1] = d.reference[1]; P.ref[2] = d.reference[2];
-    P.ref[3] = d.reference[3];
-    P.ref[4] = d.reference[0] / (2.0 * d.reference[4]);
-    P.lambda_wall = d.lambda_wall;
-    for (int k = 0; k < 3; ++k) P.vel[k] = d.velocity[k];
-  }
+  for (int p = 0; p < o->npatch; ++p) H->patches_h[p] = dev_patch(o->patches[p]);
   for (int64_t f = 0; f < nf; ++f) {
     if (m->face_neighbor[f] < 0) {
       const int p = (int)m->face_patch[f];
@@ -734,6 +738,35 @@ int gks_residual(GksHandle* G, const double* q, const double* grad, const double
   GKS_CUDA(cudaMemcpyAsync(res_out, H->res, H->nc * 5 * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
   if (with_gradients && grad_out)
     GKS_CUDA(cudaMemcpyAsync(grad_out, H->grad_new, H->nc * 15 * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaStreamSynchronize(H->stream));
+  return GKS_OK;
+}
+
+int gks_ghost_batch(int64_t n, const GksPatchDesc* patch, const double* q, const double* normal,
+                    const double* grad, double gamma, double* q_out, double* grad_out) {
+  set_error_index(-1);
+  if (n < 0 || !patch || !q || !normal || !q_out || (grad && !grad_out)) {
+    set_error("gks_ghost_batch: bad arguments");
+    return GKS_ERR_BAD_ARG;
+  }
+  if (patch->kind < PK_WALL_NOSLIP_ISOTHERMAL || patch->kind > PK_SUPERSONIC_OUTLET) {
+    set_error("patch kind %d has no ghost state", patch->kind);
+    return GKS_ERR_BAD_ARG;
+  }
+  if (n == 0) return GKS_OK;
+  if (int rc = no_device()) return rc;
+  return ghost_batch_device(n, dev_patch(*patch), q, normal, grad, make_kin(gamma), q_out, grad_out);
+}
+
+int gks_update_gradients(GksHandle* G, const double* qpt, double* grad_out) {
+  Handle* H = &G->H;
+  set_error_index(-1);
+  GKS_CUDA(cudaSetDevice(H->device));
+  if (!G->api_qpt) TRY(alloc(H, &G->api_qpt, H->nfq * 5));
+  GKS_CUDA(cudaMemcpyAsync(G->api_qpt, qpt, H->nfq * 5 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  TRY(gauss_gradients_device(H, G->api_qpt, G->api_grad));
+  GKS_CUDA(cudaMemcpyAsync(grad_out, G->api_grad, H->n_owned * 15 * sizeof(double), cudaMemcpyDeviceToHost,
+                           H->stream));
   GKS_CUDA(cudaStreamSynchronize(H->stream));
   return GKS_OK;
 }

@@ -2,6 +2,7 @@
 // error plumbing.  Replaces gks3d flux.build_interface / evolve_flux /
 // point_value (flux.py:69-188) for arbitrary point batches.
 #include <stdarg.h>
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <vector>
@@ -130,6 +131,162 @@ __global__ void __launch_bounds__(128, GKS_FLUX_MINB) k_flux_batch(int64_t n, co
 #pragma unroll
     for (int k = 0; k < 5; ++k) point[i * 5 + k] = p[k];
   }
+}
+
+// Interface intermediates of build_interface (flux.py:69-107): micro-slopes
+// al, ar (n,3,5), time slopes atl, atr (n,5), the compatibility state w0
+// (n,5) and its slopes abar (n,3,5), atbar (n,5) -- the same device
+// functions and order as interface_flux_t's side loop.
+__global__ void k_interface_data(int64_t n, const double* __restrict__ wl, const double* __restrict__ wr,
+                                 const double* __restrict__ sl, const double* __restrict__ sr, KinConst kc,
+                                 double* __restrict__ al, double* __restrict__ ar, double* __restrict__ atl,
+                                 double* __restrict__ atr, double* __restrict__ w0o, double* __restrict__ abar,
+                                 double* __restrict__ atbar, int* status) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double q0[5] = {0, 0, 0, 0, 0};
+  double dqa[3][5] = {};
+  const double zero5[5] = {0, 0, 0, 0, 0};
+  for (int side = 0; side < 2; ++side) {
+    const double* W = side ? wr : wl;
+    const double* S = side ? sr : sl;
+    double w[5], a[3][5], A[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) w[k] = W[i * 5 + k];
+    if (!prim_ok(w)) {
+      raise_dev(status, GKS_ERR_UNPHYSICAL, (int)i);
+      return;
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int k = 0; k < 5; ++k) a[d][k] = S ? S[i * 15 + d * 5 + k] : 0.0;
+    Maxw m;
+    maxw_full(m, w, kc);
+    const SlopeConst sc = slope_const(w, kc, m.h);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) micro_slope(sc, a[d], a[d]);
+    double D[5];
+    wmom<0, true>(m, zero5, a, 1.0, D);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) D[k] = -w[0] * D[k];
+    micro_slope(sc, D, A);
+    double* ao = side ? ar : al;
+    double* to = side ? atr : atl;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int k = 0; k < 5; ++k) ao[i * 15 + d * 5 + k] = a[d][k];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) to[i * 5 + k] = A[k];
+    maxw_half_u(m, w, side ? -1.0 : 1.0);
+    const double* const sv[3] = {a[0], a[1], a[2]};
+    double* const av[3] = {dqa[0], dqa[1], dqa[2]};
+    gram_scatter<0, 3>(m, w[0], sv, av, q0);
+  }
+  double w0[5], ab[3][5], Ab[5];
+  if (!cons_to_prim(q0, kc, w0)) {
+    raise_dev(status, GKS_ERR_UNPHYSICAL, (int)i);
+    return;
+  }
+  Maxw m0;
+  maxw_full(m0, w0, kc);
+  const SlopeConst sc0 = slope_const(w0, kc, m0.h);
+#pragma unroll
+  for (int d = 0; d < 3; ++d) micro_slope(sc0, dqa[d], ab[d]);
+  double D[5];
+  wmom<0, true>(m0, zero5, ab, 1.0, D);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) D[k] = -w0[0] * D[k];
+  micro_slope(sc0, D, Ab);
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    w0o[i * 5 + k] = w0[k];
+    atbar[i * 5 + k] = Ab[k];
+  }
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int k = 0; k < 5; ++k) abar[i * 15 + d * 5 + k] = ab[d][k];
+}
+
+// solve_micro_slope (kinetic.py:271-302) and solve_time_slope (:305-312)
+// of a state batch: a (n,5) from dq (n,5); A (n,5) from a (n,3,5)
+__global__ void k_slopes(int64_t n, const double* __restrict__ w, const double* __restrict__ in, int time_slope,
+                         KinConst kc, double* __restrict__ out, int* status) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double wi[5], r[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) wi[k] = w[i * 5 + k];
+  if (!prim_ok(wi)) {
+    raise_dev(status, GKS_ERR_UNPHYSICAL, (int)i);
+    return;
+  }
+  Maxw m;
+  maxw_full(m, wi, kc);
+  const SlopeConst sc = slope_const(wi, kc, m.h);
+  if (time_slope) {
+    double a[3][5], D[5];
+    const double zero5[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int k = 0; k < 5; ++k) a[d][k] = in[i * 15 + d * 5 + k];
+    wmom<0, true>(m, zero5, a, 1.0, D);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) D[k] = -wi[0] * D[k];
+    micro_slope(sc, D, r);
+  } else {
+    double dq[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) dq[k] = in[i * 5 + k];
+    micro_slope(sc, dq, r);
+  }
+#pragma unroll
+  for (int k = 0; k < 5; ++k) out[i * 5 + k] = r[k];
+}
+
+// MomentTable (kinetic.py:90-162): order-first tables <u^p> full / u>0 /
+// u<0, <v^p>, <w^p> (p <= order) and <xi^2s> (s <= 2) of a state batch.
+__global__ void k_moment_table(int64_t n, const double* __restrict__ w, KinConst kc, int order,
+                               double* __restrict__ uf, double* __restrict__ up, double* __restrict__ un,
+                               double* __restrict__ vf, double* __restrict__ wf, double* __restrict__ xi) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double lam = w[i * 5 + 4], h = 0.5 / lam;
+  auto full = [&](double mean, double* out) {
+    double m2 = 1.0, m1 = mean;
+    out[i] = 1.0;
+    if (order >= 1) out[n + i] = mean;
+    for (int p = 2; p <= order; ++p) {
+      const double m = mean * m1 + (double)(p - 1) * h * m2;
+      out[p * n + i] = m;
+      m2 = m1;
+      m1 = m;
+    }
+  };
+  full(w[i * 5 + 1], uf);
+  full(w[i * 5 + 2], vf);
+  full(w[i * 5 + 3], wf);
+  const double u = w[i * 5 + 1], sq = sqrt(lam);
+  const double gauss = 0.5 * exp(-lam * u * u) / sqrt(M_PI * lam);
+  for (int side = 0; side < 2; ++side) {
+    double* out = side ? un : up;
+    double m2 = 0.5 * erfc(side ? sq * u : -sq * u);
+    double m1 = u * m2 + (side ? -gauss : gauss);
+    out[i] = m2;
+    if (order >= 1) out[n + i] = m1;
+    for (int p = 2; p <= order; ++p) {
+      const double m = u * m1 + (double)(p - 1) * h * m2;
+      out[p * n + i] = m;
+      m2 = m1;
+      m1 = m;
+    }
+  }
+  xi[i] = 1.0;
+  xi[n + i] = kc.nd / (2.0 * lam);
+  xi[2 * n + i] = kc.nd * (kc.nd + 2.0) / (4.0 * lam * lam);
 }
 
 // FP64 DFMA throughput probe (roofline denominator; not in MEASURED_PEAKS.json)
@@ -287,6 +444,142 @@ int gks_flux_batch(int64_t n, const double* wl, const double* wr, const double* 
   if (d_f) cudaFree(d_f);
   if (d_p) cudaFree(d_p);
   return rc;
+}
+
+namespace {
+// device copies of host arrays for the batch entry points (freed on scope exit)
+struct DevArrays {
+  std::vector<void*> p;
+  ~DevArrays() {
+    for (void* x : p) cudaFree(x);
+  }
+  double* in(const double* h, size_t n) {
+    if (!h) return nullptr;
+    double* d = out(n);
+    if (d && cudaMemcpy(d, h, n * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+    return d;
+  }
+  double* out(size_t n) {
+    void* d = nullptr;
+    if (cudaMalloc(&d, std::max<size_t>(n, 1) * sizeof(double)) != cudaSuccess) return nullptr;
+    p.push_back(d);
+    return (double*)d;
+  }
+};
+
+int device_present(const char* what) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    set_error("%s: no CUDA device visible", what);
+    return GKS_ERR_NO_DEVICE;
+  }
+  return GKS_OK;
+}
+}  // namespace
+
+int gks_interface_data(int64_t n, const double* wl, const double* wr, const double* sl, const double* sr,
+                       double gamma, double* al, double* ar, double* atl, double* atr, double* w0,
+                       double* abar, double* atbar) {
+  g_err_index = -1;
+  if (n < 0 || !wl || !wr || !al || !ar || !atl || !atr || !w0 || !abar || !atbar) {
+    set_error("gks_interface_data: bad arguments");
+    return GKS_ERR_BAD_ARG;
+  }
+  if (n == 0) return GKS_OK;
+  if (int rc = device_present("gks_interface_data")) return rc;
+  DevArrays D;
+  const size_t n5 = (size_t)n * 5, n15 = 3 * n5;
+  double *dwl = D.in(wl, n5), *dwr = D.in(wr, n5), *dsl = D.in(sl, n15), *dsr = D.in(sr, n15);
+  double *dal = D.out(n15), *dar = D.out(n15), *datl = D.out(n5), *datr = D.out(n5), *dw0 = D.out(n5);
+  double *dab = D.out(n15), *datb = D.out(n5);
+  int* dst = (int*)D.out(1);
+  if (!dwl || !dwr || (sl && !dsl) || (sr && !dsr) || !dal || !dar || !datl || !datr || !dw0 || !dab || !datb ||
+      !dst) {
+    set_error("gks_interface_data: device allocation / copy failed");
+    return GKS_ERR_CUDA;
+  }
+  const int st0[2] = {0, 0x7fffffff};
+  GKS_CUDA(cudaMemcpy(dst, st0, sizeof(st0), cudaMemcpyHostToDevice));
+  GKS_LAUNCH(KC_FLUXBATCH, k_interface_data, blocks_for(n, 128), 128, 0, 0, n, dwl, dwr, dsl, dsr, make_kin(gamma),
+             dal, dar, datl, datr, dw0, dab, datb, dst);
+  GKS_CUDA(cudaGetLastError());
+  int st[2];
+  GKS_CUDA(cudaMemcpy(st, dst, sizeof(st), cudaMemcpyDeviceToHost));
+  if (st[0]) {
+    set_error("unphysical interface state at point %d", st[1]);
+    g_err_index = st[1];
+    return st[0];
+  }
+  GKS_CUDA(cudaMemcpy(al, dal, n15 * 8, cudaMemcpyDeviceToHost));
+  GKS_CUDA(cudaMemcpy(ar, dar, n15 * 8, cudaMemcpyDeviceToHost));
+  GKS_CUDA(cudaMemcpy(atl, datl, n5 * 8, cudaMemcpyDeviceToHost));
+  GKS_CUDA(cudaMemcpy(atr, datr, n5 * 8, cudaMemcpyDeviceToHost));
+  GKS_CUDA(cudaMemcpy(w0, dw0, n5 * 8, cudaMemcpyDeviceToHost));
+  GKS_CUDA(cudaMemcpy(abar, dab, n15 * 8, cudaMemcpyDeviceToHost));
+  GKS_CUDA(cudaMemcpy(atbar, datb, n5 * 8, cudaMemcpyDeviceToHost));
+  return GKS_OK;
+}
+
+int gks_slopes(int64_t n, const double* w, const double* in, int time_slope, double gamma, double* out) {
+  g_err_index = -1;
+  if (n < 0 || !w || !in || !out) {
+    set_error("gks_slopes: bad arguments");
+    return GKS_ERR_BAD_ARG;
+  }
+  if (n == 0) return GKS_OK;
+  if (int rc = device_present("gks_slopes")) return rc;
+  DevArrays D;
+  const size_t n5 = (size_t)n * 5;
+  double *dw = D.in(w, n5), *din = D.in(in, time_slope ? 3 * n5 : n5), *dout = D.out(n5);
+  int* dst = (int*)D.out(1);
+  if (!dw || !din || !dout || !dst) {
+    set_error("gks_slopes: device allocation / copy failed");
+    return GKS_ERR_CUDA;
+  }
+  const int st0[2] = {0, 0x7fffffff};
+  GKS_CUDA(cudaMemcpy(dst, st0, sizeof(st0), cudaMemcpyHostToDevice));
+  GKS_LAUNCH(KC_FLUXBATCH, k_slopes, blocks_for(n, 128), 128, 0, 0, n, dw, din, time_slope, make_kin(gamma), dout,
+             dst);
+  GKS_CUDA(cudaGetLastError());
+  int st[2];
+  GKS_CUDA(cudaMemcpy(st, dst, sizeof(st), cudaMemcpyDeviceToHost));
+  if (st[0]) {
+    set_error("invalid primitive state at %d", st[1]);
+    g_err_index = st[1];
+    return st[0];
+  }
+  GKS_CUDA(cudaMemcpy(out, dout, n5 * 8, cudaMemcpyDeviceToHost));
+  return GKS_OK;
+}
+
+int gks_moment_table(int64_t n, const double* w, double gamma, int order, double* u_full, double* u_pos,
+                     double* u_neg, double* v_full, double* w_full, double* xi) {
+  g_err_index = -1;
+  if (n < 0 || order < 1 || order > 32 || !w || !u_full || !u_pos || !u_neg || !v_full || !w_full || !xi) {
+    set_error("gks_moment_table: bad arguments");
+    return GKS_ERR_BAD_ARG;
+  }
+  if (n == 0) return GKS_OK;
+  if (int rc = device_present("gks_moment_table")) return rc;
+  DevArrays D;
+  const size_t no = (size_t)(order + 1) * n;
+  double *dw = D.in(w, (size_t)n * 5), *uf = D.out(no), *up = D.out(no), *un = D.out(no), *vf = D.out(no);
+  double *wf = D.out(no), *dxi = D.out((size_t)3 * n);
+  if (!dw || !uf || !up || !un || !vf || !wf || !dxi) {
+    set_error("gks_moment_table: device allocation / copy failed");
+    return GKS_ERR_CUDA;
+  }
+  GKS_LAUNCH(KC_FLUXBATCH, k_moment_table, blocks_for(n, 128), 128, 0, 0, n, dw, make_kin(gamma), order, uf, up, un,
+             vf, wf, dxi);
+  GKS_CUDA(cudaGetLastError());
+  GKS_CUDA(cudaMemcpy(u_full, uf, no * 8, cudaMemcpyDeviceToHost));
+  GKS_CUDA(cudaMemcpy(u_pos, up, no * 8, cudaMemcpyDeviceToHost));
+  GKS_CUDA(cudaMemcpy(u_neg, un, no * 8, cudaMemcpyDeviceToHost));
+  GKS_CUDA(cudaMemcpy(v_full, vf, no * 8, cudaMemcpyDeviceToHost));
+  GKS_CUDA(cudaMemcpy(w_full, wf, no * 8, cudaMemcpyDeviceToHost));
+  GKS_CUDA(cudaMemcpy(xi, dxi, (size_t)3 * n * 8, cudaMemcpyDeviceToHost));
+  return GKS_OK;
 }
 
 // Kernel-only timing of the fused interface flux on n device-resident random

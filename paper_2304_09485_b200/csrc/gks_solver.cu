@@ -969,6 +969,83 @@ int residual_device(Handle* H, const double* q, double* res, bool with_gradients
   return GKS_OK;
 }
 
+// ghost_state / ghost_gradients (boundary.py:66-171) of a batch of points
+// on one patch: the device functions the face kernel fuses
+__global__ void k_ghost_batch(int64_t n, DevPatch P, const double* __restrict__ q, const double* __restrict__ nrm,
+                              const double* __restrict__ grad, KinConst kc, double* __restrict__ qg,
+                              double* __restrict__ gg, int* status) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double qi[5], out[5];
+  for (int k = 0; k < 5; ++k) qi[k] = q[i * 5 + k];
+  const double nv[3] = {nrm[i * 3], nrm[i * 3 + 1], nrm[i * 3 + 2]};
+  if (!ghost_state(qi, P, nv, kc, out)) {
+    raise_dev(status, GKS_ERR_UNPHYSICAL, (int)i);
+    return;
+  }
+  for (int k = 0; k < 5; ++k) qg[i * 5 + k] = out[k];
+  if (grad) {
+    double g[3][5], o[3][5];
+    for (int x = 0; x < 3; ++x)
+      for (int k = 0; k < 5; ++k) g[x][k] = grad[(i * 3 + x) * 5 + k];
+    ghost_gradients(g, P, nv, o);
+    for (int x = 0; x < 3; ++x)
+      for (int k = 0; k < 5; ++k) gg[(i * 3 + x) * 5 + k] = o[x][k];
+  }
+}
+
+int ghost_batch_device(int64_t n, const DevPatch& P, const double* q, const double* nrm, const double* grad,
+                       const KinConst& kc, double* q_out, double* grad_out) {
+  std::vector<void*> bufs;
+  auto dev = [&](size_t cnt) -> double* {
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max<size_t>(cnt, 1) * sizeof(double)) != cudaSuccess) return nullptr;
+    bufs.push_back(p);
+    return (double*)p;
+  };
+  struct Free {
+    std::vector<void*>& b;
+    ~Free() {
+      for (void* p : b) cudaFree(p);
+    }
+  } fr{bufs};
+  double *dq = dev(n * 5), *dn = dev(n * 3), *dg = grad ? dev(n * 15) : nullptr, *dqo = dev(n * 5);
+  double* dgo = grad ? dev(n * 15) : nullptr;
+  int* dst = (int*)dev(1);
+  if (!dq || !dn || !dqo || !dst || (grad && (!dg || !dgo))) {
+    set_error("ghost batch: device allocation failed");
+    return GKS_ERR_CUDA;
+  }
+  GKS_CUDA(cudaMemcpy(dq, q, n * 5 * sizeof(double), cudaMemcpyHostToDevice));
+  GKS_CUDA(cudaMemcpy(dn, nrm, n * 3 * sizeof(double), cudaMemcpyHostToDevice));
+  if (grad) GKS_CUDA(cudaMemcpy(dg, grad, n * 15 * sizeof(double), cudaMemcpyHostToDevice));
+  const int st0[2] = {0, 0x7fffffff};
+  GKS_CUDA(cudaMemcpy(dst, st0, sizeof(st0), cudaMemcpyHostToDevice));
+  GKS_LAUNCH(KC_GHOST, k_ghost_batch, blocks_for(n, TPB), TPB, 0, 0, n, P, dq, dn, dg, kc, dqo, dgo, dst);
+  GKS_CUDA(cudaGetLastError());
+  int st[2];
+  GKS_CUDA(cudaMemcpy(st, dst, sizeof(st), cudaMemcpyDeviceToHost));
+  if (st[0]) {
+    set_error_index(st[1]);
+    set_error("unphysical interior state at point %d", st[1]);
+    return st[0];
+  }
+  GKS_CUDA(cudaMemcpy(q_out, dqo, n * 5 * sizeof(double), cudaMemcpyDeviceToHost));
+  if (grad) GKS_CUDA(cudaMemcpy(grad_out, dgo, n * 15 * sizeof(double), cudaMemcpyDeviceToHost));
+  return GKS_OK;
+}
+
+// Gauss-theorem gradient of face-point values alone (hweno.py:172-194):
+// the assembly kernel with zero flux contributions
+int gauss_gradients_device(Handle* H, const double* qpt, double* grad_out) {
+  GKS_CUDA(cudaMemsetAsync(H->contrib, 0, (size_t)H->nfq * 5 * sizeof(double), H->stream));
+  GKS_LAUNCH(KC_ASSEMBLE, k_assemble5, blocks_for(H->n_owned * 5, 160), 160, 0, H->stream, H->n_owned, H->cfq_start,
+             H->cfq, H->contrib, qpt, H->fq_face, H->fq_ws, H->f_normal, H->vol, H->res2, grad_out, nullptr,
+             FrechetEpi{});
+  GKS_CUDA(cudaGetLastError());
+  return GKS_OK;
+}
+
 int boundary_ghosts_device(Handle* H, const double* q) {
   if (H->nbf == 0) return GKS_OK;
   GKS_LAUNCH(KC_GHOST, k_boundary_ghosts, blocks_for(H->nbf, TPB), TPB, 0, H->stream, H->nbf, H->boundary_faces, H->f_own,

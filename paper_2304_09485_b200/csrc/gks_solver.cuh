@@ -309,6 +309,9 @@ double* comm_red_buffer(Comm* c, KrylovWS* W);
 int comm_red_final(Comm* c, KrylovWS* W, int ns, int nm, const RedOut& out, const int* gate, cudaStream_t s);
 int local_dt_device(Handle* H);
 int boundary_ghosts_device(Handle* H, const double* q);
+int gauss_gradients_device(Handle* H, const double* qpt, double* grad_out);
+int ghost_batch_device(int64_t n, const DevPatch& P, const double* q, const double* nrm, const double* grad,
+                       const KinConst& kc, double* q_out, double* grad_out);
 int jacobian_device(Handle* H, const double* q, bool ghosts_given);
 void count_launch(int n);
 void set_error_index(int64_t i);

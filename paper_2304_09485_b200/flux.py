@@ -2,9 +2,12 @@
 
 Mirrors gks3d/flux.py: build_interface (:69-107), evolve_flux (:162-179),
 point_value (:182-188), kfvs_flux (:200-208), collision_time (:211-227),
-rotate_to_local / rotate_to_global (:230-243).  The interface distribution
-is evaluated by the fused sm_100a kernel behind gks_flux_batch; the batch
-object only carries the local states and slopes.
+rotate_to_local / rotate_to_global (:230-243), euler_flux_local
+(:246-260), compatibility_residual (:263-268).  The interface distribution
+is evaluated by the fused sm_100a kernel behind gks_flux_batch; the
+InterfaceBatch also carries the reference's intermediates (micro-slopes,
+time slopes, compatibility state and its slopes, from gks_interface_data)
+and the three moment tables (build_moments, gks_moment_table).
 """
 
 from __future__ import annotations
@@ -14,16 +17,30 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as N
-from .kinetic import DEFAULT_GAMMA, UnphysicalStateError
+from .kinetic import DEFAULT_GAMMA, MomentTable, UnphysicalStateError, build_moments, psi_moments
 
 
 @dataclass
 class InterfaceBatch:
+    """States, micro-slopes and compatibility data of a point batch
+    (flux.py:34-66); sl / sr keep the conserved slopes the device flux
+    kernel starts from."""
+
     wl: np.ndarray
     wr: np.ndarray
     sl: np.ndarray
     sr: np.ndarray
     gamma: float = DEFAULT_GAMMA
+    al: np.ndarray = None   # (n, 3, 5) left micro-slopes along the local axes
+    ar: np.ndarray = None
+    atl: np.ndarray = None  # (n, 5) left time slope
+    atr: np.ndarray = None
+    w0: np.ndarray = None   # (n, 5) compatibility (equilibrium) state
+    abar: np.ndarray = None
+    atbar: np.ndarray = None
+    tab_l: MomentTable = None
+    tab_r: MomentTable = None
+    tab_0: MomentTable = None
 
     @property
     def n(self):
@@ -44,7 +61,16 @@ def build_interface(wl, wr, slopes_l=None, slopes_r=None, gamma: float = DEFAULT
     n = wl.shape[0]
     sl = np.zeros((n, 3, 5)) if slopes_l is None else N.f64(slopes_l, (n, 3, 5))
     sr = np.zeros((n, 3, 5)) if slopes_r is None else N.f64(slopes_r, (n, 3, 5))
-    return InterfaceBatch(wl, wr, sl, sr, gamma)
+    out = {k: np.empty((n, 3, 5) if k in ("al", "ar", "abar") else (n, 5))
+           for k in ("al", "ar", "atl", "atr", "w0", "abar", "atbar")}
+    lib = N.load()
+    rc = lib.gks_interface_data(n, N.dptr(wl), N.dptr(wr), N.dptr(sl), N.dptr(sr), float(gamma),
+                                *(N.dptr(out[k]) for k in ("al", "ar", "atl", "atr", "w0", "abar", "atbar")))
+    if rc == N.GKS_ERR_UNPHYSICAL:
+        raise UnphysicalStateError(lib.gks_last_error().decode())
+    N.check(rc)
+    return InterfaceBatch(wl, wr, sl, sr, gamma, tab_l=build_moments(wl, gamma), tab_r=build_moments(wr, gamma),
+                          tab_0=build_moments(out["w0"], gamma), **out)
 
 
 def _run(ib: InterfaceBatch, tau, dt, tp):
@@ -106,6 +132,28 @@ def rotate_to_global(q, frame):
     out = q.copy()
     out[..., 1:4] = np.einsum("...ji,...j->...i", frame, q[..., 1:4])
     return out
+
+
+def euler_flux_local(w, gamma: float = DEFAULT_GAMMA):
+    """Analytic Euler flux of a local-frame primitive state along the normal (flux.py:246-260)."""
+    from .kinetic import primitive_to_conserved
+
+    w = np.atleast_2d(np.asarray(w, dtype=float))
+    q = primitive_to_conserved(w, gamma)
+    p = w[:, 0] / (2.0 * w[:, 4])
+    u = w[:, 1]
+    out = q * u[:, None]
+    out[:, 1] += p
+    out[:, 4] += p * u
+    return out
+
+
+def compatibility_residual(ib: InterfaceBatch):
+    """max |rho0 <psi>_0 - (rho_l <psi>_{l,u>0} + rho_r <psi>_{r,u<0})| (flux.py:263-268)."""
+    lhs = ib.w0[:, 0, None] * psi_moments(ib.tab_0, 0, 0, 0)
+    rhs = ib.wl[:, 0, None] * psi_moments(ib.tab_l, 0, 0, 0, umode="pos") + \
+        ib.wr[:, 0, None] * psi_moments(ib.tab_r, 0, 0, 0, umode="neg")
+    return float(np.max(np.abs(lhs - rhs)))
 
 
 def random_interface_inputs(rng, n, slope_scale=0.3):

@@ -52,7 +52,10 @@ def make_flux():
     ib = build_interface(wl, wr, sl, sr)
     out.update(wl=wl, wr=wr, sl=sl, sr=sr, tau=tau, dt=dt, tp=tp,
                flux=evolve_flux(ib, tau, dt), point=point_value(ib, tau, tp),
-               w0=ib.w0, abar=ib.abar, atbar=ib.atbar, al=ib.al, atl=ib.atl)
+               w0=ib.w0, abar=ib.abar, atbar=ib.atbar, al=ib.al, atl=ib.atl, ar=ib.ar, atr=ib.atr)
+    for side, tab in (("l", ib.tab_l), ("r", ib.tab_r), ("0", ib.tab_0)):
+        for name in ("u_full", "u_pos", "u_neg", "v_full", "w_full", "xi"):
+            out[f"tab_{side}_{name}"] = getattr(tab, name)
     # 2) a wider-state sweep (large |U|, wide lam) to exercise the half-range tails
     rng = np.random.default_rng(7)
     m = 200

@@ -65,3 +65,63 @@ def test_unphysical_raises(F):
     w = np.array([[1.0, 0.0, 0.0, 0.0, 1.0]])
     with pytest.raises(UnphysicalStateError):
         F.build_interface(w, -w)
+
+
+def test_interface_batch_intermediates_and_tables(golden):
+    """InterfaceBatch carries the reference's intermediates (flux.py:34-66)
+    and MomentTables (kinetic.py:90-162), computed on the device."""
+    from paper_2304_09485_b200.flux import build_interface, compatibility_residual
+
+    g = golden("flux_batch")
+    ib = build_interface(g["wl"], g["wr"], g["sl"], g["sr"])
+    for k in ("al", "ar", "atl", "atr", "w0", "abar", "atbar"):
+        ref = g[k]
+        err = np.max(np.abs(getattr(ib, k) - ref)) / max(np.max(np.abs(ref)), 1e-300)
+        assert err <= 1e-12, (k, err)
+    for side, tab in (("l", ib.tab_l), ("r", ib.tab_r), ("0", ib.tab_0)):
+        for name in ("u_full", "u_pos", "u_neg", "v_full", "w_full", "xi"):
+            ref = g[f"tab_{side}_{name}"]
+            got = getattr(tab, name)
+            assert got.shape == ref.shape
+            assert np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-300)) <= 1e-12, (side, name)
+    assert compatibility_residual(ib) < 1e-12
+    # identical states give back the state (tests/test_flux.py:45-49)
+    w = np.array([[1.0, 0.4, -0.1, 0.2, 1.3]])
+    assert np.allclose(build_interface(w, w).w0, w, rtol=1e-12, atol=1e-13)
+
+
+def test_micro_and_time_slopes_match_reference(golden):
+    """kinetic.solve_micro_slope / solve_time_slope (kinetic.py:271-312) on the device."""
+    from paper_2304_09485_b200.kinetic import solve_micro_slope, solve_time_slope
+
+    g = golden("flux_batch")
+    al = np.stack([solve_micro_slope(g["wl"], g["sl"][:, k]) for k in range(3)], axis=1)
+    assert np.max(np.abs(al - g["al"])) <= 1e-12 * np.max(np.abs(g["al"]))
+    atl = solve_time_slope(g["wl"], al[:, 0], al[:, 1], al[:, 2])
+    assert np.max(np.abs(atl - g["atl"])) <= 1e-12 * np.max(np.abs(g["atl"]))
+
+
+@pytest.mark.parametrize("kind", ["wall_noslip_isothermal", "wall_noslip_adiabatic", "wall_slip_adiabatic",
+                                  "farfield_riemann", "supersonic_inlet", "supersonic_outlet"])
+def test_ghost_state_and_gradients_match_oracle(kind):
+    """boundary.ghost_state / ghost_gradients (boundary.py:66-171) on the device vs the oracle."""
+    from oracle.solver import ghost, ghost_grad
+    from paper_2304_09485_b200.boundary import PatchSpec, ghost_gradients, ghost_state
+    from paper_2304_09485_b200.kinetic import primitive_to_conserved
+
+    rng = np.random.default_rng(7)
+    n = 64
+    w = np.column_stack([rng.uniform(0.5, 1.5, n), rng.uniform(-0.8, 0.8, (n, 3)), rng.uniform(0.5, 2.0, n)])
+    q = primitive_to_conserved(w)
+    nrm = rng.normal(size=(n, 3))
+    nrm /= np.linalg.norm(nrm, axis=1)[:, None]
+    spec = PatchSpec("p", kind, reference=np.array([1.0, 0.6, 0.1, 0.0, 0.7]),
+                     lambda_wall=0.9 if kind == "wall_noslip_isothermal" else None,
+                     velocity=np.array([0.1, 0.0, 0.05]) if kind.startswith("wall_noslip") else np.zeros(3))
+    got = ghost_state(q, spec, nrm)
+    ref = np.array([ghost(q[i], spec, nrm[i])[0] for i in range(n)])
+    assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref))
+    g = rng.normal(size=(n, 3, 5))
+    gg = ghost_gradients(g, spec, nrm)
+    gref = np.array([ghost_grad(g[i], spec, nrm[i]) for i in range(n)])
+    assert np.max(np.abs(gg - gref)) <= 1e-13 * np.max(np.abs(gref))
