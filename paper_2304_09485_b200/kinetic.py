@@ -153,3 +153,20 @@ def solve_time_slope(w, a1, a2, a3, gamma: float = DEFAULT_GAMMA, tab=None):
     """Time slope A from <(a1 u + a2 v + a3 w + A) psi> = 0 (kinetic.py:305-312), on the device."""
     a = np.stack([np.asarray(a1, dtype=float), np.asarray(a2, dtype=float), np.asarray(a3, dtype=float)], axis=-2)
     return _slopes(w, a, True, gamma)
+
+
+def slope_psi_moments(tab: MomentTable, slope, p: int, q: int, r: int, umode: str = "full"):
+    """<a(c) u^p v^q w^r psi> for a(c) = a1 + a2 u + a3 v + a4 w + a5 |c|^2 / 2
+    (kinetic.py:222-255): a combination of the table's psi-moments."""
+    a = np.asarray(slope, dtype=float)
+    pm = lambda *o: psi_moments(tab, *o, umode=umode)  # noqa: E731
+    out = a[..., 0, None] * pm(p, q, r, 0) + a[..., 1, None] * pm(p + 1, q, r, 0) + \
+        a[..., 2, None] * pm(p, q + 1, r, 0) + a[..., 3, None] * pm(p, q, r + 1, 0)
+    return out + (0.5 * a[..., 4, None]) * (pm(p + 2, q, r, 0) + pm(p, q + 2, r, 0) + pm(p, q, r + 2, 0) +
+                                            pm(p, q, r, 1))
+
+
+def directional_slope_psi_moments(tab: MomentTable, a1, a2, a3, p: int, q: int, r: int, umode: str = "full"):
+    """<(a1 u + a2 v + a3 w) u^p v^q w^r psi> (kinetic.py:258-268)."""
+    return slope_psi_moments(tab, a1, p + 1, q, r, umode) + slope_psi_moments(tab, a2, p, q + 1, r, umode) + \
+        slope_psi_moments(tab, a3, p, q, r + 1, umode)
