@@ -181,6 +181,9 @@ typedef struct GksOptions {  /* stepping.SolverOptions (stepping.py:61-84) */
   int jacobian_mode;     /* GKS_JAC_ROE (reference) or GKS_JAC_FRECHET (matrix-free) */
   int npatch;            /* == number of mesh patches; indexed by mesh patch id */
   const GksPatchDesc* patches;
+  int first_order;       /* B200 build: first-order KFVS residual (piecewise-constant states,
+                            collisionless flux, flux.py:200-208) -- the paper's low-order start
+                             */
 } GksOptions;
 
 typedef struct GksHandle GksHandle;

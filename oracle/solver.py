@@ -269,8 +269,12 @@ class OracleSolver:
 
     def __init__(self, mesh, scheme="weno_gmres", model="inviscid", mu=0.0, gamma=GAMMA, cfl=2.0,
                  krylov_dim=10, restarts=3, jacobi_sweeps=2, gmres_rtol=0.0, weights="nonlinear",
-                 time_step="local", patches=None, jacobian="roe"):
+                 time_step="local", patches=None, jacobian="roe", first_order=False):
         self.mesh = mesh
+        # first order (the B200 build's low-order start option):
+        # piecewise-constant face states and the collisionless split flux
+        # kfvs_flux (flux.py:200-208); point values = the half-range blend at t=0
+        self.first_order = first_order
         self.compact = scheme.startswith("hweno")
         self.model, self.mu, self.gamma, self.cfl = model, mu, gamma, cfl
         self.m, self.restarts, self.kmax, self.rtol = krylov_dim, restarts, jacobi_sweeps, gmres_rtol
@@ -311,6 +315,8 @@ class OracleSolver:
         if with_gradients is None:
             with_gradients = self.compact
         coef = self.recon.coefficients(q, grad)
+        if self.first_order:
+            coef = np.zeros_like(coef)
         vo, go, vn, gn = self.recon.face_states(q, coef)
         for name, sel in self.patch_fq.items():
             spec = self.patches[name]
@@ -329,7 +335,7 @@ class OracleSolver:
         ib = F.Interface(wl, wr, slopes(go), slopes(gn), self.gamma)
         dtf = np.where(self.inner, np.minimum(dt[self.own], dt[np.where(self.inner, self.nbr, 0)]), dt[self.own])
         tau = F.collision_time(self.model, dtf, pressure(wl), pressure(wr), self.mu, pressure(ib.w0))
-        fl = F.evolve_flux(ib, tau, dtf)
+        fl = F.kfvs_flux(wl, wr, self.gamma) if self.first_order else F.evolve_flux(ib, tau, dtf)
         fl[self.wall, 0] = 0.0
         con = self.ws[:, None] * F.to_global(fl, fr)
         res = np.zeros_like(q)
@@ -337,7 +343,10 @@ class OracleSolver:
         np.add.at(res, self.nbr[self.inner], con[self.inner])
         gnew = None
         if with_gradients:
-            qp = F.to_global(F.point_value(ib, tau, np.zeros_like(dtf)), fr)
+            if self.first_order:
+                qp = F.to_global(prim_to_cons(ib.w0, self.gamma), fr)
+            else:
+                qp = F.to_global(F.point_value(ib, tau, np.zeros_like(dtf)), fr)
             gnew = update_gradients(self.mesh, qp)
         return res, gnew
 

@@ -234,6 +234,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   H->linear_weights = o->linear_weights;
   H->global_dt = o->global_time_step;
   H->jac_mode = o->jacobian_mode;
+  H->first_order = o->first_order;
   H->krylov_dim = o->krylov_dim; H->restarts = o->restarts; H->jacobi_sweeps = o->jacobi_sweeps;
   H->gmres_rtol = o->gmres_rtol;
   H->kc = make_kin(o->gamma);
@@ -847,7 +848,7 @@ static int enqueue_attempt(GksHandle* G) {
     TRY(boundary_ghosts_device(H, H->q));
     H->status = G->phase_status + 4 * PH_RES;
   }
-  TRY(jacobian_enqueue(H, A, H->nbf ? H->ghosts : nullptr));
+  TRY(jacobian_enqueue(H, A, H->nbf ? H->ghosts : nullptr, false));
   GmresParams P;
   P.m = H->krylov_dim;
   P.restarts = H->restarts;

@@ -177,6 +177,7 @@ __global__ void k_jac_faces(int64_t nfi, const int* __restrict__ ifaces, const i
     double* fd = fdat + (int64_t)f * MF_REC;
     fd[0] = n[0]; fd[1] = n[1]; fd[2] = n[2]; fd[3] = hs; fd[4] = lam; fd[5] = 0.0;
   }
+  if (!off) return;  // matrix-free step: the stored blocks are not needed
   double J[5][5];
   // rows of ghost cells (cut faces on a partitioned mesh) have no slot
   if (fslot[2 * f] >= 0) {
@@ -1309,12 +1310,16 @@ int gmres_device(BlockSys* A, const double* b_dev, double* x_dev, const GmresPar
 // ---------------------------------------------------------------------------
 // Jacobian assembly on the handle's mesh
 // ---------------------------------------------------------------------------
-int jacobian_enqueue(Handle* H, BlockSys* A, const double* ghosts_dev) {
+// want_blocks: also store the off-diagonal 5x5 blocks (the matrix-free
+// products of a step need only the per-face records; the API assembly
+// exports the blocks)
+int jacobian_enqueue(Handle* H, BlockSys* A, const double* ghosts_dev, bool want_blocks) {
   GKS_LAUNCH(KC_SCALAR, k_status_init, 1, 1, 0, H->stream, A->status, 1);
   if (H->nfi)
     GKS_LAUNCH(KC_JAC_FACE, k_jac_faces, blocks_for(H->nfi, 128), 128, 0, H->stream, H->nfi, H->interior_faces, H->f_own, H->f_nbr,
                                                                  H->f_normal, H->f_area, H->q, H->face_slot,
-                                                                 H->gamma, A->off, A->fdat);
+                                                                 H->gamma, (want_blocks || !A->mf) ? A->off : nullptr,
+                                                                 A->fdat);
   if (A->mf)
     GKS_LAUNCH(KC_JAC_FACE, k_roe_prim, blocks_for(H->n_recon, 128), 128, 0, H->stream, H->n_recon, H->q,
                H->gamma - 1.0, A->prim);
@@ -1326,7 +1331,7 @@ int jacobian_enqueue(Handle* H, BlockSys* A, const double* ghosts_dev) {
 }
 
 int jacobian_assemble(Handle* H, BlockSys* A, const double* ghosts_dev) {
-  TRY_GM(jacobian_enqueue(H, A, ghosts_dev));
+  TRY_GM(jacobian_enqueue(H, A, ghosts_dev, true));
   int st[4];
   GKS_CUDA(cudaMemcpyAsync(st, A->status, sizeof(st), cudaMemcpyDeviceToHost, H->stream));
   GKS_CUDA(cudaStreamSynchronize(H->stream));

@@ -104,7 +104,7 @@ int gmres_device(BlockSys* A, const double* b_dev, double* x_dev, const GmresPar
                  const MatvecFn* matvec);
 int jacobian_assemble(Handle* H, BlockSys* A, const double* ghosts_dev);
 // launch-only halves (CUDA-graph capturable) and the host readback
-int jacobian_enqueue(Handle* H, BlockSys* A, const double* ghosts_dev);
+int jacobian_enqueue(Handle* H, BlockSys* A, const double* ghosts_dev, bool want_blocks);
 int gmres_enqueue(BlockSys* A, const double* b_dev, double* x_dev, const GmresParams& P, const MatvecFn* matvec,
                   bool check_dinv);
 int gmres_result(const GmresDev* gh, GmresHost* out);

@@ -330,6 +330,12 @@ __device__ __forceinline__ TimeCoef time_coefficients(double tau, double dt, dou
     t.c5 = -(tau * c4r + c5r) * idt;
     t.c6 = -tau * c4r * idt;
   }
+  if (isinf(tau)) {
+    // collisionless point value: the initial (half-range) distribution itself
+    t.g1 = t.g2 = t.g3 = t.f2 = t.f3 = 0.0;
+    t.f1 = 1.0;
+    return t;
+  }
   const double e = exp(-tp / tau);
   t.g1 = 1.0 - e;
   t.g2 = (tp + tau) * e - tau;

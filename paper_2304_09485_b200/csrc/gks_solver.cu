@@ -453,6 +453,7 @@ struct FaceArgs {
   KinConst kc;
   int want_point;
   int fq_nq;
+  double tau_in;  // < 0: the scheme's collision time; +inf: collisionless (KFVS, first order)
   double* contrib;
   const int2* fq_slot;  // slot mode (non-null): contributions go to the assembly slots
   double* slots;
@@ -594,8 +595,8 @@ __global__ void __launch_bounds__(128, GKS_FACE_MINB) k_face(FaceArgs A) {
   };
   double fl[5], pv[5];
   int rc;
-  if (GKS_FACE_TAU == 2) rc = interface_flux_t<VISC, POINT, 2>(get, press_r, -1.0, dtf, A.mu, A.kc, fl, 0.0, pv);
-  else rc = interface_flux_t<VISC, POINT, GKS_FACE_TAU>(get, press, -1.0, dtf, A.mu, A.kc, fl, 0.0, pv);
+  if (GKS_FACE_TAU == 2) rc = interface_flux_t<VISC, POINT, 2>(get, press_r, A.tau_in, dtf, A.mu, A.kc, fl, 0.0, pv);
+  else rc = interface_flux_t<VISC, POINT, GKS_FACE_TAU>(get, press, A.tau_in, dtf, A.mu, A.kc, fl, 0.0, pv);
   if (rc) {
     if (ghost_fail) {
       atomicCAS(A.status, 0, GKS_ERR_UNPHYSICAL);
@@ -923,8 +924,13 @@ static int recon_device(Handle* H, const double* q, const int* gate) {
 
 int residual_device(Handle* H, const double* q, double* res, bool with_gradients, const int* gate,
                     const FrechetEpi* fe) {
-  // owned + layer-1 ghosts (redundant reconstruction), RT cells per CTA
-  if (int rc = recon_device(H, q, gate)) return rc;
+  // owned + layer-1 ghosts (redundant reconstruction), RT cells per CTA;
+  // first order: zero coefficients (face values = cell averages, no slopes)
+  if (H->first_order) {
+    GKS_CUDA(cudaMemsetAsync(H->coef, 0, (size_t)H->n_recon * 45 * sizeof(double), H->stream));
+  } else if (int rc = recon_device(H, q, gate)) {
+    return rc;
+  }
   FaceArgs A;
   A.nfq = H->nfq;
   A.q = q; A.coef = H->coef; A.cen = H->cen; A.h = H->h; A.avg0 = H->avg0; A.dt = H->dt;
@@ -932,6 +938,7 @@ int residual_device(Handle* H, const double* q, double* res, bool with_gradients
   A.fq_point = H->fq_point; A.fq_ws = H->fq_ws; A.f_frame = H->f_frame; A.f_normal = H->f_normal;
   A.f_shift = H->f_shift; A.patches = H->patches; A.model = H->model; A.mu = H->mu; A.kc = H->kc;
   A.want_point = with_gradients ? 1 : 0;
+  A.tau_in = H->first_order ? INFINITY : -1.0;
   A.fq_nq = H->fq_nq;
   A.contrib = H->contrib; A.qpt = H->qpt; A.status = H->status; A.gate = gate;
   static const int slot_env = [] {

@@ -69,6 +69,7 @@ struct Handle {
   int nfpc = 4;
   // options
   int scheme = 0, model = 0, compact = 0, linear_weights = 0, global_dt = 0, jac_mode = 0;
+  int first_order = 0;  // KFVS on piecewise-constant states (no reconstruction, tau = inf)
   double mu = 0, gamma = 1.4, cfl = 2, eps = 1e-6, lw = 0.025;
   KinConst kc;
   int krylov_dim = 10, restarts = 3, jacobi_sweeps = 2;

@@ -77,6 +77,7 @@ class SolverOptions:
     jacobian: str = "roe"
     device: int = 0
     reorder: str = "none"  # device-side locality renumbering: "none" | "rcm" | "morton" (reorder.py)
+    first_order: bool = False  # KFVS on piecewise-constant states (the paper's low-order start)
 
     def __post_init__(self):
         if self.scheme not in SCHEMES:
@@ -125,6 +126,7 @@ def _options_struct(opt: SolverOptions, mesh: Mesh):
     o.jacobian_mode = JACOBIANS.index(opt.jacobian)
     o.npatch = n
     o.patches = arr
+    o.first_order = int(bool(opt.first_order))
     return o, arr
 
 

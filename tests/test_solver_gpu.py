@@ -218,3 +218,40 @@ def test_gmres_multiblock_path_on_reference_system(case, monkeypatch):
     norms = np.concatenate([np.asarray(c) for c in info.cycle_residuals])
     assert np.allclose(norms, g["gmres_cycle_norms"], rtol=1e-9, atol=1e-9 * norms[0])
     assert relmax(x, g["gmres_x"]) < 1e-9
+
+
+@pytest.mark.parametrize("scheme", ["weno_gmres", "hweno_gmres"])
+def test_first_order_kfvs_residual_and_step(scheme):
+    """SolverOptions(first_order=True): piecewise-constant states and the
+    collisionless split flux (flux.py:200-208; the paper's low-order start,
+    PAPER.md:1070-1081) -- residual, gradient update and a step vs the oracle."""
+    from oracle.solver import OracleSolver
+    from paper_2304_09485_b200.boundary import PatchSpec
+    from paper_2304_09485_b200.kinetic import primitive_to_conserved
+    from paper_2304_09485_b200.mesh import generate_box_mesh
+    from paper_2304_09485_b200.stepping import SolutionField, Solver, SolverOptions
+
+    mesh = generate_box_mesh((1, 1, 1), (3, 3, 3), split="tet", perturb=0.1, seed=7)
+    ref = np.array([1.0, 2.0, 0.1, 0.05, 1.0 / 1.4])
+    kinds = {"xmin": "supersonic_inlet", "xmax": "supersonic_outlet", "ymin": "wall_slip_adiabatic",
+             "ymax": "wall_slip_adiabatic", "zmin": "farfield_riemann", "zmax": "farfield_riemann"}
+    patches = {n: PatchSpec(n, k, reference=ref if k in ("supersonic_inlet", "farfield_riemann") else None)
+               for n, k in kinds.items()}
+    rng = np.random.default_rng(3)
+    w = np.tile([1.0, 2.0, 0.1, 0.05, 0.7], (mesh.ncells, 1)) * (1 + 0.03 * rng.normal(size=(mesh.ncells, 5)))
+    q = primitive_to_conserved(w)
+    compact = scheme.startswith("hweno")
+    grad = 0.05 * rng.normal(size=(mesh.ncells, 3, 5)) if compact else None
+    s = Solver(mesh, SolverOptions(scheme=scheme, patches=patches, first_order=True))
+    o = OracleSolver(mesh, scheme=scheme, patches=patches, first_order=True)
+    fld = SolutionField(q, grad)
+    dt = s.local_time_step(fld)
+    res, gnew = s.residual(fld, dt)
+    ref_res, ref_g = o.residual(q, grad, dt)
+    assert relmax(res, ref_res) <= 1e-12
+    if compact:
+        assert relmax(gnew, ref_g) <= 1e-12
+    f1, info = s.advance(fld)
+    q1, g1, oinfo = o.advance(q, grad)
+    assert relmax(f1.q, q1) <= 1e-10
+    assert info.solver_cycles == oinfo["solver_cycles"]
