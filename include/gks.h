@@ -328,6 +328,8 @@ int gks_bad_mask(GksHandle* h, int8_t* out);
    step (no host synchronisation inside it).  enable = 0 runs every step
    uncaptured (default: on unless the environment sets GKS_GRAPH=0). */
 int gks_set_graph(GksHandle* h, int enable);
+/* change SolverOptions.cfl of a live handle (a CFL ramp; next step re-captures) */
+int gks_set_cfl(GksHandle* h, double cfl);
 /* Solver.frechet_matvec (stepping.py:298-313); sigma <= 0 selects the
    reference's automatic step.  out = (L(q + s v) - L(q)) / s */
 int gks_frechet_matvec(GksHandle* h, const double* q, const double* grad, const double* dt, const double* v,

@@ -215,6 +215,7 @@ SIGNATURES = [
     ("gks_state_download", C.c_int, [C.c_void_p, c_double_p, c_double_p]),
     ("gks_advance_resident", C.c_int, [C.c_void_p, C.c_void_p]),
     ("gks_set_graph", C.c_int, [C.c_void_p, C.c_int]),
+    ("gks_set_cfl", C.c_int, [C.c_void_p, C.c_double]),
     ("gks_bad_mask", C.c_int, [C.c_void_p, C.c_void_p]),
     ("gks_ugks_read", C.c_int, [C.c_char_p, C.c_void_p]),
     ("gks_ugks_sizes", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

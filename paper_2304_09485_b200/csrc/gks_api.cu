@@ -1292,6 +1292,20 @@ int gks_state_download(GksHandle* G, double* q, double* grad) {
   return GKS_OK;
 }
 
+int gks_set_cfl(GksHandle* G, double cfl) {
+  if (!G || !(cfl > 0.0)) {
+    set_error("gks_set_cfl: bad arguments");
+    return GKS_ERR_BAD_ARG;
+  }
+  G->H.cfl = cfl;
+  // the captured steps carry the old CFL as a kernel argument
+  for (StepGraph& g : G->graphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g = StepGraph();
+  }
+  return GKS_OK;
+}
+
 int gks_set_graph(GksHandle* G, int enable) {
   if (!G) return GKS_ERR_BAD_ARG;
   G->graph = enable ? 1 : 0;

@@ -436,6 +436,11 @@ class Solver:
         N.check(N.load().gks_state_download(self._handle, N.dptr(q), N.dptr(g)))
         return SolutionField(self._host(q), self._host(g))
 
+    def set_cfl(self, cfl: float):
+        """Change the CFL number of this solver (options.cfl) for the next steps."""
+        N.check(N.load().gks_set_cfl(self._handle, float(cfl)))
+        self.opt.cfl = float(cfl)
+
     def advance_resident(self) -> StepInfo:
         info = N.GksStepInfo()
         rc = N.load().gks_advance_resident(self._handle, C.byref(info))
