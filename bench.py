@@ -59,6 +59,8 @@ def parse():
     p.add_argument("--scheme", default=None, choices=("weno_gmres", "hweno_gmres"))
     p.add_argument("--jacobian", default=None, choices=("roe", "frechet"))
     p.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of decomposition")
+    p.add_argument("--ortho", default="mgs", choices=("mgs", "cgs2"),
+                   help="GMRES orthogonalisation: reference MGS or CGS2 with fused multi-dots")
     p.add_argument("--reorder", default="none", choices=("none", "rcm", "morton"),
                    help="device-side locality renumbering of the mesh (reorder.py)")
     p.add_argument("--cpu-n", type=int, default=None, help="bounded CPU sample size (c1 box divisions / c2 cube-face cells)")
@@ -535,7 +537,7 @@ def run_ours(args):
     t_mesh = time.perf_counter() - t0
     t0 = time.perf_counter()
     opts = SolverOptions(scheme=args.scheme, patches=patches, jacobian=args.jacobian, device=local,
-                         reorder=args.reorder, **extra)
+                         reorder=args.reorder, ortho=args.ortho, **extra)
     decomp = world > 1 and not args.replicas
     decomp_note = None
     solver = None
@@ -714,7 +716,8 @@ def run_ours(args):
         "scaling": "weak" if (world > 1 and not decomp) else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload,
                    "cells": nc, "faces": sizes["nf"], "face_points": sizes["nfq"], "scheme": args.scheme,
-                   "jacobian": args.jacobian, "reorder": args.reorder, "gmres": "m=10, restarts=3, jacobi_sweeps=2, rtol=0",
+                   "jacobian": args.jacobian, "reorder": args.reorder,
+                   "gmres": f"m=10, restarts=3, jacobi_sweeps=2, rtol=0, ortho={args.ortho}",
                    "residual_evals_per_step": evals / args.steps,
                    "parallelism": ("replicas" if not decomp else
                                    f"cell-partitioned x{world} (RCB canonical ranges), NCCL halo + group-partial "

@@ -184,6 +184,8 @@ typedef struct GksOptions {  /* stepping.SolverOptions (stepping.py:61-84) */
   int first_order;       /* B200 build: first-order KFVS residual (piecewise-constant states,
                             collisionless flux, flux.py:200-208) -- the paper's low-order start
                              */
+  int ortho;             /* B200 build: GMRES orthogonalisation, 0 = MGS + conditional second
+                            pass (krylov.py:89-106), 1 = CGS2 with fused multi-dots */
 } GksOptions;
 
 typedef struct GksHandle GksHandle;

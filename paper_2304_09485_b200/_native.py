@@ -127,7 +127,8 @@ class GksOptions(C.Structure):
                 ("cfl", C.c_double), ("krylov_dim", C.c_int), ("restarts", C.c_int), ("jacobi_sweeps", C.c_int),
                 ("gmres_rtol", C.c_double), ("weno_eps", C.c_double), ("linear_weight", C.c_double),
                 ("linear_weights", C.c_int), ("global_time_step", C.c_int), ("jacobian_mode", C.c_int),
-                ("npatch", C.c_int), ("patches", C.POINTER(GksPatchDesc)), ("first_order", C.c_int)]
+                ("npatch", C.c_int), ("patches", C.POINTER(GksPatchDesc)), ("first_order", C.c_int),
+                ("ortho", C.c_int)]
 
 
 class GksStepInfo(C.Structure):

@@ -109,10 +109,18 @@ static int upload(Handle* H, T** dst, const T* src, size_t n) {
   return GKS_OK;
 }
 
+// GKS_POISON=1 builds fill every work allocation with 0xFF bytes (NaN
+// doubles, -1 ints): a kernel reading device memory no kernel or copy wrote
+// then turns results into NaN and the parity tests fail (the initcheck of a
+// pool without compute-sanitizer).
+#ifndef GKS_POISON
+#define GKS_POISON 0
+#endif
 template <class T>
 static int alloc(Handle* H, T** dst, size_t n) {
   GKS_CUDA(cudaMalloc(dst, std::max<size_t>(n, 1) * sizeof(T) + kTailPad));
   H->allocs.push_back(*dst);
+  if (GKS_POISON) GKS_CUDA(cudaMemset(*dst, 0xFF, std::max<size_t>(n, 1) * sizeof(T) + kTailPad));
   return GKS_OK;
 }
 
@@ -128,6 +136,28 @@ static std::vector<int> to_i32(const int64_t* p, size_t n) {
     if (_rc) return _rc;       \
   } while (0)
 
+// Structural memory check of every static index array before it reaches the
+// device (compute-sanitizer is unavailable on the GPU pool): each gathered
+// or scattered index, shifted right by `shift` (tagged CSR entries), must lie
+// in [lo, hi).  All device gathers index through these arrays (or through
+// indices derived from them), so a handle that passes cannot read or write
+// out of bounds.
+static int check_range(const char* what, const int* v, size_t n, int64_t lo, int64_t hi, int shift = 0) {
+  for (size_t k = 0; k < n; ++k) {
+    const int64_t x = (int64_t)(v[k] >> shift);
+    if (x < lo || x >= hi) {
+      set_error("index check: %s[%zu] = %lld outside [%lld, %lld)", what, k, (long long)x, (long long)lo,
+                (long long)hi);
+      return GKS_ERR_BAD_ARG;
+    }
+  }
+  return GKS_OK;
+}
+template <class V>
+static int check_vec(const char* what, const V& v, int64_t lo, int64_t hi, int shift = 0) {
+  return check_range(what, v.data(), v.size(), lo, hi, shift);
+}
+
 static int upload_halo(Handle* H, HaloMap& X, const GksHaloDesc& d) {
   X.peers.assign(d.peers, d.peers + d.npeers);
   X.soff.assign(d.send_offsets, d.send_offsets + d.npeers + 1);
@@ -135,6 +165,13 @@ static int upload_halo(Handle* H, HaloMap& X, const GksHaloDesc& d) {
   X.ns = X.soff.back();
   X.nr = X.roff.back();
   auto si = to_i32(d.send_ids, X.ns), ri = to_i32(d.recv_ids, X.nr);
+  TRY(check_vec("halo send ids", si, 0, H->n_owned));
+  TRY(check_vec("halo recv ids", ri, H->n_owned, H->nc));
+  for (size_t p = 0; p + 1 < X.soff.size(); ++p)
+    if (X.soff[p] > X.soff[p + 1] || X.roff[p] > X.roff[p + 1]) {
+      set_error("halo offsets not ascending");
+      return GKS_ERR_BAD_ARG;
+    }
   TRY(upload(H, &X.sids, si.data(), si.size()));
   TRY(upload(H, &X.rids, ri.data(), ri.size()));
   return GKS_OK;
@@ -235,6 +272,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   H->global_dt = o->global_time_step;
   H->jac_mode = o->jacobian_mode;
   H->first_order = o->first_order;
+  H->ortho = o->ortho;
   H->krylov_dim = o->krylov_dim; H->restarts = o->restarts; H->jacobi_sweeps = o->jacobi_sweeps;
   H->gmres_rtol = o->gmres_rtol;
   H->kc = make_kin(o->gamma);
@@ -284,6 +322,8 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   // faces
   {
     auto own = to_i32(m->face_owner, nf), nbr = to_i32(m->face_neighbor, nf), pat = to_i32(m->face_patch, nf);
+    TRY(check_vec("face_owner", own, 0, nc));
+    TRY(check_vec("face_neighbor", nbr, -1, nc));
     TRY(upload(H, &H->f_own, own.data(), nf));
     TRY(upload(H, &H->f_nbr, nbr.data(), nf));
     TRY(upload(H, &H->f_patch, pat.data(), nf));
@@ -294,6 +334,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   TRY(upload(H, &H->f_shift, m->face_shift, nf * 3));
   {
     auto fqf = to_i32(m->fq_face, nfq);
+    TRY(check_vec("fq_face", fqf, 0, nf));
     TRY(upload(H, &H->fq_face, fqf.data(), nfq));
     // uniform points per face in face order: the face kernel derives the
     // face from the point index instead of loading it (one dependent load less)
@@ -346,6 +387,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
       if (nb >= 0) list[pos[nb]++] = (int)((i << 1) | 1);
     }
     TRY(upload(H, &H->cfq_start, cnt.data(), nc + 1));
+    TRY(check_vec("assembly list", list, 0, nfq, 1));
     TRY(upload(H, &H->cfq, list.data(), list.size()));
     {
       std::vector<int2> slot(nfq, make_int2(-1, -1));
@@ -378,6 +420,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
       if (m->face_neighbor[f] >= 0) list[pos[m->face_neighbor[f]]++] = (int)((f << 1) | 1);
     }
     TRY(upload(H, &H->cdt_start, cnt.data(), nc + 1));
+    TRY(check_vec("local-dt list", list, 0, nf, 1));
     TRY(upload(H, &H->cdt, list.data(), list.size()));
     // Jacobian diagonal: interior own, interior nbr, boundary own (jacobian.py:582-610)
     std::vector<int> pos2(cnt.begin(), cnt.end() - 1), list2(cnt[nc]);
@@ -394,6 +437,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
       if (m->face_neighbor[f] < 0) list2[pos2[m->face_owner[f]]++] = (int)(f << 1);
     }
     TRY(upload(H, &H->cjd_start, cnt.data(), nc + 1));
+    TRY(check_vec("Jacobian-diagonal list", list2, 0, nf, 1));
     TRY(upload(H, &H->cjd, list2.data(), list2.size()));
   }
   {
@@ -449,6 +493,8 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
     A->red_cell_first = H->cell_first;
     A->canonical = dom ? 1 : 0;
     GKS_CUDA(cudaMemcpy(A->rowptr, rowptr.data(), (H->n_owned + 1) * sizeof(int), cudaMemcpyHostToDevice));
+    TRY(check_vec("Jacobian columns", col, 0, H->n_recon));
+    TRY(check_range("Jacobian entries", ent.data(), (size_t)nkept, 0, nf, 1));
     if (nkept) GKS_CUDA(cudaMemcpy(A->col, col.data(), nkept * sizeof(int), cudaMemcpyHostToDevice));
     G->jac.owned = false;
     // matrix-free Roe products for the handle's Jacobian (GKS_ROE_MF=0 streams the stored blocks)
@@ -501,11 +547,23 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
         }
       TRY(upload_rec(H, &H->big_op, opt, nc));
     }
-    { auto v = pad_records(ag, nc, 1, H->HA, 1, At, self_i); TRY(upload_rec(H, &H->avg_gather, v, nc)); }
-    { auto v = pad_records(gg, nc, 1, H->HG, 1, Gt, self_i); TRY(upload_rec(H, &H->grad_gather, v, nc)); }
+    {
+      auto v = pad_records(ag, nc, 1, H->HA, 1, At, self_i);
+      TRY(check_range("HWENO average gathers", v.data(), (size_t)H->n_recon * At, 0, nc));
+      TRY(upload_rec(H, &H->avg_gather, v, nc));
+    }
+    {
+      auto v = pad_records(gg, nc, 1, H->HG, 1, Gt, self_i);
+      TRY(check_range("HWENO gradient gathers", v.data(), (size_t)H->n_recon * Gt, 0, nc));
+      TRY(upload_rec(H, &H->grad_gather, v, nc));
+    }
     { auto v = pad_records(gs, nc, 1, H->HG, 1, Gt, zero_d); TRY(upload_rec(H, &H->grad_scale, v, nc)); }
     { auto v = pad_records(so, nc, H->HM, 21, Mt, 21, zero_d); TRY(upload_rec(H, &H->sub_op, v, nc)); }
-    { auto v = pad_records(sg, nc, H->HM, 2, Mt, 2, self_i); TRY(upload_rec(H, &H->sub_gather, v, nc)); }
+    {
+      auto v = pad_records(sg, nc, H->HM, 2, Mt, 2, self_i);
+      TRY(check_range("HWENO sub-stencil gathers", v.data(), (size_t)H->n_recon * Mt * 2, 0, nc));
+      TRY(upload_rec(H, &H->sub_gather, v, nc));
+    }
     { auto v = pad_records(act, nc, 1, H->HM, 1, Mt, zero_b); TRY(upload_rec(H, &H->sub_active, v, nc)); }
   } else {
     std::vector<double> op, so;
@@ -528,7 +586,11 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
     }
     H->Kt = Kt; H->Mt = Mt; H->St = St;
     { auto v = pad_records(op, nc, 9, H->K, 9, Kt, zero_d); TRY(upload_rec(H, &H->big_op, v, nc)); }
-    { auto v = pad_records(bg, nc, 1, H->K, 1, Kt, self_i); TRY(upload_rec(H, &H->big_gather, v, nc)); }
+    {
+      auto v = pad_records(bg, nc, 1, H->K, 1, Kt, self_i);
+      TRY(check_range("WENO big-stencil gathers", v.data(), (size_t)H->n_recon * Kt, 0, nc));
+      TRY(upload_rec(H, &H->big_gather, v, nc));
+    }
     {
       // sub operator (M, 3, S) -> (Mt, 3, St)
       auto v = pad_records(so, nc * H->M, 3, H->S, 3, St, zero_d);  // pad S
@@ -541,6 +603,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
         for (int mm = 0; mm < Mt; ++mm)
           for (int s2 = 0; s2 < St; ++s2)
             v[(c * Mt + mm) * St + s2] = (mm < H->M && s2 < H->S) ? sg[(c * H->M + mm) * H->S + s2] : (int)c;
+      TRY(check_range("WENO sub-stencil gathers", v.data(), (size_t)H->n_recon * Mt * St, 0, nc));
       TRY(upload_rec(H, &H->sub_gather, v, nc));
     }
     { auto v = pad_records(act, nc, 1, H->M, 1, Mt, zero_b); TRY(upload_rec(H, &H->sub_active, v, nc)); }
@@ -854,6 +917,7 @@ static int enqueue_attempt(GksHandle* G) {
   P.restarts = H->restarts;
   P.kmax = H->jacobi_sweeps;
   P.rtol = H->gmres_rtol;
+  P.ortho = H->ortho;
   MatvecFn mf = [H, A](const double* v, double* out, const int* gate) {
     return frechet_apply(H, A, v, out, 1, gate, nullptr, true);
   };

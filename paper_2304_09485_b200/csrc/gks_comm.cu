@@ -274,7 +274,8 @@ int comm_red_final(Comm* c, KrylovWS* W, int ns, int nm, const RedOut& out, cons
     // exact: every group partial is non-zero (non-inf) on its owner only
     if (ns) GKS_NCCL(g_nccl.AllReduce(W->gpart[0], W->gall, ns * ng, ncclDouble, ncclSum, c->nccl, s));
     if (nm)
-      GKS_NCCL(g_nccl.AllReduce(W->gpart[0] + ns * ng, W->gall + ns * ng, nm * ng, ncclDouble, ncclMin, c->nccl, s));
+      GKS_NCCL(g_nccl.AllReduce(W->gpart[0] + RED_MIN_SLOT * ng, W->gall + RED_MIN_SLOT * ng, nm * ng, ncclDouble,
+                                ncclMin, c->nccl, s));
     src.p[0] = W->gall;
     src.n = 1;
   } else {
@@ -291,6 +292,26 @@ int comm_red_final(Comm* c, KrylovWS* W, int ns, int nm, const RedOut& out, cons
     set_error("no final reduction kernel for %d sums + %d mins", ns, nm);
     return GKS_ERR_BAD_ARG;
   }
+  return GKS_OK;
+}
+
+__global__ void k_red_final_n(RedSrc src, int64_t ngrp_g, int nc, RedOutN out, const int* gate);
+
+int comm_red_final_n(Comm* c, KrylovWS* W, int nc, const RedOutN& out, const int* gate, cudaStream_t s) {
+  const int64_t ng = W->red.ngrp_g;
+  RedSrc src{};
+  if (c->kind == 1) {
+    GKS_NCCL(g_nccl.AllReduce(W->gpart[0], W->gall, nc * ng, ncclDouble, ncclSum, c->nccl, s));
+    src.p[0] = W->gall;
+    src.n = 1;
+  } else {
+    const int p = (int)(c->seq++ & 1);
+    c->ws = W;
+    TRY_LB(lb_sync(c, p, s));
+    src.n = c->grp->R;
+    for (int r = 0; r < src.n; ++r) src.p[r] = c->grp->ranks[r]->ws->gpart[p];
+  }
+  GKS_LAUNCH(KC_REDUCE, k_red_final_n, 1, RED_T, 0, s, src, ng, nc, out, gate);
   return GKS_OK;
 }
 

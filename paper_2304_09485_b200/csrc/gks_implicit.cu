@@ -123,15 +123,105 @@ __global__ void __launch_bounds__(RED_T) k_red_final(RedSrc src, int64_t ngrp_g,
       }, &v);
       v = red_tree<0>(v, sm);
     } else {
+      const int64_t off = (int64_t)(RED_MIN_SLOT + c - NS) * ngrp_g;
       red_lanes<0, 1>(ngrp_g, [&](int64_t g, double* o) {
-        double x = __ldcg(src.p[0] + c * ngrp_g + g);
-        for (int r = 1; r < src.n; ++r) x = fmin(x, __ldcg(src.p[r] + c * ngrp_g + g));
+        double x = __ldcg(src.p[0] + off + g);
+        for (int r = 1; r < src.n; ++r) x = fmin(x, __ldcg(src.p[r] + off + g));
         o[0] = x;
       }, &v);
       v = red_tree<1>(v, sm);
     }
     if (threadIdx.x == 0 && out.o[c]) *out.o[c] = v;
   }
+}
+
+// the same with a runtime number of sum components (CGS2 multi-dots)
+__global__ void __launch_bounds__(RED_T) k_red_final_n(RedSrc src, int64_t ngrp_g, int nc, RedOutN out,
+                                                       const int* gate) {
+  __shared__ double sm[9];
+  if (gate && !*gate) return;
+  for (int c = 0; c < nc; ++c) {
+    double v;
+    red_lanes<1, 0>(ngrp_g, [&](int64_t g, double* o) {
+      double x = __ldcg(src.p[0] + c * ngrp_g + g);
+      for (int r = 1; r < src.n; ++r) x += __ldcg(src.p[r] + c * ngrp_g + g);
+      o[0] = x;
+    }, &v);
+    v = red_tree<0>(v, sm);
+    if (threadIdx.x == 0) {
+      double* o = c < nc - 1 ? out.base + c : out.last;
+      if (o) *o = v;
+    }
+  }
+}
+
+// CGS2 passes over the Arnoldi basis v_0 .. v_{NV-1} (one block per segment):
+//   MODE 1: c_k = v_k . w, c_NV = w . w
+//   MODE 2: w -= sum_k h_k v_k, then c_k = v_k . w, c_NV = w . w
+//   MODE 3: w -= sum_k h_k v_k, then c_0 = w . w
+// One read of each basis vector and of w per pass (all dots fused).
+template <int NV, int MODE>
+__global__ void __launch_bounds__(RED_T) k_cgs(int64_t n, int64_t ld, const double* __restrict__ V,
+                                               double* __restrict__ w, const double* h, RedDev R, RedOutN out,
+                                               const int* gate) {
+  __shared__ double sm[9];
+  if (gate && !*gate) return;
+  constexpr int NC = MODE == 3 ? 1 : NV + 1;
+  const int64_t base = (int64_t)blockIdx.x * SEG_VALS;
+  const int64_t len = min(SEG_VALS, n - base);
+  double hk[NV];
+  if (MODE >= 2) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) hk[k] = h[k];
+  }
+  double acc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+  for (int64_t i = threadIdx.x; i < len; i += RED_T) {
+    const int64_t e = base + i;
+    double vk[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) vk[k] = V[k * ld + e];
+    double wi = w[e];
+    if (MODE >= 2) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) wi -= hk[k] * vk[k];
+      w[e] = wi;
+    }
+    if (MODE <= 2) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) acc[k] += __dmul_rn(vk[k], wi);
+    }
+    acc[NC - 1] += __dmul_rn(wi, wi);
+  }
+  red_finish_n<NC>(R, acc, out, sm);
+}
+
+template <int NV>
+static void launch_cgs(int mode, int grid, cudaStream_t s, int64_t n, int64_t ld, const double* V, double* w,
+                       const double* h, const RedDev& R, const RedOutN& out, const int* gate) {
+  if (mode == 1) GKS_LAUNCH(KC_REDUCE, (k_cgs<NV, 1>), grid, RED_T, 0, s, n, ld, V, w, h, R, out, gate);
+  else if (mode == 2) GKS_LAUNCH(KC_REDUCE, (k_cgs<NV, 2>), grid, RED_T, 0, s, n, ld, V, w, h, R, out, gate);
+  else GKS_LAUNCH(KC_REDUCE, (k_cgs<NV, 3>), grid, RED_T, 0, s, n, ld, V, w, h, R, out, gate);
+}
+
+constexpr int CGS_MAXV = RED_MAXC_MD - 1;  // basis vectors per pass (krylov_dim <= 15)
+
+template <int NV>
+static void cgs_dispatch(int nv, int mode, int grid, cudaStream_t s, int64_t n, int64_t ld, const double* V,
+                         double* w, const double* h, const RedDev& R, const RedOutN& out, const int* gate) {
+  if (nv == NV) launch_cgs<NV>(mode, grid, s, n, ld, V, w, h, R, out, gate);
+  else if constexpr (NV < CGS_MAXV) cgs_dispatch<NV + 1>(nv, mode, grid, s, n, ld, V, w, h, R, out, gate);
+}
+
+// one CGS2 pass with its reduction (and, multi-rank, the partial exchange)
+static int cgs_pass(BlockSys* A, int mode, int nv, int64_t n, int64_t ld, double* w, const double* h,
+                    const RedOutN& out, const int* gate) {
+  KrylovWS* W = &A->ws;
+  W->red.gpart = A->comm ? comm_red_buffer(A->comm, W) : W->gpart[0];
+  cgs_dispatch<1>(nv, mode, (int)W->red.nseg, A->stream, n, ld, W->V, w, h, W->red, out, gate);
+  if (A->comm) return comm_red_final_n(A->comm, W, mode == 3 ? 1 : nv + 1, out, gate, A->stream);
+  return GKS_OK;
 }
 
 template __global__ void k_red_final<1, 0>(RedSrc, int64_t, RedOut, const int*);
@@ -437,6 +527,21 @@ __device__ __forceinline__ void gm_reorth_check(GmresDev* g, int j) {
 }
 
 __global__ void k_gm_reorth_check(GmresDev* g, int j) { gm_reorth_check(g, j); }
+
+// CGS2 column j: Hessenberg column = first + second projection; the norm is
+// that of the twice-orthogonalised w (no conditional pass)
+__global__ void k_gm_cgs_check(GmresDev* g, int j) {
+  if (!g->active) {
+    g->reorth_gate = 0;
+    return;
+  }
+  g->matvecs += 1;
+  for (int i = 0; i <= j; ++i) GH(i, j) = g->dots[i] + g->corr[i];
+  g->wscale = sqrt(g->wscale2);
+  GH(j + 1, j) = sqrt(g->hnext2);
+  g->reorth = 0;
+  g->reorth_gate = 0;
+}
 
 // Givens update of column j (krylov.py:107-124).  The column, the stored
 // rotations and the right-hand side entries are read into registers before
@@ -845,9 +950,9 @@ void krylov_free(KrylovWS* W) {
 }
 
 __global__ void k_red_init(int64_t ngrp_g, double* a, double* b) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < RED_MAXC * ngrp_g;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < RED_SLOTS * ngrp_g;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const double v = i < 3 * ngrp_g ? 0.0 : INFINITY;  // sums | min (the step stats' dt)
+    const double v = i < RED_MIN_SLOT * ngrp_g ? 0.0 : INFINITY;  // sums | the min slot
     a[i] = v;
     b[i] = v;
   }
@@ -874,12 +979,13 @@ static int red_setup(BlockSys* A, KrylovWS* W) {
   R.ngrp_g = (nseg_g + G - 1) / G;
   R.grp_first = first / gcells;
   R.finalize = A->comm ? 0 : 1;
-  GKS_CUDA(cudaMalloc(&R.spart, (size_t)RED_MAXC * R.nseg * sizeof(double)));
-  for (int k = 0; k < 2; ++k) GKS_CUDA(cudaMalloc(&W->gpart[k], (size_t)RED_MAXC * R.ngrp_g * sizeof(double)));
-  GKS_CUDA(cudaMalloc(&W->gall, (size_t)RED_MAXC * R.ngrp_g * sizeof(double)));
+  // (room for the CGS2 multi-dots: up to RED_MAXC_MD components)
+  GKS_CUDA(cudaMalloc(&R.spart, (size_t)RED_SLOTS * R.nseg * sizeof(double)));
+  for (int k = 0; k < 2; ++k) GKS_CUDA(cudaMalloc(&W->gpart[k], (size_t)RED_SLOTS * R.ngrp_g * sizeof(double)));
+  GKS_CUDA(cudaMalloc(&W->gall, (size_t)RED_SLOTS * R.ngrp_g * sizeof(double)));
   GKS_CUDA(cudaMalloc(&R.cnt, (size_t)(R.ngrp + 1) * sizeof(unsigned)));
   GKS_CUDA(cudaMemset(R.cnt, 0, (size_t)(R.ngrp + 1) * sizeof(unsigned)));
-  k_red_init<<<blocks_for(RED_MAXC * R.ngrp_g, 256), 256>>>(R.ngrp_g, W->gpart[0], W->gpart[1]);
+  k_red_init<<<blocks_for(RED_SLOTS * R.ngrp_g, 256), 256>>>(R.ngrp_g, W->gpart[0], W->gpart[1]);
   GKS_CUDA(cudaGetLastError());
   GKS_CUDA(cudaDeviceSynchronize());
   R.gpart = W->gpart[0];
@@ -1198,7 +1304,11 @@ int gmres_enqueue(BlockSys* A, const double* b_dev, double* x_dev, const GmresPa
   // Arnoldi column, w in shared memory (k_gm_arnoldi)
   const char* small_env = getenv("GKS_GMRES_SMALL");
   int cl = 0;  // cluster size of the fused column kernel, 0 = multi-block chain
-  if (!A->comm && !A->canonical && !(small_env && small_env[0] == '0')) cl = arnoldi_cluster(n);
+  if (P.ortho == 1 && m > CGS_MAXV) {
+    set_error("gmres: ortho=cgs2 supports krylov_dim <= %d", CGS_MAXV);
+    return GKS_ERR_BAD_ARG;
+  }
+  if (!A->comm && !A->canonical && P.ortho == 0 && !(small_env && small_env[0] == '0')) cl = arnoldi_cluster(n);
   auto Av = [&](const double* v, double* dst, const int* gate) -> int {
     if (matvec) return (*matvec)(v, dst, gate);
     bs_spmv(A, v, dst, gate);
@@ -1225,6 +1335,23 @@ int gmres_enqueue(BlockSys* A, const double* b_dev, double* x_dev, const GmresPa
       if (cl) {
         // the whole column in one kernel (k_gm_arnoldi)
         TRY_GM(launch_arnoldi(cl, s, (int)n, ld, W->V, W->w, g, j, cyc));
+        continue;
+      }
+      if (P.ortho == 1) {
+        // CGS2: three fused passes, three reductions per column (instead of
+        // j + 2 sequential MGS dots plus the conditional second sweep)
+        RedOutN o1, o2, o3;
+        o1.base = g->dots;
+        o1.last = &g->wscale2;
+        o2.base = g->corr;
+        o2.last = &g->hnext2;
+        o3.last = &g->hnext2;
+        TRY_GM(cgs_pass(A, 1, j + 1, n, ld, W->w, nullptr, o1, act));
+        TRY_GM(cgs_pass(A, 2, j + 1, n, ld, W->w, g->dots, o2, act));
+        TRY_GM(cgs_pass(A, 3, j + 1, n, ld, W->w, g->corr, o3, act));
+        GKS_LAUNCH(KC_SCALAR, k_gm_cgs_check, 1, 1, 0, s, g, j);
+        GKS_LAUNCH(KC_SCALAR, k_gm_givens, 1, 1, 0, s, g, j, cyc);
+        GKS_LAUNCH(KC_VEC, k_div, grid, RB_THREADS, 0, s, n, W->V + (int64_t)(j + 1) * ld, W->w, &g->hdiv, act);
         continue;
       }
       // ||w||^2 and w.v_0 in one pass, then fused axpy + next dot (MGS)

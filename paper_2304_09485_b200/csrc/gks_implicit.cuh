@@ -75,6 +75,7 @@ struct GmresParams {
   int m = 10, restarts = 3, kmax = 2;
   double rtol = 0.0, atol = 0.0;
   int check_ortho = 0;
+  int ortho = 0;  // 0: MGS + conditional re-orthogonalisation (krylov.py:89-106); 1: CGS2 fused multi-dots
 };
 
 struct GmresHost {

@@ -30,6 +30,12 @@ constexpr int SEG_CELLS = 768;   // cells per segment (5 * 768 = 15 * 256 vector
 constexpr int RED_T = 256;       // threads per reduction block (one segment per block)
 constexpr int RED_MAXC = 4;      // components per reduction (step stats: 3 sums + 1 min)
 constexpr int RED_MAXGRP = 1024; // groups per mesh (bounds the exchanged partials)
+constexpr int RED_MAXC_MD = 16;  // sum components of the CGS2 multi-dots (krylov_dim <= 14)
+// buffer layout [component][group]: sums at 0 .. RED_MAXC_MD-1, the min
+// component (step stats' dt) at RED_MIN_SLOT, +inf outside the owner's range
+constexpr int RED_MIN_SLOT = RED_MAXC_MD;
+constexpr int RED_SLOTS = RED_MAXC_MD + 1;
+__host__ __device__ constexpr int red_slot(int c, int ns) { return c < ns ? c : RED_MIN_SLOT + (c - ns); }
 
 // Segments per group for a mesh of nc_global cells: the smallest power of two
 // that keeps the number of groups <= RED_MAXGRP.  A function of the global
@@ -51,8 +57,8 @@ struct RedDev {
   int64_t ngrp = 0;       // local groups
   int64_t ngrp_g = 0;     // global groups
   int64_t grp_first = 0;  // global index of local group 0
-  double* spart = nullptr;  // [RED_MAXC][nseg] segment partials
-  double* gpart = nullptr;  // [RED_MAXC][ngrp_g] group partials (this rank's entries only)
+  double* spart = nullptr;  // [RED_SLOTS][nseg] segment partials
+  double* gpart = nullptr;  // [RED_SLOTS][ngrp_g] group partials (this rank's entries only)
   unsigned* cnt = nullptr;  // [ngrp + 1] arrival counters (self-resetting)
   int finalize = 1;         // single rank: the last block folds the group partials
 };
@@ -147,6 +153,54 @@ __device__ __forceinline__ void red_finish(const RedDev& R, const double* v, con
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     const double t = c < NS ? red_tree<0>(v[c], sm) : red_tree<1>(v[c], sm);
+    if (threadIdx.x == 0) R.spart[red_slot(c, NS) * R.nseg + b] = t;
+  }
+  const int64_t gl = b / R.G;
+  const int64_t g0 = gl * R.G;
+  const int gsz = (int)min((int64_t)R.G, R.nseg - g0);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicInc(R.cnt + gl, (unsigned)gsz - 1u) == (unsigned)gsz - 1u;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const double* sp = R.spart + red_slot(c, NS) * R.nseg + g0;
+    const double t = c < NS ? red_fold_arr<0>(sp, gsz, sm) : red_fold_arr<1>(sp, gsz, sm);
+    if (threadIdx.x == 0) R.gpart[red_slot(c, NS) * R.ngrp_g + R.grp_first + gl] = t;
+  }
+  if (!R.finalize) return;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicInc(R.cnt + R.ngrp, (unsigned)R.ngrp - 1u) == (unsigned)R.ngrp - 1u;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const double* gp = R.gpart + red_slot(c, NS) * R.ngrp_g;
+    const double t = c < NS ? red_fold_arr<0>(gp, R.ngrp_g, sm) : red_fold_arr<1>(gp, R.ngrp_g, sm);
+    if (threadIdx.x == 0 && out.o[c]) *out.o[c] = t;
+  }
+}
+
+// Multi-component sums (the CGS2 multi-dots): NC components written to
+// base[0..NC-2] and last, folded like red_finish (one tree per component).
+struct RedOutN {
+  double* base = nullptr;  // components 0 .. NC-2
+  double* last = nullptr;  // component NC-1
+};
+
+template <int NC>
+__device__ __forceinline__ void red_finish_n(const RedDev& R, const double* v, const RedOutN& out, double* sm) {
+  __shared__ bool last;
+  const int64_t b = blockIdx.x;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const double t = red_tree<0>(v[c], sm);
     if (threadIdx.x == 0) R.spart[c * R.nseg + b] = t;
   }
   const int64_t gl = b / R.G;
@@ -161,8 +215,7 @@ __device__ __forceinline__ void red_finish(const RedDev& R, const double* v, con
   __threadfence();
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
-    const double* sp = R.spart + c * R.nseg + g0;
-    const double t = c < NS ? red_fold_arr<0>(sp, gsz, sm) : red_fold_arr<1>(sp, gsz, sm);
+    const double t = red_fold_arr<0>(R.spart + c * R.nseg + g0, gsz, sm);
     if (threadIdx.x == 0) R.gpart[c * R.ngrp_g + R.grp_first + gl] = t;
   }
   if (!R.finalize) return;
@@ -175,9 +228,11 @@ __device__ __forceinline__ void red_finish(const RedDev& R, const double* v, con
   __threadfence();
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
-    const double* gp = R.gpart + c * R.ngrp_g;
-    const double t = c < NS ? red_fold_arr<0>(gp, R.ngrp_g, sm) : red_fold_arr<1>(gp, R.ngrp_g, sm);
-    if (threadIdx.x == 0 && out.o[c]) *out.o[c] = t;
+    const double t = red_fold_arr<0>(R.gpart + c * R.ngrp_g, R.ngrp_g, sm);
+    if (threadIdx.x == 0) {
+      double* o = c < NC - 1 ? out.base + c : out.last;
+      if (o) *o = t;
+    }
   }
 }
 

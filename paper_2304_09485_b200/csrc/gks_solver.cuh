@@ -70,6 +70,7 @@ struct Handle {
   // options
   int scheme = 0, model = 0, compact = 0, linear_weights = 0, global_dt = 0, jac_mode = 0;
   int first_order = 0;  // KFVS on piecewise-constant states (no reconstruction, tau = inf)
+  int ortho = 0;        // GMRES orthogonalisation: 0 MGS, 1 CGS2
   double mu = 0, gamma = 1.4, cfl = 2, eps = 1e-6, lw = 0.025;
   KinConst kc;
   int krylov_dim = 10, restarts = 3, jacobi_sweeps = 2;
@@ -308,6 +309,7 @@ void comm_destroy(Handle* H);
 struct KrylovWS;
 double* comm_red_buffer(Comm* c, KrylovWS* W);
 int comm_red_final(Comm* c, KrylovWS* W, int ns, int nm, const RedOut& out, const int* gate, cudaStream_t s);
+int comm_red_final_n(Comm* c, KrylovWS* W, int nc, const RedOutN& out, const int* gate, cudaStream_t s);
 int local_dt_device(Handle* H);
 int boundary_ghosts_device(Handle* H, const double* q);
 int gauss_gradients_device(Handle* H, const double* qpt, double* grad_out);

@@ -78,6 +78,7 @@ class SolverOptions:
     device: int = 0
     reorder: str = "none"  # device-side locality renumbering: "none" | "rcm" | "morton" (reorder.py)
     first_order: bool = False  # KFVS on piecewise-constant states (the paper's low-order start)
+    ortho: str = "mgs"  # GMRES orthogonalisation: "mgs" (reference, krylov.py:89-106) | "cgs2" (fused multi-dots)
 
     def __post_init__(self):
         if self.scheme not in SCHEMES:
@@ -90,6 +91,8 @@ class SolverOptions:
             raise ValueError(f"weights must be 'nonlinear' or 'linear', got {self.weights!r}")
         if self.jacobian not in JACOBIANS:
             raise ValueError(f"jacobian must be one of {JACOBIANS}")
+        if self.ortho not in ("mgs", "cgs2"):
+            raise ValueError("ortho must be 'mgs' or 'cgs2'")
         from .reorder import METHODS
 
         if self.reorder not in METHODS:
@@ -127,6 +130,7 @@ def _options_struct(opt: SolverOptions, mesh: Mesh):
     o.npatch = n
     o.patches = arr
     o.first_order = int(bool(opt.first_order))
+    o.ortho = ("mgs", "cgs2").index(opt.ortho)
     return o, arr
 
 

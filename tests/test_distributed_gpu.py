@@ -212,3 +212,28 @@ def test_device_dot_is_the_specified_fold(nc):
     N.check(lib.gks_blocksys_dot(h, N.dptr(x), N.dptr(y), C.byref(out)))
     lib.gks_blocksys_destroy(h)
     assert out.value == _fold.dot(x, y)
+
+
+@pytest.mark.parametrize("jac", ["roe", "frechet"])
+def test_cgs2_multidot_gmres(jac):
+    """ortho="cgs2": three fused multi-dot passes per Arnoldi column.  Same
+    step results as the reference MGS to rounding, partition-invariant
+    (2-rank loopback bitwise equal to the canonical 1-rank run)."""
+    from paper_2304_09485_b200.stepping import SolutionField, Solver
+
+    mesh, opts, q, grad = setup_case("weno", 4)
+    mgs = dataclasses.replace(opts, jacobian=jac)
+    cgs = dataclasses.replace(opts, jacobian=jac, ortho="cgs2")
+    a, b = Solver(mesh, mgs), Solver(mesh, cgs)
+    a.upload(SolutionField(q, grad))
+    b.upload(SolutionField(q, grad))
+    tol = 1e-9 if jac == "roe" else 1e-6
+    for _ in range(4):
+        ia, ib = a.advance_resident(), b.advance_resident()
+        assert ia.solver_cycles == ib.solver_cycles and ia.matvecs == ib.matvecs
+        assert abs(ia.res_rho_l1 - ib.res_rho_l1) <= tol * abs(ia.res_rho_l1)
+    assert np.max(np.abs(a.download().q - b.download().q)) <= tol * np.max(np.abs(a.download().q))
+    h1, q1, _ = _run_ranks(mesh, cgs, q, grad, 1, 3)
+    h2, q2, _ = _run_ranks(mesh, cgs, q, grad, 2, 3)
+    assert [(x.res_rho_l1, x.res_l2) for x in h1] == [(x.res_rho_l1, x.res_l2) for x in h2]
+    assert np.array_equal(q1, q2)

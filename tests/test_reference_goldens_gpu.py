@@ -125,8 +125,8 @@ def decade_crossings(traj, decades):
     return out
 
 
-@pytest.mark.parametrize("case", ["cavity4", "cavity8"])
-def test_converged_cavity_matches_reference(golden, case):
+@pytest.mark.parametrize("case,ortho", [("cavity4", "mgs"), ("cavity8", "mgs"), ("cavity8", "cgs2")])
+def test_converged_cavity_matches_reference(golden, case, ortho):
     from paper_2304_09485_b200.boundary import PatchSpec
     from paper_2304_09485_b200.mesh import generate_box_mesh
     from paper_2304_09485_b200.stepping import SolutionField, Solver, SolverOptions, initial_field
@@ -140,7 +140,8 @@ def test_converged_cavity_matches_reference(golden, case):
     patches = {nm: PatchSpec(nm, "wall_noslip_isothermal", lambda_wall=lam_wall) for nm in mesh.patch_names}
     patches["ymax"] = PatchSpec("ymax", "wall_noslip_isothermal", lambda_wall=lam_wall,
                                 velocity=np.array([0.15, 0.0, 0.0]))
-    s = Solver(mesh, SolverOptions(scheme="weno_gmres", model="viscous", mu=0.15 / 100.0, patches=patches, cfl=2.0))
+    s = Solver(mesh, SolverOptions(scheme="weno_gmres", model="viscous", mu=0.15 / 100.0, patches=patches, cfl=2.0,
+                                   ortho=ortho))
     s.upload(initial_field(mesh, [1.0, 0.0, 0.0, 0.0, 1.0 / GAMMA]))
     traj, steps = [], None
     for k in range(1, ref_steps + 50):

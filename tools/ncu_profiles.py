@@ -22,6 +22,9 @@ FP64 = 33.77  # live DFMA probe (gks_fp64_peak) on this pool, TFLOP/s
 C2 = dict(nc=1474560, nf=2955264, nfq=8865792)
 C2["nfi"] = C2["nf"] - 6 * 16 * 16 * 4 * 2  # interior faces: two spherical shells of boundary faces
 C1 = dict(nc=6 * 16 ** 3)
+# C1 n=64 periodic box (Roe GMRES): 4 faces per tet shared -> 2 nc interior faces, nnz = 4 nc
+_n1 = 6 * 64 ** 3
+C1B = {"spmv": _n1 * (4 + 4 * 8 + 2 * 40 + 40 + 40 + 200 + 40 + 40) + _n1 * (200 + 40)}
 K, M, S = 13, 4, 6  # padded WENO record of the sphere (k_recon_weno<13, 4, 6>)
 HA, HG, HM = 4, 5, 4  # padded HWENO record (k_recon_hweno<4, 5, 4>)
 
@@ -39,7 +42,7 @@ def model():
         "c3_recon_hweno": ("bytes", nc * (9 * (HA + 3 * HG) * 8 + (HA + HG) * 4 + HG * 8 + 360 + 40 + 120 + 360),
                            "operator records (linear weights: no sub-stencils) + Q, grad + C write"),
         "c2_assemble5": ("bytes", nfq * 40 + nc * 44 + 2 * nfq * 4, "contributions + CSR list + res write"),
-        "c2_roe_mf5": ("bytes", sweep + nc * 200, "CSR + face (n,S/2,lam) + prims + x + D + D^-1 + out"),
+        "c1_roe_mf5": ("bytes", C1B["spmv"], "C1 n=64: CSR + face records + prims + x + D + D^-1 + out (+pre)"),
         "c2_roe_mf6": ("bytes", sweep, "CSR + face records + prims + x + D^-1 + b + out"),
         "c2_axpy_dot": ("bytes", 4 * 8 * n5, "w read+write, v_i, v_(i+1)"),
         "c2_dot2": ("bytes", 2 * 8 * n5, "w (twice, one pass) and v_0"),
