@@ -332,6 +332,8 @@ int gks_bad_mask(GksHandle* h, int8_t* out);
 int gks_set_graph(GksHandle* h, int enable);
 /* change SolverOptions.cfl of a live handle (a CFL ramp; next step re-captures) */
 int gks_set_cfl(GksHandle* h, double cfl);
+/* GMRES orthogonalisation of a live handle: 0 MGS (reference), 1 CGS2 */
+int gks_set_ortho(GksHandle* h, int ortho);
 /* Solver.frechet_matvec (stepping.py:298-313); sigma <= 0 selects the
    reference's automatic step.  out = (L(q + s v) - L(q)) / s */
 int gks_frechet_matvec(GksHandle* h, const double* q, const double* grad, const double* dt, const double* v,

@@ -217,6 +217,7 @@ SIGNATURES = [
     ("gks_advance_resident", C.c_int, [C.c_void_p, C.c_void_p]),
     ("gks_set_graph", C.c_int, [C.c_void_p, C.c_int]),
     ("gks_set_cfl", C.c_int, [C.c_void_p, C.c_double]),
+    ("gks_set_ortho", C.c_int, [C.c_void_p, C.c_int]),
     ("gks_bad_mask", C.c_int, [C.c_void_p, C.c_void_p]),
     ("gks_ugks_read", C.c_int, [C.c_char_p, C.c_void_p]),
     ("gks_ugks_sizes", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

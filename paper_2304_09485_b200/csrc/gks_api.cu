@@ -1370,6 +1370,19 @@ int gks_set_cfl(GksHandle* G, double cfl) {
   return GKS_OK;
 }
 
+int gks_set_ortho(GksHandle* G, int ortho) {
+  if (!G || ortho < 0 || ortho > 1) {
+    set_error("gks_set_ortho: bad arguments");
+    return GKS_ERR_BAD_ARG;
+  }
+  G->H.ortho = ortho;
+  for (StepGraph& g : G->graphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g = StepGraph();
+  }
+  return GKS_OK;
+}
+
 int gks_set_graph(GksHandle* G, int enable) {
   if (!G) return GKS_ERR_BAD_ARG;
   G->graph = enable ? 1 : 0;

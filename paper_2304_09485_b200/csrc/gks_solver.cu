@@ -453,7 +453,6 @@ struct FaceArgs {
   KinConst kc;
   int want_point;
   int fq_nq;
-  double tau_in;  // < 0: the scheme's collision time; +inf: collisionless (KFVS, first order)
   double* contrib;
   const int2* fq_slot;  // slot mode (non-null): contributions go to the assembly slots
   double* slots;
@@ -466,7 +465,10 @@ struct FaceArgs {
 // cp.async before the compute was measured 32 % slower: 3.52 vs 2.66 ms on
 // C2 -- the CTA-wide barrier serialises load and compute phases and the
 // 45 KB of records per CTA take L1 from the spills.)
-template <bool VISC, bool POINT>
+// KFVS: first-order collisionless flux (tau = inf, SolverOptions.first_order)
+// -- a compile-time branch, so the high-order kernel keeps its constant
+// tau_in and register allocation
+template <bool VISC, bool POINT, bool KFVS>
 __global__ void __launch_bounds__(128, GKS_FACE_MINB) k_face(FaceArgs A) {
   if (A.gate && !*A.gate) return;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -595,8 +597,9 @@ __global__ void __launch_bounds__(128, GKS_FACE_MINB) k_face(FaceArgs A) {
   };
   double fl[5], pv[5];
   int rc;
-  if (GKS_FACE_TAU == 2) rc = interface_flux_t<VISC, POINT, 2>(get, press_r, A.tau_in, dtf, A.mu, A.kc, fl, 0.0, pv);
-  else rc = interface_flux_t<VISC, POINT, GKS_FACE_TAU>(get, press, A.tau_in, dtf, A.mu, A.kc, fl, 0.0, pv);
+  constexpr double tau_in = KFVS ? INFINITY : -1.0;
+  if (GKS_FACE_TAU == 2) rc = interface_flux_t<VISC, POINT, 2>(get, press_r, tau_in, dtf, A.mu, A.kc, fl, 0.0, pv);
+  else rc = interface_flux_t<VISC, POINT, GKS_FACE_TAU>(get, press, tau_in, dtf, A.mu, A.kc, fl, 0.0, pv);
   if (rc) {
     if (ghost_fail) {
       atomicCAS(A.status, 0, GKS_ERR_UNPHYSICAL);
@@ -938,7 +941,6 @@ int residual_device(Handle* H, const double* q, double* res, bool with_gradients
   A.fq_point = H->fq_point; A.fq_ws = H->fq_ws; A.f_frame = H->f_frame; A.f_normal = H->f_normal;
   A.f_shift = H->f_shift; A.patches = H->patches; A.model = H->model; A.mu = H->mu; A.kc = H->kc;
   A.want_point = with_gradients ? 1 : 0;
-  A.tau_in = H->first_order ? INFINITY : -1.0;
   A.fq_nq = H->fq_nq;
   A.contrib = H->contrib; A.qpt = H->qpt; A.status = H->status; A.gate = gate;
   static const int slot_env = [] {
@@ -950,13 +952,19 @@ int residual_device(Handle* H, const double* q, double* res, bool with_gradients
   A.fq_slot = slot_mode ? H->fq_slot : nullptr;
   A.slots = H->slots;
   const int fb = blocks_for(H->nfq, 128);
+#define GKS_FACE(V, P)                                                                    \
+  do {                                                                                    \
+    if (H->first_order) GKS_LAUNCH(KC_FACE, (k_face<V, P, true>), fb, 128, 0, H->stream, A); \
+    else GKS_LAUNCH(KC_FACE, (k_face<V, P, false>), fb, 128, 0, H->stream, A);            \
+  } while (0)
   if (H->model == 1) {
-    if (with_gradients) GKS_LAUNCH(KC_FACE, (k_face<true, true>), fb, 128, 0, H->stream, A);
-    else GKS_LAUNCH(KC_FACE, (k_face<true, false>), fb, 128, 0, H->stream, A);
+    if (with_gradients) GKS_FACE(true, true);
+    else GKS_FACE(true, false);
   } else {
-    if (with_gradients) GKS_LAUNCH(KC_FACE, (k_face<false, true>), fb, 128, 0, H->stream, A);
-    else GKS_LAUNCH(KC_FACE, (k_face<false, false>), fb, 128, 0, H->stream, A);
+    if (with_gradients) GKS_FACE(false, true);
+    else GKS_FACE(false, false);
   }
+#undef GKS_FACE
   static const int asm5 = [] {
     const char* e = getenv("GKS_ASSEMBLE5");
     return e ? atoi(e) : 1;

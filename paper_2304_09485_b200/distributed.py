@@ -37,6 +37,17 @@ from .partition import Decomposition, LocalMesh, SetupMesh, build_domain
 from .stepping import Solver, SolverOptions, SolutionField, _info, _options_struct
 
 
+def _bind_torch_nccl():
+    """libgks dlopens libnccl.so.2 with RTLD_NOLOAD first: importing torch
+    before the first NCCL call makes that the NCCL build torch ships (and
+    keeps torch importable afterwards -- the reverse order leaves the older
+    system NCCL bound in front of torch's)."""
+    try:
+        import torch  # noqa: F401
+    except Exception:
+        pass
+
+
 def _halo_desc(send: dict, recv: dict, keep):
     peers = sorted(set(send) | set(recv))
     so = np.zeros(len(peers) + 1, dtype=np.int64)
@@ -156,6 +167,7 @@ class DistributedSolver:
         self._sub = None
         self._setup = None
         if comm_id is not None:
+            _bind_torch_nccl()
             buf = (C.c_char * 128).from_buffer_copy(bytes(comm_id))
             N.check(lib.gks_comm_init(h, buf, nranks, rank))
         elif loopback is not None:
@@ -166,6 +178,7 @@ class DistributedSolver:
 
     @staticmethod
     def unique_id() -> bytes:
+        _bind_torch_nccl()
         buf = (C.c_char * 128)()
         N.check(N.load().gks_comm_unique_id(buf, 128))
         return bytes(buf)

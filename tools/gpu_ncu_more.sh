@@ -7,7 +7,7 @@ cap() {  # tag regex bench-args...
     > gpurun_out/ncu/$tag.log 2>&1
   echo "$tag rc=$?"
 }
-cap c2_face "k_face<.bool.0, .bool.0>"
+cap c2_face "k_face<.bool.0, .bool.0, .bool.0>"
 cap c2_roe_mf6 "k_roe_mf<.int.6>"
 cap c1_roe_mf5 "k_roe_mf<.int.5>" --workload c1 --n 64
-cap c3_face11 "k_face<.bool.1, .bool.1>" --workload c3
+cap c3_face11 "k_face<.bool.1, .bool.1, .bool.0>" --workload c3
