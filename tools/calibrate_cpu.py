@@ -51,12 +51,11 @@ def main(ns):
         for _ in range(3):
             s.residual(fld, dt)
         ref_res = (time.perf_counter() - t0) / 3
-        sys.argv = ["bench.py", "--cpu-n", str(n)]
+        sys.argv = ["bench.py", "--cpu-n", str(n), "--n", str(n)]
         args = bench.parse()
         o = bench.cpu_sample((dict(vars(args)), "roe", 3))
-        os_ = OracleSolver(bench.build_workload(args, False)[0], scheme="weno_gmres",
-                           patches=bench.c2_problem(bench.build_workload(args, False)[0], False)[0], jacobian="roe")
-        q = bench.build_workload(args, False)[2]
+        omesh, opatches, q, _, _, _ = bench.build_workload(args, False)
+        os_ = OracleSolver(omesh, scheme="weno_gmres", patches=opatches, jacobian="roe")
         dto = os_.local_dt(q)
         os_.residual(q, None, dto)
         t0 = time.perf_counter()
