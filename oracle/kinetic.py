@@ -108,6 +108,7 @@ class Moments:
         self.xi[0] = 1.0
         self.xi[1] = nd / (2.0 * lam)
         self.xi[2] = nd * (nd + 2.0) / (4.0 * lam * lam)
+        self._psi = {}  # psi(a, b, c, s) memo: directional / slope revisit the same orders
 
     def m(self, a, b, c, s):
         """<u^a v^b w^c xi^(2s)> (kinetic.py:173-188)."""
@@ -122,6 +123,10 @@ class Moments:
 
     def psi(self, a, b, c, s=0):
         """<u^a v^b w^c xi^2s psi>, shape (n, 5)  (kinetic.py:191-213)."""
+        key = (a, b, c, s)
+        hit = self._psi.get(key)
+        if hit is not None:
+            return hit
         m = self.m
         out = np.empty((self.rho.shape[0], 5))
         out[:, 0] = m(a, b, c, s)
@@ -129,6 +134,8 @@ class Moments:
         out[:, 2] = m(a, b + 1, c, s)
         out[:, 3] = m(a, b, c + 1, s)
         out[:, 4] = 0.5 * (m(a + 2, b, c, s) + m(a, b + 2, c, s) + m(a, b, c + 2, s) + m(a, b, c, s + 1))
+        out.flags.writeable = False
+        self._psi[key] = out
         return out
 
     def slope(self, coef, a, b, c):

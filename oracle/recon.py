@@ -288,20 +288,21 @@ class Recon:
         qc = q[:, None, :]
         if self.compact:
             h = self.mesh.cell_h
-            cb = np.einsum("cda,cav->cdv", self.P_bigA, q[self.P_aid] - qc)
-            cb += np.einsum("cdgx,cgxv->cdv", self.P_bigG, h[self.P_gid][:, :, None, None] * grad[self.P_gid])
+            cb = np.matmul(self.P_bigA, q[self.P_aid] - qc)
+            gg = h[self.P_gid][:, :, None, None] * grad[self.P_gid]  # (nc, g, 3, 5)
+            cb += np.matmul(self.P_bigG.reshape(gg.shape[0], -1, gg.shape[1] * 3), gg.reshape(gg.shape[0], -1, 5))
             if self.linear:
                 return cb
             j = self.P_sj
             hg = h[:, None, None] * grad  # (nc, 3, 5)
             rhs = np.concatenate([(q[j] - qc)[:, :, None, :], np.broadcast_to(hg[:, None], j.shape + (3, 5)),
                                   hg[j]], axis=2)  # (nc, M, 7, 5)
-            bs = np.einsum("cmds,cmsv->cmdv", self.P_sub, rhs)
+            bs = np.matmul(self.P_sub, rhs)
         else:
-            cb = np.einsum("cdk,ckv->cdv", self.P_big, q[self.P_gid] - qc)
+            cb = np.matmul(self.P_big, q[self.P_gid] - qc)
             if self.linear:
                 return cb
-            bs = np.einsum("cmds,cmsv->cmdv", self.P_sub, q[self.P_sid] - q[:, None, None, :])
+            bs = np.matmul(self.P_sub, q[self.P_sid] - q[:, None, None, :])
         return self._combine_all(cb, bs, self.P_act)
 
     def _combine_all(self, cb, bs, act):
@@ -310,7 +311,7 @@ class Recon:
         m = act.sum(axis=1).astype(float)  # (nc,)
         has = m > 0
         ms = np.where(has, m, 1.0)
-        b0 = np.einsum("cdv,cde,cev->cv", cb, self.beta, cb)
+        b0 = np.sum(cb * np.matmul(self.beta, cb), axis=1)
         bm = np.sum(bs * bs, axis=2)  # (nc, M, 5)
         g0 = (1.0 - self.lw * m)[:, None]
         tau = np.sum(np.where(act[:, :, None], np.abs(b0[:, None, :] - bm), 0.0), axis=1) / ms[:, None]
@@ -320,7 +321,7 @@ class Recon:
         g0s = np.where(has[:, None], g0, 1.0)
         out = (w0 / tot / g0s)[:, None, :] * cb
         f = np.where(act[:, :, None], wm / tot[:, None, :] - (w0 / tot * self.lw / g0s)[:, None, :], 0.0)
-        out[:, :3] += np.einsum("cmv,cmdv->cdv", f, bs)
+        out[:, :3] += np.sum(f[:, :, None, :] * bs, axis=1)
         return np.where(has[:, None, None], out, cb)
 
     def face_states(self, q, coef):
@@ -337,7 +338,7 @@ class Recon:
             phi = mono(x) - self.avg0[cells]
             dphi = dmono(x) / h[:, None, None]
             cf = coef[cells]
-            sides.append((q[cells] + np.einsum("fd,fdk->fk", phi, cf), np.einsum("fxd,fdk->fxk", dphi, cf)))
+            sides.append((q[cells] + np.matmul(phi[:, None, :], cf)[:, 0], np.matmul(dphi, cf)))
         (vo, go), (vn, gn) = sides
         return vo, go, np.where(inner[:, None], vn, vo), np.where(inner[:, None, None], gn, go)
 

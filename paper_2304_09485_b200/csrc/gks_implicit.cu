@@ -843,6 +843,9 @@ __global__ void k_roe_prim(int64_t n, const double* __restrict__ q, double gm1, 
 // records into shared memory by bulk copies, as the reconstruction does, was
 // measured 2x slower here: each CTA then waits for its whole tile.)
 static constexpr int MF_CELLS = 128;
+#ifndef GKS_ROE_BATCH
+#define GKS_ROE_BATCH 1
+#endif
 
 template <int MODE>
 __global__ void __launch_bounds__(MF_CELLS) k_roe_mf(int64_t nc, const int* __restrict__ rowptr,
@@ -856,17 +859,11 @@ __global__ void __launch_bounds__(MF_CELLS) k_roe_mf(int64_t nc, const int* __re
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nc) return;
   double o[5] = {0, 0, 0, 0, 0};
-  for (int e = rowptr[c]; e < rowptr[c + 1]; ++e) {
-    const int64_t j = col[e];
-    const int en = __ldg(ent + e);
-    const double2* fd = (const double2*)(fdat + (int64_t)(en >> 1) * MF_REC);
-    const double2 f01 = __ldg(fd), f23 = __ldg(fd + 1), f45 = __ldg(fd + 2);
+  auto term = [&](int64_t j, int en, double2 f01, double2 f23, double2 f45, double2 p01, double2 p23, double2 p45,
+                  const double* xj) {
     const double sg = (en & 1) ? -1.0 : 1.0;
     const double nx = f01.x, ny = f01.y, nz = f23.x, hs = f23.y, lam = f45.x;
-    const double2* P = (const double2*)(prim + j * MF_REC);
-    const double2 p01 = __ldg(P), p23 = __ldg(P + 1), p45 = __ldg(P + 2);
     const double vx = p01.x, vy = p01.y, vz = p23.x, H = p23.y, ke = p45.x;
-    const double* xj = x + j * 5;
     const double x0 = xj[0], x1 = xj[1], x2 = xj[2], x3 = xj[3], x4 = xj[4];
     const double mx = nx * x1 + ny * x2 + nz * x3;
     const double un = nx * vx + ny * vy + nz * vz;
@@ -878,6 +875,39 @@ __global__ void __launch_bounds__(MF_CELLS) k_roe_mf(int64_t nc, const int* __re
     o[2] += sh * (vy * a + un * x2 + ny * bb) - lh * x2;
     o[3] += sh * (vz * a + un * x3 + nz * bb) - lh * x3;
     o[4] += sh * (H * a + un * (bb + x4)) - lh * x4;
+  };
+  const int e0 = rowptr[c], e1 = rowptr[c + 1];
+  int e = e0;
+#if GKS_ROE_BATCH
+  // pairs of entries: both index loads, then both entries' face / cell /
+  // x records in flight, then the terms in CSR order
+  for (; e + 2 <= e1; e += 2) {
+    const int64_t ja = col[e], jb = col[e + 1];
+    const int ea = __ldg(ent + e), eb = __ldg(ent + e + 1);
+    const double2* fa = (const double2*)(fdat + (int64_t)(ea >> 1) * MF_REC);
+    const double2* fb = (const double2*)(fdat + (int64_t)(eb >> 1) * MF_REC);
+    const double2* pa = (const double2*)(prim + ja * MF_REC);
+    const double2* pb = (const double2*)(prim + jb * MF_REC);
+    const double2 fa0 = __ldg(fa), fa1 = __ldg(fa + 1), fa2 = __ldg(fa + 2);
+    const double2 fb0 = __ldg(fb), fb1 = __ldg(fb + 1), fb2 = __ldg(fb + 2);
+    const double2 pa0 = __ldg(pa), pa1 = __ldg(pa + 1), pa2 = __ldg(pa + 2);
+    const double2 pb0 = __ldg(pb), pb1 = __ldg(pb + 1), pb2 = __ldg(pb + 2);
+    double xa[5], xb[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      xa[k] = x[ja * 5 + k];
+      xb[k] = x[jb * 5 + k];
+    }
+    term(ja, ea, fa0, fa1, fa2, pa0, pa1, pa2, xa);
+    term(jb, eb, fb0, fb1, fb2, pb0, pb1, pb2, xb);
+  }
+#endif
+  for (; e < e1; ++e) {
+    const int64_t j = col[e];
+    const int en = __ldg(ent + e);
+    const double2* fd = (const double2*)(fdat + (int64_t)(en >> 1) * MF_REC);
+    const double2* P = (const double2*)(prim + j * MF_REC);
+    term(j, en, __ldg(fd), __ldg(fd + 1), __ldg(fd + 2), __ldg(P), __ldg(P + 1), __ldg(P + 2), x + j * 5);
   }
   double r[5];
 #pragma unroll
