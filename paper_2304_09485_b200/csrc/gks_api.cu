@@ -2,6 +2,7 @@
 // residual / Jacobian / GMRES / advance entry points.  Every entry point
 // copies host arrays in, runs the device path and copies results out; the
 // *_device variants keep the state resident for the benchmark loop.
+#include <chrono>
 #include <stddef.h>
 #include <stdlib.h>
 #include <string.h>
@@ -245,6 +246,15 @@ static DevPatch dev_patch(const GksPatchDesc& d) {
 int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const GksOptions* o, int device,
                   const GksDomainDesc* dom) {
   Handle* H = &G->H;
+  // GKS_SETUP_TIMING=1: host wall time of each construction phase on stderr
+  const bool timing = getenv("GKS_SETUP_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto tick = [&](const char* what) {
+    if (!timing) return;
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "gks_create %-16s %8.3f s\n", what, std::chrono::duration<double>(now - t_last).count());
+    t_last = now;
+  };
   H->device = device;
   GKS_CUDA(cudaSetDevice(device));
   GKS_CUDA(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
@@ -277,6 +287,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   H->gmres_rtol = o->gmres_rtol;
   H->kc = make_kin(o->gamma);
 
+  tick("init");
   // patches
   int maxpatch = -1;
   for (int64_t f = 0; f < nf; ++f) maxpatch = std::max<int>(maxpatch, (int)m->face_patch[f]);
@@ -298,6 +309,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   }
   TRY(upload(H, &H->patches, H->patches_h.data(), H->patches_h.size()));
 
+  tick("patches");
   // cells
   std::vector<double> hf;
   std::vector<int64_t> hi, shp;
@@ -319,6 +331,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
     TRY(upload_rec(H, &H->beta, packed, nc));
   }
 
+  tick("cells");
   // faces
   {
     auto own = to_i32(m->face_owner, nf), nbr = to_i32(m->face_neighbor, nf), pat = to_i32(m->face_patch, nf);
@@ -351,6 +364,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   }
   TRY(upload(H, &H->fq_point, m->fq_point, nfq * 3));
 
+  tick("faces");
   // visiting orders: the reference's face / face-point order (identity
   // unless the mesh was renumbered, reorder.py)
   std::vector<int64_t> forder(nf), qorder(nfq);
@@ -365,6 +379,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
     std::iota(qorder.begin(), qorder.end(), 0);
   }
 
+  tick("orders");
   // CSR lists (counting sorts keep ascending order inside each group)
   {
     // assembly: owner fq entries, then neighbour fq entries (stepping.py:225-228),
@@ -506,6 +521,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
     TRY(alloc(H, &A->prim, (size_t)nc * MF_REC));
   }
 
+  tick("csr+jacobian");
   // reconstruction operators
   // (records padded to the kernel's stencil shape, see pad_records)
   auto zero_d = [](int64_t) { return 0.0; };
@@ -609,6 +625,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
     { auto v = pad_records(act, nc, 1, H->M, 1, Mt, zero_b); TRY(upload_rec(H, &H->sub_active, v, nc)); }
   }
 
+  tick("operators");
   // state and work buffers
   TRY(alloc(H, &H->q, nc * 5));
   TRY(alloc(H, &G->api_q, nc * 5));
@@ -642,6 +659,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
     H->hsend_half = std::max<int64_t>(mx, 1) * 15;
     TRY(alloc(H, &H->hrecv, std::max<int64_t>(mx, 1) * 15));
   }
+  tick("buffers");
   return GKS_OK;
 }
 

@@ -1,6 +1,11 @@
 // Host-side native setup: stencil selection and reconstruction operators.
 //
-// Restates, per cell and in parallel (OpenMP):
+// Runs the per-cell arithmetic of gks_setup_cell.cuh over all cells in
+// parallel (OpenMP) and keeps the reference's padded operator layout
+// (exported through gks_setup_query / gks_setup_copy).  The same per-cell
+// code also runs on the device (gks_setup_dev.cu, the default path of
+// gks_create); this build serves the host API (StencilTable, the operator
+// arrays) and the per-rank setups of the distributed solver.
 //   gks3d/mesh/stencils.py:72-192   _ordered_neighbors, _dedup, build_stencils
 //   gks3d/recon.py:60-69            _pinv (SVD pseudo-inverse, rank tol 1e-10)
 //   gks3d/recon.py:104-164          ReconGeometry (avg0, beta matrices)
@@ -12,7 +17,8 @@
 // reference).
 //
 // This file must be compiled without FP contraction (-ffp-contract=off) so
-// the hex-face angle ordering reproduces numpy's arithmetic exactly.
+// the hex-face angle ordering reproduces numpy's arithmetic exactly and the
+// operators equal the device build's bit for bit.
 #include <math.h>
 #include <omp.h>
 #include <stdint.h>
@@ -25,161 +31,13 @@
 #include <vector>
 
 #include "gks.h"
+#include "gks_setup_cell.cuh"
 
 namespace gks {
 void set_error(const char* fmt, ...);
 }
 
-namespace {
-
-constexpr int NCOEF = 9;
-constexpr double RANK_TOL = 1e-10;
-
-struct V3 {
-  double x, y, z;
-};
-inline V3 add(V3 a, V3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
-inline V3 neg(V3 a) { return {-a.x, -a.y, -a.z}; }
-
-struct Member {
-  int64_t id;
-  V3 s;
-};
-
-inline std::array<int64_t, 3> skey(const V3& s) {
-  return {llround(s.x * 1e9), llround(s.y * 1e9), llround(s.z * 1e9)};
-}
-
-// _dedup (stencils.py:106-116): keep the first occurrence of (id, rounded shift)
-std::vector<Member> dedup(const std::vector<Member>& in) {
-  std::vector<Member> out;
-  std::vector<std::array<int64_t, 4>> seen;
-  out.reserve(in.size());
-  seen.reserve(in.size());
-  for (const Member& m : in) {
-    auto k = skey(m.s);
-    std::array<int64_t, 4> key{m.id, k[0], k[1], k[2]};
-    bool dup = false;
-    for (auto& q : seen)
-      if (q == key) { dup = true; break; }
-    if (dup) continue;
-    seen.push_back(key);
-    out.push_back(m);
-  }
-  return out;
-}
-
-inline double dot3(const double* a, const double* b) {
-  double acc = 0.0;
-  acc += a[0] * b[0];
-  acc += a[1] * b[1];
-  acc += a[2] * b[2];
-  return acc;
-}
-
-const int TET_KEPT[4][3] = {{0, 1, 2}, {0, 1, 3}, {1, 2, 3}, {2, 0, 3}};
-const int TET_ENL[4] = {0, 1, 2, 3};
-const int HEX_PAT[8][3] = {{0, 1, 2}, {0, 2, 3}, {0, 3, 4}, {0, 4, 1},
-                           {5, 1, 2}, {5, 2, 3}, {5, 3, 4}, {5, 4, 1}};
-
-// ---------------------------------------------------------------------------
-// small dense linear algebra
-// ---------------------------------------------------------------------------
-
-// One-sided Jacobi SVD of A (m x n, row-major, m >= n).  Returns singular
-// values s (descending), U (m x n), V (n x n), both column-orthonormal.
-void svd_jacobi(int m, int n, const double* A, double* s, double* U, double* V) {
-  std::vector<double> a(A, A + (size_t)m * n);
-  for (int i = 0; i < n * n; ++i) V[i] = 0.0;
-  for (int i = 0; i < n; ++i) V[i * n + i] = 1.0;
-  for (int sweep = 0; sweep < 60; ++sweep) {
-    double off = 0.0;
-    for (int p = 0; p < n - 1; ++p)
-      for (int q = p + 1; q < n; ++q) {
-        double al = 0, be = 0, ga = 0;
-        for (int i = 0; i < m; ++i) {
-          const double x = a[i * n + p], y = a[i * n + q];
-          al += x * x;
-          be += y * y;
-          ga += x * y;
-        }
-        if (ga == 0.0) continue;
-        const double rel = fabs(ga) / sqrt(al * be);
-        if (!(rel > 1e-17)) continue;
-        off = std::max(off, rel);
-        const double zeta = (be - al) / (2.0 * ga);
-        const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
-        for (int i = 0; i < m; ++i) {
-          const double x = a[i * n + p], y = a[i * n + q];
-          a[i * n + p] = c * x - sn * y;
-          a[i * n + q] = sn * x + c * y;
-        }
-        for (int i = 0; i < n; ++i) {
-          const double x = V[i * n + p], y = V[i * n + q];
-          V[i * n + p] = c * x - sn * y;
-          V[i * n + q] = sn * x + c * y;
-        }
-      }
-    if (off < 1e-16) break;
-  }
-  std::vector<double> sv(n);
-  for (int j = 0; j < n; ++j) {
-    double acc = 0;
-    for (int i = 0; i < m; ++i) acc += a[i * n + j] * a[i * n + j];
-    sv[j] = sqrt(acc);
-  }
-  std::vector<int> ord(n);
-  for (int j = 0; j < n; ++j) ord[j] = j;
-  std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return sv[x] > sv[y]; });
-  std::vector<double> Vs(V, V + n * n);
-  for (int jj = 0; jj < n; ++jj) {
-    const int j = ord[jj];
-    s[jj] = sv[j];
-    for (int i = 0; i < m; ++i) U[i * n + jj] = sv[j] > 0 ? a[i * n + j] / sv[j] : 0.0;
-    for (int i = 0; i < n; ++i) V[i * n + jj] = Vs[i * n + j];
-  }
-}
-
-// _pinv (recon.py:60-69): pinv of A (m x n) -> P (n x m), or false if rank <
-// rank_needed.  Requires m >= n (always true at the call sites).
-bool pinv(int m, int n, const double* A, int rank_needed, double* P) {
-  if (m < n || n == 0) return false;
-  std::vector<double> s(n), U((size_t)m * n), V((size_t)n * n);
-  svd_jacobi(m, n, A, s.data(), U.data(), V.data());
-  if (s[0] == 0.0) return false;
-  int rank = 0;
-  for (int j = 0; j < n; ++j)
-    if (s[j] >= RANK_TOL * s[0]) ++rank;
-  if (rank < rank_needed) return false;
-  for (int i = 0; i < n; ++i)
-    for (int k = 0; k < m; ++k) {
-      double acc = 0;
-      for (int j = 0; j < rank; ++j) acc += V[i * n + j] * (1.0 / s[j]) * U[k * n + j];
-      P[i * m + k] = acc;
-    }
-  return true;
-}
-
-inline void mono_rows(const double* xt, double* r) {
-  const double x = xt[0], y = xt[1], z = xt[2];
-  r[0] = x; r[1] = y; r[2] = z;
-  r[3] = x * x; r[4] = x * y; r[5] = x * z; r[6] = y * y; r[7] = y * z; r[8] = z * z;
-}
-
-inline void mono_grad_rows(const double* xt, double g[3][NCOEF]) {
-  const double x = xt[0], y = xt[1], z = xt[2];
-  const double gx[9] = {1, 0, 0, 2 * x, y, z, 0, 0, 0};
-  const double gy[9] = {0, 1, 0, 0, x, 0, 2 * y, z, 0};
-  const double gz[9] = {0, 0, 1, 0, 0, x, 0, y, 2 * z};
-  for (int d = 0; d < 9; ++d) { g[0][d] = gx[d]; g[1][d] = gy[d]; g[2][d] = gz[d]; }
-}
-
-}  // namespace
-
-// ---------------------------------------------------------------------------
-// setup object
-// ---------------------------------------------------------------------------
+using gks::su::NCOEF;
 
 struct GksSetup {
   int64_t nc = 0;
@@ -224,174 +82,59 @@ struct GksSetup {
   }
 };
 
+
 namespace {
 
-struct MeshView {
-  const GksMeshDesc* m;
-  std::vector<Member> neighbors_of(int64_t c) const {
-    std::vector<Member> out;
-    for (int64_t k = m->cell_face_start[c]; k < m->cell_face_start[c + 1]; ++k) {
-      const int64_t f = m->cell_face_list[k];
-      if (m->face_neighbor[f] < 0) continue;
-      const double* s = m->face_shift + 3 * f;
-      if (m->face_owner[f] == c)
-        out.push_back({m->face_neighbor[f], {s[0], s[1], s[2]}});
-      else
-        out.push_back({m->face_owner[f], {-s[0], -s[1], -s[2]}});
+using gks::su::Stencil;
+using gks::su::build_stencil;
+
+// reference-layout sinks of the per-cell operator builders
+struct HostWenoSink {
+  GksSetup* S;
+  int64_t c, mup, sup, kmax;
+  void sub_op(int slot, int d, int k, double v) { S->w_sub_op[((c * mup + slot) * 3 + d) * sup + k] = v; }
+  void sub_gather(int slot, int k, int64_t id) { S->w_sub_gather[(c * mup + slot) * sup + k] = id; }
+  void sub_active(int slot) { S->w_sub_active[c * mup + slot] = 1; }
+  void drop_subs(int n) {
+    for (int mm = 0; mm < n; ++mm) {
+      S->w_sub_active[c * mup + mm] = 0;
+      for (int64_t k = 0; k < 3 * sup; ++k) S->w_sub_op[(c * mup + mm) * 3 * sup + k] = 0.0;
+      for (int64_t k = 0; k < sup; ++k) S->w_sub_gather[(c * mup + mm) * sup + k] = 0;
     }
-    return out;
   }
+  void big_op(int d, int k, double v) { S->w_big_op[(c * NCOEF + d) * kmax + k] = v; }
+  void big_gather(int k, int64_t id) { S->w_big_gather[c * kmax + k] = id; }
+  void big_degree(int deg) { S->w_big_degree[c] = (int8_t)deg; }
 };
 
-// _ordered_neighbors (stencils.py:72-103)
-void ordered_neighbors(const GksMeshDesc* m, int64_t c, std::vector<int64_t>& ids,
-                       std::vector<V3>& sh) {
-  const int64_t f0 = m->cell_face_start[c];
-  const int nf = (int)(m->cell_face_start[c + 1] - f0);
-  ids.assign(nf, -1);
-  sh.assign(nf, V3{0, 0, 0});
-  std::vector<std::array<double, 3>> nrm(nf);
-  for (int k = 0; k < nf; ++k) {
-    const int64_t f = m->cell_face_list[f0 + k];
-    const double sg = m->face_owner[f] == c ? 1.0 : -1.0;
-    for (int d = 0; d < 3; ++d) nrm[k][d] = sg * m->face_normal[3 * f + d];
-    if (m->face_neighbor[f] < 0) continue;
-    const double* s = m->face_shift + 3 * f;
-    if (m->face_owner[f] == c) {
-      ids[k] = m->face_neighbor[f];
-      sh[k] = {s[0], s[1], s[2]};
-    } else {
-      ids[k] = m->face_owner[f];
-      sh[k] = {-s[0], -s[1], -s[2]};
-    }
-  }
-  if (m->cell_kind[c] != 1) return;
-  // hex: (pole a, equator by angle, pole b)
-  int pole_b = 1;
-  double best = 0;
-  for (int k = 1; k < 6; ++k) {
-    const double d = dot3(nrm[k].data(), nrm[0].data());
-    if (k == 1 || d < best) { best = d; pole_b = k; }
-  }
-  std::vector<int> rest;
-  for (int k = 1; k < 6; ++k)
-    if (k != pole_b) rest.push_back(k);
-  const double* axis = nrm[0].data();
-  const double* r0 = nrm[rest[0]].data();
-  const double pr = dot3(r0, axis);
-  double b1[3] = {r0[0] - pr * axis[0], r0[1] - pr * axis[1], r0[2] - pr * axis[2]};
-  const double nb = sqrt(dot3(b1, b1));
-  for (double& x : b1) x /= nb;
-  const double b2[3] = {axis[1] * b1[2] - axis[2] * b1[1], axis[2] * b1[0] - axis[0] * b1[2],
-                        axis[0] * b1[1] - axis[1] * b1[0]};
-  std::vector<double> ang(4);
-  for (int i = 0; i < 4; ++i) ang[i] = atan2(dot3(nrm[rest[i]].data(), b2), dot3(nrm[rest[i]].data(), b1));
-  std::vector<int> o = {0, 1, 2, 3};
-  std::stable_sort(o.begin(), o.end(), [&](int a, int b) { return ang[a] < ang[b]; });
-  std::vector<int> order = {0, rest[o[0]], rest[o[1]], rest[o[2]], rest[o[3]], pole_b};
-  std::vector<int64_t> ids2(6);
-  std::vector<V3> sh2(6);
-  for (int k = 0; k < 6; ++k) { ids2[k] = ids[order[k]]; sh2[k] = sh[order[k]]; }
-  ids = ids2;
-  sh = sh2;
-}
-
-struct CellStencil {
-  std::vector<int64_t> nbr;
-  std::vector<V3> nbr_s;
-  std::vector<Member> big;
-  std::vector<std::vector<Member>> subs;
-  bool weno_fallback = false, hweno_fallback = false;
-};
-
-void build_cell_stencil(const GksMeshDesc* m, const MeshView& mv, int64_t c, CellStencil& st) {
-  ordered_neighbors(m, c, st.nbr, st.nbr_s);
-  const int nf = (int)st.nbr.size();
-  std::vector<Member> big;
-  big.push_back({c, {0, 0, 0}});
-  for (int k = 0; k < nf; ++k)
-    if (st.nbr[k] >= 0) big.push_back({st.nbr[k], st.nbr_s[k]});
-  for (int k = 0; k < nf; ++k) {
-    if (st.nbr[k] < 0) continue;
-    for (const Member& jt : mv.neighbors_of(st.nbr[k])) big.push_back({jt.id, add(st.nbr_s[k], jt.s)});
-  }
-  st.big = dedup(big);
-  st.subs.clear();
-  if (m->cell_kind[c] == 1) {
-    for (auto& pat : HEX_PAT) {
-      if (st.nbr[pat[0]] < 0 || st.nbr[pat[1]] < 0 || st.nbr[pat[2]] < 0) continue;
-      std::vector<Member> mi = {{c, {0, 0, 0}}};
-      for (int k : pat) mi.push_back({st.nbr[k], st.nbr_s[k]});
-      auto di = dedup(mi);
-      if (di.size() == 4) st.subs.push_back(di);
-    }
-  } else {
-    for (int p = 0; p < 4; ++p) {
-      const int* kept = TET_KEPT[p];
-      if (st.nbr[kept[0]] < 0 || st.nbr[kept[1]] < 0 || st.nbr[kept[2]] < 0) continue;
-      std::vector<Member> mi = {{c, {0, 0, 0}}};
-      for (int q = 0; q < 3; ++q) mi.push_back({st.nbr[kept[q]], st.nbr_s[kept[q]]});
-      const int64_t host = st.nbr[TET_ENL[p]];
-      const V3 hs = st.nbr_s[TET_ENL[p]];
-      std::vector<Member> added;
-      for (const Member& jt : mv.neighbors_of(host)) {
-        const V3 tot = add(hs, jt.s);
-        const double mx = std::max(fabs(tot.x), std::max(fabs(tot.y), fabs(tot.z)));
-        if (jt.id == c && mx < 1e-12) continue;
-        added.push_back({jt.id, tot});
-      }
-      std::stable_sort(added.begin(), added.end(), [](const Member& a, const Member& b) {
-        if (a.id != b.id) return a.id < b.id;
-        return skey(a.s) < skey(b.s);
-      });
-      for (size_t q = 0; q < added.size() && q < 3; ++q) mi.push_back(added[q]);
-      auto di = dedup(mi);
-      if (di.size() == 7) st.subs.push_back(di);
-    }
-  }
-  if (st.subs.size() < 2) {
-    st.subs.clear();
-    st.weno_fallback = true;
-  }
-  int present = 0;
-  for (int k = 0; k < nf; ++k) present += st.nbr[k] >= 0;
-  st.hweno_fallback = present < 2;
-}
-
-struct Geo {
+struct HostHwenoSink {
+  GksSetup* S;
   const GksMeshDesc* m;
-  // cell-average rows of the basis over member (j, shift) in the chart of c
-  void avg_row(int64_t c, int64_t j, const V3& s, double* row) const {
-    const double* c0 = m->cell_centroid + 3 * c;
-    const double h0 = m->cell_h[c];
-    for (int d = 0; d < NCOEF; ++d) row[d] = 0.0;
-    for (int64_t q = m->cell_cq_start[j]; q < m->cell_cq_start[j + 1]; ++q) {
-      const double* p = m->cq_point + 3 * q;
-      const double xt[3] = {((p[0] + s.x) - c0[0]) / h0, ((p[1] + s.y) - c0[1]) / h0,
-                            ((p[2] + s.z) - c0[2]) / h0};
-      double r[NCOEF];
-      mono_rows(xt, r);
-      const double w = m->cq_weight[q];
-      for (int d = 0; d < NCOEF; ++d) row[d] += w * r[d];
-    }
+  int64_t c, mup, amax, gmax, W;
+  int na;
+  void big_op(int d, int k, double v) {
+    S->h_big_op[(c * NCOEF + d) * W + (k < na ? k : amax + (k - na))] = v;
   }
-  // h_j * mean gradient rows of the basis over member (j, s), chart of c (hweno.py:45-60)
-  void grad_rows(int64_t c, int64_t j, const V3& s, double out[3][NCOEF]) const {
-    const double* c0 = m->cell_centroid + 3 * c;
-    const double h0 = m->cell_h[c];
-    double acc[3][NCOEF] = {};
-    for (int64_t q = m->cell_cq_start[j]; q < m->cell_cq_start[j + 1]; ++q) {
-      const double* p = m->cq_point + 3 * q;
-      const double xt[3] = {((p[0] + s.x) - c0[0]) / h0, ((p[1] + s.y) - c0[1]) / h0,
-                            ((p[2] + s.z) - c0[2]) / h0};
-      double g[3][NCOEF];
-      mono_grad_rows(xt, g);
-      const double w = m->cq_weight[q];
-      for (int x = 0; x < 3; ++x)
-        for (int d = 0; d < NCOEF; ++d) acc[x][d] += w * g[x][d];
+  void avg_gather(int k, int64_t id) { S->h_big_avg_gather[c * amax + k] = id; }
+  void grad_gather(int k, int64_t id, double h) {
+    S->h_big_grad_gather[c * gmax + k] = id;
+    S->h_big_grad_scale[c * gmax + k] = h;
+  }
+  void big_ncols(int R) { S->h_big_ncols[c] = R; }
+  void big_degree(int deg) { S->h_big_degree[c] = (int8_t)deg; }
+  void sub_op(int slot, int i, double v) { S->h_sub_op[(c * mup + slot) * 21 + i] = v; }
+  void sub_gather(int slot, int64_t id) {
+    S->h_sub_gather[(c * mup + slot) * 2 + 0] = c;
+    S->h_sub_gather[(c * mup + slot) * 2 + 1] = id;
+  }
+  void sub_active(int slot) { S->h_sub_active[c * mup + slot] = 1; }
+  void drop_subs(int n) {
+    for (int mm = 0; mm < n; ++mm) {
+      S->h_sub_active[c * mup + mm] = 0;
+      for (int i = 0; i < 21; ++i) S->h_sub_op[(c * mup + mm) * 21 + i] = 0.0;
+      S->h_sub_gather[(c * mup + mm) * 2] = 0;
+      S->h_sub_gather[(c * mup + mm) * 2 + 1] = 0;
     }
-    for (int x = 0; x < 3; ++x)
-      for (int d = 0; d < NCOEF; ++d) out[x][d] = m->cell_h[j] * (acc[x][d] / h0);
   }
 };
 
@@ -409,14 +152,20 @@ int gks_setup_build(const GksMeshDesc* m, int schemes, int nthreads, GksSetup** 
     return GKS_ERR_BAD_ARG;
   }
   if (nthreads > 0) omp_set_num_threads(nthreads);
-  GksSetup* S = new GksSetup();
   const int64_t nc = m->ncells;
-  S->nc = nc;
   int nfpc = 0;
-  for (int64_t c = 0; c < nc; ++c)
-    nfpc = std::max<int>(nfpc, (int)(m->cell_face_start[c + 1] - m->cell_face_start[c]));
+  for (int64_t c = 0; c < nc; ++c) {
+    const int nf = (int)(m->cell_face_start[c + 1] - m->cell_face_start[c]);
+    if (nf > gks::su::NF || (m->cell_kind[c] == 1 && nf != 6) || (m->cell_kind[c] != 1 && nf != 4)) {
+      gks::set_error("gks_setup_build: cell %lld has %d faces (tet 4 / hex 6 only)", (long long)c, nf);
+      return GKS_ERR_BAD_ARG;
+    }
+    nfpc = std::max(nfpc, nf);
+  }
+  GksSetup* S = new GksSetup();
+  S->nc = nc;
   S->nfpc = nfpc;
-  MeshView mv{m};
+  const GksMeshDesc& M = *m;
   const bool want_weno = schemes & 1, want_hweno = schemes & 2;
   const bool want_stencils = schemes == 0 || (schemes & 4);
 
@@ -426,16 +175,14 @@ int gks_setup_build(const GksMeshDesc* m, int schemes, int nthreads, GksSetup** 
   int64_t sub_len_max = 0;
 #pragma omp parallel for schedule(dynamic, 256) reduction(max : sub_len_max)
   for (int64_t c = 0; c < nc; ++c) {
-    CellStencil st;
-    build_cell_stencil(m, mv, c, st);
-    big_n[c] = (int32_t)st.big.size();
-    sub_n[c] = (int32_t)st.subs.size();
-    int present = 0;
-    for (int64_t id : st.nbr) present += id >= 0;
-    nbr_n[c] = present;
+    Stencil st;
+    build_stencil(M, c, st);
+    big_n[c] = st.nbig;
+    sub_n[c] = st.nsub;
+    nbr_n[c] = st.present();
     wfb[c] = st.weno_fallback;
     hfb[c] = st.hweno_fallback;
-    for (auto& sub : st.subs) sub_len_max = std::max<int64_t>(sub_len_max, (int64_t)sub.size() - 1);
+    for (int k = 0; k < st.nsub; ++k) sub_len_max = std::max<int64_t>(sub_len_max, st.sublen[k] - 1);
   }
   S->weno_fallback = wfb;
   S->hweno_fallback = hfb;
@@ -453,13 +200,12 @@ int gks_setup_build(const GksMeshDesc* m, int schemes, int nthreads, GksSetup** 
     S->big_ids.resize(S->big_start[nc]);
     S->big_shift.resize(S->big_start[nc] * 3);
     std::vector<int64_t> sub_len(S->sub_cell_start[nc], 0);
-    // member counts per sub need the stencils: one more pass
 #pragma omp parallel for schedule(dynamic, 256)
     for (int64_t c = 0; c < nc; ++c) {
-      CellStencil st;
-      build_cell_stencil(m, mv, c, st);
+      Stencil st;
+      build_stencil(M, c, st);
       int64_t si = S->sub_cell_start[c];
-      for (auto& sub : st.subs) sub_len[si++] = (int64_t)sub.size();
+      for (int k = 0; k < st.nsub; ++k) sub_len[si++] = st.sublen[k];
     }
     S->sub_member_start.assign(sub_len.size() + 1, 0);
     for (size_t k = 0; k < sub_len.size(); ++k) S->sub_member_start[k + 1] = S->sub_member_start[k] + sub_len[k];
@@ -467,24 +213,26 @@ int gks_setup_build(const GksMeshDesc* m, int schemes, int nthreads, GksSetup** 
     S->sub_shift.resize(S->sub_member_start.back() * 3);
 #pragma omp parallel for schedule(dynamic, 256)
     for (int64_t c = 0; c < nc; ++c) {
-      CellStencil st;
-      build_cell_stencil(m, mv, c, st);
-      for (size_t k = 0; k < st.nbr.size(); ++k) {
+      Stencil st;
+      build_stencil(M, c, st);
+      for (int k = 0; k < st.nf; ++k) {
         S->nbr_ids[c * nfpc + k] = st.nbr[k];
         S->nbr_shift[(c * nfpc + k) * 3 + 0] = st.nbr_s[k].x;
         S->nbr_shift[(c * nfpc + k) * 3 + 1] = st.nbr_s[k].y;
         S->nbr_shift[(c * nfpc + k) * 3 + 2] = st.nbr_s[k].z;
       }
       int64_t b = S->big_start[c];
-      for (auto& mb : st.big) {
+      for (int k = 0; k < st.nbig; ++k) {
+        const auto& mb = st.big[k];
         S->big_ids[b] = mb.id;
         S->big_shift[3 * b] = mb.s.x; S->big_shift[3 * b + 1] = mb.s.y; S->big_shift[3 * b + 2] = mb.s.z;
         ++b;
       }
       int64_t si = S->sub_cell_start[c];
-      for (auto& sub : st.subs) {
+      for (int k = 0; k < st.nsub; ++k) {
         int64_t q = S->sub_member_start[si++];
-        for (auto& mb : sub) {
+        for (int j = 0; j < st.sublen[k]; ++j) {
+          const auto& mb = st.sub[k][j];
           S->sub_ids[q] = mb.id;
           S->sub_shift[3 * q] = mb.s.x; S->sub_shift[3 * q + 1] = mb.s.y; S->sub_shift[3 * q + 2] = mb.s.z;
           ++q;
@@ -494,32 +242,10 @@ int gks_setup_build(const GksMeshDesc* m, int schemes, int nthreads, GksSetup** 
   }
 
   // ---- recon geometry (recon.py:104-146) ----------------------------------
-  Geo geo{m};
   S->avg0.assign(nc * NCOEF, 0.0);
   S->beta.assign(nc * NCOEF * NCOEF, 0.0);
 #pragma omp parallel for schedule(static)
-  for (int64_t c = 0; c < nc; ++c) {
-    geo.avg_row(c, c, V3{0, 0, 0}, &S->avg0[c * NCOEF]);
-    double* B = &S->beta[c * 81];
-    const double* c0 = m->cell_centroid + 3 * c;
-    const double h0 = m->cell_h[c];
-    for (int64_t q = m->cell_cq_start[c]; q < m->cell_cq_start[c + 1]; ++q) {
-      const double* p = m->cq_point + 3 * q;
-      const double xt[3] = {(p[0] - c0[0]) / h0, (p[1] - c0[1]) / h0, (p[2] - c0[2]) / h0};
-      double g[3][NCOEF];
-      mono_grad_rows(xt, g);
-      const double w = m->cq_weight[q];
-      for (int d = 0; d < 9; ++d)
-        for (int e = 0; e < 9; ++e) B[d * 9 + e] += w * (g[0][d] * g[0][e] + g[1][d] * g[1][e] + g[2][d] * g[2][e]);
-    }
-    // + B2 (second-derivative rows, recon.py:28-36)
-    B[3 * 9 + 3] += 4.0; B[4 * 9 + 4] += 1.0; B[5 * 9 + 5] += 1.0;
-    B[6 * 9 + 6] += 4.0; B[7 * 9 + 7] += 1.0; B[8 * 9 + 8] += 4.0;
-  }
-  auto member_row = [&](int64_t c, const Member& mb, double* row) {
-    geo.avg_row(c, mb.id, mb.s, row);
-    for (int d = 0; d < NCOEF; ++d) row[d] -= S->avg0[c * NCOEF + d];
-  };
+  for (int64_t c = 0; c < nc; ++c) gks::su::cell_geometry(M, c, &S->avg0[c * NCOEF], &S->beta[c * 81]);
 
   if (want_weno) {
     // WENO operators (recon.py:216-274) written in place with upper-bound widths
@@ -538,61 +264,12 @@ int gks_setup_build(const GksMeshDesc* m, int schemes, int nthreads, GksSetup** 
     std::vector<int32_t> msurv(nc, 0), ssurv(nc, 0);
 #pragma omp parallel for schedule(dynamic, 64)
     for (int64_t c = 0; c < nc; ++c) {
-      CellStencil st;
-      build_cell_stencil(m, mv, c, st);
-      int nsurv = 0, scols = 0;
-      for (auto& sub : st.subs) {
-        const int S1 = (int)sub.size() - 1;
-        std::vector<double> rows(S1 * 3), full(NCOEF), op(3 * S1);
-        for (int k = 1; k <= S1; ++k) {
-          member_row(c, sub[k], full.data());
-          for (int d = 0; d < 3; ++d) rows[(k - 1) * 3 + d] = full[d];
-        }
-        if (!pinv(S1, 3, rows.data(), 3, op.data())) continue;
-        for (int d = 0; d < 3; ++d)
-          for (int k = 0; k < S1; ++k) S->w_sub_op[((c * mup + nsurv) * 3 + d) * sup + k] = op[d * S1 + k];
-        for (int k = 0; k < S1; ++k) S->w_sub_gather[(c * mup + nsurv) * sup + k] = sub[k + 1].id;
-        S->w_sub_active[c * mup + nsurv] = 1;
-        scols = std::max(scols, S1);
-        ++nsurv;
-      }
-      if (nsurv < 2) {  // fewer than two candidates: drop them all
-        for (int mm = 0; mm < nsurv; ++mm) {
-          S->w_sub_active[c * mup + mm] = 0;
-          for (int64_t k = 0; k < 3 * sup; ++k) S->w_sub_op[(c * mup + mm) * 3 * sup + k] = 0.0;
-          for (int64_t k = 0; k < sup; ++k) S->w_sub_gather[(c * mup + mm) * sup + k] = 0;
-        }
-        nsurv = 0;
-        scols = 0;
-      }
-      msurv[c] = nsurv;
-      ssurv[c] = scols;
-      const int R = (int)st.big.size() - 1;
-      std::vector<double> rows((size_t)std::max(R, 0) * NCOEF);
-      for (int k = 1; k <= R; ++k) member_row(c, st.big[k], &rows[(k - 1) * NCOEF]);
-      std::vector<double> op;
-      bool ok = false;
-      if (nsurv && R >= NCOEF) {
-        op.assign((size_t)NCOEF * R, 0.0);
-        ok = pinv(R, NCOEF, rows.data(), NCOEF, op.data());
-      }
-      int cols = R;
-      if (!ok) {
-        S->w_big_degree[c] = 1;
-        cols = std::max(R, 1);
-        op.assign((size_t)NCOEF * cols, 0.0);
-        if (R >= 3) {
-          std::vector<double> lr(R * 3), lin(3 * R);
-          for (int k = 0; k < R; ++k)
-            for (int d = 0; d < 3; ++d) lr[k * 3 + d] = rows[k * NCOEF + d];
-          if (pinv(R, 3, lr.data(), 3, lin.data()))
-            for (int d = 0; d < 3; ++d)
-              for (int k = 0; k < R; ++k) op[d * cols + k] = lin[d * R + k];
-        }
-      }
-      for (int d = 0; d < NCOEF; ++d)
-        for (int k = 0; k < cols; ++k) S->w_big_op[(c * NCOEF + d) * kmax + k] = op[d * cols + k];
-      for (int k = 1; k <= R; ++k) S->w_big_gather[c * kmax + k - 1] = st.big[k].id;
+      Stencil st;
+      build_stencil(M, c, st);
+      HostWenoSink sink{S, c, mup, sup, kmax};
+      const int r = gks::su::weno_cell(M, c, st, &S->avg0[c * NCOEF], sink);
+      msurv[c] = r & 0xff;
+      ssurv[c] = r >> 8;
     }
     // reference widths: mmax = max(surviving subs, 1), smax = max surviving sub columns (default 1)
     int64_t mmax = 0, smax = 0;
@@ -645,81 +322,10 @@ int gks_setup_build(const GksMeshDesc* m, int schemes, int nthreads, GksSetup** 
     std::vector<int32_t> msurv(nc, 0);
 #pragma omp parallel for schedule(dynamic, 64)
     for (int64_t c = 0; c < nc; ++c) {
-      CellStencil st;
-      build_cell_stencil(m, mv, c, st);
-      std::vector<Member> ids = {{c, {0, 0, 0}}};
-      for (size_t k = 0; k < st.nbr.size(); ++k)
-        if (st.nbr[k] >= 0) ids.push_back({st.nbr[k], st.nbr_s[k]});
-      const int na = (int)ids.size() - 1;
-      const int R = na + 3 * (int)ids.size();
-      std::vector<double> rows((size_t)R * NCOEF);
-      for (int k = 1; k <= na; ++k) member_row(c, ids[k], &rows[(k - 1) * NCOEF]);
-      for (size_t k = 0; k < ids.size(); ++k) {
-        double g[3][NCOEF];
-        geo.grad_rows(c, ids[k].id, ids[k].s, g);
-        for (int x = 0; x < 3; ++x)
-          for (int d = 0; d < NCOEF; ++d) rows[(na + 3 * k + x) * NCOEF + d] = g[x][d];
-      }
-      std::vector<double> op((size_t)NCOEF * R, 0.0);
-      bool ok = false;
-      if (!st.hweno_fallback && R >= NCOEF) ok = pinv(R, NCOEF, rows.data(), NCOEF, op.data());
-      if (!ok) {
-        S->h_big_degree[c] = 1;
-        std::fill(op.begin(), op.end(), 0.0);
-        std::vector<double> lr(R * 3), lin(3 * R);
-        for (int k = 0; k < R; ++k)
-          for (int d = 0; d < 3; ++d) lr[k * 3 + d] = rows[k * NCOEF + d];
-        if (pinv(R, 3, lr.data(), 3, lin.data()))
-          for (int d = 0; d < 3; ++d)
-            for (int k = 0; k < R; ++k) op[d * R + k] = lin[d * R + k];
-      }
-      S->h_big_ncols[c] = R;
-      for (int d = 0; d < NCOEF; ++d) {
-        for (int k = 0; k < na; ++k) S->h_big_op[(c * NCOEF + d) * W + k] = op[d * R + k];
-        for (int k = na; k < R; ++k) S->h_big_op[(c * NCOEF + d) * W + amax + (k - na)] = op[d * R + k];
-      }
-      S->h_big_grad_gather[c * gmax] = c;
-      S->h_big_grad_scale[c * gmax] = m->cell_h[c];
-      for (int k = 1; k <= na; ++k) {
-        S->h_big_avg_gather[c * amax + k - 1] = ids[k].id;
-        S->h_big_grad_gather[c * gmax + k] = ids[k].id;
-        S->h_big_grad_scale[c * gmax + k] = m->cell_h[ids[k].id];
-      }
-      int nsurv = 0;
-      if (!st.hweno_fallback) {
-        double g0[3][NCOEF];
-        geo.grad_rows(c, c, V3{0, 0, 0}, g0);
-        for (int k = 1; k <= na; ++k) {
-          // rows: [avg row of the neighbour (3 cols); grad rows of target; grad rows of neighbour]
-          double srows[7 * 3];
-          double full[NCOEF];
-          member_row(c, ids[k], full);
-          for (int d = 0; d < 3; ++d) srows[d] = full[d];
-          for (int x = 0; x < 3; ++x)
-            for (int d = 0; d < 3; ++d) srows[(1 + x) * 3 + d] = g0[x][d];
-          double g[3][NCOEF];
-          geo.grad_rows(c, ids[k].id, ids[k].s, g);
-          for (int x = 0; x < 3; ++x)
-            for (int d = 0; d < 3; ++d) srows[(4 + x) * 3 + d] = g[x][d];
-          double sop[21];
-          if (!pinv(7, 3, srows, 3, sop)) continue;
-          for (int i = 0; i < 21; ++i) S->h_sub_op[(c * mup + nsurv) * 21 + i] = sop[i];
-          S->h_sub_gather[(c * mup + nsurv) * 2 + 0] = c;
-          S->h_sub_gather[(c * mup + nsurv) * 2 + 1] = ids[k].id;
-          S->h_sub_active[c * mup + nsurv] = 1;
-          ++nsurv;
-        }
-        if (nsurv < 2) {
-          for (int mm = 0; mm < nsurv; ++mm) {
-            S->h_sub_active[c * mup + mm] = 0;
-            for (int i = 0; i < 21; ++i) S->h_sub_op[(c * mup + mm) * 21 + i] = 0.0;
-            S->h_sub_gather[(c * mup + mm) * 2] = 0;
-            S->h_sub_gather[(c * mup + mm) * 2 + 1] = 0;
-          }
-          nsurv = 0;
-        }
-      }
-      msurv[c] = nsurv;
+      Stencil st;
+      build_stencil(M, c, st);
+      HostHwenoSink sink{S, m, c, mup, amax, gmax, W, st.present()};
+      msurv[c] = gks::su::hweno_cell(M, c, st, &S->avg0[c * NCOEF], sink);
     }
     int64_t mmax = 0;
     for (int64_t c = 0; c < nc; ++c) mmax = std::max<int64_t>(mmax, msurv[c]);
