@@ -190,10 +190,18 @@ typedef struct GksOptions {  /* stepping.SolverOptions (stepping.py:61-84) */
 
 typedef struct GksHandle GksHandle;
 
-/* Build device state; setup may be NULL (built internally). */
+/* Build device state.  setup == NULL: stencil selection, reconstruction
+   geometry and operators are built on the GPU (gks_setup_dev.cu), bit-
+   identical to the records built from gks_setup_build's arrays. */
 int gks_create(const GksMeshDesc* mesh, const GksSetup* setup, const GksOptions* opt, int device,
                GksHandle** out);
 void gks_destroy(GksHandle* h);
+/* Diagnostic copy of a device setup array of a handle (B200 build):
+   "avg0", "beta", "big_op", "big_gather", "sub_op", "sub_gather",
+   "sub_active", "avg_gather", "grad_gather", "grad_scale" (the padded
+   per-cell records the reconstruction kernels read).  dst == NULL: only
+   *nbytes is set. */
+int gks_handle_array(GksHandle* h, const char* name, void* dst, int64_t* nbytes);
 
 /* ------------------------------------------------------------------ */
 /* Domain decomposition (multi-GPU; no reference counterpart) */

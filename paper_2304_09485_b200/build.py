@@ -73,8 +73,10 @@ def build(verbose=False, force=False, ptxas_verbose=False, defines=(), out=None)
     nvcc = _nvcc()
     extra = ["-Xptxas", "-v"] if ptxas_verbose else []
     dflags = [f"-D{d}" for d in defines] + os.environ.get("GKS_NVCC_EXTRA", "").split()
-    jobs = [([nvcc, *ARCH, *NVCC_FLAGS, *dflags, *extra, "-c", str(src), "-o", str(BUILD / (src.stem + ".o"))],
-             verbose or ptxas_verbose) for src in cu]
+    # gks_setup_dev.cu: no FMA contraction, so the device-built operators
+    # equal the host build (g++ -ffp-contract=off) bit for bit
+    jobs = [([nvcc, *ARCH, *NVCC_FLAGS, *dflags, *extra, *(["-fmad=false"] if src.stem == "gks_setup_dev" else []),
+              "-c", str(src), "-o", str(BUILD / (src.stem + ".o"))], verbose or ptxas_verbose) for src in cu]
     jobs += [(["g++", *CXX_FLAGS, "-ffp-contract=off", "-c", str(src), "-o", str(BUILD / (src.stem + ".o"))], verbose)
              for src in cpp]
     # translation units compile independently: run them concurrently

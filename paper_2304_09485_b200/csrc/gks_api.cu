@@ -213,14 +213,16 @@ static int upload_rec(Handle* H, T** dst, const std::vector<T>& src, int64_t nc)
   return upload(H, dst, v.data(), v.size());
 }
 
-static bool weno_shape(int K, int M, int S, int* Kt, int* Mt, int* St) {
+int device_setup(Handle* H, const GksMeshDesc* m);  // gks_setup_dev.cu
+
+bool weno_shape(int K, int M, int S, int* Kt, int* Mt, int* St) {
   if (M <= 4 && S <= 6 && K <= 16) { *Kt = std::max(K, 13); *Mt = 4; *St = 6; return true; }
   if (M <= 8 && S <= 3 && K <= 24) { *Kt = 24; *Mt = 8; *St = 3; return true; }
   if (M <= 8 && S <= 8 && K <= 32) { *Kt = 32; *Mt = 8; *St = 8; return true; }
   return false;
 }
 
-static bool hweno_shape(int HA, int HG, int M, int* At, int* Gt, int* Mt) {
+bool hweno_shape(int HA, int HG, int M, int* At, int* Gt, int* Mt) {
   if (HA <= 4 && HG <= 5 && M <= 4) { *At = 4; *Gt = 5; *Mt = 4; return true; }
   if (HA <= 6 && HG <= 7 && M <= 6) { *At = 6; *Gt = 7; *Mt = 6; return true; }
   if (HA <= 16 && HG <= 17 && M <= 8) { *At = 16; *Gt = 17; *Mt = 8; return true; }
@@ -317,6 +319,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   TRY(upload(H, &H->vol, m->cell_volume, nc));
   TRY(upload(H, &H->h, m->cell_h, nc));
   TRY(upload(H, &H->cen, m->cell_centroid, nc * 3));
+  if (S) {  // host setup; otherwise device_setup builds avg0 / beta with the operators
   TRY(setup_array(S, "avg0", &hf, &hi, &hb, &shp));
   TRY(upload(H, &H->avg0, hf.data(), hf.size()));
   TRY(setup_array(S, "beta_mat", &hf, &hi, &hb, &shp));
@@ -329,6 +332,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
         for (int e = d; e < 9; ++e) packed[c * 45 + idx++] = hf[c * 81 + d * 9 + e];
     }
     TRY(upload_rec(H, &H->beta, packed, nc));
+  }
   }
 
   tick("cells");
@@ -527,7 +531,11 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   auto zero_d = [](int64_t) { return 0.0; };
   auto self_i = [](int64_t c) { return (int)c; };
   auto zero_b = [](int64_t) { return (int8_t)0; };
-  if (H->compact) {
+  if (!S) {
+    // device-side setup (gks_setup_dev.cu): stencils, geometry and operators
+    // built on the GPU into the same records
+    TRY(device_setup(H, m));
+  } else if (H->compact) {
     std::vector<double> op, gs, so;
     std::vector<int> ag, gg, sg;
     std::vector<int8_t> act;
@@ -702,16 +710,9 @@ int gks_create(const GksMeshDesc* mesh, const GksSetup* setup, const GksOptions*
     return GKS_ERR_BAD_ARG;
   }
   if (int rc = no_device()) return rc;
-  GksSetup* own = nullptr;
-  if (!setup) {
-    const int schemes = opt->scheme == GKS_SCHEME_HWENO_GMRES ? 2 : 1;
-    int rc = gks_setup_build(mesh, schemes, 0, &own);
-    if (rc) return rc;
-    setup = own;
-  }
+  // setup == NULL: stencils and operators are built on the device
   GksHandle* G = new GksHandle();
   int rc = create_handle(G, mesh, setup, opt, device, nullptr);
-  if (own) gks_setup_free(own);
   if (rc) {
     destroy_handle(G);
     delete G;
@@ -784,6 +785,39 @@ void gks_destroy(GksHandle* G) {
 }
 
 int64_t gks_num_boundary_faces(const GksHandle* G) { return G ? G->H.nbf : -1; }
+
+int gks_handle_array(GksHandle* G, const char* name, void* dst, int64_t* nbytes) {
+  if (!G || !name || !nbytes) return GKS_ERR_BAD_ARG;
+  Handle* H = &G->H;
+  const int64_t nc = H->nc;
+  const std::string n(name);
+  const void* src = nullptr;
+  int64_t bytes = 0;
+  const bool c = H->compact;
+  if (n == "avg0") { src = H->avg0; bytes = nc * 9 * 8; }
+  else if (n == "beta") { src = H->beta; bytes = nc * rec_stride_f64(45) * 8; }
+  else if (n == "big_op") { src = H->big_op; bytes = nc * rec_stride_f64(9 * (c ? H->Kt + 3 * H->St : H->Kt)) * 8; }
+  else if (n == "big_gather" && !c) { src = H->big_gather; bytes = nc * rec_stride_i32(H->Kt) * 4; }
+  else if (n == "sub_op") { src = H->sub_op; bytes = nc * rec_stride_f64(c ? H->Mt * 21 : H->Mt * 3 * H->St) * 8; }
+  else if (n == "sub_gather") { src = H->sub_gather; bytes = nc * rec_stride_i32(c ? H->Mt * 2 : H->Mt * H->St) * 4; }
+  else if (n == "sub_active") { src = H->sub_active; bytes = nc * H->Mt; }
+  else if (n == "avg_gather" && c) { src = H->avg_gather; bytes = nc * rec_stride_i32(H->Kt) * 4; }
+  else if (n == "grad_gather" && c) { src = H->grad_gather; bytes = nc * rec_stride_i32(H->St) * 4; }
+  else if (n == "grad_scale" && c) { src = H->grad_scale; bytes = nc * rec_stride_f64(H->St) * 8; }
+  else {
+    set_error("gks_handle_array: unknown array '%s' for this scheme", name);
+    return GKS_ERR_BAD_ARG;
+  }
+  if (!dst) { *nbytes = bytes; return GKS_OK; }
+  if (*nbytes != bytes) {
+    set_error("gks_handle_array: '%s' needs %lld bytes", name, (long long)bytes);
+    return GKS_ERR_BAD_ARG;
+  }
+  GKS_CUDA(cudaSetDevice(H->device));
+  GKS_CUDA(cudaStreamSynchronize(H->stream));
+  GKS_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+  return GKS_OK;
+}
 
 int64_t gks_reduction_granularity(int64_t nc_global) { return red_group_cells(nc_global); }
 

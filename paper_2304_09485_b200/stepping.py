@@ -79,6 +79,7 @@ class SolverOptions:
     reorder: str = "none"  # device-side locality renumbering: "none" | "rcm" | "morton" (reorder.py)
     first_order: bool = False  # KFVS on piecewise-constant states (the paper's low-order start)
     ortho: str = "mgs"  # GMRES orthogonalisation: "mgs" (reference, krylov.py:89-106) | "cgs2" (fused multi-dots)
+    setup: str = "device"  # stencils + operators built on the GPU ("device", gks_setup_dev.cu) or host C++ ("host")
 
     def __post_init__(self):
         if self.scheme not in SCHEMES:
@@ -93,6 +94,8 @@ class SolverOptions:
             raise ValueError(f"jacobian must be one of {JACOBIANS}")
         if self.ortho not in ("mgs", "cgs2"):
             raise ValueError("ortho must be 'mgs' or 'cgs2'")
+        if self.setup not in ("device", "host"):
+            raise ValueError("setup must be 'device' or 'host'")
         from .reorder import METHODS
 
         if self.reorder not in METHODS:
@@ -160,23 +163,28 @@ class Solver:
         self.bfaces = np.flatnonzero(mesh.face_neighbor < 0)
         self.bface_patch = [mesh.patch_names[p] for p in mesh.face_patch[self.bfaces]]
 
-        # native setup (stencils + operators, always on the reference's
-        # numbering) and the device handle (optionally renumbered, reorder.py)
-        self._setup = N.NativeSetup(mesh, schemes=2 if self.compact else 1)
+        # stencils + operators: built on the device by gks_create (setup
+        # NULL, the default) or by the host native setup on the reference's
+        # numbering; the device handle is optionally renumbered (reorder.py)
         self._opts, self._patch_arr = _options_struct(options, mesh)
         lib = N.load()
         self._perm = self._sub = None
-        setup = self._setup.handle
+        self._setup = None
+        setup = None
+        if options.setup == "host":
+            self._setup = N.NativeSetup(mesh, schemes=2 if self.compact else 1)
+            setup = self._setup.handle
         dev_mesh = mesh
         if options.reorder != "none":
             from .reorder import PermutedMesh, cell_order
 
             dev_mesh = PermutedMesh(mesh, cell_order(mesh, options.reorder))
             self._perm = dev_mesh.perm
-            sub = C.c_void_p()
-            N.check(lib.gks_setup_subset(setup, N.iptr(dev_mesh.perm), mesh.ncells, N.iptr(dev_mesh.inv),
-                                         mesh.ncells, C.byref(sub)))
-            self._sub = setup = sub
+            if setup is not None:
+                sub = C.c_void_p()
+                N.check(lib.gks_setup_subset(setup, N.iptr(dev_mesh.perm), mesh.ncells, N.iptr(dev_mesh.inv),
+                                             mesh.ncells, C.byref(sub)))
+                self._sub = setup = sub
         self._desc, self._keep = N.mesh_desc(dev_mesh)
         h = C.c_void_p()
         rc = lib.gks_create(C.byref(self._desc), setup, C.byref(self._opts), int(self.device), C.byref(h))

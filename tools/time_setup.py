@@ -35,5 +35,9 @@ h = C.c_void_p()
 t0 = time.perf_counter()
 N.check(lib.gks_create(C.byref(desc), st.handle, C.byref(o), 0, C.byref(h)))
 out["gks_create"] = time.perf_counter() - t0
+h2 = C.c_void_p()
+t0 = time.perf_counter()
+N.check(lib.gks_create(C.byref(desc), None, C.byref(o), 0, C.byref(h2)))
+out["gks_create_device_setup"] = time.perf_counter() - t0
 out["cells"] = mesh.ncells
 print(json.dumps(out), flush=True)
