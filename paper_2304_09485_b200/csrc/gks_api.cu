@@ -478,29 +478,36 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
       erow[2 * k] = m->face_owner[f]; ecol[2 * k] = m->face_neighbor[f];
       erow[2 * k + 1] = m->face_neighbor[f]; ecol[2 * k + 1] = m->face_owner[f];
     }
-    std::vector<int64_t> order;
-    order.reserve(nnz);
-    for (int64_t e = 0; e < nnz; ++e)
-      if (erow[e] < H->n_owned) order.push_back(e);  // rows of ghost cells live on their owner rank
     // columns ascending in the REFERENCE numbering (jacobian.py:181-196
     // lexsort), so a renumbered or rank-local handle sums every row's
-    // off-diagonal products in the reference's order
+    // off-diagonal products in the reference's order.  Stable counting sort
+    // by row (rows of ghost cells live on their owner rank), then a stable
+    // insertion sort of each row (at most one entry per cell face).
     const int64_t* cref = m->cell_rank;
-    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
-      if (erow[a] != erow[b]) return erow[a] < erow[b];
-      return cref ? cref[ecol[a]] < cref[ecol[b]] : ecol[a] < ecol[b];
-    });
-    const int64_t nkept = order.size();
+    std::vector<int> rowptr(H->n_owned + 1, 0);
+    for (int64_t e = 0; e < nnz; ++e)
+      if (erow[e] < H->n_owned) rowptr[erow[e] + 1]++;
+    std::partial_sum(rowptr.begin(), rowptr.end(), rowptr.begin());
+    const int64_t nkept = rowptr[H->n_owned];
+    std::vector<int64_t> order(std::max<int64_t>(nkept, 1));
+    {
+      std::vector<int> pos(rowptr.begin(), rowptr.end() - 1);
+      for (int64_t e = 0; e < nnz; ++e)
+        if (erow[e] < H->n_owned) order[pos[erow[e]]++] = e;
+    }
+    auto ckey = [&](int64_t e) { return cref ? cref[ecol[e]] : ecol[e]; };
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < H->n_owned; ++r)
+      for (int64_t i = rowptr[r] + 1; i < rowptr[r + 1]; ++i)
+        for (int64_t j = i; j > rowptr[r] && ckey(order[j]) < ckey(order[j - 1]); --j) std::swap(order[j], order[j - 1]);
     H->nnz = nkept;
-    std::vector<int> rowptr(H->n_owned + 1, 0), col(nkept), fslot(2 * nf, -1), ent(std::max<int64_t>(nkept, 1));
+    std::vector<int> col(std::max<int64_t>(nkept, 1)), fslot(2 * nf, -1), ent(std::max<int64_t>(nkept, 1));
     for (int64_t p = 0; p < nkept; ++p) {
       const int64_t e = order[p];
       col[p] = (int)ecol[e];
       ent[p] = (ifaces[e / 2] << 1) | (int)(e & 1);
-      rowptr[erow[e] + 1]++;
       fslot[2 * ifaces[e / 2] + (e & 1)] = (int)p;
     }
-    std::partial_sum(rowptr.begin(), rowptr.end(), rowptr.begin());
     TRY(upload(H, &H->interior_faces, ifaces.data(), ifaces.size()));
     TRY(upload(H, &H->boundary_faces, bfaces.data(), bfaces.size()));
     TRY(upload(H, &H->face_slot, fslot.data(), fslot.size()));
