@@ -227,6 +227,14 @@ typedef struct GksDomainDesc {
      gks_reduction_granularity(nc_global) cells (the last rank may end at
      nc_global), which makes every reduction partition-invariant */
   int64_t owned_offset;
+  /* device-side setup of a rank-local handle (gks_create_local with setup
+     == NULL; B200 build): the rank's native-setup view -- its local cells
+     in ascending reference id with every face of every such cell
+     (partition.py SetupMesh) -- and the maps between that order and the
+     local one.  NULL when a host setup is passed. */
+  const struct GksMeshDesc* setup_mesh;
+  const int64_t* local_to_setup;  /* (n_local) */
+  const int64_t* setup_to_local;  /* (setup_mesh->ncells) */
 } GksDomainDesc;
 /* cells per reduction group of a mesh of nc_global cells (partition alignment) */
 int64_t gks_reduction_granularity(int64_t nc_global);

@@ -144,7 +144,8 @@ class GksHaloDesc(C.Structure):
 
 class GksDomainDesc(C.Structure):
     _fields_ = [("n_owned", C.c_int64), ("n_recon", C.c_int64), ("nc_global", C.c_int64),
-                ("q", GksHaloDesc), ("x", GksHaloDesc), ("owned_offset", C.c_int64)]
+                ("q", GksHaloDesc), ("x", GksHaloDesc), ("owned_offset", C.c_int64),
+                ("setup_mesh", C.c_void_p), ("local_to_setup", C.c_void_p), ("setup_to_local", C.c_void_p)]
 
 
 class GksError(RuntimeError):

@@ -213,7 +213,7 @@ static int upload_rec(Handle* H, T** dst, const std::vector<T>& src, int64_t nc)
   return upload(H, dst, v.data(), v.size());
 }
 
-int device_setup(Handle* H, const GksMeshDesc* m);  // gks_setup_dev.cu
+int device_setup(Handle* H, const GksMeshDesc* m, const GksDomainDesc* dom);  // gks_setup_dev.cu
 
 bool weno_shape(int K, int M, int S, int* Kt, int* Mt, int* St) {
   if (M <= 4 && S <= 6 && K <= 16) { *Kt = std::max(K, 13); *Mt = 4; *St = 6; return true; }
@@ -541,7 +541,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   if (!S) {
     // device-side setup (gks_setup_dev.cu): stencils, geometry and operators
     // built on the GPU into the same records
-    TRY(device_setup(H, m));
+    TRY(device_setup(H, m, dom));
   } else if (H->compact) {
     std::vector<double> op, gs, so;
     std::vector<int> ag, gg, sg;
@@ -732,7 +732,7 @@ int gks_create(const GksMeshDesc* mesh, const GksSetup* setup, const GksOptions*
 int gks_create_local(const GksMeshDesc* mesh, const GksSetup* setup, const GksOptions* opt,
                      const GksDomainDesc* domain, int device, GksHandle** out) {
   set_error_index(-1);
-  if (!mesh || !opt || !out || !setup || !domain) {
+  if (!mesh || !opt || !out || !domain || (!setup && !domain->setup_mesh)) {
     set_error("gks_create_local: bad arguments");
     return GKS_ERR_BAD_ARG;
   }

@@ -212,12 +212,55 @@ int dalloc(Handle* H, T** p, size_t n) {
 
 inline unsigned grid_of(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// rank-local records from the setup-mesh build: rows in local order,
+// gathers renumbered to local ids, padding as k_setup_fix (pad0 = the local
+// id of setup cell 0: gks_setup_subset renumbers the reference arrays' zero
+// padding the same way)
+template <bool COMPACT>
+__global__ void __launch_bounds__(256) k_setup_place(int64_t nl, Recs s, Recs d, const int64_t* __restrict__ l2s,
+                                                     const int64_t* __restrict__ s2l, int w0, int w1, int w2,
+                                                     int pad0) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= nl) return;
+  const int64_t c = l2s[l];
+  const int self = (int)l;
+  auto map = [&](int v, bool inside) { return v < 0 ? (inside ? pad0 : self) : (int)s2l[v]; };
+  for (int k = 0; k < 9; ++k) d.avg0[l * 9 + k] = s.avg0[c * 9 + k];
+  for (int k = 0; k < 45; ++k) d.beta[l * 45 + k] = s.beta[c * 45 + k];
+  for (int k = 0; k < s.e_bop; ++k) d.big_op[l * d.e_bop + k] = s.big_op[c * s.e_bop + k];
+  for (int k = 0; k < s.e_sop; ++k) d.sub_op[l * d.e_sop + k] = s.sub_op[c * s.e_sop + k];
+  for (int k = 0; k < s.Mt; ++k) d.sub_active[l * d.Mt + k] = s.sub_active[c * s.Mt + k];
+  if (!COMPACT) {
+    for (int k = 0; k < s.Kt; ++k) d.big_gather[l * d.e_bg + k] = map(s.big_gather[c * s.e_bg + k], k < w0);
+    for (int mm = 0; mm < s.Mt; ++mm)
+      for (int k = 0; k < s.St; ++k)
+        d.sub_gather[l * d.e_sg + mm * s.St + k] = map(s.sub_gather[c * s.e_sg + mm * s.St + k], mm < w1 && k < w2);
+  } else {
+    for (int k = 0; k < s.Kt; ++k) d.avg_gather[l * d.e_ag + k] = map(s.avg_gather[c * s.e_ag + k], k < w0);
+    for (int k = 0; k < s.St; ++k) {
+      d.grad_gather[l * d.e_gg + k] = map(s.grad_gather[c * s.e_gg + k], k < w1);
+      d.grad_scale[l * d.e_gs + k] = s.grad_scale[c * s.e_gs + k];
+    }
+    for (int mm = 0; mm < s.Mt; ++mm)
+      for (int j = 0; j < 2; ++j) d.sub_gather[l * d.e_sg + mm * 2 + j] = map(s.sub_gather[c * s.e_sg + mm * 2 + j], mm < w2);
+  }
+}
+
 }  // namespace
 
-// Build avg0, beta and the reconstruction records of all nc cells on the
-// device (the host path's "cells" geometry + "operators" phases).
-int device_setup(Handle* H, const GksMeshDesc* m) {
-  const int64_t nc = m->ncells;
+// Build avg0, beta and the reconstruction records of the handle's cells on
+// the device (the host path's "cells" geometry + "operators" phases).  A
+// rank-local handle (dom->setup_mesh set) builds on its setup mesh -- the
+// local cells in ascending reference id with all their faces, so stencil
+// choices match the global build -- and places the records in local order.
+int device_setup(Handle* H, const GksMeshDesc* local, const GksDomainDesc* dom) {
+  const bool mapped = dom && dom->setup_mesh;
+  const GksMeshDesc* m = mapped ? dom->setup_mesh : local;
+  const int64_t nc = m->ncells, nl = local->ncells;
+  if (mapped && (!dom->local_to_setup || !dom->setup_to_local)) {
+    set_error("device setup: a setup mesh needs local_to_setup / setup_to_local");
+    return GKS_ERR_BAD_ARG;
+  }
   int nfpc = 0;
   for (int64_t c = 0; c < nc; ++c) {
     const int nf = (int)(m->cell_face_start[c + 1] - m->cell_face_start[c]);
@@ -227,10 +270,23 @@ int device_setup(Handle* H, const GksMeshDesc* m) {
     }
     nfpc = std::max(nfpc, nf);
   }
-  int pad0 = 0;  // device id of reference cell 0 (renumbered meshes)
-  if (m->cell_rank)
+  int pad0 = 0;  // handle id of reference cell 0 (renumbered meshes / rank-local handles)
+  if (mapped) {
+    for (int64_t l = 0; l < nl; ++l)
+      if (dom->local_to_setup[l] < 0 || dom->local_to_setup[l] >= nc) {
+        set_error("device setup: local_to_setup[%lld] out of range", (long long)l);
+        return GKS_ERR_BAD_ARG;
+      }
+    for (int64_t c = 0; c < nc; ++c)
+      if (dom->setup_to_local[c] < 0 || dom->setup_to_local[c] >= nl) {
+        set_error("device setup: setup_to_local[%lld] out of range", (long long)c);
+        return GKS_ERR_BAD_ARG;
+      }
+    pad0 = (int)dom->setup_to_local[0];
+  } else if (m->cell_rank) {
     for (int64_t c = 0; c < nc; ++c)
       if (m->cell_rank[c] == 0) { pad0 = (int)c; break; }
+  }
   DevMeshCopy dm;
   GksMeshDesc& d = dm.d;
   d.ncells = nc; d.nfaces = m->nfaces; d.nfq = m->nfq; d.ncq = m->ncq;
@@ -248,6 +304,12 @@ int device_setup(Handle* H, const GksMeshDesc* m) {
   TRY(dm.put(d.face_normal, m->face_normal, nf * 3));
   TRY(dm.put(d.face_shift, m->face_shift, nf * 3));
   TRY(dm.put(d.cell_rank, m->cell_rank, nc));
+  const int64_t* l2s = nullptr;
+  const int64_t* s2l = nullptr;
+  if (mapped) {
+    TRY(dm.put(l2s, dom->local_to_setup, nl));
+    TRY(dm.put(s2l, dom->setup_to_local, nc));
+  }
 
   int* sz = nullptr;
   GKS_CUDA(cudaMalloc(&sz, SZ_N * sizeof(int)));
@@ -259,15 +321,44 @@ int device_setup(Handle* H, const GksMeshDesc* m) {
   GKS_CUDA(cudaMemcpyAsync(hs, sz, sizeof(hs), cudaMemcpyDeviceToHost, H->stream));
   GKS_CUDA(cudaStreamSynchronize(H->stream));
 
-  TRY(dalloc(H, &H->avg0, nc * 9));
-  Recs r{};
-  r.avg0 = H->avg0;
-  if (rec_stride_f64(45) != 45) {
-    set_error("device setup: beta record stride");
-    return GKS_ERR_BAD_ARG;
-  }
-  TRY(dalloc(H, &H->beta, nc * 45));
-  r.beta = H->beta;
+  // build records: the handle's own (single handle) or temporaries in
+  // setup-mesh order (rank-local handle)
+  auto balloc = [&](auto** p, size_t n) -> int {
+    if (!mapped) return dalloc(H, p, n);
+    const size_t bytes = std::max<size_t>(n, 1) * sizeof(**p) + kTail;
+    GKS_CUDA(cudaMalloc(p, bytes));
+    dm.bufs.push_back(*p);
+    GKS_CUDA(cudaMemset(*p, 0, bytes));
+    return GKS_OK;
+  };
+  auto alloc_recs = [&](Recs& r, int64_t rows, auto&& al) -> int {
+    TRY(al(&r.avg0, rows * 9));
+    TRY(al(&r.beta, rows * 45));
+    if (!H->compact) {
+      r.e_bop = rec_stride_f64(9 * r.Kt);
+      r.e_bg = rec_stride_i32(r.Kt);
+      r.e_sop = rec_stride_f64(r.Mt * 3 * r.St);
+      r.e_sg = rec_stride_i32(r.Mt * r.St);
+      TRY(al(&r.big_op, (size_t)rows * r.e_bop));
+      TRY(al(&r.big_gather, (size_t)rows * r.e_bg));
+    } else {
+      r.e_bop = rec_stride_f64(9 * (r.Kt + 3 * r.St));
+      r.e_ag = rec_stride_i32(r.Kt);
+      r.e_gg = rec_stride_i32(r.St);
+      r.e_gs = rec_stride_f64(r.St);
+      r.e_sop = rec_stride_f64(r.Mt * 21);
+      r.e_sg = rec_stride_i32(r.Mt * 2);
+      TRY(al(&r.big_op, (size_t)rows * r.e_bop));
+      TRY(al(&r.avg_gather, (size_t)rows * r.e_ag));
+      TRY(al(&r.grad_gather, (size_t)rows * r.e_gg));
+      TRY(al(&r.grad_scale, (size_t)rows * r.e_gs));
+    }
+    TRY(al(&r.sub_op, (size_t)rows * r.e_sop));
+    TRY(al(&r.sub_gather, (size_t)rows * r.e_sg));
+    TRY(al(&r.sub_active, (size_t)rows * r.Mt));
+    return GKS_OK;
+  };
+  static_assert(rec_stride_f64(45) == 45, "beta records are stored unpadded");
 
   const bool compact = H->compact;
   const int K = std::max(hs[SZ_K], 1), mup = std::max(hs[SZ_MUP], 1), sup = std::max(hs[SZ_SUP], 1);
@@ -278,34 +369,13 @@ int device_setup(Handle* H, const GksMeshDesc* m) {
     return GKS_ERR_BAD_ARG;
   }
   for (int attempt = 0; attempt < 2; ++attempt) {
+    Recs r{};
     r.Kt = Kt; r.Mt = Mt; r.St = St;
-    if (!compact) {
-      r.e_bop = rec_stride_f64(9 * Kt);
-      r.e_bg = rec_stride_i32(Kt);
-      r.e_sop = rec_stride_f64(Mt * 3 * St);
-      r.e_sg = rec_stride_i32(Mt * St);
-      TRY(dalloc(H, &r.big_op, (size_t)nc * r.e_bop));
-      TRY(dalloc(H, &r.big_gather, (size_t)nc * r.e_bg));
-      TRY(dalloc(H, &r.sub_op, (size_t)nc * r.e_sop));
-      TRY(dalloc(H, &r.sub_gather, (size_t)nc * r.e_sg));
-      TRY(dalloc(H, &r.sub_active, (size_t)nc * Mt));
+    TRY(alloc_recs(r, nc, balloc));
+    if (!compact)
       k_setup_ops<false><<<grid_of(nc, SETUP_T), SETUP_T, 0, H->stream>>>(d, nc, r, sz);
-    } else {
-      r.e_bop = rec_stride_f64(9 * (Kt + 3 * St));
-      r.e_ag = rec_stride_i32(Kt);
-      r.e_gg = rec_stride_i32(St);
-      r.e_gs = rec_stride_f64(St);
-      r.e_sop = rec_stride_f64(Mt * 21);
-      r.e_sg = rec_stride_i32(Mt * 2);
-      TRY(dalloc(H, &r.big_op, (size_t)nc * r.e_bop));
-      TRY(dalloc(H, &r.avg_gather, (size_t)nc * r.e_ag));
-      TRY(dalloc(H, &r.grad_gather, (size_t)nc * r.e_gg));
-      TRY(dalloc(H, &r.grad_scale, (size_t)nc * r.e_gs));
-      TRY(dalloc(H, &r.sub_op, (size_t)nc * r.e_sop));
-      TRY(dalloc(H, &r.sub_gather, (size_t)nc * r.e_sg));
-      TRY(dalloc(H, &r.sub_active, (size_t)nc * Mt));
+    else
       k_setup_ops<true><<<grid_of(nc, SETUP_T), SETUP_T, 0, H->stream>>>(d, nc, r, sz);
-    }
     GKS_CUDA(cudaGetLastError());
     GKS_CUDA(cudaMemcpyAsync(hs, sz, sizeof(hs), cudaMemcpyDeviceToHost, H->stream));
     GKS_CUDA(cudaStreamSynchronize(H->stream));
@@ -321,30 +391,45 @@ int device_setup(Handle* H, const GksMeshDesc* m) {
         set_error("device setup: record shape did not settle");
         return GKS_ERR_BAD_ARG;
       }
-      // rebuild with the exact shape (the oversized records stay allocated
-      // until the handle is destroyed; this only happens for mixed meshes)
+      // rebuild with the exact shape (an oversized single-handle build stays
+      // allocated until the handle is destroyed; only mixed meshes get here)
       Kt = Kx; Mt = Mx; St = Sx;
       GKS_CUDA(cudaMemsetAsync(sz + SZ_M, 0, 3 * sizeof(int), H->stream));
       continue;
     }
-    if (!compact) {
-      k_setup_fix<false><<<grid_of(nc, 256), 256, 0, H->stream>>>(nc, r, K, M, S, pad0);
-      H->K = K; H->M = M; H->S = S;
-      H->big_gather = r.big_gather;
+    const int w0 = compact ? HA : K, w1 = compact ? HG : M, w2 = compact ? HM : S;
+    Recs f = r;
+    if (mapped) {
+      f = Recs{};
+      f.Kt = Kt; f.Mt = Mt; f.St = St;
+      TRY(alloc_recs(f, nl, [&](auto** p, size_t n) { return dalloc(H, p, n); }));
+      if (!compact)
+        k_setup_place<false><<<grid_of(nl, 256), 256, 0, H->stream>>>(nl, r, f, l2s, s2l, w0, w1, w2, pad0);
+      else
+        k_setup_place<true><<<grid_of(nl, 256), 256, 0, H->stream>>>(nl, r, f, l2s, s2l, w0, w1, w2, pad0);
+    } else if (!compact) {
+      k_setup_fix<false><<<grid_of(nc, 256), 256, 0, H->stream>>>(nc, r, w0, w1, w2, pad0);
     } else {
-      k_setup_fix<true><<<grid_of(nc, 256), 256, 0, H->stream>>>(nc, r, HA, HG, HM, pad0);
-      H->HA = HA; H->HG = HG; H->HM = HM;
-      H->avg_gather = r.avg_gather;
-      H->grad_gather = r.grad_gather;
-      H->grad_scale = r.grad_scale;
+      k_setup_fix<true><<<grid_of(nc, 256), 256, 0, H->stream>>>(nc, r, w0, w1, w2, pad0);
     }
     GKS_CUDA(cudaGetLastError());
     GKS_CUDA(cudaStreamSynchronize(H->stream));
+    if (!compact) {
+      H->K = K; H->M = M; H->S = S;
+    } else {
+      H->HA = HA; H->HG = HG; H->HM = HM;
+    }
+    H->avg0 = f.avg0;
+    H->beta = f.beta;
+    H->big_gather = f.big_gather;
+    H->avg_gather = f.avg_gather;
+    H->grad_gather = f.grad_gather;
+    H->grad_scale = f.grad_scale;
     H->Kt = Kt; H->Mt = Mt; H->St = St;
-    H->big_op = r.big_op;
-    H->sub_op = r.sub_op;
-    H->sub_gather = r.sub_gather;
-    H->sub_active = r.sub_active;
+    H->big_op = f.big_op;
+    H->sub_op = f.sub_op;
+    H->sub_gather = f.sub_gather;
+    H->sub_active = f.sub_active;
     return GKS_OK;
   }
   set_error("device setup: record shape did not settle");

@@ -138,14 +138,18 @@ class DistributedSolver:
         self.dom = build_domain(mesh, self.dec, rank, layers)
         self.local_mesh = LocalMesh(mesh, self.dom)
         lib = N.load()
-        # per-rank native setup on the local cells only (SetupMesh), restricted
-        # and reordered to the rank-local numbering
+        # per-rank setup on the local cells only (SetupMesh: local cells in
+        # reference order with all their faces): built on the device and
+        # placed in the rank-local order by gks_create_local (setup="device"),
+        # or by the host native setup, restricted and reordered here
         self._setup_mesh = SetupMesh(mesh, self.dom)
-        self._setup = N.NativeSetup(self._setup_mesh, schemes=2 if self.compact else 1)
+        self._setup = None
         sub = C.c_void_p()
-        N.check(lib.gks_setup_subset(self._setup.handle, N.iptr(self._setup_mesh.local_to_sub), self.dom.n_local,
-                                     N.iptr(self._setup_mesh.sub_to_local), self._setup_mesh.ncells,
-                                     C.byref(sub)))
+        if options.setup == "host":
+            self._setup = N.NativeSetup(self._setup_mesh, schemes=2 if self.compact else 1)
+            N.check(lib.gks_setup_subset(self._setup.handle, N.iptr(self._setup_mesh.local_to_sub),
+                                         self.dom.n_local, N.iptr(self._setup_mesh.sub_to_local),
+                                         self._setup_mesh.ncells, C.byref(sub)))
         self._sub = sub
         self._keep = []
         dd = N.GksDomainDesc()
@@ -155,6 +159,14 @@ class DistributedSolver:
         dd.owned_offset = self.dom.owned_offset
         dd.q = _halo_desc(self.dom.q_send, self.dom.q_recv, self._keep)
         dd.x = _halo_desc(self.dom.x_send, self.dom.x_recv, self._keep)
+        if options.setup != "host":
+            sdesc, skeep = N.mesh_desc(self._setup_mesh)
+            l2s = np.ascontiguousarray(self._setup_mesh.local_to_sub, dtype=np.int64)
+            s2l = np.ascontiguousarray(self._setup_mesh.sub_to_local, dtype=np.int64)
+            self._keep += [sdesc, skeep, l2s, s2l]
+            dd.setup_mesh = C.cast(C.pointer(sdesc), C.c_void_p)
+            dd.local_to_setup = l2s.ctypes.data
+            dd.setup_to_local = s2l.ctypes.data
         self._dd = dd
         self._desc, self._dkeep = N.mesh_desc(self.local_mesh)
         self._opts, self._parr = _options_struct(options, mesh)
@@ -163,7 +175,8 @@ class DistributedSolver:
                                      C.byref(h)))
         self._handle = h
         # the setup tables are no longer needed once the operators are on the device
-        lib.gks_setup_free(sub)
+        if sub.value:
+            lib.gks_setup_free(sub)
         self._sub = None
         self._setup = None
         if comm_id is not None:

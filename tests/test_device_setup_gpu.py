@@ -99,3 +99,26 @@ def test_device_setup_default_and_c2_size():
     host = make(mesh, "weno_gmres", "host")
     for arr in WENO_ARRAYS:
         assert np.array_equal(handle_array(dev, arr), handle_array(host, arr)), arr
+
+
+@pytest.mark.parametrize("scheme", ["weno_gmres", "hweno_gmres"])
+def test_device_setup_rank_local_handles(scheme):
+    """Rank-local handles (DistributedSolver, no communicator) build on
+    their SetupMesh on the device and place the records in local order:
+    equal to the host per-rank setup + gks_setup_subset path."""
+    from paper_2304_09485_b200.distributed import DistributedSolver
+    from paper_2304_09485_b200.partition import Decomposition
+
+    mesh = MG.generate_sphere_mesh(4, radius=0.5, far=10.0)
+    patches = {n: PatchSpec(n, "farfield_riemann", reference=REF) for n in mesh.patch_names}
+    dec = Decomposition.build(mesh, 3)
+    arrays = HWENO_ARRAYS if scheme == "hweno_gmres" else WENO_ARRAYS
+    for rank in range(3):
+        d = DistributedSolver(mesh, SolverOptions(scheme=scheme, patches=patches, setup="device"), rank=rank,
+                              nranks=3, dec=dec)
+        h = DistributedSolver(mesh, SolverOptions(scheme=scheme, patches=patches, setup="host"), rank=rank,
+                              nranks=3, dec=dec)
+        for k in (6, 7, 8):
+            assert info(d, k) == info(h, k), (rank, k)
+        for arr in arrays:
+            assert np.array_equal(handle_array(d, arr), handle_array(h, arr)), (rank, arr)
