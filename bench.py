@@ -323,9 +323,10 @@ def kernel_model(solver, compact):
 
 # -- CPU baseline (oracle) -------------------------------------------------------------
 
-CPU_NOTE = ("oracle/ numpy restatement of the reference, single-threaded (OMP/OPENBLAS threads = 1); measured "
-            "in the build container on C2 n=2 at 0.7-0.9x the reference package's own s/step (profiles/r02/"
-            "cpu_calibration.json), i.e. a slightly faster-than-reference baseline")
+CPU_NOTE = ("oracle/ numpy restatement of the reference, single-threaded (OMP/OPENBLAS threads = 1); timed "
+            "against the reference package itself in the build container (profiles/r02/cpu_calibration.json): "
+            "0.81x / 0.98x its s per Roe step and 0.82x / 1.04x its s per residual on C2 n=2 / n=4 (the sample "
+            "size), i.e. a baseline at the reference's own speed")
 
 
 def cpu_sample(payload):
