@@ -196,6 +196,27 @@ typedef struct GksHandle GksHandle;
 int gks_create(const GksMeshDesc* mesh, const GksSetup* setup, const GksOptions* opt, int device,
                GksHandle** out);
 void gks_destroy(GksHandle* h);
+/* Reconstruction pieces of recon.py / hweno.py (the reference's
+   WenoReconstructor / HwenoReconstructor / evaluate_faces API) on a
+   handle's cells, 5 components, host arrays:
+   gks_recon_coeffs      combined_coeffs (recon.py:285-294, hweno.py:162-169),
+                         linear = 1: the big candidate alone -> coef (nc,9,5);
+                         the solver's own k_recon_* kernel
+   gks_recon_candidates  candidate_coeffs (recon.py:276-283, hweno.py:139-160)
+                         -> c_big (nc,9,5), b_sub (nc,M,3,5), M = reference
+                         sub-stencil width (gks_handle_info(h, 7))
+   gks_face_values       evaluate_faces (recon.py:297-314) from coef (nc,9,5)
+                         -> val_o, val_n (nfq,5), grad_o, grad_n (nfq,3,5)
+   gks_combine_candidates combine_candidates (recon.py:167-195) on an
+                         (n,9,k) / (n,m,3,k) batch, active (n,m), beta (n,9,9)
+                         -> out (n,9,k), w0n (n,k), wmn (n,m,k); m <= 16 */
+int gks_recon_coeffs(GksHandle* h, const double* q, const double* grad, int linear, double* coef);
+int gks_recon_candidates(GksHandle* h, const double* q, const double* grad, double* c_big, double* b_sub);
+int gks_face_values(GksHandle* h, const double* q, const double* coef, double* val_o, double* grad_o,
+                    double* val_n, double* grad_n);
+int gks_combine_candidates(int64_t n, int k, int m, const double* c_big, const double* b_sub,
+                           const int8_t* active, const double* beta, double eps, double lin_weight,
+                           double* out, double* w0n, double* wmn);
 /* Diagnostic copy of a device setup array of a handle (B200 build):
    "avg0", "beta", "big_op", "big_gather", "sub_op", "sub_gather",
    "sub_active", "avg_gather", "grad_gather", "grad_scale" (the padded

@@ -198,6 +198,11 @@ SIGNATURES = [
     ("gks_slopes", C.c_int, [C.c_int64, c_double_p, c_double_p, C.c_int, C.c_double, c_double_p]),
     ("gks_num_boundary_faces", C.c_int64, [C.c_void_p]),
     ("gks_handle_array", C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.POINTER(C.c_int64)]),
+    ("gks_recon_coeffs", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
+    ("gks_recon_candidates", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("gks_face_values", C.c_int, [C.c_void_p] + [C.c_void_p] * 6),
+    ("gks_combine_candidates", C.c_int, [C.c_int64, C.c_int, C.c_int] + [C.c_void_p] * 4 +
+     [C.c_double, C.c_double] + [C.c_void_p] * 3),
     ("gks_assemble_jacobian", C.c_int, [C.c_void_p, c_double_p, c_double_p, c_double_p]),
     ("gks_jacobian", C.c_void_p, [C.c_void_p]),
     ("gks_blocksys_create", C.c_int, [C.c_int64, C.c_int64, c_double_p, c_double_p, c_int64_p, c_int64_p,

@@ -697,6 +697,25 @@ int jacobian_assemble(Handle* H, BlockSys* A, const double* ghosts_dev);
 
 using namespace gks;
 
+namespace {
+struct DevTmp {
+  std::vector<void*> p;
+  ~DevTmp() {
+    for (void* x : p) cudaFree(x);
+  }
+  template <class T>
+  T* get(size_t n) {
+    void* x = nullptr;
+    if (cudaMalloc(&x, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    p.push_back(x);
+    return (T*)x;
+  }
+};
+}  // namespace
+
 static int no_device() {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
@@ -879,6 +898,119 @@ int gks_ghost_batch(int64_t n, const GksPatchDesc* patch, const double* q, const
   if (n == 0) return GKS_OK;
   if (int rc = no_device()) return rc;
   return ghost_batch_device(n, dev_patch(*patch), q, normal, grad, make_kin(gamma), q_out, grad_out);
+}
+
+// reconstruction pieces of recon.py / hweno.py on the handle's cells
+int gks_recon_coeffs(GksHandle* G, const double* q, const double* grad, int linear, double* coef) {
+  Handle* H = &G->H;
+  set_error_index(-1);
+  if (!q || !coef || (H->compact && !grad)) {
+    set_error("gks_recon_coeffs: bad arguments (the compact scheme needs gradients)");
+    return GKS_ERR_BAD_ARG;
+  }
+  if (H->n_recon != H->nc) {
+    set_error("gks_recon_coeffs: rank-local handles reconstruct owned + layer-1 cells only");
+    return GKS_ERR_BAD_ARG;
+  }
+  GKS_CUDA(cudaSetDevice(H->device));
+  ApiStage stage(G);
+  GKS_CUDA(cudaMemcpyAsync(H->q, q, H->nc * 5 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  if (grad) GKS_CUDA(cudaMemcpyAsync(H->grad, grad, H->nc * 15 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  if (int rc = recon_coeffs_device(H, H->q, linear ? 1 : 0)) return rc;
+  GKS_CUDA(cudaMemcpyAsync(coef, H->coef, H->nc * 45 * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaStreamSynchronize(H->stream));
+  return GKS_OK;
+}
+
+
+int gks_recon_candidates(GksHandle* G, const double* q, const double* grad, double* c_big, double* b_sub) {
+  Handle* H = &G->H;
+  set_error_index(-1);
+  if (!q || !c_big || !b_sub || (H->compact && !grad)) {
+    set_error("gks_recon_candidates: bad arguments (the compact scheme needs gradients)");
+    return GKS_ERR_BAD_ARG;
+  }
+  GKS_CUDA(cudaSetDevice(H->device));
+  const int M = H->compact ? H->HM : H->M;
+  DevTmp t;
+  double* cb = t.get<double>(H->nc * 45);
+  double* bs = t.get<double>(H->nc * M * 15);
+  if (!cb || !bs) {
+    set_error("gks_recon_candidates: device allocation failed");
+    return GKS_ERR_CUDA;
+  }
+  ApiStage stage(G);
+  GKS_CUDA(cudaMemcpyAsync(H->q, q, H->nc * 5 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  if (grad) GKS_CUDA(cudaMemcpyAsync(H->grad, grad, H->nc * 15 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  if (int rc = recon_candidates_device(H, H->q, M, cb, bs)) return rc;
+  GKS_CUDA(cudaMemcpyAsync(c_big, cb, H->nc * 45 * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaMemcpyAsync(b_sub, bs, H->nc * M * 15 * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaStreamSynchronize(H->stream));
+  return GKS_OK;
+}
+
+int gks_face_values(GksHandle* G, const double* q, const double* coef, double* val_o, double* grad_o, double* val_n,
+                    double* grad_n) {
+  Handle* H = &G->H;
+  set_error_index(-1);
+  if (!q || !coef || !val_o || !grad_o || !val_n || !grad_n) {
+    set_error("gks_face_values: bad arguments");
+    return GKS_ERR_BAD_ARG;
+  }
+  GKS_CUDA(cudaSetDevice(H->device));
+  const int64_t nfq = H->nfq;
+  DevTmp t;
+  double* vo = t.get<double>(nfq * 5);
+  double* go = t.get<double>(nfq * 15);
+  double* vn = t.get<double>(nfq * 5);
+  double* gn = t.get<double>(nfq * 15);
+  if (!vo || !go || !vn || !gn) {
+    set_error("gks_face_values: device allocation failed");
+    return GKS_ERR_CUDA;
+  }
+  ApiStage stage(G);
+  GKS_CUDA(cudaMemcpyAsync(H->q, q, H->nc * 5 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  GKS_CUDA(cudaMemcpyAsync(H->coef, coef, H->nc * 45 * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  if (int rc = face_values_device(H, H->q, H->coef, vo, go, vn, gn)) return rc;
+  GKS_CUDA(cudaMemcpyAsync(val_o, vo, nfq * 5 * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaMemcpyAsync(grad_o, go, nfq * 15 * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaMemcpyAsync(val_n, vn, nfq * 5 * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaMemcpyAsync(grad_n, gn, nfq * 15 * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  GKS_CUDA(cudaStreamSynchronize(H->stream));
+  return GKS_OK;
+}
+
+int gks_combine_candidates(int64_t n, int k, int m, const double* c_big, const double* b_sub, const int8_t* active,
+                           const double* beta, double eps, double lin_weight, double* out, double* w0n,
+                           double* wmn) {
+  set_error_index(-1);
+  if (n < 0 || k < 1 || m < 1 || !c_big || !b_sub || !active || !beta || !out || !w0n || !wmn) {
+    set_error("gks_combine_candidates: bad arguments");
+    return GKS_ERR_BAD_ARG;
+  }
+  if (n == 0) return GKS_OK;
+  if (int rc = no_device()) return rc;
+  DevTmp t;
+  double* cb = t.get<double>(n * 9 * k);
+  double* bs = t.get<double>(n * m * 3 * k);
+  int8_t* ac = t.get<int8_t>(n * m);
+  double* be = t.get<double>(n * 81);
+  double* o = t.get<double>(n * 9 * k);
+  double* w0 = t.get<double>(n * k);
+  double* wm = t.get<double>(n * m * k);
+  if (!cb || !bs || !ac || !be || !o || !w0 || !wm) {
+    set_error("gks_combine_candidates: device allocation failed");
+    return GKS_ERR_CUDA;
+  }
+  GKS_CUDA(cudaMemcpy(cb, c_big, n * 9 * k * sizeof(double), cudaMemcpyHostToDevice));
+  GKS_CUDA(cudaMemcpy(bs, b_sub, n * m * 3 * k * sizeof(double), cudaMemcpyHostToDevice));
+  GKS_CUDA(cudaMemcpy(ac, active, n * m, cudaMemcpyHostToDevice));
+  GKS_CUDA(cudaMemcpy(be, beta, n * 81 * sizeof(double), cudaMemcpyHostToDevice));
+  if (int rc = combine_batch_device(n, k, m, cb, bs, ac, be, eps, lin_weight, o, w0, wm, 0)) return rc;
+  GKS_CUDA(cudaMemcpy(out, o, n * 9 * k * sizeof(double), cudaMemcpyDeviceToHost));
+  GKS_CUDA(cudaMemcpy(w0n, w0, n * k * sizeof(double), cudaMemcpyDeviceToHost));
+  GKS_CUDA(cudaMemcpy(wmn, wm, n * m * k * sizeof(double), cudaMemcpyDeviceToHost));
+  return GKS_OK;
 }
 
 int gks_update_gradients(GksHandle* G, const double* qpt, double* grad_out) {

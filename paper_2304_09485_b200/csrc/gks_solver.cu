@@ -121,9 +121,12 @@ static constexpr int RT_THREADS = RT * 5;
 
 // recon.py:167-195 on one (cell, component); beta packed as the upper
 // triangle (45 entries, row-major).
+// (w0n / wmn: optional outputs of the normalised weights, the API's
+// combine_candidates; wmn[m * wstride])
 template <int M>
 __device__ __forceinline__ void combine(double cb[9], const double (&b)[M][3], const int8_t* act,
-                                        const double* B, double eps, double lw) {
+                                        const double* B, double eps, double lw, double* w0n_out = nullptr,
+                                        double* wmn_out = nullptr, int wstride = 0) {
   double beta0 = 0.0;
   {
     int idx = 0;
@@ -157,6 +160,11 @@ __device__ __forceinline__ void combine(double cb[9], const double (&b)[M][3], c
     total += wm[m];
   }
   const double w0n = w0 / total;
+  if (w0n_out) {
+    *w0n_out = w0n;
+#pragma unroll
+    for (int m = 0; m < M; ++m) wmn_out[m * wstride] = wm[m] / total;
+  }
   const double c0 = w0n / g0;
   const double sub0 = w0n * lw / g0;
 #pragma unroll
@@ -1066,6 +1074,193 @@ int boundary_ghosts_device(Handle* H, const double* q) {
   GKS_LAUNCH(KC_GHOST, k_boundary_ghosts, blocks_for(H->nbf, TPB), TPB, 0, H->stream, H->nbf, H->boundary_faces, H->f_own,
                                                                      H->f_patch, H->f_normal, H->patches, q,
                                                                      H->kc, H->ghosts, H->status);
+  GKS_CUDA(cudaGetLastError());
+  return GKS_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// reconstruction pieces of the host API (recon.py / hweno.py): candidate
+// coefficients, the nonlinear combination of given candidates, and face-
+// point values from given coefficients.  Generic (runtime-shaped) kernels
+// over the handle's records -- the solver's own step runs the fused
+// k_recon_* / k_face kernels above.
+// ---------------------------------------------------------------------------
+
+// kernel-argument view of the handle's records and geometry
+struct RecView {
+  int Kt, Mt, St;
+  const double *big_op, *sub_op, *grad_scale, *cen, *h, *avg0, *fq_point, *f_shift;
+  const int *big_gather, *sub_gather, *avg_gather, *grad_gather, *fq_face, *f_own, *f_nbr;
+};
+
+static RecView rec_view(const Handle* H) {
+  return RecView{H->Kt,         H->Mt,         H->St,         H->big_op,      H->sub_op,      H->grad_scale,
+                 H->cen,        H->h,          H->avg0,       H->fq_point,    H->f_shift,     H->big_gather,
+                 H->sub_gather, H->avg_gather, H->grad_gather, H->fq_face,    H->f_own,       H->f_nbr};
+}
+
+// candidate_coeffs (recon.py:276-283, hweno.py:139-160): the quadratic big
+// candidate (nc, 9, 5) and the linear sub candidates (nc, Mout, 3, 5)
+template <bool COMPACT>
+__global__ void __launch_bounds__(TPB) k_recon_candidates(int64_t nc, const double* __restrict__ q,
+                                                          const double* __restrict__ grad,
+                                                          const double* __restrict__ h, RecView R, int Mout,
+                                                          double* __restrict__ cbig, double* __restrict__ bsub) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nc * 5) return;
+  const int64_t c = i / 5;
+  const int k = (int)(i - c * 5);
+  const double qc = q[c * 5 + k];
+  const int Kt = R.Kt, Mt = R.Mt, St = R.St;
+  if (!COMPACT) {
+    const double* op = R.big_op + c * rec_stride_f64(9 * Kt);
+    const int* gi = R.big_gather + c * rec_stride_i32(Kt);
+    for (int d = 0; d < 9; ++d) {
+      double acc = 0.0;
+      for (int j = 0; j < Kt; ++j) acc += op[d * Kt + j] * (q[(int64_t)gi[j] * 5 + k] - qc);
+      cbig[(c * 9 + d) * 5 + k] = acc;
+    }
+    const double* so = R.sub_op + c * rec_stride_f64(3 * Mt * St);
+    const int* sg = R.sub_gather + c * rec_stride_i32(Mt * St);
+    for (int m = 0; m < Mout; ++m)
+      for (int d = 0; d < 3; ++d) {
+        double acc = 0.0;
+        for (int s2 = 0; s2 < St; ++s2) acc += so[(m * 3 + d) * St + s2] * (q[(int64_t)sg[m * St + s2] * 5 + k] - qc);
+        bsub[((c * Mout + m) * 3 + d) * 5 + k] = acc;
+      }
+  } else {
+    const int HA = Kt, HG = St, W = HA + 3 * HG;
+    const double* op = R.big_op + c * rec_stride_f64(9 * W);
+    const int* ag = R.avg_gather + c * rec_stride_i32(HA);
+    const int* gg = R.grad_gather + c * rec_stride_i32(HG);
+    const double* gs = R.grad_scale + c * rec_stride_f64(HG);
+    for (int d = 0; d < 9; ++d) {
+      double acc = 0.0;
+      for (int j = 0; j < HA; ++j) acc += op[d * W + j] * (q[(int64_t)ag[j] * 5 + k] - qc);
+      for (int g = 0; g < HG; ++g)
+        for (int x = 0; x < 3; ++x) acc += op[d * W + HA + 3 * g + x] * (gs[g] * grad[((int64_t)gg[g] * 3 + x) * 5 + k]);
+      cbig[(c * 9 + d) * 5 + k] = acc;
+    }
+    const double* so = R.sub_op + c * rec_stride_f64(21 * Mt);
+    const int* sg = R.sub_gather + c * rec_stride_i32(2 * Mt);
+    for (int m = 0; m < Mout; ++m) {
+      const int64_t s0 = sg[m * 2], s1 = sg[m * 2 + 1];
+      double rhs[7];
+      rhs[0] = q[s1 * 5 + k] - qc;
+      for (int x = 0; x < 3; ++x) {
+        rhs[1 + x] = h[s0] * grad[(s0 * 3 + x) * 5 + k];
+        rhs[4 + x] = h[s1] * grad[(s1 * 3 + x) * 5 + k];
+      }
+      for (int d = 0; d < 3; ++d) {
+        double acc = 0.0;
+        for (int s2 = 0; s2 < 7; ++s2) acc += so[(m * 3 + d) * 7 + s2] * rhs[s2];
+        bsub[((c * Mout + m) * 3 + d) * 5 + k] = acc;
+      }
+    }
+  }
+}
+
+// combine_candidates (recon.py:167-195) on given candidates: one thread per
+// (cell, component) of an (n, 9, k) / (n, M, 3, k) batch, M <= 16; the
+// same combine() as the fused kernels, beta symmetrised to its packed form
+constexpr int CB_MAXM = 16;
+__global__ void __launch_bounds__(TPB) k_combine_batch(int64_t n, int nk, int M, const double* __restrict__ cbig,
+                                                       const double* __restrict__ bsub,
+                                                       const int8_t* __restrict__ act,
+                                                       const double* __restrict__ beta, double eps, double lw,
+                                                       double* __restrict__ out, double* __restrict__ w0n,
+                                                       double* __restrict__ wmn) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * nk) return;
+  const int64_t c = i / nk;
+  const int k = (int)(i - c * nk);
+  double cb[9], B[45], b[CB_MAXM][3];
+  int8_t a[CB_MAXM];
+  for (int d = 0; d < 9; ++d) cb[d] = cbig[(c * 9 + d) * nk + k];
+  {
+    int idx = 0;
+    const double* Bc = beta + c * 81;
+    for (int d = 0; d < 9; ++d)
+      for (int e = d; e < 9; ++e) B[idx++] = e == d ? Bc[d * 9 + d] : 0.5 * (Bc[d * 9 + e] + Bc[e * 9 + d]);
+  }
+  for (int m = 0; m < CB_MAXM; ++m) {
+    a[m] = m < M ? act[c * M + m] : 0;
+    for (int d = 0; d < 3; ++d) b[m][d] = m < M ? bsub[((c * M + m) * 3 + d) * nk + k] : 0.0;
+  }
+  double wtmp[CB_MAXM];
+  combine<CB_MAXM>(cb, b, a, B, eps, lw, w0n + c * nk + k, wtmp, 1);
+  for (int m = 0; m < M; ++m) wmn[(c * M + m) * nk + k] = wtmp[m];
+  for (int d = 0; d < 9; ++d) out[(c * 9 + d) * nk + k] = cb[d];
+}
+
+// evaluate_faces (recon.py:297-314): both sides' values / gradients at every
+// face point from given coefficients; boundary points repeat the owner side
+__global__ void __launch_bounds__(TPB) k_face_values(int64_t nfq, RecView R, const double* __restrict__ q,
+                                                     const double* __restrict__ coef, double* __restrict__ vo,
+                                                     double* __restrict__ go, double* __restrict__ vn,
+                                                     double* __restrict__ gn) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nfq) return;
+  const int f = R.fq_face[i];
+  const int64_t own = R.f_own[f], nbr = R.f_nbr[f];
+  const double x[3] = {R.fq_point[3 * i], R.fq_point[3 * i + 1], R.fq_point[3 * i + 2]};
+  double v[5], g[3][5];
+  eval_side(q, coef, R.cen, R.h, R.avg0, own, x, v, g);
+  for (int k = 0; k < 5; ++k) {
+    vo[i * 5 + k] = v[k];
+    for (int d = 0; d < 3; ++d) go[(i * 3 + d) * 5 + k] = g[d][k];
+  }
+  if (nbr >= 0) {
+    const double xn[3] = {x[0] - R.f_shift[3 * f], x[1] - R.f_shift[3 * f + 1], x[2] - R.f_shift[3 * f + 2]};
+    eval_side(q, coef, R.cen, R.h, R.avg0, nbr, xn, v, g);
+  }
+  for (int k = 0; k < 5; ++k) {
+    vn[i * 5 + k] = v[k];
+    for (int d = 0; d < 3; ++d) gn[(i * 3 + d) * 5 + k] = g[d][k];
+  }
+}
+
+int recon_coeffs_device(Handle* H, const double* q, int linear) {
+  const int saved = H->linear_weights;
+  H->linear_weights = linear;
+  const int rc = recon_device(H, q, nullptr);
+  H->linear_weights = saved;
+  return rc;
+}
+
+int recon_candidates_device(Handle* H, const double* q, int Mout, double* cbig, double* bsub) {
+  if (Mout > H->Mt) {
+    set_error("candidate width %d exceeds the records (%d)", Mout, H->Mt);
+    return GKS_ERR_BAD_ARG;
+  }
+  if (H->compact)
+    GKS_LAUNCH(KC_RECON, k_recon_candidates<true>, blocks_for(H->nc * 5, TPB), TPB, 0, H->stream, H->nc, q, H->grad,
+               H->h, rec_view(H), Mout, cbig, bsub);
+  else
+    GKS_LAUNCH(KC_RECON, k_recon_candidates<false>, blocks_for(H->nc * 5, TPB), TPB, 0, H->stream, H->nc, q, H->grad,
+               H->h, rec_view(H), Mout, cbig, bsub);
+  GKS_CUDA(cudaGetLastError());
+  return GKS_OK;
+}
+
+int combine_batch_device(int64_t n, int nk, int M, const double* cbig, const double* bsub, const int8_t* act,
+                         const double* beta, double eps, double lw, double* out, double* w0n, double* wmn,
+                         cudaStream_t s) {
+  if (M < 1 || M > CB_MAXM) {
+    set_error("combine: %d sub-stencil slots (1..%d supported)", M, CB_MAXM);
+    return GKS_ERR_BAD_ARG;
+  }
+  if (n * nk == 0) return GKS_OK;
+  GKS_LAUNCH(KC_RECON, k_combine_batch, blocks_for(n * nk, TPB), TPB, 0, s, n, nk, M, cbig, bsub, act, beta, eps, lw,
+             out, w0n, wmn);
+  GKS_CUDA(cudaGetLastError());
+  return GKS_OK;
+}
+
+int face_values_device(Handle* H, const double* q, const double* coef, double* vo, double* go, double* vn,
+                       double* gn) {
+  GKS_LAUNCH(KC_FACE, k_face_values, blocks_for(H->nfq, TPB), TPB, 0, H->stream, H->nfq, rec_view(H), q, coef, vo, go, vn, gn);
   GKS_CUDA(cudaGetLastError());
   return GKS_OK;
 }

@@ -316,6 +316,14 @@ int gauss_gradients_device(Handle* H, const double* qpt, double* grad_out);
 int ghost_batch_device(int64_t n, const DevPatch& P, const double* q, const double* nrm, const double* grad,
                        const KinConst& kc, double* q_out, double* grad_out);
 int jacobian_device(Handle* H, const double* q, bool ghosts_given);
+// reconstruction pieces of the host API (gks_solver.cu)
+int recon_coeffs_device(Handle* H, const double* q, int linear);  // -> H->coef
+int recon_candidates_device(Handle* H, const double* q, int Mout, double* cbig, double* bsub);
+int combine_batch_device(int64_t n, int nk, int M, const double* cbig, const double* bsub, const int8_t* act,
+                         const double* beta, double eps, double lw, double* out, double* w0n, double* wmn,
+                         cudaStream_t s);
+int face_values_device(Handle* H, const double* q, const double* coef, double* vo, double* go, double* vn,
+                       double* gn);
 void count_launch(int n);
 void set_error_index(int64_t i);
 int check_status(Handle* H, const char* what);

@@ -1,4 +1,10 @@
-"""Compact-scheme gradient update (mirrors gks3d/hweno.py:172-194).
+"""Compact HWENO reconstruction API and gradient update (mirrors gks3d/hweno.py).
+
+HwenoReconstructor (hweno.py:32-169): the operators of the native setup in
+the reference's padded layout; candidate_coeffs / combined_coeffs run on the
+GPU (gks_recon_candidates, and the solver's own k_recon_hweno through
+gks_recon_coeffs).  fit_big_hermite / fit_sub_hermite (hweno.py:200-245)
+select one cell's device-computed candidates.
 
 update_gradients(mesh, point_values): cell-averaged gradients from the
 interface point values by the Gauss theorem, |Omega| grad Q = sum over the
@@ -15,6 +21,55 @@ import numpy as np
 
 from . import _native as N
 from .kinetic import DEFAULT_GAMMA
+from .recon import (LINEAR_WEIGHT, WENO_EPS, ReconGeometry, ReconPolynomial, _device_candidates, _device_combined,
+                    _field, _handle, _linear, _poly)
+
+
+def _grad(grad):
+    grad = np.asarray(grad, dtype=float)
+    return grad[:, :, None] if grad.ndim == 2 else grad
+
+
+class HwenoReconstructor:
+    """Compact reconstruction from averages and average gradients."""
+
+    def __init__(self, geom: ReconGeometry, eps=WENO_EPS, lin_weight=LINEAR_WEIGHT, weights="nonlinear"):
+        if weights not in ("nonlinear", "linear"):
+            raise ValueError(f"weights must be 'nonlinear' or 'linear', got {weights!r}")
+        self.geom = geom
+        self.eps = eps
+        self.lin_weight = lin_weight
+        self.weights = weights
+        ops = N.NativeSetup(geom.mesh, schemes=2)
+        for name in ("big_op", "big_avg_gather", "big_grad_gather", "big_grad_scale", "big_ncols", "big_degree",
+                     "sub_op", "sub_gather"):
+            setattr(self, name, np.array(ops.array("hweno_" + name)))
+        self.sub_active = np.array(ops.array("hweno_sub_active")).astype(bool)
+
+    def _solver(self):
+        return _handle(self.geom.mesh, "hweno_gmres", self.eps, self.lin_weight)
+
+    def candidate_coeffs(self, field, grad):
+        """(c_big (nc, 9, m), b_sub (nc, M, 3, m)) from an (nc, m) field and its (nc, 3, m) gradients."""
+        return _device_candidates(self._solver(), _field(field), _grad(grad))
+
+    def combined_coeffs(self, field, grad):
+        return _device_combined(self._solver(), _field(field), _grad(grad), self.weights == "linear")
+
+
+def fit_big_hermite(recon: HwenoReconstructor, c, field, grad) -> ReconPolynomial:
+    """The quadratic compact candidate of cell c."""
+    field = _field(field)
+    c_big, _ = recon.candidate_coeffs(field, grad)
+    return _poly(recon.geom, c, field[c], c_big[c], recon.big_degree[c])
+
+
+def fit_sub_hermite(recon: HwenoReconstructor, c, field, grad) -> list[ReconPolynomial]:
+    """The linear two-cell candidates of cell c, one per surviving face neighbour."""
+    field = _field(field)
+    _, b_sub = recon.candidate_coeffs(field, grad)
+    return [_poly(recon.geom, c, field[c], _linear(b_sub[c, mm], field.shape[1]), 1)
+            for mm in np.flatnonzero(recon.sub_active[c])]
 
 
 def update_gradients(mesh, point_values, gamma: float = DEFAULT_GAMMA):

@@ -33,7 +33,7 @@ ALIAS = {
     "gks3d.mesh.boxgen": ["paper_2304_09485_b200.mesh"],
     "gks3d.mesh.fileio": ["paper_2304_09485_b200.mesh"],
     "gks3d.mesh.stencils": ["paper_2304_09485_b200.stencils"],
-    "gks3d.recon": [],
+    "gks3d.recon": ["paper_2304_09485_b200.recon"],
     "gks3d.cli": [],
     "gks3d.report": [],
 }
