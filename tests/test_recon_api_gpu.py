@@ -65,7 +65,7 @@ def test_candidates_and_combine(compact):
         # hweno.py:139-160 on the API's own reference-layout operators
         nc = mesh.ncells
         ga = q[rec.big_avg_gather] - q[:, None, :]
-        gg = (rec.big_grad_scale[:, :, None, None] * g[rec.big_grad_gather]).reshape(nc, -1, 3)
+        gg = (rec.big_grad_scale[:, :, None, None] * g[rec.big_grad_gather]).reshape(nc, -1, q.shape[1])
         amax = rec.big_avg_gather.shape[1]
         ref_big = np.einsum("cdk,ckm->cdm", rec.big_op[:, :, :amax], ga) + \
             np.einsum("cdk,ckm->cdm", rec.big_op[:, :, amax:], gg)
