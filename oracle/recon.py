@@ -289,8 +289,8 @@ class Recon:
         if self.compact:
             h = self.mesh.cell_h
             cb = np.matmul(self.P_bigA, q[self.P_aid] - qc)
-            gg = h[self.P_gid][:, :, None, None] * grad[self.P_gid]  # (nc, g, 3, 5)
-            cb += np.matmul(self.P_bigG.reshape(gg.shape[0], -1, gg.shape[1] * 3), gg.reshape(gg.shape[0], -1, 5))
+            gg = h[self.P_gid][:, :, None, None] * grad[self.P_gid]  # (nc, g, 3, m)
+            cb += np.matmul(self.P_bigG.reshape(gg.shape[0], -1, gg.shape[1] * 3), gg.reshape(gg.shape[0], -1, gg.shape[-1]))
             if self.linear:
                 return cb
             j = self.P_sj
