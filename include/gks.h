@@ -60,6 +60,12 @@ int64_t gks_kernel_launches(void);
 int gks_flux_batch(int64_t n, const double* wl, const double* wr, const double* sl,
                    const double* sr, const double* tau, const double* dt, const double* tp,
                    double gamma, double* flux_out, double* point_out);
+/* instantaneous_flux (flux.py:191-197): the moment flux of the interface
+   distribution at time t (n), the same kernel with the point-value time
+   coefficients */
+int gks_instant_flux_batch(int64_t n, const double* wl, const double* wr, const double* sl,
+                           const double* sr, const double* tau, const double* t, double gamma,
+                           double* flux_out);
 
 /* build_interface intermediates (flux.py:69-107, InterfaceBatch fields):
    al, ar (n,3,5) micro-slopes, atl, atr (n,5) time slopes, w0 (n,5)

@@ -295,7 +295,7 @@ class Recon:
                 return cb
             j = self.P_sj
             hg = h[:, None, None] * grad  # (nc, 3, 5)
-            rhs = np.concatenate([(q[j] - qc)[:, :, None, :], np.broadcast_to(hg[:, None], j.shape + (3, 5)),
+            rhs = np.concatenate([(q[j] - qc)[:, :, None, :], np.broadcast_to(hg[:, None], j.shape + hg.shape[1:]),
                                   hg[j]], axis=2)  # (nc, M, 7, 5)
             bs = np.matmul(self.P_sub, rhs)
         else:

@@ -165,6 +165,7 @@ SIGNATURES = [
     ("gks_flux_batch", C.c_int, [C.c_int64, c_double_p, c_double_p, c_double_p, c_double_p,
                                  c_double_p, c_double_p, c_double_p, C.c_double, c_double_p,
                                  c_double_p]),
+    ("gks_instant_flux_batch", C.c_int, [C.c_int64] + [C.c_void_p] * 6 + [C.c_double, C.c_void_p]),
     ("gks_flux_bench", C.c_int, [C.c_int64, C.c_int, C.c_double, c_double_p]),
     ("gks_interface_data", C.c_int, [C.c_int64, c_double_p, c_double_p, c_double_p, c_double_p, C.c_double,
                                      c_double_p, c_double_p, c_double_p, c_double_p, c_double_p, c_double_p,

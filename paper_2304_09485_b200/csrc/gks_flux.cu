@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(128, GKS_FLUX_MINB) k_flux_batch(int64_t n, co
                                                     const double* __restrict__ dt,
                                                     const double* __restrict__ tp, KinConst kc,
                                                     double* __restrict__ flux,
-                                                    double* __restrict__ point, int* status) {
+                                                    double* __restrict__ point, int* status, int instant) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   auto get = [&](int side, double w[5], double s5[3][5]) {
@@ -117,8 +117,9 @@ __global__ void __launch_bounds__(128, GKS_FLUX_MINB) k_flux_batch(int64_t n, co
     return true;
   };
   double f[5], p[5];
-  const int rc = tp ? interface_flux_t<false, true>(get, press, tau[i], dt[i], 0.0, kc, f, tp[i], p)
-                    : interface_flux_t<false, false>(get, press, tau[i], dt[i], 0.0, kc, f, 0.0, p);
+  const int rc = instant ? interface_flux_t<false, false, 0, true>(get, press, tau[i], dt[i], 0.0, kc, f, dt[i], p)
+                 : tp    ? interface_flux_t<false, true>(get, press, tau[i], dt[i], 0.0, kc, f, tp[i], p)
+                         : interface_flux_t<false, false>(get, press, tau[i], dt[i], 0.0, kc, f, 0.0, p);
   if (rc) {
     raise_dev(status, GKS_ERR_UNPHYSICAL, (int)i);
     return;
@@ -379,9 +380,28 @@ const char* gks_last_error(void) { return g_err.c_str(); }
 int64_t gks_last_error_index(void) { return g_err_index; }
 int64_t gks_kernel_launches(void) { return g_launches.load(); }
 
+static int flux_batch(int64_t n, const double* wl, const double* wr, const double* sl, const double* sr,
+                      const double* tau, const double* dt, const double* tp, double gamma, double* flux_out,
+                      double* point_out, int instant);
+
 int gks_flux_batch(int64_t n, const double* wl, const double* wr, const double* sl,
                    const double* sr, const double* tau, const double* dt, const double* tp,
                    double gamma, double* flux_out, double* point_out) {
+  return flux_batch(n, wl, wr, sl, sr, tau, dt, tp, gamma, flux_out, point_out, 0);
+}
+
+int gks_instant_flux_batch(int64_t n, const double* wl, const double* wr, const double* sl, const double* sr,
+                           const double* tau, const double* t, double gamma, double* flux_out) {
+  if (!flux_out) {
+    set_error("gks_instant_flux_batch: bad arguments");
+    return GKS_ERR_BAD_ARG;
+  }
+  return flux_batch(n, wl, wr, sl, sr, tau, t, nullptr, gamma, flux_out, nullptr, 1);
+}
+
+static int flux_batch(int64_t n, const double* wl, const double* wr, const double* sl, const double* sr,
+                      const double* tau, const double* dt, const double* tp, double gamma, double* flux_out,
+                      double* point_out, int instant) {
   g_err_index = -1;
   if (n < 0 || !wl || !wr || !tau || !dt) {
     set_error("gks_flux_batch: bad arguments");
@@ -424,7 +444,7 @@ int gks_flux_batch(int64_t n, const double* wl, const double* wr, const double* 
   const int st0[4] = {0, 0x7fffffff, 0, 0};
   GKS_CUDA(cudaMemcpy(d_status, st0, sizeof(st0), cudaMemcpyHostToDevice));
   GKS_LAUNCH(KC_FLUXBATCH, k_flux_batch, blocks_for(n, 128), 128, 0, 0, n, d_wl, d_wr, d_sl, d_sr, d_tau,
-             d_dt, point_out ? d_tp : nullptr, make_kin(gamma), d_f, d_p, d_status);
+             d_dt, point_out ? d_tp : nullptr, make_kin(gamma), d_f, d_p, d_status, instant);
   GKS_CUDA(cudaGetLastError());
   int st[4];
   GKS_CUDA(cudaMemcpy(st, d_status, sizeof(st), cudaMemcpyDeviceToHost));
@@ -619,10 +639,10 @@ int gks_flux_bench(int64_t n, int reps, double gamma, double* ms_per_launch) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   for (int r = 0; r < 3; ++r)
-    k_flux_batch<<<blocks_for(n, 128), 128>>>(n, dwl, dwr, dsl, dsr, dtau, ddt, nullptr, make_kin(gamma), df, nullptr, d_status);
+    k_flux_batch<<<blocks_for(n, 128), 128>>>(n, dwl, dwr, dsl, dsr, dtau, ddt, nullptr, make_kin(gamma), df, nullptr, d_status, 0);
   cudaEventRecord(e0);
   for (int r = 0; r < reps; ++r)
-    k_flux_batch<<<blocks_for(n, 128), 128>>>(n, dwl, dwr, dsl, dsr, dtau, ddt, nullptr, make_kin(gamma), df, nullptr, d_status);
+    k_flux_batch<<<blocks_for(n, 128), 128>>>(n, dwl, dwr, dsl, dsr, dtau, ddt, nullptr, make_kin(gamma), df, nullptr, d_status, 0);
   cudaEventRecord(e1);
   GKS_CUDA(cudaEventSynchronize(e1));
   count_launch(3 + reps);

@@ -387,7 +387,16 @@ __device__ __forceinline__ double dt_value(const DT& d) {
   else return d();
 }
 
-template <bool VISCOUS, bool POINT, int TAU = 0, class SideFn, class PressFn, class DT = double>
+// INSTANT: the moment flux of the distribution at the instant tp instead of
+// its average over [0, dt] (flux.py:191-197 instantaneous_flux): the flux
+// families take the point-value time coefficients
+__device__ __forceinline__ TimeCoef instant_coefficients(TimeCoef t) {
+  t.c1 = t.g1; t.c2 = t.g2; t.c3 = t.g3;
+  t.c4 = t.f1; t.c5 = t.f2; t.c6 = t.f3;
+  return t;
+}
+
+template <bool VISCOUS, bool POINT, int TAU = 0, bool INSTANT = false, class SideFn, class PressFn, class DT = double>
 __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const PressFn& get_pressures, double tau_in,
                                                 const DT& dt_in, double mu, const KinConst& kc, double flux[5], double tp,
                                                 double point[5]) {
@@ -416,6 +425,7 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
     if (tau_known && !(PRE_R && tau < 0.0)) {
       dt = dt_value(dt_in);
       tc = time_coefficients(tau, dt, tp);
+      if (INSTANT) tc = instant_coefficients(tc);
     }
   }
 #pragma unroll 1
@@ -437,6 +447,7 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
       dt = dt_value(dt_in);
       tau = collision_tau(pl, pr, dt, false, mu, nullptr);
       tc = time_coefficients(tau, dt, tp);
+      if (INSTANT) tc = instant_coefficients(tc);
     }
     double A[5];
     Maxw m;
@@ -518,6 +529,7 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
     dt = dt_value(dt_in);
     if (tau < 0.0) tau = collision_tau(pl, pr, dt, VISCOUS, mu, w0);
     tc = time_coefficients(tau, dt, tp);
+      if (INSTANT) tc = instant_coefficients(tc);
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
       F[i] = tc.c4 * F[i] + tc.c5 * F5[i] + tc.c6 * F6[i];

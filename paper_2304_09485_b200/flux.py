@@ -1,7 +1,7 @@
 """Gas-kinetic interface flux API (device-backed).
 
 Mirrors gks3d/flux.py: build_interface (:69-107), evolve_flux (:162-179),
-point_value (:182-188), kfvs_flux (:200-208), collision_time (:211-227),
+point_value (:182-188), instantaneous_flux (:191-197), kfvs_flux (:200-208), collision_time (:211-227),
 rotate_to_local / rotate_to_global (:230-243), euler_flux_local
 (:246-260), compatibility_residual (:263-268).  The interface distribution
 is evaluated by the fused sm_100a kernel behind gks_flux_batch; the
@@ -94,6 +94,21 @@ def _run(ib: InterfaceBatch, tau, dt, tp):
 def evolve_flux(ib: InterfaceBatch, tau, dt):
     """Time-averaged local-frame flux (1/dt) int_0^dt int u psi f."""
     return _run(ib, tau, dt, None)[0]
+
+
+def instantaneous_flux(ib: InterfaceBatch, tau, t):
+    """Local-frame moment flux int u psi f at the instant t (flux.py:191-197)."""
+    n = ib.n
+    tau = N.f64(np.broadcast_to(np.asarray(tau, dtype=float), (n,)))
+    t = N.f64(np.broadcast_to(np.asarray(t, dtype=float), (n,)))
+    flux = np.empty((n, 5))
+    lib = N.load()
+    rc = lib.gks_instant_flux_batch(n, N.dptr(ib.wl), N.dptr(ib.wr), N.dptr(ib.sl), N.dptr(ib.sr), N.dptr(tau),
+                                    N.dptr(t), ib.gamma, N.dptr(flux))
+    if rc == N.GKS_ERR_UNPHYSICAL:
+        raise UnphysicalStateError(lib.gks_last_error().decode())
+    N.check(rc)
+    return flux
 
 
 def point_value(ib: InterfaceBatch, tau, t):

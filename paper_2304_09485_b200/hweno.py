@@ -49,6 +49,20 @@ class HwenoReconstructor:
     def _solver(self):
         return _handle(self.geom.mesh, "hweno_gmres", self.eps, self.lin_weight)
 
+    def _grad_rows(self, c, ids, shifts):
+        """h_j * cell-mean gradient rows of the basis over members (j, s),
+        target included, in the chart of c (hweno.py:45-60): (3 len(ids), 9)."""
+        from .recon import monomial_grad_rows
+
+        mesh = self.geom.mesh
+        h0 = mesh.cell_h[c]
+        out = np.empty((3 * len(ids), 9))
+        for r, (j, s) in enumerate(zip(ids, shifts)):
+            pts, w = mesh.cell_quadrature_of(int(j), s)
+            out[3 * r:3 * r + 3] = mesh.cell_h[j] * (np.tensordot(w, monomial_grad_rows((pts - mesh.cell_centroid[c]) / h0),
+                                                                  axes=1) / h0)
+        return out
+
     def candidate_coeffs(self, field, grad):
         """(c_big (nc, 9, m), b_sub (nc, M, 3, m)) from an (nc, m) field and its (nc, 3, m) gradients."""
         return _device_candidates(self._solver(), _field(field), _grad(grad))

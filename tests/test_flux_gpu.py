@@ -125,3 +125,26 @@ def test_ghost_state_and_gradients_match_oracle(kind):
     gg = ghost_gradients(g, spec, nrm)
     gref = ghost_grad(g, spec, nrm)
     assert np.max(np.abs(gg - gref)) <= 1e-13 * np.max(np.abs(gref))
+
+
+def test_instantaneous_flux_integrates_to_time_average():
+    """instantaneous_flux (flux.py:191-197) is the integrand of evolve_flux:
+    Gauss-Legendre over [0, dt] of the device's instantaneous flux equals
+    the device's analytic time average; at t = 0 with tau = inf it is the
+    KFVS split flux."""
+    from paper_2304_09485_b200 import flux as F
+
+    rng = np.random.default_rng(31)
+    n = 64
+    wl, wr, sl, sr = F.random_interface_inputs(rng, n)
+    ib = F.build_interface(wl, wr, sl, sr)
+    tau = rng.uniform(0.05, 0.5, n)
+    dt = rng.uniform(0.2, 1.0, n)
+    x, w = np.polynomial.legendre.leggauss(24)
+    avg = np.zeros((n, 5))
+    for xi, wi in zip(x, w):
+        avg += 0.5 * wi * F.instantaneous_flux(ib, tau, 0.5 * dt * (xi + 1.0))
+    ref = F.evolve_flux(ib, tau, dt)
+    assert np.max(np.abs(avg - ref)) <= 1e-11 * np.max(np.abs(ref))
+    kf = F.instantaneous_flux(F.build_interface(wl, wr), np.inf, 0.0)
+    assert np.max(np.abs(kf - F.kfvs_flux(wl, wr))) <= 1e-13 * np.max(np.abs(kf))
