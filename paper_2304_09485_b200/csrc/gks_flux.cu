@@ -255,13 +255,19 @@ __global__ void k_moment_table(int64_t n, const double* __restrict__ w, KinConst
                                double* __restrict__ vf, double* __restrict__ wf, double* __restrict__ xi) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  // the reference's recurrence operation by operation, without FMA
+  // contraction (kinetic.py:113-137): the deep-tail half-range moments come
+  // from cancelling terms, where a fused multiply-add changes the rounding
   const double lam = w[i * 5 + 4], h = 0.5 / lam;
+  auto step = [](double mean, double m1, double c, double m2) {
+    return __dadd_rn(__dmul_rn(mean, m1), __dmul_rn(c, m2));
+  };
   auto full = [&](double mean, double* out) {
     double m2 = 1.0, m1 = mean;
     out[i] = 1.0;
     if (order >= 1) out[n + i] = mean;
     for (int p = 2; p <= order; ++p) {
-      const double m = mean * m1 + (double)(p - 1) * h * m2;
+      const double m = step(mean, m1, __dmul_rn((double)(p - 1), h), m2);
       out[p * n + i] = m;
       m2 = m1;
       m1 = m;
@@ -271,15 +277,15 @@ __global__ void k_moment_table(int64_t n, const double* __restrict__ w, KinConst
   full(w[i * 5 + 2], vf);
   full(w[i * 5 + 3], wf);
   const double u = w[i * 5 + 1], sq = sqrt(lam);
-  const double gauss = 0.5 * exp(-lam * u * u) / sqrt(M_PI * lam);
+  const double gauss = __dmul_rn(0.5, exp(__dmul_rn(__dmul_rn(-lam, u), u))) / sqrt(__dmul_rn(M_PI, lam));
   for (int side = 0; side < 2; ++side) {
     double* out = side ? un : up;
     double m2 = 0.5 * erfc(side ? sq * u : -sq * u);
-    double m1 = u * m2 + (side ? -gauss : gauss);
+    double m1 = __dadd_rn(__dmul_rn(u, m2), side ? -gauss : gauss);
     out[i] = m2;
     if (order >= 1) out[n + i] = m1;
     for (int p = 2; p <= order; ++p) {
-      const double m = u * m1 + (double)(p - 1) * h * m2;
+      const double m = step(u, m1, __dmul_rn((double)(p - 1), h), m2);
       out[p * n + i] = m;
       m2 = m1;
       m1 = m;
