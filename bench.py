@@ -458,10 +458,12 @@ def cavity_problem(n, compact, re=100.0):
     return mesh, patches, fld.q, fld.grad, dict(model="viscous", mu=0.15 / re)
 
 
-def converge_leg(args, threshold=1e-10, max_steps=12000):
+def converge_leg(args, threshold=1e-10, max_steps=12000, rel_steps=16000, rel_budget_s=30.0):
     """Run the cavity case to the reference driver's convergence test
     (res_rho_l1 < thr and res_l2 < 1e4 thr, driver.py:71-76) and time it
-    (host wall clock around the device-resident loop, one step per call)."""
+    (host wall clock around the device-resident loop, one step per call);
+    then keep stepping to SURVEY D8's second definition, a 10-decade drop
+    relative to max(res_rho_l1 over steps 1-5), within a bounded budget."""
     from paper_2304_09485_b200.stepping import SolutionField, Solver, SolverOptions
 
     mesh, patches, q, g, extra = cavity_problem(args.converge_n, False)
@@ -471,18 +473,40 @@ def converge_leg(args, threshold=1e-10, max_steps=12000):
     s.upload(SolutionField(q, g))
     t0 = time.perf_counter()
     steps = None
+    hist = []
     for k in range(1, max_steps + 1):
         info = s.advance_resident()
+        hist.append(info.res_rho_l1)
         if info.res_rho_l1 < threshold and info.res_l2 < 1e4 * threshold:
             steps = k
             break
     el = time.perf_counter() - t0
+    final = info.res_rho_l1
+    # D8 relative: 10 decades below max(res_rho_l1, steps 1-5)
+    ref5 = max(hist[:5])
+    rel_target = 1e-10 * ref5
+    steps_rel = secs_rel = None
+    kk = k
+    floor = min(h for h in hist if h > 0.0) if any(h > 0.0 for h in hist) else None
+    if steps is not None:
+        while kk < rel_steps and time.perf_counter() - t0 < el + rel_budget_s:
+            if hist[-1] <= rel_target:
+                steps_rel, secs_rel = kk, time.perf_counter() - t0
+                break
+            kk += 1
+            hist.append(s.advance_resident().res_rho_l1)
+        if steps_rel is None and hist[-1] <= rel_target:
+            steps_rel, secs_rel = kk, time.perf_counter() - t0
+        pos = [h for h in hist if h > 0.0]
+        floor = min(pos) if pos else None
+    rel = {"target": rel_target, "max_res_steps_1_5": ref5, "steps": steps_rel, "seconds": secs_rel,
+           "steps_run": kk, "lowest_res_rho_l1": floor}
     return {"case": f"lid-driven cavity Re 100 (cases/cavity_re100_desk.ini physics), 6*{args.converge_n}^3 = "
                     f"{mesh.ncells} tets, weno_gmres, Roe Jacobian, CFL 2",
             "threshold": threshold, "criterion": "res_rho_l1 < thr and res_l2 < 1e4 thr (driver.py:71-76)",
             "steps": steps, "seconds": el if steps else None, "steps_run": k, "seconds_run": el,
-            "ms_per_step": 1000.0 * el / k, "final_res_rho_l1": info.res_rho_l1, "setup_s": round(setup, 2),
-            "cells": mesh.ncells}
+            "ms_per_step": 1000.0 * el / k, "final_res_rho_l1": final, "setup_s": round(setup, 2),
+            "cells": mesh.ncells, "relative_10_decades": rel}
 
 
 def paper_table_leg(steps=100, warmup=5):
