@@ -500,7 +500,8 @@ def converge_leg(args, threshold=1e-10, max_steps=12000, rel_steps=16000, rel_bu
         pos = [h for h in hist if h > 0.0]
         floor = min(pos) if pos else None
     rel = {"target": rel_target, "max_res_steps_1_5": ref5, "steps": steps_rel, "seconds": secs_rel,
-           "steps_run": kk, "lowest_res_rho_l1": floor}
+           "steps_run": kk, "lowest_res_rho_l1": floor,
+           "decades_reached": (float(np.log10(ref5 / floor)) if floor else None)}
     return {"case": f"lid-driven cavity Re 100 (cases/cavity_re100_desk.ini physics), 6*{args.converge_n}^3 = "
                     f"{mesh.ncells} tets, weno_gmres, Roe Jacobian, CFL 2",
             "threshold": threshold, "criterion": "res_rho_l1 < thr and res_l2 < 1e4 thr (driver.py:71-76)",
