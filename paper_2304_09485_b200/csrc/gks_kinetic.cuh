@@ -529,7 +529,7 @@ __device__ __forceinline__ int interface_flux_t(const SideFn& get_side, const Pr
     dt = dt_value(dt_in);
     if (tau < 0.0) tau = collision_tau(pl, pr, dt, VISCOUS, mu, w0);
     tc = time_coefficients(tau, dt, tp);
-      if (INSTANT) tc = instant_coefficients(tc);
+    if (INSTANT) tc = instant_coefficients(tc);
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
       F[i] = tc.c4 * F[i] + tc.c5 * F5[i] + tc.c6 * F6[i];
