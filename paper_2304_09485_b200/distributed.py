@@ -86,13 +86,15 @@ class LoopbackGroup:
         self.nranks = nranks
         self.members = []
 
-    def advance_all(self, solvers):
+    def advance_all(self, solvers, step=None):
+        """One step on every rank; step(k, solver) -> StepInfo replaces the
+        default advance_resident (e.g. the host-array advance_inplace)."""
         out = [None] * len(solvers)
         err = [None] * len(solvers)
 
         def run(k, s):
             try:
-                out[k] = s.advance_resident()
+                out[k] = step(k, s) if step else s.advance_resident()
             except BaseException as e:  # re-raised on the caller's thread
                 err[k] = e
 
@@ -228,6 +230,21 @@ class DistributedSolver:
     def advance_resident(self):
         info = N.GksStepInfo()
         rc = N.load().gks_advance_resident(self._handle, C.byref(info))
+        if rc:
+            Solver._raise(self, rc, "advance")
+        return _info(info)
+
+    def advance_inplace(self, q_local, grad_local=None):
+        """One step from the rank's HOST field (all local cells, local order:
+        q_local = q[dom.cells]), written back in place -- the gks_advance path
+        behind Solver.advance_inplace, halos exchanged on the device."""
+        if q_local.dtype != np.float64 or not q_local.flags.c_contiguous or q_local.shape != (self.dom.n_local, 5):
+            raise ValueError("advance_inplace needs a C-contiguous float64 (n_local, 5) field")
+        if self.compact and (grad_local is None or not grad_local.flags.c_contiguous):
+            raise ValueError("compact scheme needs a C-contiguous gradient field")
+        info = N.GksStepInfo()
+        rc = N.load().gks_advance(self._handle, N.dptr(q_local), N.dptr(grad_local) if self.compact else None,
+                                  C.byref(info))
         if rc:
             Solver._raise(self, rc, "advance")
         return _info(info)

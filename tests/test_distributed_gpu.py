@@ -237,3 +237,31 @@ def test_cgs2_multidot_gmres(jac):
     h2, q2, _ = _run_ranks(mesh, cgs, q, grad, 2, 3)
     assert [(x.res_rho_l1, x.res_l2) for x in h1] == [(x.res_rho_l1, x.res_l2) for x in h2]
     assert np.array_equal(q1, q2)
+
+
+@pytest.mark.parametrize("kind", ["weno", "c3"])
+def test_loopback_host_array_steps_equal_resident(kind):
+    """The bench's end-to-end path on rank-local handles: gks_advance from
+    each rank's host field (H2D, step with device halo exchanges, D2H) on 2
+    loopback ranks reproduces the 1-rank resident run bit for bit."""
+    from paper_2304_09485_b200.distributed import DistributedSolver, LoopbackGroup
+    from paper_2304_09485_b200.partition import Decomposition
+
+    mesh, opts, q, grad = setup_case(kind, 4)
+    steps = 3
+    h1, q1, g1 = _run_ranks(mesh, opts, q, grad, 1, steps)
+    dec = Decomposition.build(mesh, 2)
+    grp = LoopbackGroup(2)
+    ss = [DistributedSolver(mesh, opts, rank=r, nranks=2, dec=dec, loopback=grp) for r in range(2)]
+    fq = [np.ascontiguousarray(q[s.dom.cells]) for s in ss]
+    fg = [None if grad is None else np.ascontiguousarray(grad[s.dom.cells]) for s in ss]
+    for k in range(steps):
+        infos = grp.advance_all(ss, step=lambda r, s: s.advance_inplace(fq[r], fg[r]))
+        assert infos[0].res_rho_l1 == h1[k].res_rho_l1 and infos[0].solver_cycles == h1[k].solver_cycles
+    for r, s in enumerate(ss):
+        n = s.dom.n_owned
+        own = s.dom.cells[:n]
+        assert np.array_equal(fq[r][:n], q1[own])
+        if grad is not None:
+            assert np.array_equal(fg[r][:n], g1[own])
+    grp.close()
