@@ -276,10 +276,12 @@ CONVERGE_CASES = {
     # physics) run to the driver's convergence test (driver.py:71-76)
     "cavity4": dict(n=4, threshold=1e-10, max_steps=8000),
     "cavity8": dict(n=8, threshold=1e-10, max_steps=8000),
+    # the compact scheme (HWENO + Gauss gradient update) on the same case
+    "cavity4_hweno": dict(n=4, threshold=1e-10, max_steps=8000, scheme="hweno_gmres"),
 }
 
 
-def cavity_setup(n):
+def cavity_setup(n, scheme="weno_gmres"):
     from gks3d.boundary import PatchSpec
     from gks3d.mesh import generate_box_mesh
     from gks3d.stepping import SolverOptions, initial_field
@@ -289,8 +291,8 @@ def cavity_setup(n):
     patches = {nm: PatchSpec(nm, "wall_noslip_isothermal", lambda_wall=lam_wall) for nm in mesh.patch_names}
     patches["ymax"] = PatchSpec("ymax", "wall_noslip_isothermal", lambda_wall=lam_wall,
                                 velocity=np.array([0.15, 0.0, 0.0]))
-    opts = SolverOptions(scheme="weno_gmres", model="viscous", mu=0.15 / 100.0, patches=patches, cfl=2.0)
-    return mesh, opts, initial_field(mesh, [1.0, 0.0, 0.0, 0.0, 1.0 / GAMMA])
+    opts = SolverOptions(scheme=scheme, model="viscous", mu=0.15 / 100.0, patches=patches, cfl=2.0)
+    return mesh, opts, initial_field(mesh, [1.0, 0.0, 0.0, 0.0, 1.0 / GAMMA], compact=scheme.startswith("hweno"))
 
 
 def make_converge(names=None):
@@ -301,7 +303,7 @@ def make_converge(names=None):
     for name, case in CONVERGE_CASES.items():
         if names and name not in names:
             continue
-        mesh, opts, fld = cavity_setup(case["n"])
+        mesh, opts, fld = cavity_setup(case["n"], case.get("scheme", "weno_gmres"))
         solver = Solver(mesh, opts)
         hist = []
         t0 = time.time()
@@ -314,6 +316,8 @@ def make_converge(names=None):
                 break
         out = dict(hist=np.array(hist), q_final=fld.q, steps=np.array(steps if steps else -1),
                    threshold=np.array(case["threshold"]), n=np.array(case["n"]))
+        if fld.grad is not None:
+            out["grad_final"] = fld.grad
         np.savez_compressed(HERE / f"converge_{name}.npz", **out)
         print(f"converge_{name}.npz", mesh.ncells, "cells, converged at", steps, f"({time.time() - t0:.0f} s)",
               flush=True)

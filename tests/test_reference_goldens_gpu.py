@@ -8,7 +8,8 @@
 * a step the reference rejects once and redoes at halved dt
   (stepping.py:286-296): the device takes the same branch;
 * the reference's lid-driven cavity run to its own convergence test
-  (driver.py:71-76): converged fields within 1e-8, the convergence step and
+  (driver.py:71-76), non-compact and compact (HWENO, with the converged
+  gradient field): converged fields within 1e-8, the convergence step and
   every decade crossing of the residual history within +-1 step
   (north_star "Correctness").
 """
@@ -125,7 +126,8 @@ def decade_crossings(traj, decades):
     return out
 
 
-@pytest.mark.parametrize("case,ortho", [("cavity4", "mgs"), ("cavity8", "mgs"), ("cavity8", "cgs2")])
+@pytest.mark.parametrize("case,ortho", [("cavity4", "mgs"), ("cavity8", "mgs"), ("cavity8", "cgs2"),
+                                        ("cavity4_hweno", "mgs")])
 def test_converged_cavity_matches_reference(golden, case, ortho):
     from paper_2304_09485_b200.boundary import PatchSpec
     from paper_2304_09485_b200.mesh import generate_box_mesh
@@ -140,9 +142,10 @@ def test_converged_cavity_matches_reference(golden, case, ortho):
     patches = {nm: PatchSpec(nm, "wall_noslip_isothermal", lambda_wall=lam_wall) for nm in mesh.patch_names}
     patches["ymax"] = PatchSpec("ymax", "wall_noslip_isothermal", lambda_wall=lam_wall,
                                 velocity=np.array([0.15, 0.0, 0.0]))
-    s = Solver(mesh, SolverOptions(scheme="weno_gmres", model="viscous", mu=0.15 / 100.0, patches=patches, cfl=2.0,
+    scheme = "hweno_gmres" if case.endswith("_hweno") else "weno_gmres"
+    s = Solver(mesh, SolverOptions(scheme=scheme, model="viscous", mu=0.15 / 100.0, patches=patches, cfl=2.0,
                                    ortho=ortho))
-    s.upload(initial_field(mesh, [1.0, 0.0, 0.0, 0.0, 1.0 / GAMMA]))
+    s.upload(initial_field(mesh, [1.0, 0.0, 0.0, 0.0, 1.0 / GAMMA], compact=scheme == "hweno_gmres"))
     traj, steps = [], None
     for k in range(1, ref_steps + 50):
         info = s.advance_resident()
@@ -151,8 +154,10 @@ def test_converged_cavity_matches_reference(golden, case, ortho):
             steps = k
             break
     assert steps is not None and abs(steps - ref_steps) <= 1, (steps, ref_steps)
-    q = s.download().q
-    assert relmax(q, g["q_final"]) <= 1e-8
+    final = s.download()
+    assert relmax(final.q, g["q_final"]) <= 1e-8
+    if "grad_final" in g:
+        assert relmax(final.grad, g["grad_final"]) <= 1e-8
     # residual-drop history: every decade crossing within +-1 nonlinear step
     ref_traj = g["hist"][:, 0]
     dec = range(1, 11)
