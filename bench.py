@@ -69,6 +69,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-converge", action="store_true", help="skip the wall-time-to-1e-10 leg")
     p.add_argument("--converge-n", type=int, default=8, help="cavity lattice for the convergence leg (6 n^3 tets)")
+    p.add_argument("--no-c5", action="store_true", help="skip the C5 (~10M-cell) scale leg of the default run")
     a = p.parse_args()
     # configs[1]: inviscid subsonic sphere, non-compact HGKS + matrix-free GMRES
     defaults = {"c1": (64, "weno_gmres", "roe"), "c2": (16, "weno_gmres", "frechet"),
@@ -510,6 +511,40 @@ def converge_leg(args, threshold=1e-10, max_steps=12000, rel_steps=16000, rel_bu
             "cells": mesh.ncells, "relative_10_decades": rel}
 
 
+def c5_leg(device, steps=5, warmup=2):
+    """The north-star scale case on the same GPU (configs[4] shape: ~10M-tet
+    sphere, compact HWENO, Roe GMRES), state resident in HBM, CUDA events
+    around `steps` steps after `warmup`; setup = device-side stencils and
+    operators (gks_create)."""
+    import ctypes as C
+
+    from paper_2304_09485_b200 import _native as N
+    from paper_2304_09485_b200.stepping import SolutionField, Solver, SolverOptions
+
+    a = argparse.Namespace(workload="c5", n=30)
+    t0 = time.perf_counter()
+    mesh, patches, q, g, label, extra = build_workload(a, True)
+    t_mesh = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    s = Solver(mesh, SolverOptions(scheme="hweno_gmres", patches=patches, jacobian="roe", device=device, **extra))
+    t_setup = time.perf_counter() - t0
+    s.upload(SolutionField(q, g))
+    lib = N.load()
+    for _ in range(warmup):
+        s.advance_resident()
+    N.check(lib.gks_event_record(s._handle, 0))
+    infos = [s.advance_resident() for _ in range(steps)]
+    N.check(lib.gks_event_record(s._handle, 1))
+    ms = C.c_double()
+    N.check(lib.gks_event_elapsed(s._handle, 0, 1, C.byref(ms)))
+    nc = mesh.ncells
+    out = {"workload": label, "cells": nc, "steps": steps, "warmup": warmup, "ms_per_step": ms.value / steps,
+           "value": nc * steps / (ms.value / 1000.0), "unit": UNIT + " (Roe: one residual per step)",
+           "setup_s": round(t_setup, 2), "mesh_s": round(t_mesh, 2), "res_rho_l1_last": infos[-1].res_rho_l1}
+    del s
+    return out
+
+
 def paper_table_leg(steps=100, warmup=5):
     """The paper's only published performance table:
     computational time per 100 implicit steps of the Re 1000 lid-driven cavity
@@ -750,6 +785,13 @@ def run_ours(args):
         except Exception as exc:
             paper = {"error": str(exc)}
 
+    c5 = None
+    if not args.no_c5 and world == 1 and args.workload == "c2" and not decomp:
+        try:
+            c5 = c5_leg(local)
+        except Exception as exc:
+            c5 = {"error": str(exc)}
+
     cb = None
     if cpu_collect is not None:
         try:
@@ -788,6 +830,7 @@ def run_ours(args):
                       "solver_cycles": infos[-1].solver_cycles},
         "time_to_threshold": conv,
         "paper_table": paper,
+        "c5_scale": c5,
         "paper_gpu_derived": {"value": 1.60e5, "unit": UNIT, "note": "Quadro RTX 8000, cavity 48k tets (BASELINE.md)"},
     }
     print(json.dumps(line), flush=True)

@@ -7,7 +7,7 @@ for spec in "$@"; do
   tag=${spec%%=*}; lib=${spec#*=}
   if [ "$lib" = "base" ]; then unset GKS_LIB; else export GKS_LIB=$PWD/$lib; fi
   for rep in 1 2; do
-    timeout 600 python bench.py --no-cpu-baseline --no-converge --steps 5 ${BENCH_ARGS} > gpurun_out/ab_${tag}_${rep}.json 2> gpurun_out/ab_${tag}_${rep}.err
+    timeout 600 python bench.py --no-cpu-baseline --no-converge --no-c5 --steps 5 ${BENCH_ARGS} > gpurun_out/ab_${tag}_${rep}.json 2> gpurun_out/ab_${tag}_${rep}.err
     python - "$tag" "$rep" <<'PY'
 import json,sys
 t,r=sys.argv[1],sys.argv[2]
