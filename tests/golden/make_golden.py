@@ -277,7 +277,7 @@ CONVERGE_CASES = {
     "cavity4": dict(n=4, threshold=1e-10, max_steps=8000),
     "cavity8": dict(n=8, threshold=1e-10, max_steps=8000),
     # the compact scheme (HWENO + Gauss gradient update) on the same case
-    "cavity4_hweno": dict(n=4, threshold=1e-10, max_steps=8000, scheme="hweno_gmres"),
+    "cavity4_hweno": dict(n=4, threshold=1e-10, max_steps=12000, scheme="hweno_gmres"),
 }
 
 
