@@ -730,6 +730,7 @@ extern "C" {
 
 int gks_create(const GksMeshDesc* mesh, const GksSetup* setup, const GksOptions* opt, int device,
                GksHandle** out) {
+  GKS_NVTX("gks_create");
   set_error_index(-1);
   if (!mesh || !opt || !out) {
     set_error("gks_create: bad arguments");
@@ -750,6 +751,7 @@ int gks_create(const GksMeshDesc* mesh, const GksSetup* setup, const GksOptions*
 
 int gks_create_local(const GksMeshDesc* mesh, const GksSetup* setup, const GksOptions* opt,
                      const GksDomainDesc* domain, int device, GksHandle** out) {
+  GKS_NVTX("gks_create_local");
   set_error_index(-1);
   if (!mesh || !opt || !out || !domain || (!setup && !domain->setup_mesh)) {
     set_error("gks_create_local: bad arguments");
@@ -848,6 +850,7 @@ int gks_handle_array(GksHandle* G, const char* name, void* dst, int64_t* nbytes)
 int64_t gks_reduction_granularity(int64_t nc_global) { return red_group_cells(nc_global); }
 
 int gks_local_dt(GksHandle* G, const double* q, double* dt_out) {
+  GKS_NVTX("gks_local_dt");
   Handle* H = &G->H;
   set_error_index(-1);
   GKS_CUDA(cudaSetDevice(H->device));
@@ -863,6 +866,7 @@ int gks_local_dt(GksHandle* G, const double* q, double* dt_out) {
 
 int gks_residual(GksHandle* G, const double* q, const double* grad, const double* dt, int with_gradients,
                  double* res_out, double* grad_out) {
+  GKS_NVTX("gks_residual");
   Handle* H = &G->H;
   set_error_index(-1);
   GKS_CUDA(cudaSetDevice(H->device));
@@ -1313,6 +1317,7 @@ static int bs_check_size(GksBlockSystem* a) {
 extern "C" {
 
 int gks_assemble_jacobian(GksHandle* G, const double* q, const double* dt, const double* ghosts) {
+  GKS_NVTX("gks_assemble_jacobian");
   Handle* H = &G->H;
   set_error_index(-1);
   GKS_CUDA(cudaSetDevice(H->device));
@@ -1454,6 +1459,7 @@ int gks_blocksys_jacobi(GksBlockSystem* a, const double* b, int k_max, double* z
 
 int gks_gmres(GksBlockSystem* a, const double* b, double* x_out, int m, int restarts, int k_max, double rtol,
               double atol, int check_orthogonality, GksGmresInfo* info) {
+  GKS_NVTX("gks_gmres");
   TRY(bs_check_size(a));
   set_error_index(-1);
   BlockSys* A = &a->sys;
@@ -1589,12 +1595,14 @@ int gks_bad_mask(GksHandle* G, int8_t* out) {
 }
 
 int gks_advance_resident(GksHandle* G, GksStepInfo* info) {
+  GKS_NVTX("gks_advance_resident");
   set_error_index(-1);
   GKS_CUDA(cudaSetDevice(G->H.device));
   return advance_device(G, info);
 }
 
 int gks_advance(GksHandle* G, double* q_inout, double* grad_inout, GksStepInfo* info) {
+  GKS_NVTX("gks_advance");
   Handle* H = &G->H;
   if (H->compact && !grad_inout) {
     set_error("compact scheme needs a gradient field");
@@ -1607,6 +1615,7 @@ int gks_advance(GksHandle* G, double* q_inout, double* grad_inout, GksStepInfo* 
 
 int gks_frechet_matvec(GksHandle* G, const double* q, const double* grad, const double* dt, const double* v,
                        double sigma, double* out) {
+  GKS_NVTX("gks_frechet_matvec");
   Handle* H = &G->H;
   set_error_index(-1);
   GKS_CUDA(cudaSetDevice(H->device));

@@ -22,7 +22,21 @@
 #define GKS_RECON_MINB 4
 #endif
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace gks {
+
+// NVTX range over a host API call (header-only NVTX3: a no-op unless a
+// profiler such as nsys / ncu --nvtx injects itself)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define GKS_NVTX_CAT2(a, b) a##b
+#define GKS_NVTX_CAT(a, b) GKS_NVTX_CAT2(a, b)
+#define GKS_NVTX(name) ::gks::NvtxRange GKS_NVTX_CAT(gks_nvtx_, __LINE__)(name)
 
 void set_error(const char* fmt, ...);
 int cuda_fail(cudaError_t e, const char* what, const char* file, int line);

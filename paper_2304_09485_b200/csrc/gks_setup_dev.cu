@@ -254,6 +254,7 @@ __global__ void __launch_bounds__(256) k_setup_place(int64_t nl, Recs s, Recs d,
 // local cells in ascending reference id with all their faces, so stencil
 // choices match the global build -- and places the records in local order.
 int device_setup(Handle* H, const GksMeshDesc* local, const GksDomainDesc* dom) {
+  GKS_NVTX("gks_device_setup");
   const bool mapped = dom && dom->setup_mesh;
   const GksMeshDesc* m = mapped ? dom->setup_mesh : local;
   const int64_t nc = m->ncells, nl = local->ncells;
