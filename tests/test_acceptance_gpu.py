@@ -251,16 +251,16 @@ def test_frechet_gmres_step_parity_with_oracle():
     o = OracleSolver(mesh, scheme="weno_gmres", patches=patches, jacobian="frechet")
     fld = SolutionField(q, g)
     # every JVP is a finite difference with sigma ~ 1e-8 (stepping.py:298-313),
-    # so residual rounding (1e-16) reaches the update at ~1e-8 relative: the
-    # bar is the Frechet JVP's 1e-6 (tests/test_solver_gpu.py), not 1e-9
-    # (the step-2 residual norm, a small difference of fluxes at the updated
-    # state, inherits that ~1e-7 state difference amplified: rel 1e-4)
-    for k in range(2):
+    # so residual rounding (1e-16) reaches the update at ~1e-8 relative, and a
+    # state difference carried into the next step's JVPs is amplified by
+    # ~1/sigma again: measured on B200, fields 5e-10 after step 1 and <= 1.5e-7
+    # after steps 2-4, residual norms <= 4.5e-8 -- bars 1e-6 / 1e-6
+    for k in range(4):
         fld, info = s.advance(fld)
         q, g, oinfo = o.advance(q, g)
-        assert np.max(np.abs(fld.q - q)) <= 1e-6 * np.max(np.abs(q))
+        assert np.max(np.abs(fld.q - q)) <= (1e-8 if k == 0 else 1e-6) * np.max(np.abs(q))
         assert info.matvecs == oinfo["matvecs"]
-        assert info.res_rho_l1 == pytest.approx(oinfo["res_rho_l1"], rel=1e-10 if k == 0 else 1e-4)
+        assert info.res_rho_l1 == pytest.approx(oinfo["res_rho_l1"], rel=1e-10 if k == 0 else 1e-6)
 
 
 def test_c3_physics_ten_step_history_with_oracle():
