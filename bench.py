@@ -291,7 +291,8 @@ def kernel_model(solver, compact):
     lib = N.load()
     info = [int(lib.gks_handle_info(solver._handle, k)) for k in range(11)]
     nc, nf, nfq, nfi, nbf, nnz, K, M, S, _, nent = info
-    slots = os.environ.get("GKS_ASSEMBLE_SLOTS", "1") != "0"
+    # the library's default is the CSR walk (GKS_ASSEMBLE_SLOTS unset / 0)
+    slots = os.environ.get("GKS_ASSEMBLE_SLOTS", "0") not in ("", "0")
     per_row = nnz / nc
     mf = os.environ.get("GKS_ROE_MF", "1") != "0"
     if mf:
