@@ -1,3 +1,5 @@
+#!/bin/bash
+# Ma 3 study runs (profiles/r02/ma3/): KFVS first-order start, then high-order switches
 mkdir -p gpurun_out/ma3
 t() { tag=$1; shift; timeout 900 python tools/ma3_kfvs.py "$@" --out gpurun_out/ma3/$tag.json > gpurun_out/ma3/$tag.log 2>&1; python -c "
 import json,sys; d=json.load(open('gpurun_out/ma3/$tag.json')); d.pop('hist_every_50',None); print('$tag', json.dumps(d))" 2>/dev/null || tail -c 400 gpurun_out/ma3/$tag.log; }
