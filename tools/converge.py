@@ -34,6 +34,7 @@ def main():
     p.add_argument("--cfl", type=float, default=2.0)
     p.add_argument("--weights", default="nonlinear")
     p.add_argument("--every", type=int, default=50)
+    p.add_argument("--stop-abs", action="store_true", help="stop at the absolute test (skip the relative drop)")
     a = p.parse_args()
     compact = a.scheme.startswith("hweno")
     extra = {}
@@ -72,7 +73,7 @@ def main():
             t_abs, s_abs = t, k
         if k >= 5 and t_rel is None and info.res_rho_l1 <= 1e-10 * max(hist[:5]):
             t_rel, s_rel = t, k
-        if t_abs is not None and t_rel is not None:
+        if t_abs is not None and (t_rel is not None or a.stop_abs):
             break
     el = time.perf_counter() - t0
     if not hist:
