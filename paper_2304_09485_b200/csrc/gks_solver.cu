@@ -752,6 +752,40 @@ __global__ void k_assemble5(int64_t nc, const int* __restrict__ cfq_start, const
       for (int u = 0; u < 8; ++u) r = (ce[u] & 1) ? r + cc[u] : r - cc[u];
     }
   }
+  if (wantg) {
+    // gradient update too (compact scheme): batches of 4 -- index loads, then
+    // each entry's contribution / point value / weight / face, then the
+    // normals, then the sums in list order
+    for (; e + 4 <= e1; e += 4) {
+      int ce[4], f[4];
+      double cc[4], pv[4], ws[4], nr[4][3];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) ce[u] = __ldg(cfq + e + u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = ce[u] >> 1;
+        cc[u] = contrib[i * 5 + k];
+        pv[u] = qpt[i * 5 + k];
+        ws[u] = __ldg(fq_ws + i);
+        f[u] = __ldg(fq_face + i);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int x = 0; x < 3; ++x) nr[u][x] = __ldg(f_normal + 3 * f[u] + x);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const bool is_nbr = ce[u] & 1;
+        r = is_nbr ? r + cc[u] : r - cc[u];
+#pragma unroll
+        for (int x = 0; x < 3; ++x) {
+          const double wn = ws[u] * nr[u][x];
+          const double tt = wn * pv[u];
+          g[x] = is_nbr ? g[x] - tt : g[x] + tt;
+        }
+      }
+    }
+  }
 #pragma unroll 4
   for (; e < e1; ++e) {
     const int ce = cfq[e];
