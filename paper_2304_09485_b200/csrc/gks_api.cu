@@ -406,6 +406,7 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
       if (nb >= 0) list[pos[nb]++] = (int)((i << 1) | 1);
     }
     TRY(upload(H, &H->cfq_start, cnt.data(), nc + 1));
+    H->asm_tile = assemble_tile_fits(cnt.data(), H->n_owned);
     TRY(check_vec("assembly list", list, 0, nfq, 1));
     TRY(upload(H, &H->cfq, list.data(), list.size()));
     {

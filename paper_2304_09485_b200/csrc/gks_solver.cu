@@ -819,6 +819,60 @@ __global__ void k_assemble5(int64_t nc, const int* __restrict__ cfq_start, const
   }
 }
 
+// Tiled assembly (residuals without the gradient update): a CTA of 32 cells
+// x 5 components first loads its cells' whole CSR list segment into shared
+// memory with coalesced loads (one copy for the five component threads),
+// then every thread issues its contribution loads from the staged indices
+// -- the dependent index round trip leaves the per-thread chain.  Same
+// entries, order and signs as k_assemble5: bitwise-identical results.
+constexpr int AT_CELLS = 32;
+constexpr int AT_MAXE = AT_CELLS * 18;  // hex cells: at most 6 faces x 3 points
+__global__ void __launch_bounds__(AT_CELLS * 5) k_assemble_tile(int64_t nc, const int* __restrict__ cfq_start,
+                                                                const int* __restrict__ cfq,
+                                                                const double* __restrict__ contrib,
+                                                                const double* __restrict__ vol,
+                                                                double* __restrict__ res, const int* gate,
+                                                                FrechetEpi fe) {
+  if (gate && !*gate) return;
+  __shared__ int sidx[AT_MAXE];
+  const int64_t c0 = (int64_t)blockIdx.x * AT_CELLS;
+  const int64_t cend = c0 + AT_CELLS < nc ? c0 + AT_CELLS : nc;
+  const int base = __ldg(cfq_start + c0);
+  const int ne = __ldg(cfq_start + cend) - base;
+  for (int i = threadIdx.x; i < ne; i += blockDim.x) sidx[i] = __ldg(cfq + base + i);
+  __syncthreads();
+  const int64_t t = c0 * 5 + threadIdx.x;
+  if (t >= nc * 5) return;
+  const int64_t c = t / 5;
+  const int k = (int)(t - c * 5);
+  int e = __ldg(cfq_start + c) - base;
+  const int e1 = __ldg(cfq_start + c + 1) - base;
+  double r = 0.0;
+  for (; e + 8 <= e1; e += 8) {
+    double cc[8];
+    int ce[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) ce[u] = sidx[e + u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) cc[u] = contrib[(int64_t)(ce[u] >> 1) * 5 + k];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) r = (ce[u] & 1) ? r + cc[u] : r - cc[u];
+  }
+#pragma unroll 4
+  for (; e < e1; ++e) {
+    const int ce = sidx[e];
+    const double cc = contrib[(int64_t)(ce >> 1) * 5 + k];
+    r = (ce & 1) ? r + cc : r - cc;
+  }
+  if (fe.out) {
+    const double sg = *fe.sigma;
+    const double d = sg == 0.0 ? 0.0 : (r - fe.r0[t]) / sg;
+    fe.out[t] = fe.mode ? (vol[c] / fe.dt[c]) * fe.v[t] - d : d;
+  } else {
+    res[t] = r;
+  }
+}
+
 // Slot assembly: the face kernel has written every signed contribution into
 // its cell's CSR slot, so a cell's residual is a contiguous segmented sum
 // (one thread per (cell, component), coalesced 40-byte slot records, no
@@ -1011,9 +1065,16 @@ int residual_device(Handle* H, const double* q, double* res, bool with_gradients
     const char* e = getenv("GKS_ASSEMBLE5");
     return e ? atoi(e) : 1;
   }();
+  static const int tile = [] {
+    const char* e = getenv("GKS_ASSEMBLE_TILE");
+    return e ? atoi(e) : 1;
+  }();
   if (slot_mode)
     GKS_LAUNCH(KC_ASSEMBLE, k_assemble_slots, blocks_for(H->n_owned * 5, 160), 160, 0, H->stream, H->n_owned,
                H->cfq_start, H->slots, H->vol, res, gate, fe ? *fe : FrechetEpi{});
+  else if (asm5 && tile && H->asm_tile && !with_gradients)
+    GKS_LAUNCH(KC_ASSEMBLE, k_assemble_tile, blocks_for(H->n_owned, AT_CELLS), AT_CELLS * 5, 0, H->stream, H->n_owned,
+               H->cfq_start, H->cfq, H->contrib, H->vol, res, gate, fe ? *fe : FrechetEpi{});
   else if (asm5)
     GKS_LAUNCH(KC_ASSEMBLE, k_assemble5, blocks_for(H->n_owned * 5, 160), 160, 0, H->stream, H->n_owned, H->cfq_start,
                H->cfq, H->contrib, H->qpt, H->fq_face, H->fq_ws, H->f_normal, H->vol, res,
@@ -1253,6 +1314,16 @@ __global__ void __launch_bounds__(TPB) k_face_values(int64_t nfq, RecView R, con
     vn[i * 5 + k] = v[k];
     for (int d = 0; d < 3; ++d) gn[(i * 3 + d) * 5 + k] = g[d][k];
   }
+}
+
+// entries of the largest 32-cell tile of the assembly list fit the staging buffer
+// 1 if every 32-cell tile's list segment fits k_assemble_tile's staging
+int assemble_tile_fits(const int* cfq_start_host, int64_t n_owned) {
+  for (int64_t c0 = 0; c0 < n_owned; c0 += AT_CELLS) {
+    const int64_t ce = c0 + AT_CELLS < n_owned ? c0 + AT_CELLS : n_owned;
+    if (cfq_start_host[ce] - cfq_start_host[c0] > AT_MAXE) return 0;
+  }
+  return 1;
 }
 
 int recon_coeffs_device(Handle* H, const double* q, int linear) {

@@ -90,6 +90,7 @@ struct Handle {
   double *fq_point = nullptr, *fq_ws = nullptr;
   // cell -> fq CSR (assembly order), entries fq<<1 | is_neighbor
   int *cfq_start = nullptr, *cfq = nullptr;
+  int asm_tile = 0;  // every 32-cell tile's list segment fits k_assemble_tile's staging
   // slot assembly: per fq point the CSR positions of its owner / neighbour
   // entries (int2, -1 = none or not an owned cell); the face kernel writes
   // its signed contribution into both, the assembly is a contiguous
@@ -316,6 +317,7 @@ int gauss_gradients_device(Handle* H, const double* qpt, double* grad_out);
 int ghost_batch_device(int64_t n, const DevPatch& P, const double* q, const double* nrm, const double* grad,
                        const KinConst& kc, double* q_out, double* grad_out);
 int jacobian_device(Handle* H, const double* q, bool ghosts_given);
+int assemble_tile_fits(const int* cfq_start_host, int64_t n_owned);
 // reconstruction pieces of the host API (gks_solver.cu)
 int recon_coeffs_device(Handle* H, const double* q, int linear);  // -> H->coef
 int recon_candidates_device(Handle* H, const double* q, int Mout, double* cbig, double* bsub);
