@@ -825,7 +825,10 @@ __global__ void k_assemble5(int64_t nc, const int* __restrict__ cfq_start, const
 // then every thread issues its contribution loads from the staged indices
 // -- the dependent index round trip leaves the per-thread chain.  Same
 // entries, order and signs as k_assemble5: bitwise-identical results.
-constexpr int AT_CELLS = 32;
+#ifndef GKS_AT_CELLS
+#define GKS_AT_CELLS 32
+#endif
+constexpr int AT_CELLS = GKS_AT_CELLS;
 constexpr int AT_MAXE = AT_CELLS * 18;  // hex cells: at most 6 faces x 3 points
 __global__ void __launch_bounds__(AT_CELLS * 5) k_assemble_tile(int64_t nc, const int* __restrict__ cfq_start,
                                                                 const int* __restrict__ cfq,
