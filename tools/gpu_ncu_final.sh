@@ -13,6 +13,7 @@ cap() {  # tag regex bench-args...
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ncu/launches_c2.csv \
   python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-converge --no-c5 > /dev/null 2>&1
 echo "launches c2 rc=$?"
+cap c2_assemble_tile "k_assemble_tile"
 cap c2_roe_mf6 "k_roe_mf<.int.6>"
 cap c2_face "k_face<.bool.0, .bool.0, .bool.0>"
 cap c2_recon_weno "k_recon_weno"

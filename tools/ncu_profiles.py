@@ -42,6 +42,7 @@ def model():
         "c3_recon_hweno": ("bytes", nc * (9 * (HA + 3 * HG) * 8 + (HA + HG) * 4 + HG * 8 + 360 + 40 + 120 + 360),
                            "operator records (linear weights: no sub-stencils) + Q, grad + C write"),
         "c2_assemble5": ("bytes", nfq * 40 + nc * 44 + 2 * nfq * 4, "contributions + CSR list + res write"),
+        "c2_assemble_tile": ("bytes", nfq * 40 + nc * 44 + 2 * nfq * 4, "contributions + CSR list + res write"),
         "c1_roe_mf5": ("bytes", C1B["spmv"], "C1 n=64: CSR + face records + prims + x + D + D^-1 + out (+pre)"),
         "c2_roe_mf6": ("bytes", sweep, "CSR + face records + prims + x + D^-1 + b + out"),
         "c2_axpy_dot": ("bytes", 4 * 8 * n5, "w read+write, v_i, v_(i+1)"),
