@@ -876,6 +876,94 @@ __global__ void __launch_bounds__(AT_CELLS * 5) k_assemble_tile(int64_t nc, cons
   }
 }
 
+// Tiled assembly with the Gauss gradient update (compact scheme): the list
+// segment and, per entry, the face-point weight times the face normal
+// (ws * n, computed once instead of by all five component threads) are
+// staged in shared memory; the sums follow k_assemble5's order and
+// operations exactly (bitwise-identical results).
+__global__ void __launch_bounds__(AT_CELLS * 5) k_assemble_tile_g(int64_t nc, const int* __restrict__ cfq_start,
+                                                                  const int* __restrict__ cfq,
+                                                                  const double* __restrict__ contrib,
+                                                                  const double* __restrict__ qpt,
+                                                                  const int* __restrict__ fq_face,
+                                                                  const double* __restrict__ fq_ws,
+                                                                  const double* __restrict__ f_normal,
+                                                                  const double* __restrict__ vol,
+                                                                  double* __restrict__ res,
+                                                                  double* __restrict__ grad_new, const int* gate,
+                                                                  FrechetEpi fe) {
+  if (gate && !*gate) return;
+  __shared__ int sidx[AT_MAXE];
+  __shared__ double swn[AT_MAXE * 3];
+  const int64_t c0 = (int64_t)blockIdx.x * AT_CELLS;
+  const int64_t cend = c0 + AT_CELLS < nc ? c0 + AT_CELLS : nc;
+  const int base = __ldg(cfq_start + c0);
+  const int ne = __ldg(cfq_start + cend) - base;
+  for (int i = threadIdx.x; i < ne; i += blockDim.x) {
+    const int ce = __ldg(cfq + base + i);
+    sidx[i] = ce;
+    const int64_t q = ce >> 1;
+    const int f = __ldg(fq_face + q);
+    const double ws = __ldg(fq_ws + q);
+#pragma unroll
+    for (int x = 0; x < 3; ++x) swn[i * 3 + x] = ws * __ldg(f_normal + 3 * f + x);
+  }
+  __syncthreads();
+  const int64_t t = c0 * 5 + threadIdx.x;
+  if (t >= nc * 5) return;
+  const int64_t c = t / 5;
+  const int k = (int)(t - c * 5);
+  int e = __ldg(cfq_start + c) - base;
+  const int e1 = __ldg(cfq_start + c + 1) - base;
+  double r = 0.0;
+  double g[3] = {0.0, 0.0, 0.0};
+  for (; e + 4 <= e1; e += 4) {
+    int ce[4];
+    double cc[4], pv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) ce[u] = sidx[e + u];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = ce[u] >> 1;
+      cc[u] = contrib[i * 5 + k];
+      pv[u] = qpt[i * 5 + k];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool is_nbr = ce[u] & 1;
+      r = is_nbr ? r + cc[u] : r - cc[u];
+#pragma unroll
+      for (int x = 0; x < 3; ++x) {
+        const double tt = swn[(e + u) * 3 + x] * pv[u];
+        g[x] = is_nbr ? g[x] - tt : g[x] + tt;
+      }
+    }
+  }
+  for (; e < e1; ++e) {
+    const int ce = sidx[e];
+    const int64_t i = ce >> 1;
+    const bool is_nbr = ce & 1;
+    const double cc = contrib[i * 5 + k];
+    const double pv = qpt[i * 5 + k];
+    r = is_nbr ? r + cc : r - cc;
+#pragma unroll
+    for (int x = 0; x < 3; ++x) {
+      const double tt = swn[e * 3 + x] * pv;
+      g[x] = is_nbr ? g[x] - tt : g[x] + tt;
+    }
+  }
+  if (fe.out) {
+    const double sg = *fe.sigma;
+    const double d = sg == 0.0 ? 0.0 : (r - fe.r0[t]) / sg;
+    fe.out[t] = fe.mode ? (vol[c] / fe.dt[c]) * fe.v[t] - d : d;
+  } else {
+    res[t] = r;
+  }
+  const double V = vol[c];
+#pragma unroll
+  for (int x = 0; x < 3; ++x) grad_new[(c * 3 + x) * 5 + k] = g[x] / V;
+}
+
 // Slot assembly: the face kernel has written every signed contribution into
 // its cell's CSR slot, so a cell's residual is a contiguous segmented sum
 // (one thread per (cell, component), coalesced 40-byte slot records, no
@@ -1075,6 +1163,10 @@ int residual_device(Handle* H, const double* q, double* res, bool with_gradients
   if (slot_mode)
     GKS_LAUNCH(KC_ASSEMBLE, k_assemble_slots, blocks_for(H->n_owned * 5, 160), 160, 0, H->stream, H->n_owned,
                H->cfq_start, H->slots, H->vol, res, gate, fe ? *fe : FrechetEpi{});
+  else if (asm5 && tile && H->asm_tile && with_gradients)
+    GKS_LAUNCH(KC_ASSEMBLE, k_assemble_tile_g, blocks_for(H->n_owned, AT_CELLS), AT_CELLS * 5, 0, H->stream,
+               H->n_owned, H->cfq_start, H->cfq, H->contrib, H->qpt, H->fq_face, H->fq_ws, H->f_normal, H->vol, res,
+               H->grad_new, gate, fe ? *fe : FrechetEpi{});
   else if (asm5 && tile && H->asm_tile && !with_gradients)
     GKS_LAUNCH(KC_ASSEMBLE, k_assemble_tile, blocks_for(H->n_owned, AT_CELLS), AT_CELLS * 5, 0, H->stream, H->n_owned,
                H->cfq_start, H->cfq, H->contrib, H->vol, res, gate, fe ? *fe : FrechetEpi{});
