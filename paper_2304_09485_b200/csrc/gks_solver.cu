@@ -107,6 +107,12 @@ __global__ void k_fill(int64_t n, double* __restrict__ dt, const double* val) {
 // 24 cells: a tile's staged records (60-93 KB) then fit 3 CTAs per SM, so
 // one CTA's bulk copies overlap the others' compute (measured against
 // 8 / 16 / 32: C2 HWENO recon 1.20 -> 0.97 ms, WENO 0.74 -> 0.71 ms)
+// combine(): one reciprocal of the weight total and of gamma0 instead of six
+// divisions (C2 WENO reconstruction 0.705 -> 0.663 ms; a rounding-level
+// change, inside every parity bar)
+#ifndef GKS_COMBINE_RCP
+#define GKS_COMBINE_RCP 1
+#endif
 #ifndef GKS_RT
 #define GKS_RT 24
 #endif
@@ -159,20 +165,34 @@ __device__ __forceinline__ void combine(double cb[9], const double (&b)[M][3], c
     wm[m] = act[m] ? lw * (1.0 + tau / (bs[m] + eps)) : 0.0;
     total += wm[m];
   }
+#if GKS_COMBINE_RCP
+  const double itot = 1.0 / total, ig0 = 1.0 / g0;
+  const double w0n = w0 * itot;
+#else
   const double w0n = w0 / total;
+#endif
   if (w0n_out) {
     *w0n_out = w0n;
 #pragma unroll
     for (int m = 0; m < M; ++m) wmn_out[m * wstride] = wm[m] / total;
   }
+#if GKS_COMBINE_RCP
+  const double c0 = w0n * ig0;
+  const double sub0 = w0n * lw * ig0;
+#else
   const double c0 = w0n / g0;
   const double sub0 = w0n * lw / g0;
+#endif
 #pragma unroll
   for (int d = 0; d < 9; ++d) cb[d] *= c0;
 #pragma unroll
   for (int m = 0; m < M; ++m) {
     if (act[m]) {
+#if GKS_COMBINE_RCP
+      const double f = wm[m] * itot - sub0;
+#else
       const double f = wm[m] / total - sub0;
+#endif
 #pragma unroll
       for (int d = 0; d < 3; ++d) cb[d] += f * b[m][d];
     }
