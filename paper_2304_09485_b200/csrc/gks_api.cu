@@ -318,6 +318,11 @@ int create_handle(GksHandle* G, const GksMeshDesc* m, const GksSetup* S, const G
   std::vector<int8_t> hb;
   TRY(upload(H, &H->vol, m->cell_volume, nc));
   TRY(upload(H, &H->h, m->cell_h, nc));
+  {
+    std::vector<double> ih(nc);
+    for (int64_t c = 0; c < nc; ++c) ih[c] = 1.0 / m->cell_h[c];
+    TRY(upload(H, &H->ih, ih.data(), nc));
+  }
   TRY(upload(H, &H->cen, m->cell_centroid, nc * 3));
   if (S) {  // host setup; otherwise device_setup builds avg0 / beta with the operators
   TRY(setup_array(S, "avg0", &hf, &hi, &hb, &shp));

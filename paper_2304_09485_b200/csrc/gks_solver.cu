@@ -402,10 +402,10 @@ __global__ void __launch_bounds__(RT_THREADS, GKS_RECON_MINB) k_recon_hweno(int6
 // FP64 divisions per face point before).  Rounding differs from the
 // reference's stored tables by an ulp (parity bar 1e-12, tests/).
 __device__ __forceinline__ void eval_side(const double* __restrict__ q, const double* __restrict__ coef,
-                                          const double* __restrict__ cen, const double* __restrict__ h,
+                                          const double* __restrict__ cen, const double* __restrict__ inv_h,
                                           const double* __restrict__ avg0, int64_t c, const double x[3],
                                           double val[5], double g[3][5]) {
-  const double ih = 1.0 / h[c];
+  const double ih = inv_h[c];  // 1 / h_c, precomputed once per handle (the same IEEE quotient)
   const double x0 = (x[0] - cen[3 * c]) * ih, x1 = (x[1] - cen[3 * c + 1]) * ih, x2 = (x[2] - cen[3 * c + 2]) * ih;
   const double* A = avg0 + c * 9;
   const double phi[9] = {x0 - A[0],      x1 - A[1],      x2 - A[2],      x0 * x0 - A[3], x0 * x1 - A[4],
@@ -429,10 +429,10 @@ __device__ __forceinline__ void eval_side(const double* __restrict__ q, const do
 
 // value only (no gradients): the pre-loop pressures of the inviscid collision time
 __device__ __forceinline__ void eval_value(const double* __restrict__ q, const double* __restrict__ coef,
-                                           const double* __restrict__ cen, const double* __restrict__ h,
+                                           const double* __restrict__ cen, const double* __restrict__ inv_h,
                                            const double* __restrict__ avg0, int64_t c, const double x[3],
                                            double val[5]) {
-  const double ih = 1.0 / h[c];
+  const double ih = inv_h[c];
   const double x0 = (x[0] - cen[3 * c]) * ih, x1 = (x[1] - cen[3 * c + 1]) * ih, x2 = (x[2] - cen[3 * c + 2]) * ih;
   const double* A = avg0 + c * 9;
   const double phi[9] = {x0 - A[0],      x1 - A[1],      x2 - A[2],      x0 * x0 - A[3], x0 * x1 - A[4],
@@ -472,7 +472,7 @@ __device__ __forceinline__ void local_slopes(const double g[3][5], const double*
 
 struct FaceArgs {
   int64_t nfq;
-  const double *q, *coef, *cen, *h, *avg0, *dt;
+  const double *q, *coef, *cen, *h, *ih, *avg0, *dt;
   const int *fq_face, *f_own, *f_nbr, *f_patch;
   const double *fq_point, *fq_ws, *f_frame, *f_normal, *f_shift;
   const DevPatch* patches;
@@ -507,10 +507,10 @@ __global__ void __launch_bounds__(128, GKS_FACE_MINB) k_face(FaceArgs A) {
   const int p = nb >= 0 ? -1 : A.f_patch[f];
   const bool wall = p >= 0 && A.patches[p].wall;
   auto eval_cell = [&](bool own, const double x[3], double v[5], double g[3][5]) {
-    eval_side(A.q, A.coef, A.cen, A.h, A.avg0, own ? o : nb, x, v, g);
+    eval_side(A.q, A.coef, A.cen, A.ih, A.avg0, own ? o : nb, x, v, g);
   };
   auto eval_cell_value = [&](bool own, const double x[3], double v[5]) {
-    eval_value(A.q, A.coef, A.cen, A.h, A.avg0, own ? o : nb, x, v);
+    eval_value(A.q, A.coef, A.cen, A.ih, A.avg0, own ? o : nb, x, v);
   };
 #if GKS_FACE_PREFETCH
   {
@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(128, GKS_FACE_MINB) k_face(FaceArgs A) {
   auto dtf = [&]() { return nb >= 0 ? fmin(A.dt[o], A.dt[nb]) : A.dt[o]; };
   int ghost_fail = 0;
   // side 0: owner reconstruction; side 1: neighbour (shifted chart) or ghost
-  auto get = [&](int side, double w[5], double sl[3][5]) {
+  auto get = [&](int side, double w[5], double sl[3][5], double& hside) {
     const double x[3] = {A.fq_point[3 * i], A.fq_point[3 * i + 1], A.fq_point[3 * i + 2]};
     double v[5], g[3][5];
     if (side == 0 || nb < 0) {
@@ -568,7 +568,12 @@ __global__ void __launch_bounds__(128, GKS_FACE_MINB) k_face(FaceArgs A) {
     const double* F = A.f_frame + 9 * f;
     double ql[5];
     to_local_state(v, F, ql);
+#if GKS_H_MUL
+    if (!cons_to_prim_h(ql, A.kc, w, hside)) return false;
+#else
     if (!cons_to_prim(ql, A.kc, w)) return false;
+    hside = 0.5 / w[4];
+#endif
     local_slopes(g, F, sl);
     return true;
   };
@@ -1143,7 +1148,7 @@ int residual_device(Handle* H, const double* q, double* res, bool with_gradients
   }
   FaceArgs A;
   A.nfq = H->nfq;
-  A.q = q; A.coef = H->coef; A.cen = H->cen; A.h = H->h; A.avg0 = H->avg0; A.dt = H->dt;
+  A.q = q; A.coef = H->coef; A.cen = H->cen; A.h = H->h; A.ih = H->ih; A.avg0 = H->avg0; A.dt = H->dt;
   A.fq_face = H->fq_face; A.f_own = H->f_own; A.f_nbr = H->f_nbr; A.f_patch = H->f_patch;
   A.fq_point = H->fq_point; A.fq_ws = H->fq_ws; A.f_frame = H->f_frame; A.f_normal = H->f_normal;
   A.f_shift = H->f_shift; A.patches = H->patches; A.model = H->model; A.mu = H->mu; A.kc = H->kc;
@@ -1300,14 +1305,14 @@ int boundary_ghosts_device(Handle* H, const double* q) {
 // kernel-argument view of the handle's records and geometry
 struct RecView {
   int Kt, Mt, St;
-  const double *big_op, *sub_op, *grad_scale, *cen, *h, *avg0, *fq_point, *f_shift;
+  const double *big_op, *sub_op, *grad_scale, *cen, *h, *ih, *avg0, *fq_point, *f_shift;
   const int *big_gather, *sub_gather, *avg_gather, *grad_gather, *fq_face, *f_own, *f_nbr;
 };
 
 static RecView rec_view(const Handle* H) {
-  return RecView{H->Kt,         H->Mt,         H->St,         H->big_op,      H->sub_op,      H->grad_scale,
-                 H->cen,        H->h,          H->avg0,       H->fq_point,    H->f_shift,     H->big_gather,
-                 H->sub_gather, H->avg_gather, H->grad_gather, H->fq_face,    H->f_own,       H->f_nbr};
+  return RecView{H->Kt,         H->Mt,         H->St,          H->big_op,   H->sub_op,  H->grad_scale, H->cen,
+                 H->h,          H->ih,         H->avg0,        H->fq_point, H->f_shift, H->big_gather, H->sub_gather,
+                 H->avg_gather, H->grad_gather, H->fq_face,    H->f_own,    H->f_nbr};
 }
 
 // candidate_coeffs (recon.py:276-283, hweno.py:139-160): the quadratic big
@@ -1416,14 +1421,14 @@ __global__ void __launch_bounds__(TPB) k_face_values(int64_t nfq, RecView R, con
   const int64_t own = R.f_own[f], nbr = R.f_nbr[f];
   const double x[3] = {R.fq_point[3 * i], R.fq_point[3 * i + 1], R.fq_point[3 * i + 2]};
   double v[5], g[3][5];
-  eval_side(q, coef, R.cen, R.h, R.avg0, own, x, v, g);
+  eval_side(q, coef, R.cen, R.ih, R.avg0, own, x, v, g);
   for (int k = 0; k < 5; ++k) {
     vo[i * 5 + k] = v[k];
     for (int d = 0; d < 3; ++d) go[(i * 3 + d) * 5 + k] = g[d][k];
   }
   if (nbr >= 0) {
     const double xn[3] = {x[0] - R.f_shift[3 * f], x[1] - R.f_shift[3 * f + 1], x[2] - R.f_shift[3 * f + 2]};
-    eval_side(q, coef, R.cen, R.h, R.avg0, nbr, xn, v, g);
+    eval_side(q, coef, R.cen, R.ih, R.avg0, nbr, xn, v, g);
   }
   for (int k = 0; k < 5; ++k) {
     vn[i * 5 + k] = v[k];

@@ -81,6 +81,7 @@ struct Handle {
   int npatch = 0;
   // cell geometry
   double *vol = nullptr, *h = nullptr, *cen = nullptr, *avg0 = nullptr;
+  double* ih = nullptr;  // 1 / h per cell (face-point evaluation)
   // faces
   int *f_own = nullptr, *f_nbr = nullptr, *f_patch = nullptr;
   double *f_area = nullptr, *f_normal = nullptr, *f_frame = nullptr, *f_shift = nullptr;
