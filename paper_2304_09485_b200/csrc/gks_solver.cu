@@ -110,6 +110,11 @@ __global__ void k_fill(int64_t n, double* __restrict__ dt, const double* val) {
 // combine(): one reciprocal of the weight total and of gamma0 instead of six
 // divisions (C2 WENO reconstruction 0.705 -> 0.663 ms; a rounding-level
 // change, inside every parity bar)
+// combine(): the candidate weights over a common denominator (one division
+// for the normalisation instead of M + 1): C2 reconstruction 0.663 -> 0.656 ms
+#ifndef GKS_COMBINE_PROD
+#define GKS_COMBINE_PROD 1
+#endif
 #ifndef GKS_COMBINE_RCP
 #define GKS_COMBINE_RCP 1
 #endif
@@ -157,6 +162,30 @@ __device__ __forceinline__ void combine(double cb[9], const double (&b)[M][3], c
   for (int m = 0; m < M; ++m)
     if (act[m]) tau += fabs(beta0 - bs[m]);
   tau /= (double)(nact > 1 ? nact : 1);
+#if GKS_COMBINE_PROD
+  // common denominator: with D = beta + eps, w = g (D + tau) / D; scaling
+  // every weight by prod(D) leaves the normalised weights unchanged and
+  // turns the M + 1 divisions into products (prefix / suffix products of the
+  // active D's)
+  double D[M + 1], pre[M + 2], suf[M + 2];
+  D[0] = beta0 + eps;
+#pragma unroll
+  for (int m = 0; m < M; ++m) D[m + 1] = act[m] ? bs[m] + eps : 1.0;
+  pre[0] = 1.0;
+#pragma unroll
+  for (int i = 0; i <= M; ++i) pre[i + 1] = pre[i] * D[i];
+  suf[M + 1] = 1.0;
+#pragma unroll
+  for (int i = M; i >= 0; --i) suf[i] = suf[i + 1] * D[i];
+  const double w0 = g0 * (D[0] + tau) * suf[1];
+  double wm[M];
+  double total = w0;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    wm[m] = act[m] ? lw * (D[m + 1] + tau) * (pre[m + 1] * suf[m + 2]) : 0.0;
+    total += wm[m];
+  }
+#else
   const double w0 = g0 * (1.0 + tau / (beta0 + eps));
   double wm[M];
   double total = w0;
@@ -165,6 +194,7 @@ __device__ __forceinline__ void combine(double cb[9], const double (&b)[M][3], c
     wm[m] = act[m] ? lw * (1.0 + tau / (bs[m] + eps)) : 0.0;
     total += wm[m];
   }
+#endif
 #if GKS_COMBINE_RCP
   const double itot = 1.0 / total, ig0 = 1.0 / g0;
   const double w0n = w0 * itot;
