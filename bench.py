@@ -61,8 +61,9 @@ def parse():
     p.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of decomposition")
     p.add_argument("--decompose", action="store_true",
                    help="N=1: run the decomposition path anyway (a 1-rank NCCL communicator)")
-    p.add_argument("--ortho", default="mgs", choices=("mgs", "cgs2"),
-                   help="GMRES orthogonalisation: reference MGS or CGS2 with fused multi-dots")
+    p.add_argument("--ortho", default="cgs2", choices=("mgs", "cgs2"),
+                   help="GMRES orthogonalisation: CGS2 with fused multi-dots (the north star's 'fused "
+                        "multi-dot' Gram-Schmidt, default) or the reference's MGS (also timed, 'ortho_alt')")
     p.add_argument("--reorder", default="none", choices=("none", "rcm", "morton"),
                    help="device-side locality renumbering of the mesh (reorder.py)")
     p.add_argument("--cpu-n", type=int, default=None, help="bounded CPU sample size (c1 box divisions / c2 cube-face cells)")
@@ -512,7 +513,7 @@ def converge_leg(args, threshold=1e-10, max_steps=12000, rel_steps=16000, rel_bu
             "cells": mesh.ncells, "relative_10_decades": rel}
 
 
-def c5_leg(device, steps=5, warmup=2):
+def c5_leg(device, steps=5, warmup=2, ortho="cgs2"):
     """The north-star scale case on the same GPU (configs[4] shape: ~10M-tet
     sphere, compact HWENO, Roe GMRES), state resident in HBM, CUDA events
     around `steps` steps after `warmup`; setup = device-side stencils and
@@ -527,7 +528,8 @@ def c5_leg(device, steps=5, warmup=2):
     mesh, patches, q, g, label, extra = build_workload(a, True)
     t_mesh = time.perf_counter() - t0
     t0 = time.perf_counter()
-    s = Solver(mesh, SolverOptions(scheme="hweno_gmres", patches=patches, jacobian="roe", device=device, **extra))
+    s = Solver(mesh, SolverOptions(scheme="hweno_gmres", patches=patches, jacobian="roe", device=device, ortho=ortho,
+                                   **extra))
     t_setup = time.perf_counter() - t0
     s.upload(SolutionField(q, g))
     lib = N.load()
@@ -541,7 +543,8 @@ def c5_leg(device, steps=5, warmup=2):
     nc = mesh.ncells
     out = {"workload": label, "cells": nc, "steps": steps, "warmup": warmup, "ms_per_step": ms.value / steps,
            "value": nc * steps / (ms.value / 1000.0), "unit": UNIT + " (Roe: one residual per step)",
-           "setup_s": round(t_setup, 2), "mesh_s": round(t_mesh, 2), "res_rho_l1_last": infos[-1].res_rho_l1}
+           "setup_s": round(t_setup, 2), "mesh_s": round(t_mesh, 2), "res_rho_l1_last": infos[-1].res_rho_l1,
+           "ortho": ortho}
     del s
     return out
 
@@ -652,11 +655,12 @@ def run_ours(args):
         ms = C.c_double()
         N.check(lib.gks_event_elapsed(solver._handle, 0, 1, C.byref(ms)))
     launches = N.kernel_launches() - launches0
-    # the same step with CGS2 multi-dot orthogonalisation (SolverOptions(ortho="cgs2")),
-    # on the live handle, for the record; the headline keeps the reference MGS
+    # the same step with the other orthogonalisation on the live handle, for
+    # the record: the reference's MGS (or CGS2 when --ortho mgs is the headline)
     cgs2 = None
-    if args.ortho == "mgs":
-        N.check(lib.gks_set_ortho(solver._handle, 1))
+    alt = 0 if args.ortho == "cgs2" else 1
+    if True:
+        N.check(lib.gks_set_ortho(solver._handle, alt))
         for _ in range(2):
             solver.advance_resident()
         barrier(dist)
@@ -667,9 +671,13 @@ def run_ours(args):
         N.check(lib.gks_event_elapsed(solver._handle, 4, 5, C.byref(ms_c)))
         ms_c = max_over_ranks(dist, ms_c.value, local)
         ev_c = sum(1 + i.matvecs for i in ci) if args.jacobian == "frechet" else args.steps
-        cgs2 = {"ms_per_step": ms_c / args.steps, "value": (1 if decomp else world) * nc * ev_c / (ms_c / 1000.0),
-                "note": "same handle, GMRES with CGS2 fused multi-dots (3 reductions per Arnoldi column)"}
-        N.check(lib.gks_set_ortho(solver._handle, 0))
+        cgs2 = {"ortho": "mgs" if alt == 0 else "cgs2", "ms_per_step": ms_c / args.steps,
+                "value": (1 if decomp else world) * nc * ev_c / (ms_c / 1000.0),
+                "matvecs_per_step": ev_c / args.steps - (1 if args.jacobian == "frechet" else 0),
+                "note": ("same handle, GMRES with the reference's modified Gram-Schmidt (j + 2 reductions per "
+                         "Arnoldi column)" if alt == 0 else
+                         "same handle, GMRES with CGS2 fused multi-dots (3 reductions per Arnoldi column)")}
+        N.check(lib.gks_set_ortho(solver._handle, 1 if args.ortho == "cgs2" else 0))
     # per-kernel breakdown: the timed region replays one CUDA graph per step,
     # so kernel durations come from a second, uncaptured pass of the same
     # step with CUDA events around every launch (on the launching stream)
@@ -789,7 +797,7 @@ def run_ours(args):
     c5 = None
     if not args.no_c5 and world == 1 and args.workload == "c2" and not decomp:
         try:
-            c5 = c5_leg(local)
+            c5 = c5_leg(local, ortho=args.ortho)
         except Exception as exc:
             c5 = {"error": str(exc)}
 
@@ -818,7 +826,7 @@ def run_ours(args):
                    "setup_s": round(t_setup, 2), "mesh_s": round(t_mesh, 2)},
         "e2e": e2e,
         "gpu_launches": launches,
-        "ortho_cgs2": cgs2,
+        "ortho_alt": cgs2,
         "roofline": roof,
         "kernels": kernels,
         "kernel_timing": ("CUDA events around every launch on the launching stream, in an uncaptured pass of "
