@@ -8,12 +8,14 @@
 
 #include "../../include/gks.h"
 
-// Minimum resident CTAs per SM (register budgets), chosen by measurement
-// (profiles/r01): the 128-thread FP64 flux kernels run best at 168
-// regs/thread (3 CTAs; 4 CTAs / 128 regs was 5 % slower after the division
-// cuts), the 160-thread reconstruction kernels at 96 (4 CTAs).
+// Minimum resident CTAs per SM (register budgets), chosen by measurement:
+// the 128-thread face kernel runs best at 255 regs/thread (2 CTAs, 8
+// warps/SM, nearly spill-free) since round 2 removed three FP64 divisions
+// per point -- C2 2.570 -> 2.558 ms, C3 (viscous + point value) 3.202 ->
+// 3.009 ms; it was 168 regs / 3 CTAs before (profiles/r01); 4 CTAs / 128
+// regs: 2.93 ms.  The 160-thread reconstruction kernels run at 96 (4 CTAs).
 #ifndef GKS_FACE_MINB
-#define GKS_FACE_MINB 3
+#define GKS_FACE_MINB 2
 #endif
 #ifndef GKS_FLUX_MINB
 #define GKS_FLUX_MINB 3
