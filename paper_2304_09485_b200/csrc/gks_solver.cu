@@ -32,9 +32,11 @@ static constexpr int TPB = 128;
 #ifndef GKS_FACE_TAU
 #define GKS_FACE_TAU 1  // interface_flux_t TAU mode of the inviscid face kernel (gks_kinetic.cuh)
 #endif
-// L2 prefetch of the neighbour side's records at kernel start (1 %, measured)
+// L2 prefetch of the neighbour side's records at kernel start: 1 % faster
+// at 168 registers (round 1), 0.4 % slower at 255 (both sides overlapped):
+// off
 #ifndef GKS_FACE_PREFETCH
-#define GKS_FACE_PREFETCH 1
+#define GKS_FACE_PREFETCH 0
 #endif
 
 // ---------------------------------------------------------------------------
@@ -117,6 +119,9 @@ __global__ void k_fill(int64_t n, double* __restrict__ dt, const double* val) {
 #endif
 #ifndef GKS_COMBINE_RCP
 #define GKS_COMBINE_RCP 1
+#endif
+#ifndef GKS_FACE_T
+#define GKS_FACE_T 128  // face kernel CTA size
 #endif
 #ifndef GKS_RT
 #define GKS_RT 24
@@ -527,7 +532,7 @@ struct FaceArgs {
 // -- a compile-time branch, so the high-order kernel keeps its constant
 // tau_in and register allocation
 template <bool VISC, bool POINT, bool KFVS>
-__global__ void __launch_bounds__(128, GKS_FACE_MINB) k_face(FaceArgs A) {
+__global__ void __launch_bounds__(GKS_FACE_T, GKS_FACE_MINB) k_face(FaceArgs A) {
   if (A.gate && !*A.gate) return;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.nfq) return;
@@ -1193,11 +1198,11 @@ int residual_device(Handle* H, const double* q, double* res, bool with_gradients
   const bool slot_mode = slot_env && !with_gradients;
   A.fq_slot = slot_mode ? H->fq_slot : nullptr;
   A.slots = H->slots;
-  const int fb = blocks_for(H->nfq, 128);
+  const int fb = blocks_for(H->nfq, GKS_FACE_T);
 #define GKS_FACE(V, P)                                                                    \
   do {                                                                                    \
-    if (H->first_order) GKS_LAUNCH(KC_FACE, (k_face<V, P, true>), fb, 128, 0, H->stream, A); \
-    else GKS_LAUNCH(KC_FACE, (k_face<V, P, false>), fb, 128, 0, H->stream, A);            \
+    if (H->first_order) GKS_LAUNCH(KC_FACE, (k_face<V, P, true>), fb, GKS_FACE_T, 0, H->stream, A); \
+    else GKS_LAUNCH(KC_FACE, (k_face<V, P, false>), fb, GKS_FACE_T, 0, H->stream, A);            \
   } while (0)
   if (H->model == 1) {
     if (with_gradients) GKS_FACE(true, true);
