@@ -35,6 +35,7 @@ def main():
     p.add_argument("--weights", default="nonlinear")
     p.add_argument("--every", type=int, default=50)
     p.add_argument("--stop-abs", action="store_true", help="stop at the absolute test (skip the relative drop)")
+    p.add_argument("--ortho", default="mgs", choices=("mgs", "cgs2"))
     a = p.parse_args()
     compact = a.scheme.startswith("hweno")
     extra = {}
@@ -53,7 +54,7 @@ def main():
         mesh, patches, q, g, extra = cavity_problem(a.n, compact, a.re)
     t0 = time.perf_counter()
     s = Solver(mesh, SolverOptions(scheme=a.scheme, patches=patches, jacobian=a.jacobian, cfl=a.cfl,
-                                   weights=a.weights, **extra))
+                                   weights=a.weights, ortho=a.ortho, **extra))
     t_setup = time.perf_counter() - t0
     s.upload(SolutionField(q, g))
     hist = []
@@ -79,6 +80,7 @@ def main():
     if not hist:
         hist = [float("nan")]
     print(json.dumps({"case": a.case, "n": a.n, "cells": mesh.ncells, "scheme": a.scheme, "jacobian": a.jacobian,
+                      "ortho": a.ortho,
                       "error": error,
                       "cfl": a.cfl, "weights": a.weights, "setup_s": round(t_setup, 2),
                       "steps_abs": s_abs, "seconds_abs": t_abs, "steps_rel10": s_rel, "seconds_rel10": t_rel,
