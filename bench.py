@@ -199,8 +199,34 @@ class ClockSampler:
         self.rows = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._nvml = None
+        try:  # NVML directly (microseconds per query), initialised before the timed region
+            import pynvml as nv
+
+            nv.nvmlInit()
+            self._nvml = (nv, nv.nvmlDeviceGetHandleByIndex(index))
+        except Exception:
+            self._nvml = None
+
+    def _run_nvml(self):
+        """A sample every 20 ms."""
+        nv, h = self._nvml
+        bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.rows.append([str(sm), str(mx), ""] + ["Active" if r & b else "Not Active" for b in bits])
+            self._stop.wait(0.02)
 
     def _run(self):
+        if self._nvml is not None:
+            try:
+                self._run_nvml()
+                return
+            except Exception:
+                pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -219,6 +245,11 @@ class ClockSampler:
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=6)
+        if self._nvml is not None:
+            try:
+                self._nvml[0].nvmlShutdown()
+            except Exception:
+                pass
 
     def summary(self):
         if not self.rows:
