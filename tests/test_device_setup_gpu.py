@@ -78,15 +78,16 @@ def test_device_setup_records_bitwise_equal_host(name, scheme):
     assert np.array_equal(r1, r2)
 
 
+@pytest.mark.parametrize("scheme", ["weno_gmres", "hweno_gmres"])
 @pytest.mark.parametrize("reorder", ["rcm", "morton"])
-def test_device_setup_on_renumbered_mesh(reorder):
+def test_device_setup_on_renumbered_mesh(reorder, scheme):
     """A renumbered handle builds its stencils on the permuted mesh: the
     enlarged tet members sort by the reference id (cell_rank), so the
     records equal the host setup restricted to the permutation."""
     mesh = MG.generate_sphere_mesh(2, radius=0.5, far=10.0)
-    dev = make(mesh, "weno_gmres", "device", reorder)
-    host = make(mesh, "weno_gmres", "host", reorder)
-    for arr in WENO_ARRAYS:
+    dev = make(mesh, scheme, "device", reorder)
+    host = make(mesh, scheme, "host", reorder)
+    for arr in (HWENO_ARRAYS if scheme == "hweno_gmres" else WENO_ARRAYS):
         assert np.array_equal(handle_array(dev, arr), handle_array(host, arr)), arr
 
 
