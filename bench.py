@@ -788,6 +788,10 @@ def run_ours(args):
             roof = {"kernel": name, "bound": "fp64", "achieved": round(ach, 3), "peak": round(fp64, 2),
                     "unit": "TFLOP/s", "frac": round(ach / fp64, 4), "traffic": None,
                     "algorithmic_flops_per_launch": model_flops[name],
+                    "flop_model": ("reference-model FP64 count per face point (4,648 + 720, SURVEY 8d); the kernel "
+                                   "does fewer (closed-form time slopes, folded weight monomials), so this "
+                                   "'achieved' is the reference work rate -- the FP64-pipe utilisation ncu "
+                                   "measures is in profiles/r02/ncu_kernels.md") if name == "face_flux" else None,
                     "peak_source": "live DFMA probe gks_fp64_peak (FP64 absent from MEASURED_PEAKS.json)"}
             break
     for name in kernels:
