@@ -13,9 +13,14 @@
 // warps/SM, nearly spill-free) since round 2 removed three FP64 divisions
 // per point -- C2 2.570 -> 2.558 ms, C3 (viscous + point value) 3.202 ->
 // 3.009 ms; it was 168 regs / 3 CTAs before (profiles/r01); 4 CTAs / 128
-// regs: 2.93 ms.  The 160-thread reconstruction kernels run at 96 (4 CTAs).
+// regs: 2.93 ms.  The closed-form time slopes and equilibrium terms shrank
+// the live state enough that 168 regs / 3 CTAs (12 warps/SM) spill only
+// 80 B/thread: C2 face 2.203 -> 1.867 ms, C1 2.55 -> 2.06, C3 2.68 -> 2.58,
+// C5 19.1 -> 18.0 ms (4 CTAs / 128 regs: 2.18 ms; 160 threads x 3: 2.28 ms;
+// the side loop rolled at 3 CTAs: 2.00 ms).  The 160-thread reconstruction
+// kernels run at 96 (4 CTAs).
 #ifndef GKS_FACE_MINB
-#define GKS_FACE_MINB 2
+#define GKS_FACE_MINB 3
 #endif
 #ifndef GKS_FLUX_MINB
 #define GKS_FLUX_MINB 3
